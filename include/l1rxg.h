@@ -175,6 +175,7 @@ typedef struct {
     double carrier_doppler_hz, code_freq_hz, code_phase_chips;
     double carrier_phase_rad, chi_chips, cn0_dbhz, carrier_lock_ratio;
     double dll_integrator, pll_integrator, mu_smoothed;
+    double dll_prev_error, pll_prev_error;
 } l1rxg_epoch_record;
 
 typedef struct l1rxg_ctx l1rxg_ctx;
@@ -270,6 +271,10 @@ int l1rxg_tracker_records(l1rxg_tracker* trk, int channel, int64_t e0,
  * device buffer (for an NCCL gather) or host buffer. */
 int l1rxg_tracker_records_raw(l1rxg_tracker* trk, void* dst, int dst_is_device,
                               int64_t* bytes_out);
+/* Reads back ingested baseband samples [s0, s0+count) of stream s as
+ * interleaved doubles (ingest parity checks against SampleSource). */
+int l1rxg_tracker_read_samples(l1rxg_tracker* trk, int stream, int64_t s0,
+                               int64_t count, double* iq_out);
 /* Milliseconds of device time of the last run() (CUDA events on the
  * tracker's stream), split into ingest and tracking kernels. */
 int l1rxg_tracker_timing(l1rxg_tracker* trk, double* ingest_ms,

@@ -325,7 +325,7 @@ double orc_fll_discriminator_di(double pi_, double pq, double ci, double cq,
 }
 
 double orc_carrier_aid(double doppler, double dll) {
-    return CHIP_RATE_HZ * (1.0 + doppler / F_L1_HZ) + dll;
+    return fma(CHIP_RATE_HZ, 1.0 + doppler / F_L1_HZ, dll); /* contracted as compiled */
 }
 
 /* update_quality_metrics (tracking.hpp:459-515) */
@@ -454,6 +454,8 @@ int orc_track_epoch(l1rxg_channel* ch, const double* iq, int n,
         rec->dll_integrator = ch->dll_integrator;
         rec->pll_integrator = ch->pll_integrator;
         rec->mu_smoothed = ch->mu_smoothed;
+        rec->dll_prev_error = ch->dll_prev_error;
+        rec->pll_prev_error = ch->pll_prev_error;
     }
     return 0;
 }

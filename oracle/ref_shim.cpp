@@ -232,6 +232,8 @@ void fill_record(const ChannelState& ch, const CorrelatorOutputs& o,
     r->dll_integrator = ch.dll_filter.integrator;
     r->pll_integrator = ch.pll_filter.integrator;
     r->mu_smoothed = ch.mu_smoothed;
+    r->dll_prev_error = ch.dll_filter.prev_error;
+    r->pll_prev_error = ch.pll_filter.prev_error;
 }
 
 // One tracking step of the reference on a channel (track_epoch,

@@ -147,7 +147,8 @@ class EpochRecord(C.Structure):
             "ie", "qe", "ip", "qp", "il", "ql", "ip_h1", "qp_h1", "ip_h2", "qp_h2",
             "carrier_doppler_hz", "code_freq_hz", "code_phase_chips", "carrier_phase_rad",
             "chi_chips", "cn0_dbhz", "carrier_lock_ratio",
-            "dll_integrator", "pll_integrator", "mu_smoothed")]
+            "dll_integrator", "pll_integrator", "mu_smoothed",
+            "dll_prev_error", "pll_prev_error")]
 
 
 class TrackerDesc(C.Structure):

@@ -1,0 +1,870 @@
+// l1rxg.cu -- host runtime (C++) and C ABI of the B200 tracking correlator.
+//
+// One context per device owns the C/A code table (33 x 1023 int8, built
+// once like ca_code_table(), cacode.hpp:99-107), two CUDA streams (compute
+// and H2D copy) and scratch buffers.  A tracker owns per-stream device
+// rings of complex baseband (float2) fed by the ingest kernels, the channel
+// states, and per-channel epoch-record rings.  See include/l1rxg.h for the
+// reference interface each entry point replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "l1rxg.h"
+
+using namespace l1rxg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                 \
+    do {                                                                         \
+        cudaError_t e_ = (expr);                                                 \
+        if (e_ != cudaSuccess)                                                   \
+            return set_err(e_ == cudaErrorMemoryAllocation ? L1RXG_ENOMEM        \
+                                                           : L1RXG_ECUDA,        \
+                           std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+    } while (0)
+
+// ---- C/A code generation (cacode.hpp:20-64), host side ---------------
+const int k_g2_taps[33][2] = {
+    {0, 0},  {2, 6}, {3, 7}, {4, 8},  {5, 9}, {1, 9},  {2, 10}, {1, 8}, {2, 9},
+    {3, 10}, {2, 3}, {3, 4}, {5, 6},  {6, 7}, {7, 8},  {8, 9},  {9, 10}, {1, 4},
+    {2, 5},  {3, 6}, {4, 7}, {5, 8},  {6, 9}, {1, 3},  {4, 6},  {5, 7},  {6, 8},
+    {7, 9},  {8, 10}, {1, 6}, {2, 7}, {3, 8}, {4, 9},
+};
+
+void gold_code(int prn, int8_t* out) {
+    // G1 = x^10+x^3+1, G2 = x^10+x^9+x^8+x^6+x^3+x^2+1 as 10-bit shift
+    // registers (bit j = stage j+1), G2 output from the phase-select taps.
+    unsigned g1 = 0x3FF, g2 = 0x3FF;
+    const int t1 = k_g2_taps[prn][0] - 1, t2 = k_g2_taps[prn][1] - 1;
+    for (int i = 0; i < 1023; ++i) {
+        const unsigned o = ((g1 >> 9) ^ (g2 >> t1) ^ (g2 >> t2)) & 1u;
+        out[i] = static_cast<int8_t>(1 - 2 * static_cast<int>(o));
+        const unsigned f1 = ((g1 >> 2) ^ (g1 >> 9)) & 1u;
+        const unsigned f2 = ((g2 >> 1) ^ (g2 >> 2) ^ (g2 >> 5) ^ (g2 >> 7) ^ (g2 >> 8) ^ (g2 >> 9)) & 1u;
+        g1 = ((g1 << 1) | f1) & 0x3FF;
+        g2 = ((g2 << 1) | f2) & 0x3FF;
+    }
+}
+
+void halfband(double* h) {  // samples.hpp:89-108
+    double sum = 0.0;
+    for (int n = 0; n < 23; ++n) {
+        const double k = static_cast<double>(n - 11);
+        double v = (n == 11) ? 0.5 : std::sin(PI_D * k / 2.0) / (PI_D * k);
+        v *= 0.54 - 0.46 * std::cos(2.0 * PI_D * n / 22.0);
+        h[n] = v;
+        sum += v;
+    }
+    for (int n = 0; n < 23; ++n)
+        h[n] /= sum;
+}
+
+std::once_flag g_const_once;
+int g_const_rc = 0;
+
+int upload_constants() {
+    std::call_once(g_const_once, [] {
+        double h[23];
+        halfband(h);
+        float re[4][23], im[4][23], h2[23];
+        // mixed(g) = v/128 * P[g mod 4], P = {1, -j, -1, j}
+        const double pr[4] = {1, 0, -1, 0}, pi[4] = {0, -1, 0, 1};
+        for (int r = 0; r < 4; ++r)
+            for (int t = 0; t < 23; ++t) {
+                const int p = ((r - t) % 4 + 4) % 4;
+                re[r][t] = static_cast<float>(2.0 * h[t] / 128.0 * pr[p]);
+                im[r][t] = static_cast<float>(2.0 * h[t] / 128.0 * pi[p]);
+            }
+        for (int t = 0; t < 23; ++t)
+            h2[t] = static_cast<float>(2.0 * h[t]);
+        if (cudaMemcpyToSymbol(c_if4_re, re, sizeof re) != cudaSuccess ||
+            cudaMemcpyToSymbol(c_if4_im, im, sizeof im) != cudaSuccess ||
+            cudaMemcpyToSymbol(c_halfband2, h2, sizeof h2) != cudaSuccess)
+            g_const_rc = 1;
+    });
+    return g_const_rc;
+}
+
+// instantiated tap counts; a request for K taps runs the smallest T >= K
+// with the extra taps padded (their sums are discarded)
+const int k_inst[] = {3, 5, 7, 9, 11, 13, 16};
+int pick_T(int K) {
+    for (int t : k_inst)
+        if (t >= K)
+            return t;
+    return -1;
+}
+
+// Block size: enough RUN-sample runs to cover the epoch in the fewest
+// sub-tiles of at most 768 threads (<= 190 KB of shared tile).
+int pick_threads(int n, int* subtiles) {
+    const int max_nt = 768;
+    const int k = (n + max_nt * RUN - 1) / (max_nt * RUN);
+    const int runs = (n + k * RUN - 1) / (k * RUN);
+    int nt = ((runs + 31) / 32) * 32;
+    nt = std::max(64, std::min(max_nt, nt));
+    if (subtiles)
+        *subtiles = (n + nt * RUN - 1) / (nt * RUN);
+    return nt;
+}
+
+template <int T>
+size_t smem_bytes(int nt) {
+    return ((sizeof(CorrSmem<T>) + 15) & ~size_t(15)) + static_cast<size_t>(nt) * RUN * sizeof(float2);
+}
+
+template <int T>
+int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
+    const size_t sm = smem_bytes<T>(nt);
+    CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    track_kernel<T><<<n_ch, nt, sm, s>>>(a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <int T>
+int launch_jobs(const JobArgs& a, int n_jobs, int nt, cudaStream_t s) {
+    const size_t sm = smem_bytes<T>(nt);
+    CK(cudaFuncSetAttribute(correlate_jobs_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    correlate_jobs_kernel<T><<<n_jobs, nt, sm, s>>>(a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+#define DISPATCH_T(T_, FN, ...)            \
+    switch (T_) {                          \
+    case 3: return FN<3>(__VA_ARGS__);     \
+    case 5: return FN<5>(__VA_ARGS__);     \
+    case 7: return FN<7>(__VA_ARGS__);     \
+    case 9: return FN<9>(__VA_ARGS__);     \
+    case 11: return FN<11>(__VA_ARGS__);   \
+    case 13: return FN<13>(__VA_ARGS__);   \
+    case 16: return FN<16>(__VA_ARGS__);   \
+    default: return set_err(L1RXG_EINVAL, "unsupported tap count"); \
+    }
+
+int validate_taps(const l1rxg_taps* t) {
+    if (!t || t->n_taps < 1 || t->n_taps > L1RXG_MAX_TAPS)
+        return set_err(L1RXG_EINVAL, "n_taps must be in 1..16");
+    for (int k : {t->early, t->prompt, t->late})
+        if (k < 0 || k >= t->n_taps)
+            return set_err(L1RXG_EINVAL, "early/prompt/late must index a tap");
+    for (int k = 0; k < t->n_taps; ++k)
+        if (!(std::fabs(t->offsets_chips[k]) <= 1.0))
+            return set_err(L1RXG_EINVAL, "tap offsets must be within +/-1 chip");
+    return 0;
+}
+
+// tracking.hpp:47-57
+int validate_cfg(const l1rxg_tracking_cfg* c) {
+    if (c->el_spacing_chips <= 0 || c->el_spacing_chips > 1)
+        return set_err(L1RXG_EINVAL, "el_spacing_chips must be in (0,1]");
+    if (c->dll_bandwidth_hz <= 0 || c->pll_bandwidth_hz <= 0 || c->fll_bandwidth_hz <= 0)
+        return set_err(L1RXG_EINVAL, "loop bandwidths must be positive");
+    if (c->epoch_ms != 1)
+        return set_err(L1RXG_EINVAL, "only 1 ms epochs are supported");
+    if (c->cn0_window_ms < 2)
+        return set_err(L1RXG_EINVAL, "cn0_window_ms must be >= 2");
+    if (c->cn0_window_ms > L1RXG_WIN_MAX)
+        return set_err(L1RXG_EINVAL, "cn0_window_ms must be <= 64 on the GPU path");
+    return 0;
+}
+
+l1rxg_taps padded_taps(const l1rxg_taps& t, int T) {
+    l1rxg_taps p = t;
+    for (int k = t.n_taps; k < T; ++k)
+        p.offsets_chips[k] = t.offsets_chips[t.prompt];
+    return p;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n)
+            return 0;
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, bytes));
+        n = bytes;
+        return 0;
+    }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct l1rxg_ctx {
+    int device = 0;
+    cudaStream_t compute = nullptr, copy = nullptr;
+    int8_t* d_codes = nullptr;
+    DevBuf iq64, iq32, states, prns, sums, corr;
+    std::mutex mu;  // serialises the per-call path
+    int64_t launches = 0;
+};
+
+struct StreamRing {
+    float2* ring = nullptr;  // R + apron
+    int64_t pushed = 0;      // samples ingested
+    int8_t* hist8[2] = {nullptr, nullptr};
+    float2* histf[2] = {nullptr, nullptr};
+    int hist_cur = 0;
+};
+
+struct l1rxg_tracker {
+    l1rxg_ctx* ctx = nullptr;
+    l1rxg_tracker_desc d{};
+    int T = 3;
+    int nt = 64;
+    int64_t R = 0, apron = 0;
+    std::vector<StreamRing> streams;
+    float2* d_ring = nullptr;
+    int64_t* d_avail = nullptr;
+    l1rxg_channel* d_chans = nullptr;
+    int32_t* d_chan_stream = nullptr;
+    l1rxg_epoch_record* d_recs = nullptr;
+    double* d_tapsums = nullptr;
+    int64_t* d_ecount = nullptr;
+    int32_t* d_status = nullptr;
+    DevBuf staging[2];
+    DevBuf mixed;
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+    int stage_cur = 0;
+    struct Timed {
+        cudaEvent_t a, b;
+        int kind;  // 0 ingest, 1 track
+    };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    int64_t launches = 0;
+};
+
+namespace {
+
+cudaEvent_t get_event(l1rxg_tracker* t) {
+    if (!t->ev_pool.empty()) {
+        cudaEvent_t e = t->ev_pool.back();
+        t->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+int ingest_launch(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nsamp,
+                  cudaStream_t st) {
+    StreamRing& r = t->streams[static_cast<size_t>(s)];
+    const int64_t g0 = r.pushed;
+    const int64_t pos0 = g0 % t->R;
+    int64_t* slot = t->d_avail + s;
+    const int fmt = t->d.format;
+    cudaEvent_t a = get_event(t), b = get_event(t);
+    cudaEventRecord(a, st);
+    if (fmt == L1RXG_FMT_INT8_REAL_IF) {
+        const double w = -2.0 * PI_D * t->d.if_frequency_hz / t->d.sample_rate_hz;
+        if (w == -PI_D / 2.0) {
+            const int cur = r.hist_cur;
+            const int64_t blocks = (nsamp + ING_TILE - 1) / ING_TILE;
+            ingest_if4_kernel<<<(unsigned)blocks, ING_TPB, 0, st>>>(
+                static_cast<const int8_t*>(dev_bytes), r.hist8[cur], r.hist8[cur ^ 1], g0, nsamp,
+                r.ring, t->R, t->apron, pos0, slot);
+            r.hist_cur ^= 1;
+            t->launches += 1;
+        } else {
+            if (t->mixed.ensure(static_cast<size_t>(nsamp + 22) * sizeof(float2)))
+                return L1RXG_ENOMEM;
+            float2* mixed = static_cast<float2*>(t->mixed.p);
+            const int cur = r.hist_cur;
+            CK(cudaMemcpyAsync(mixed, r.histf[cur], 22 * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+            const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
+            mix_generic_kernel<<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(dev_bytes), g0,
+                                                       nsamp, w, mixed);
+            fir_generic_kernel<<<blocks, 256, 0, st>>>(mixed, nsamp, r.ring, t->R, t->apron, pos0,
+                                                       r.histf[cur ^ 1], slot, g0 + nsamp);
+            r.hist_cur ^= 1;
+            t->launches += 2;
+        }
+    } else {
+        const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
+        decode_iq_kernel<<<blocks, 256, 0, st>>>(dev_bytes, fmt, nsamp, r.ring, t->R, t->apron,
+                                                 pos0, slot, g0 + nsamp);
+        t->launches += 1;
+    }
+    CK(cudaGetLastError());
+    cudaEventRecord(b, st);
+    t->timed.push_back({a, b, 0});
+    r.pushed += nsamp;
+    return 0;
+}
+
+int bytes_per_sample(int fmt) {
+    switch (fmt) {
+    case L1RXG_FMT_INT8_IQ: return 2;
+    case L1RXG_FMT_INT16_IQ: return 4;
+    case L1RXG_FMT_INT8_REAL_IF: return 1;
+    default: return 0;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int l1rxg_abi_version(void) { return L1RXG_ABI_VERSION; }
+const char* l1rxg_last_error(void) { return g_err.c_str(); }
+
+void l1rxg_default_tracking_cfg(l1rxg_tracking_cfg* c) {
+    std::memset(c, 0, sizeof *c);
+    c->epoch_ms = 1;
+    c->el_spacing_chips = 0.5;
+    c->dll_bandwidth_hz = 2.0;
+    c->dll_damping = 0.707;
+    c->pll_bandwidth_hz = 25.0;
+    c->pll_damping = 0.707;
+    c->fll_bandwidth_hz = 15.0;
+    c->fll_pull_in_ms = 400;
+    c->fll_coarse_ms = 100;
+    c->cn0_window_ms = 20;
+    c->lock_fail_limit = 50;
+    c->cn0_drop_dbhz = 28.0;
+    c->carrier_lock_drop = 0.6;
+}
+
+void l1rxg_epl_taps(double el_spacing, l1rxg_taps* t) {
+    std::memset(t, 0, sizeof *t);
+    t->n_taps = 3;
+    t->n_counted = 3;
+    t->early = 0;
+    t->prompt = 1;
+    t->late = 2;
+    t->offsets_chips[0] = el_spacing / 2.0;
+    t->offsets_chips[1] = 0.0;
+    t->offsets_chips[2] = -el_spacing / 2.0;
+}
+
+int l1rxg_ca_code(int prn, int8_t* out) {
+    if (prn < 1 || prn > 32)
+        return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
+    gold_code(prn, out);
+    return 0;
+}
+
+void l1rxg_halfband_taps(double* out) { halfband(out); }
+
+int l1rxg_create(int device, l1rxg_ctx** out) {
+    if (!out)
+        return set_err(L1RXG_EINVAL, "null out");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(L1RXG_EINVAL, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    if (upload_constants())
+        return set_err(L1RXG_ECUDA, "constant upload failed");
+    auto* c = new l1rxg_ctx();
+    c->device = device;
+    std::vector<int8_t> codes(33 * 1023, 0);
+    for (int p = 1; p <= 32; ++p)
+        gold_code(p, codes.data() + p * 1023);
+    cudaError_t e = cudaMalloc(&c->d_codes, codes.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(c->d_codes, codes.data(), codes.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return set_err(L1RXG_ECUDA, std::string("context init: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return 0;
+}
+
+int l1rxg_destroy(l1rxg_ctx* c) {
+    if (!c)
+        return 0;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (DevBuf* b : {&c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr})
+        b->release();
+    cudaFree(c->d_codes);
+    cudaStreamDestroy(c->compute);
+    cudaStreamDestroy(c->copy);
+    delete c;
+    return 0;
+}
+
+int l1rxg_host_alloc(l1rxg_ctx* c, int64_t bytes, void** out) {
+    if (!c || !out || bytes <= 0)
+        return set_err(L1RXG_EINVAL, "bad host_alloc arguments");
+    CK(cudaSetDevice(c->device));
+    CK(cudaHostAlloc(out, static_cast<size_t>(bytes), cudaHostAllocPortable));
+    return 0;
+}
+
+int l1rxg_host_free(l1rxg_ctx* c, void* p) {
+    (void)c;
+    CK(cudaFreeHost(p));
+    return 0;
+}
+
+int l1rxg_correlate_batch(l1rxg_ctx* c, const double* iq, int n, int n_jobs,
+                          l1rxg_nco* states, const int32_t* prns, const l1rxg_taps* taps,
+                          double fs, double* tap_sums, l1rxg_corr* corr_out) {
+    if (!c)
+        return set_err(L1RXG_EINVAL, "null context");
+    if (n <= 0)
+        return set_err(L1RXG_EINVAL, "empty epoch view");  // tracking.hpp:232-233
+    if (n_jobs <= 0)
+        return 0;
+    if (int rc = validate_taps(taps))
+        return rc;
+    if (!(fs > 0))
+        return set_err(L1RXG_EINVAL, "sample_rate_hz must be positive");
+    for (int j = 0; j < n_jobs; ++j) {
+        if (prns[j] < 1 || prns[j] > 32)
+            return set_err(L1RXG_ERANGE, "PRN must be in 1..32");  // cacode.hpp:38-39
+        const l1rxg_nco& st = states[j];
+        if (!(st.code_freq_hz > 0) || !(st.code_phase_chips >= 0.0) ||
+            !(st.code_phase_chips + 1023.0 + n * (st.code_freq_hz / fs) + 1.0 < 2147483000.0))
+            return set_err(L1RXG_EINVAL, "code NCO state out of the correlator's domain "
+                                         "(code_phase >= 0, code_freq > 0)");
+    }
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    const int T = pick_T(taps->n_taps);
+    const size_t ns = static_cast<size_t>(n) * n_jobs;
+    if (c->iq64.ensure(ns * 16) || c->iq32.ensure(ns * 8) ||
+        c->states.ensure(sizeof(l1rxg_nco) * n_jobs) || c->prns.ensure(4 * (size_t)n_jobs) ||
+        c->sums.ensure(sizeof(double) * 2 * T * (size_t)n_jobs) ||
+        c->corr.ensure(sizeof(l1rxg_corr) * n_jobs))
+        return L1RXG_ENOMEM;
+    cudaStream_t s = c->compute;
+    CK(cudaMemcpyAsync(c->iq64.p, iq, ns * 16, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->states.p, states, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->prns.p, prns, 4 * (size_t)n_jobs, cudaMemcpyHostToDevice, s));
+    cf64_to_f32_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(
+        static_cast<const double2*>(c->iq64.p), static_cast<float2*>(c->iq32.p), (int64_t)ns);
+    CK(cudaGetLastError());
+    JobArgs a{};
+    a.samples = static_cast<const float2*>(c->iq32.p);
+    a.states = static_cast<l1rxg_nco*>(c->states.p);
+    a.prns = static_cast<const int32_t*>(c->prns.p);
+    a.codes = c->d_codes;
+    a.tap_sums = static_cast<double*>(c->sums.p);
+    a.corr = static_cast<l1rxg_corr*>(c->corr.p);
+    a.n = n;
+    a.kp = taps->prompt;
+    a.ke = taps->early;
+    a.kl = taps->late;
+    a.kernel = L1RXG_KERNEL_SCALAR;
+    a.fs = fs;
+    a.taps = padded_taps(*taps, T);
+    const int nt = pick_threads(n, nullptr);
+    int rc = 0;
+    auto go = [&]() -> int { DISPATCH_T(T, launch_jobs, a, n_jobs, nt, s); };
+    rc = go();
+    if (rc)
+        return rc;
+    c->launches += 2;
+    CK(cudaMemcpyAsync(states, c->states.p, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyDeviceToHost, s));
+    std::vector<double> sums(static_cast<size_t>(2 * T) * n_jobs);
+    CK(cudaMemcpyAsync(sums.data(), c->sums.p, sums.size() * 8, cudaMemcpyDeviceToHost, s));
+    if (corr_out)
+        CK(cudaMemcpyAsync(corr_out, c->corr.p, sizeof(l1rxg_corr) * n_jobs, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (tap_sums)
+        for (int j = 0; j < n_jobs; ++j)
+            std::memcpy(tap_sums + (size_t)j * 2 * taps->n_taps, sums.data() + (size_t)j * 2 * T,
+                        sizeof(double) * 2 * taps->n_taps);
+    return 0;
+}
+
+int l1rxg_correlate_epoch(l1rxg_ctx* c, int kernel, const double* iq, int n,
+                          l1rxg_nco* st, int prn, double el_spacing, double fs,
+                          l1rxg_corr* out) {
+    if (n <= 0)
+        return set_err(L1RXG_EINVAL, "empty epoch view");  // tracking.hpp:232-233
+    if (kernel == L1RXG_KERNEL_NOOP) {  // tracking.hpp:434-452: state only
+        const double w = 2.0 * PI_D * st->carrier_doppler_hz / fs;
+        st->carrier_phase_rad = std::fmod(std::fma(w, (double)n, st->carrier_phase_rad), 2.0 * PI_D);
+        const double adv = static_cast<double>(n) * st->code_freq_hz / fs;
+        st->code_phase_chips = std::fmod(st->code_phase_chips + adv, 1023.0);
+        st->chi_chips += adv;
+        std::memset(out, 0, sizeof *out);
+        out->n_samples = n;
+        return 0;
+    }
+    l1rxg_taps t;
+    l1rxg_epl_taps(el_spacing, &t);
+    int32_t p = prn;
+    return l1rxg_correlate_batch(c, iq, n, 1, st, &p, &t, fs, nullptr, out);
+}
+
+// ---- tracker -----------------------------------------------------------
+
+int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_channel* chans,
+                         const int32_t* chan_stream, l1rxg_tracker** out) {
+    if (!c || !d || !out || (!chans && d->n_channels > 0))
+        return set_err(L1RXG_EINVAL, "null argument");
+    if (bytes_per_sample(d->format) == 0)
+        return set_err(L1RXG_EINVAL, "tracker format must be int8_iq, int16_iq or int8_real_if");
+    if (!(d->sample_rate_hz >= 2.046e6))  // samples.hpp:61-76
+        return set_err(L1RXG_EINVAL, "sample_rate_hz must be >= 2.046 MHz to cover the C/A main lobe");
+    const bool is_if = d->format == L1RXG_FMT_INT8_REAL_IF;
+    if (is_if && d->if_frequency_hz <= 0.0)
+        return set_err(L1RXG_EINVAL, "if_frequency_hz required for Int8RealIF format");
+    if (!is_if && d->if_frequency_hz != 0.0)
+        return set_err(L1RXG_EINVAL, "if_frequency_hz must be 0 for complex-baseband formats");
+    if (d->if_frequency_hz >= d->sample_rate_hz / 2.0)
+        return set_err(L1RXG_EINVAL, "if_frequency_hz must be < fs/2");
+    if (int rc = validate_taps(&d->taps))
+        return rc;
+    if (int rc = validate_cfg(&d->cfg))
+        return rc;
+    if (d->n_streams < 1 || d->n_channels < 0 || d->max_records < 1)
+        return set_err(L1RXG_EINVAL, "n_streams >= 1, n_channels >= 0, max_records >= 1");
+    const int n = static_cast<int>(std::llround(d->sample_rate_hz / 1000.0));
+    if (d->ring_samples < 2 * (int64_t)n)
+        return set_err(L1RXG_EINVAL, "ring_samples must hold at least two epochs");
+    for (int k = 0; k < d->n_channels; ++k) {
+        if (chan_stream[k] < 0 || chan_stream[k] >= d->n_streams)
+            return set_err(L1RXG_EINVAL, "channel bound to a missing stream");
+        if (chans[k].prn < 1 || chans[k].prn > 32)
+            return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
+        if (!(chans[k].code_phase_chips >= 0.0) || !(chans[k].code_freq_hz > 0))
+            return set_err(L1RXG_EINVAL, "channel code NCO out of domain");
+        if (chans[k].win_len < 0 || chans[k].win_len >= d->cfg.cn0_window_ms)
+            return set_err(L1RXG_EINVAL, "channel C/N0 window length out of range");
+    }
+    CK(cudaSetDevice(c->device));
+    auto* t = new l1rxg_tracker();
+    t->ctx = c;
+    t->d = *d;
+    t->T = pick_T(d->taps.n_taps);
+    t->nt = pick_threads(n, nullptr);
+    t->R = d->ring_samples;
+    t->apron = n + 64;
+    t->streams.resize(static_cast<size_t>(d->n_streams));
+    auto fail = [&](cudaError_t e) {
+        l1rxg_tracker_destroy(t);
+        return set_err(e == cudaErrorMemoryAllocation ? L1RXG_ENOMEM : L1RXG_ECUDA,
+                       std::string("tracker alloc: ") + cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    const int64_t stride = t->R + t->apron;
+    if ((e = cudaMalloc(&t->d_ring, sizeof(float2) * static_cast<size_t>(stride) * t->streams.size())) !=
+        cudaSuccess)
+        return fail(e);
+    for (size_t k = 0; k < t->streams.size(); ++k)
+        t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride;
+    for (auto& r : t->streams) {
+        for (int k = 0; k < 2; ++k) {
+            if ((e = cudaMalloc(&r.hist8[k], 32)) != cudaSuccess ||
+                (e = cudaMalloc(&r.histf[k], 32 * sizeof(float2))) != cudaSuccess)
+                return fail(e);
+            cudaMemset(r.hist8[k], 0, 32);
+            cudaMemset(r.histf[k], 0, 32 * sizeof(float2));
+        }
+    }
+    const size_t C = static_cast<size_t>(std::max(1, d->n_channels));
+    const size_t nrec = C * static_cast<size_t>(d->max_records);
+    if ((e = cudaMalloc(&t->d_avail, 8 * t->streams.size())) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_chans, sizeof(l1rxg_channel) * C)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_chan_stream, 4 * C)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_recs, sizeof(l1rxg_epoch_record) * nrec)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_tapsums, sizeof(double) * 2 * t->T * nrec)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_ecount, 8 * C)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_status, 4 * C)) != cudaSuccess)
+        return fail(e);
+    cudaMemset(t->d_avail, 0, 8 * t->streams.size());
+    cudaMemset(t->d_ecount, 0, 8 * C);
+    cudaMemset(t->d_status, 0, 4 * C);
+    if (d->n_channels > 0) {
+        cudaMemcpy(t->d_chans, chans, sizeof(l1rxg_channel) * d->n_channels, cudaMemcpyHostToDevice);
+        cudaMemcpy(t->d_chan_stream, chan_stream, 4 * (size_t)d->n_channels, cudaMemcpyHostToDevice);
+    }
+    for (int k = 0; k < 2; ++k) {
+        cudaEventCreateWithFlags(&t->ev_copy[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&t->ev_used[k], cudaEventDisableTiming);
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess)
+        return fail(e);
+    *out = t;
+    return 0;
+}
+
+int l1rxg_tracker_destroy(l1rxg_tracker* t) {
+    if (!t)
+        return 0;
+    cudaSetDevice(t->ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(t->d_ring);
+    for (auto& r : t->streams) {
+        for (int k = 0; k < 2; ++k) {
+            cudaFree(r.hist8[k]);
+            cudaFree(r.histf[k]);
+        }
+    }
+    cudaFree(t->d_avail);
+    cudaFree(t->d_chans);
+    cudaFree(t->d_chan_stream);
+    cudaFree(t->d_recs);
+    cudaFree(t->d_tapsums);
+    cudaFree(t->d_ecount);
+    cudaFree(t->d_status);
+    for (int k = 0; k < 2; ++k) {
+        t->staging[k].release();
+        if (t->ev_copy[k]) cudaEventDestroy(t->ev_copy[k]);
+        if (t->ev_used[k]) cudaEventDestroy(t->ev_used[k]);
+    }
+    t->mixed.release();
+    for (auto& x : t->timed) {
+        cudaEventDestroy(x.a);
+        cudaEventDestroy(x.b);
+    }
+    for (auto e : t->ev_pool)
+        cudaEventDestroy(e);
+    delete t;
+    return 0;
+}
+
+int l1rxg_tracker_push_device(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nbytes) {
+    if (!t || s < 0 || s >= (int)t->streams.size())
+        return set_err(L1RXG_EINVAL, "bad stream");
+    const int bps = bytes_per_sample(t->d.format);
+    if (nbytes <= 0)
+        return 0;
+    if (nbytes % bps)
+        return set_err(L1RXG_EINVAL, "byte count is not a whole number of samples");
+    const int64_t nsamp = nbytes / bps;
+    if (nsamp > t->R - t->nt)
+        return set_err(L1RXG_EINVAL, "push larger than the device ring");
+    CK(cudaSetDevice(t->ctx->device));
+    return ingest_launch(t, s, dev_bytes, nsamp, t->ctx->compute);
+}
+
+int l1rxg_tracker_push(l1rxg_tracker* t, int s, const void* bytes, int64_t nbytes) {
+    if (!t || s < 0 || s >= (int)t->streams.size())
+        return set_err(L1RXG_EINVAL, "bad stream");
+    const int bps = bytes_per_sample(t->d.format);
+    if (nbytes <= 0)
+        return 0;
+    if (nbytes % bps)
+        return set_err(L1RXG_EINVAL, "byte count is not a whole number of samples");
+    if (nbytes / bps > t->R - t->nt)
+        return set_err(L1RXG_EINVAL, "push larger than the device ring");
+    CK(cudaSetDevice(t->ctx->device));
+    // double-buffered staging: copy k+1 overlaps ingest/track of k
+    const int k = t->stage_cur;
+    t->stage_cur ^= 1;
+    if (t->staging[k].ensure(static_cast<size_t>(nbytes)))
+        return L1RXG_ENOMEM;
+    CK(cudaStreamWaitEvent(t->ctx->copy, t->ev_used[k], 0));
+    CK(cudaMemcpyAsync(t->staging[k].p, bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice,
+                       t->ctx->copy));
+    CK(cudaEventRecord(t->ev_copy[k], t->ctx->copy));
+    CK(cudaStreamWaitEvent(t->ctx->compute, t->ev_copy[k], 0));
+    if (int rc = ingest_launch(t, s, t->staging[k].p, nbytes / bps, t->ctx->compute))
+        return rc;
+    CK(cudaEventRecord(t->ev_used[k], t->ctx->compute));
+    return 0;
+}
+
+int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
+    if (!t)
+        return set_err(L1RXG_EINVAL, "null tracker");
+    if (t->d.n_channels == 0)
+        return 0;
+    CK(cudaSetDevice(t->ctx->device));
+    TrackArgs a{};
+    a.ring = t->d_ring;
+    a.ring_stride = t->R + t->apron;
+    a.ring_cap = t->R;
+    a.avail = t->d_avail;
+    a.chans = t->d_chans;
+    a.chan_stream = t->d_chan_stream;
+    a.recs = t->d_recs;
+    a.tap_sums = t->d_tapsums;
+    a.ecount = t->d_ecount;
+    a.status = t->d_status;
+    a.codes = t->ctx->d_codes;
+    a.max_records = t->d.max_records;
+    a.max_epochs = max_epochs < 0 ? 0x7fffffff : max_epochs;
+    a.n = static_cast<int>(std::llround(t->d.sample_rate_hz / 1000.0));
+    a.kp = t->d.taps.prompt;
+    a.ke = t->d.taps.early;
+    a.kl = t->d.taps.late;
+    a.taps = padded_taps(t->d.taps, t->T);
+    a.lc.cfg = t->d.cfg;
+    a.lc.kernel = t->d.kernel;
+    a.lc.fs = t->d.sample_rate_hz;
+    cudaStream_t st = t->ctx->compute;
+    cudaEvent_t e0 = get_event(t), e1 = get_event(t);
+    cudaEventRecord(e0, st);
+    auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st); };
+    if (int rc = go())
+        return rc;
+    t->launches += 1;
+    cudaEventRecord(e1, st);
+    t->timed.push_back({e0, e1, 1});
+    return 0;
+}
+
+int l1rxg_tracker_sync(l1rxg_tracker* t) {
+    if (!t)
+        return set_err(L1RXG_EINVAL, "null tracker");
+    CK(cudaSetDevice(t->ctx->device));
+    CK(cudaStreamSynchronize(t->ctx->copy));
+    CK(cudaStreamSynchronize(t->ctx->compute));
+    std::vector<int32_t> status(static_cast<size_t>(std::max(1, t->d.n_channels)));
+    if (t->d.n_channels > 0) {
+        CK(cudaMemcpy(status.data(), t->d_status, 4 * status.size(), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < t->d.n_channels; ++k)
+            if (status[static_cast<size_t>(k)])
+                return set_err(L1RXG_EINVAL, "ring overrun: a channel's window was overwritten "
+                                             "before it was tracked (ring_samples too small)");
+    }
+    return 0;
+}
+
+int l1rxg_tracker_channels(l1rxg_tracker* t, l1rxg_channel* out) {
+    if (int rc = l1rxg_tracker_sync(t))
+        return rc;
+    if (t->d.n_channels > 0)
+        CK(cudaMemcpy(out, t->d_chans, sizeof(l1rxg_channel) * t->d.n_channels, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int l1rxg_tracker_epoch_counts(l1rxg_tracker* t, int64_t* out) {
+    if (int rc = l1rxg_tracker_sync(t))
+        return rc;
+    if (t->d.n_channels > 0)
+        CK(cudaMemcpy(out, t->d_ecount, 8 * (size_t)t->d.n_channels, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int l1rxg_tracker_records(l1rxg_tracker* t, int ch, int64_t e0, int64_t count,
+                          l1rxg_epoch_record* out, double* tap_sums_out) {
+    if (!t || ch < 0 || ch >= t->d.n_channels)
+        return set_err(L1RXG_EINVAL, "bad channel");
+    if (int rc = l1rxg_tracker_sync(t))
+        return rc;
+    int64_t done = 0;
+    CK(cudaMemcpy(&done, t->d_ecount + ch, 8, cudaMemcpyDeviceToHost));
+    const int64_t M = t->d.max_records;
+    if (e0 < 0 || count < 0 || e0 + count > done || e0 < done - M)
+        return set_err(L1RXG_EINVAL, "records not available (outside the record ring)");
+    const int K = t->d.taps.n_taps, T = t->T;
+    std::vector<double> sums;
+    for (int64_t e = e0; e < e0 + count;) {
+        const int64_t slot = e % M;
+        const int64_t run = std::min<int64_t>(count - (e - e0), M - slot);
+        const size_t base = static_cast<size_t>(ch) * M + slot;
+        if (out)
+            CK(cudaMemcpy(out + (e - e0), t->d_recs + base, sizeof(l1rxg_epoch_record) * run,
+                          cudaMemcpyDeviceToHost));
+        if (tap_sums_out) {
+            sums.resize(static_cast<size_t>(run) * 2 * T);
+            CK(cudaMemcpy(sums.data(), t->d_tapsums + base * 2 * T, sums.size() * 8,
+                          cudaMemcpyDeviceToHost));
+            for (int64_t q = 0; q < run; ++q)
+                std::memcpy(tap_sums_out + (e - e0 + q) * 2 * K, sums.data() + q * 2 * T,
+                            sizeof(double) * 2 * K);
+        }
+        e += run;
+    }
+    return 0;
+}
+
+int l1rxg_tracker_records_raw(l1rxg_tracker* t, void* dst, int dst_is_device, int64_t* bytes_out) {
+    if (!t)
+        return set_err(L1RXG_EINVAL, "null tracker");
+    const size_t bytes = sizeof(l1rxg_epoch_record) * static_cast<size_t>(std::max(1, t->d.n_channels)) *
+                         static_cast<size_t>(t->d.max_records);
+    if (bytes_out)
+        *bytes_out = static_cast<int64_t>(bytes);
+    if (!dst)
+        return 0;
+    CK(cudaSetDevice(t->ctx->device));
+    CK(cudaMemcpyAsync(dst, t->d_recs, bytes,
+                       dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       t->ctx->compute));
+    CK(cudaStreamSynchronize(t->ctx->compute));
+    return 0;
+}
+
+int l1rxg_tracker_read_samples(l1rxg_tracker* t, int s, int64_t s0, int64_t count, double* iq_out) {
+    if (!t || s < 0 || s >= (int)t->streams.size())
+        return set_err(L1RXG_EINVAL, "bad stream");
+    if (int rc = l1rxg_tracker_sync(t))
+        return rc;
+    const StreamRing& r = t->streams[static_cast<size_t>(s)];
+    if (s0 < 0 || count < 0 || s0 + count > r.pushed || s0 < r.pushed - t->R)
+        return set_err(L1RXG_EINVAL, "samples not in the ring");
+    std::vector<float2> tmp(static_cast<size_t>(count));
+    for (int64_t k = 0; k < count;) {
+        const int64_t pos = (s0 + k) % t->R;
+        const int64_t run = std::min(count - k, t->R - pos);
+        CK(cudaMemcpy(tmp.data() + k, r.ring + pos, sizeof(float2) * run, cudaMemcpyDeviceToHost));
+        k += run;
+    }
+    for (int64_t k = 0; k < count; ++k) {
+        iq_out[2 * k] = tmp[static_cast<size_t>(k)].x;
+        iq_out[2 * k + 1] = tmp[static_cast<size_t>(k)].y;
+    }
+    return 0;
+}
+
+int l1rxg_tracker_timing(l1rxg_tracker* t, double* ingest_ms, double* track_ms, int64_t* launches) {
+    if (!t)
+        return set_err(L1RXG_EINVAL, "null tracker");
+    CK(cudaSetDevice(t->ctx->device));
+    double ing = 0, trk = 0;
+    for (auto& x : t->timed) {
+        CK(cudaEventSynchronize(x.b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, x.a, x.b));
+        (x.kind == 0 ? ing : trk) += ms;
+        t->ev_pool.push_back(x.a);
+        t->ev_pool.push_back(x.b);
+    }
+    t->timed.clear();
+    if (ingest_ms) *ingest_ms = ing;
+    if (track_ms) *track_ms = trk;
+    if (launches) *launches = t->launches;
+    t->launches = 0;
+    return 0;
+}
+
+int l1rxg_search_grid(l1rxg_ctx*, int, const void*, int, int64_t, double, double, int,
+                      const int32_t*, int, const double*, int, int, int, double*) {
+    return set_err(L1RXG_EINVAL, "search grid: not built in this version");
+}
+
+}  // extern "C"

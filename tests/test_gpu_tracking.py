@@ -1,0 +1,230 @@
+"""Closed-loop tracking on the GPU (K1 ingest + K2 correlator + K3 loop
+update on device) against the oracle, through the C ABI.
+
+The binding parity check is per-epoch replay: every GPU
+epoch is re-run by the oracle from the GPU's own pre-epoch state.  Whole-run
+behaviour is checked with the reference's own closed-loop criteria
+(test_tracking.cpp:403-479)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1907_00463_b200 import abi, simsource as ss
+from paper_1907_00463_b200.tracking import Tracker, init_channel_from_acquisition
+
+from helpers import replay_check
+
+pytestmark = pytest.mark.gpu
+
+IF_FS, IF_HZ = 16.368e6, 4.092e6
+
+
+def _raw(n_ms, fs, svs, fmt, if_hz=0.0, seed=1):
+    return ss.synth(n_ms, fs, svs, fmt=fmt, if_hz=if_hz, seed=seed, device="cuda").cpu().numpy()
+
+
+def _init(sv, fs, dop_err=0.0, samp_err=0):
+    b, d = ss.truth_channel_start(sv, fs)
+    return init_channel_from_acquisition(sv.prn, d - dop_err, 0, b + samp_err, 0, fs)
+
+
+def test_ingest_real_if_matches_sample_source(ctx, oracle_mod):
+    """K1 vs SampleSource's mixer + half-band FIR (samples.hpp:215-253),
+    pushed in uneven chunks so the carried FIR history is exercised."""
+    rng = np.random.default_rng(3)
+    raw = rng.integers(-128, 128, 200_003).astype(np.int8)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, IF_FS, IF_HZ, [], ring_samples=1 << 20)
+    pos = 0
+    for step in (17, 16368, 5, 100_000, 83_613):
+        trk.push(0, raw[pos:pos + step])
+        pos += step
+    got = trk.read_samples(0, 0, raw.size)
+    want = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, IF_FS, IF_HZ)
+    if oracle_mod.ref_available():
+        ref = oracle_mod.ref_ingest(raw, abi.FMT_INT8_REAL_IF, IF_FS, IF_HZ)
+        assert np.abs(ref - want).max() < 1e-12
+    assert np.abs(got - want).max() < 2e-6
+
+
+def test_ingest_generic_if_and_complex_formats(ctx, oracle_mod):
+    rng = np.random.default_rng(4)
+    # non-fs/4 IF (GN3S rates of test_samples.cpp:174-227): generic mixer path
+    fs, ifz = 16.3676e6, 4.1304e6
+    raw = rng.integers(-128, 128, 50_000).astype(np.int8)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, ifz, [], ring_samples=1 << 18)
+    trk.push(0, raw[:20_000])
+    trk.push(0, raw[20_000:])
+    got = trk.read_samples(0, 0, raw.size)
+    want = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, ifz)
+    assert np.abs(got - want).max() < 2e-6
+    # int8 / int16 IQ decode is exact (samples.hpp:188-205)
+    for fmt, dt in ((abi.FMT_INT8_IQ, np.int8), (abi.FMT_INT16_IQ, np.int16)):
+        info = np.iinfo(dt)
+        raw = rng.integers(info.min, info.max + 1, 2 * 30_001).astype(dt)
+        trk = Tracker(ctx, fmt, 5e6, 0.0, [], ring_samples=1 << 17)
+        trk.push(0, raw)
+        got = trk.read_samples(0, 0, 30_001)
+        want = oracle_mod.ingest(raw.view(np.uint8), fmt, 5e6)
+        assert np.array_equal(got, want)
+
+
+def test_config1_shape_replay_parity(ctx, oracle_mod):
+    """Config 1 shape: PRN 1, int8 real IF at 16.368 MHz / 4.092 MHz IF,
+    +1.2 kHz, 45 dB-Hz, E/P/L 0.5 chip, PLL+DLL closed, 1000 blocks."""
+    fs, n = IF_FS, 16368
+    sv = ss.Sv(prn=1, cn0_dbhz=45.0, doppler_hz=1200.0, delay_chips=511.3)
+    raw = _raw(1000, fs, [sv], "int8_real_if", IF_HZ, seed=1)
+    init = _init(sv, fs, dop_err=120.0, samp_err=-1)
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, [init], ring_samples=1100 * n,
+                  max_records=1000, cfg=cfg, taps=taps)
+    trk.push(0, raw)
+    trk.run()
+    recs, tsums = trk.records(0, tap_sums=True)
+    assert len(recs) >= 998
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, IF_HZ)
+    worst = replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=tsums)
+    print("replay worst", worst)
+    # reference closed-loop criteria (test_tracking.cpp:403-417)
+    last = recs[-1]
+    assert last["state"] == abi.TRACKING
+    assert last["carrier_lock_ratio"] > 0.9
+    assert abs(last["carrier_doppler_hz"] - 1200.0) < 5.0
+    assert last["cn0_dbhz"] == pytest.approx(45.0, abs=3.0)
+
+
+def test_trajectory_agrees_with_reference_until_first_tie(ctx, oracle_mod):
+    """Whole-run agreement with the reference's own closed loop
+    (oracle/_ref: SampleSource + track_epoch) on the same bytes; reported up
+    to the first chip-decision tie."""
+    if not oracle_mod.ref_available():
+        pytest.skip("reference library not built")
+    fs, n = IF_FS, 16368
+    sv = ss.Sv(prn=3, cn0_dbhz=47.0, doppler_hz=-2100.0, delay_chips=100.7)
+    raw = _raw(400, fs, [sv], "int8_real_if", IF_HZ, seed=5)
+    init = _init(sv, fs)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, [init], ring_samples=500 * n,
+                  max_records=400)
+    trk.push(0, raw)
+    trk.run()
+    g = trk.records(0)
+    x = oracle_mod.ref_ingest(raw, abi.FMT_INT8_REAL_IF, fs, IF_HZ)
+    _, r = oracle_mod.ref_track_buffer(init, x, n, abi.TrackingCfg.default(), fs, kernel=0)
+    m = min(len(g), len(r))
+    assert m >= 398
+    d = np.abs(g["carrier_doppler_hz"][:m] - r["carrier_doppler_hz"][:m])
+    chi = np.abs(g["chi_chips"][:m] - r["chi_chips"][:m])
+    print("max |dDoppler| %.3g Hz, max |dchi| %.3g chips over %d epochs" % (d.max(), chi.max(), m))
+    assert d.max() < 0.05 and chi.max() < 1e-3
+
+
+def test_twelve_channel_shared_stream(ctx, oracle_mod):
+    """Config 2 shape (scaled to 300 blocks): 12 channels, PRNs 1-12, one
+    shared int8 real-IF stream, replay parity for every channel."""
+    fs, n = IF_FS, 16368
+    rng = np.random.default_rng(2)
+    svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(35, 50), doppler_hz=rng.uniform(-5000, 5000),
+                 delay_chips=rng.uniform(0, 1023)) for p in range(1, 13)]
+    raw = _raw(300, fs, svs, "int8_real_if", IF_HZ, seed=2)
+    inits = [_init(sv, fs) for sv in svs]
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, inits, ring_samples=400 * n,
+                  max_records=300)
+    for c0 in range(0, raw.size, 37 * n):  # chunked pushes + runs
+        trk.push(0, raw[c0:c0 + 37 * n])
+        trk.run()
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, IF_HZ)
+    counts = trk.epoch_counts()
+    for c in range(12):
+        recs = trk.records(c)
+        assert len(recs) == counts[c] >= 297
+        replay_check(oracle_mod, inits[c], recs, x, n, cfg, taps, fs)
+
+
+@pytest.mark.parametrize("shape", ["monitor", "wideband"])
+def test_multitap_replay_parity(ctx, oracle_mod, shape):
+    """Configs 3 and 4 shapes (scaled): 11 taps at 0.1 chip (+2 loop taps)
+    on complex int16 at 16.368 MHz; 7 taps at 0.25 chip at 65.472 MHz."""
+    if shape == "monitor":
+        fs = 16.368e6
+        taps = abi.Taps.make([round(-0.5 + 0.1 * k, 10) for k in range(11)] + [0.25, -0.25],
+                             early=11, prompt=5, late=12, n_counted=11)
+        svs = [ss.Sv(prn=5, cn0_dbhz=46.0, doppler_hz=800.0, delay_chips=300.0),
+               ss.Sv(prn=5, cn0_dbhz=49.0, doppler_hz=800.0, delay_chips=300.4)]
+        ms = 120
+    else:
+        fs = 65.472e6
+        taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+        svs = [ss.Sv(prn=9, cn0_dbhz=44.0, doppler_hz=-3300.0, delay_chips=12.5)]
+        ms = 60
+    n = int(round(fs / 1000))
+    raw = _raw(ms, fs, svs, "int16_iq", seed=11)
+    init = _init(svs[0], fs)
+    cfg = abi.TrackingCfg.default()
+    trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, [init], ring_samples=(ms + 8) * n,
+                  max_records=ms, taps=taps, cfg=cfg)
+    trk.push(0, raw.view(np.int16))
+    trk.run()
+    recs, tsums = trk.records(0, tap_sums=True)
+    x = oracle_mod.ingest(raw, abi.FMT_INT16_IQ, fs)
+    replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=tsums)
+
+
+def test_silence_drops_to_idle(ctx):
+    """test_tracking.cpp:431-447: zero input -> Idle after lock_fail_limit+1."""
+    fs = 2.048e6
+    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, fs)
+    trk = Tracker(ctx, abi.FMT_INT8_IQ, fs, 0.0, [init], ring_samples=100 * 2048)
+    trk.push(0, np.zeros(2 * 2048 * 80, np.int8))
+    trk.run()
+    ch = trk.channels()[0]
+    assert ch.state == abi.IDLE
+    assert trk.epoch_counts()[0] == abi.TrackingCfg.default().lock_fail_limit + 1
+
+
+def test_code_advance_and_sample_accounting(ctx):
+    """test_tracking.cpp:449-465."""
+    fs = 2.048e6
+    sv = ss.Sv(prn=7, cn0_dbhz=48.0, doppler_hz=-2200.0, delay_chips=100.25)
+    raw = _raw(200, fs, [sv], "int8_iq", seed=79)
+    init = _init(sv, fs, dop_err=100.0)
+    trk = Tracker(ctx, abi.FMT_INT8_IQ, fs, 0.0, [init], ring_samples=300 * 2048, max_records=256)
+    trk.push(0, raw.view(np.int8))
+    trk.run()
+    h = trk.records(0)
+    assert len(h) >= 150
+    for k in range(1, len(h)):
+        assert abs((h[k]["chi_chips"] - h[k - 1]["chi_chips"]) - h[k - 1]["code_freq_hz"] / 1000.0) < 1e-9
+    ch = trk.channels()[0]
+    assert ch.sample_offset_next_epoch == h[0]["sample_offset_end"] + 2048 * (len(h) - 1)
+
+
+def test_deterministic(ctx):
+    """test_tracking.cpp:467-479: bitwise-identical reruns."""
+    fs = 2.048e6
+    sv = ss.Sv(prn=7, cn0_dbhz=45.0, doppler_hz=500.0, delay_chips=100.25)
+    raw = _raw(300, fs, [sv], "int8_iq", seed=80)
+    outs = []
+    for _ in range(2):
+        trk = Tracker(ctx, abi.FMT_INT8_IQ, fs, 0.0, [_init(sv, fs, dop_err=200.0)],
+                      ring_samples=400 * 2048, max_records=300)
+        trk.push(0, raw.view(np.int8))
+        trk.run()
+        outs.append(trk.records(0))
+    assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_noop_kernel_closed_loop(ctx):
+    """test_tracking.cpp:481-493."""
+    fs = 2.048e6
+    init = init_channel_from_acquisition(7, 1000.0, 0, 0, 0, fs)
+    cf = init.code_freq_hz
+    trk = Tracker(ctx, abi.FMT_INT8_IQ, fs, 0.0, [init], ring_samples=8 * 2048,
+                  kernel=abi.KERNEL_NOOP)
+    trk.push(0, np.tile(np.array([64, -32], np.int8), 2048))
+    trk.run(max_epochs=1)
+    r = trk.records(0)[0]
+    assert r["ip"] == 0.0
+    assert r["chi_chips"] == pytest.approx(cf / 1000.0, abs=1e-9)
+    assert trk.channels()[0].sample_offset_next_epoch == 2048
