@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""bench.py -- tracking-correlator throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gpu|reference]
+                    [--config 2|1|3|4]
+
+Metric (BASELINE.json): correlator throughput in G sample-taps/s (one input
+sample x one code tap, I and Q), and the real-time channel count per B200
+(channel-epochs/s / 1000, the analogue of capacity = 1e6/avg_ns,
+bench.hpp:26-30).
+
+Workload at N=1 (BASELINE.json configs[1], "config 2"): 12 channels, PRNs
+1-12, one shared int8 real-IF stream at 16.368 MHz with a 4.092 MHz IF,
+Doppler U(+-5 kHz), code phase U[0,1023), C/N0 U[35,50] dB-Hz + AWGN,
+E/P/L at 0.5 chip, 10000 1-ms blocks, PLL/DLL/FLL closed on device.
+A step = ingest (mixer + half-band FIR) of the whole recording + closed-loop
+tracking of every channel over every block.  Synthetic seeded data
+(paper_1907_00463_b200/simsource.py); loops start from truth
+(test_tracking.cpp:378-384) with lock_fail_limit = INT_MAX so every channel
+computes every epoch.
+
+value: device time (CUDA events on the library's stream) with the raw bytes
+already resident in HBM.  e2e: the same step through the public API from
+pinned host memory -- chunked H2D + ingest + tracking, then the epoch
+records read back to the host -- all inside the timed region.
+Multi-GPU: one process per GPU, each rank tracks its own seeded recording
+(weak scaling, no collective on the data path); max over ranks; the epoch
+records are gathered to rank 0 over NCCL after the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "correlator throughput (G sample-taps/s) and real-time channel count per B200"
+UNIT = "G sample-taps/s"
+
+CONFIGS = {
+    # name: (fmt, fs, if_hz, n_channels, taps kind, blocks, seed)
+    1: dict(fmt="int8_real_if", fs=16.368e6, if_hz=4.092e6, channels=1, taps="epl", blocks=1000, seed=1,
+            desc="config1: PRN 1, int8 real IF 16.368 MHz / 4.092 MHz IF, +1.2 kHz, 45 dB-Hz, E/P/L, 1000 blocks"),
+    2: dict(fmt="int8_real_if", fs=16.368e6, if_hz=4.092e6, channels=12, taps="epl", blocks=10000, seed=2,
+            desc="config2: 12 channels PRN 1-12 on one int8 real-IF stream, 16.368 MHz / 4.092 MHz IF, "
+                 "E/P/L 0.5 chip, 10000 1-ms blocks, closed loop"),
+    3: dict(fmt="int16_iq", fs=16.368e6, if_hz=0.0, channels=32, taps="monitor", blocks=10000, seed=3,
+            desc="config3: 32 channels x 11 taps (0.1 chip over +-0.5) + 2 loop taps, complex int16 at "
+                 "16.368 MHz, 8 authentic + 8 spoofed PRNs, 10000 blocks"),
+    4: dict(fmt="int16_iq", fs=65.472e6, if_hz=0.0, channels=12, taps="wide7", blocks=1000, seed=1000,
+            desc="config4 (one recording per GPU-rank slice): 12 channels x 7 taps (0.25 chip), complex "
+                 "int16 at 65.472 MHz, 1000 blocks"),
+}
+
+
+def make_taps(kind):
+    from paper_1907_00463_b200 import abi
+    if kind == "epl":
+        return abi.Taps.epl(0.5)
+    if kind == "monitor":
+        return abi.Taps.make([round(-0.5 + 0.1 * k, 10) for k in range(11)] + [0.25, -0.25],
+                             early=11, prompt=5, late=12, n_counted=11)
+    return abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+
+
+def scenario(cfg_id, seed):
+    """Satellites and channel hand-offs of a config (seeded)."""
+    from paper_1907_00463_b200 import simsource as ss
+    c = CONFIGS[cfg_id]
+    rng = np.random.default_rng(seed)
+    if cfg_id == 1:
+        svs = [ss.Sv(prn=1, cn0_dbhz=45.0, doppler_hz=1200.0, delay_chips=rng.uniform(0, 1023))]
+        chans = [(svs[0], 1)]
+    elif cfg_id == 2:
+        svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(35, 50), doppler_hz=rng.uniform(-5000, 5000),
+                     delay_chips=rng.uniform(0, 1023)) for p in range(1, 13)]
+        chans = [(sv, sv.prn) for sv in svs]
+    elif cfg_id == 3:
+        auth = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(38, 48), doppler_hz=rng.uniform(-5000, 5000),
+                      delay_chips=rng.uniform(0, 1000)) for p in (1, 3, 6, 9, 12, 17, 22, 28)]
+        spoof = [ss.Sv(prn=a.prn, cn0_dbhz=a.cn0_dbhz + 3.0, doppler_hz=a.doppler_hz,
+                       delay_chips=a.delay_chips + rng.uniform(0.2, 0.6)) for a in auth]
+        svs = auth + spoof
+        chans = [(a, a.prn) for a in auth for _ in range(4)]  # 4 monitor channels per PRN
+    else:
+        nvis = int(rng.integers(8, 13))
+        prns = rng.choice(np.arange(1, 33), 12, replace=False)
+        svs = [ss.Sv(prn=int(p), cn0_dbhz=rng.uniform(30, 50), doppler_hz=rng.uniform(-5000, 5000),
+                     delay_chips=rng.uniform(0, 1023)) for p in prns[:nvis]]
+        absent = [ss.Sv(prn=int(p), cn0_dbhz=30.0, doppler_hz=rng.uniform(-5000, 5000),
+                        delay_chips=rng.uniform(0, 1023)) for p in prns[nvis:]]
+        chans = [(sv, sv.prn) for sv in svs + absent]
+    return c, svs, chans
+
+
+def channel_inits(chans, fs, lock_fail_limit_inf=True):
+    from paper_1907_00463_b200 import simsource as ss
+    from paper_1907_00463_b200.tracking import init_channel_from_acquisition
+    out = []
+    for sv, prn in chans:
+        b, d = ss.truth_channel_start(sv, fs)
+        out.append(init_channel_from_acquisition(prn, d, 0, b, 0, fs))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent NVML sampling of SM clock and throttle reasons
+    during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def fp32_peak_tflops(sm_mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flop (FMA) at the SM clock -- the FP32
+    # pipe issue roof (not in MEASURED_PEAKS.json, which has HBM and bf16)
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def ops_per_sample_tap(T, C, real_if):
+    # FP32-pipe instructions per sample-tap (FMA = 1) of the
+    # direct algorithm: I/Q MAC 2 + carrier wipe 4/T + IF FIR F/(C T)
+    return 2.0 + 4.0 / T + (13.0 / (C * T) if real_if else 0.0)
+
+
+def cpu_reference_run(raw_np, c, inits, cfg_struct, blocks, threads):
+    """The reference's own receiver tracking path on host cores
+    (oracle/_ref: SampleSource producer + track_epoch pool, batched kernel)."""
+    import ctypes as C
+    import oracle
+    from paper_1907_00463_b200 import abi
+    n = int(round(c["fs"] / 1000))
+    fmt = {"int8_real_if": abi.FMT_INT8_REAL_IF, "int16_iq": abi.FMT_INT16_IQ,
+           "int8_iq": abi.FMT_INT8_IQ}[c["fmt"]]
+    bps = abi.BYTES_PER_SAMPLE[fmt]
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False, dir="/dev/shm" if os.path.isdir("/dev/shm") else None) as f:
+        f.write(raw_np[: blocks * n * bps].tobytes())
+        path = f.name
+    try:
+        arr = (abi.Channel * len(inits))(*inits)
+        wall, trk = C.c_double(), C.c_double()
+        ce = C.c_int64()
+        rc = oracle.ref().ref_bench_pipeline(path.encode(), fmt, c["fs"], c["if_hz"], len(inits), arr,
+                                             C.byref(cfg_struct), abi.KERNEL_BATCHED, threads,
+                                             blocks, C.byref(wall), C.byref(trk), C.byref(ce), None)
+        if rc:
+            raise RuntimeError(oracle.ref().ref_last_error().decode())
+    finally:
+        os.unlink(path)
+    return wall.value, trk.value, ce.value
+
+
+def cpu_port_run(x_cplx, inits, cfg_struct, taps, fs, blocks, threads):
+    """Builder K-tap restatement (oracle port) for multi-tap configs."""
+    import oracle
+    n = int(round(fs / 1000))
+    t = time.perf_counter()
+    _, done, _, _ = oracle.track_run(inits, [0] * len(inits), [x_cplx], n, cfg_struct, taps, fs,
+                                     blocks, threads=threads, records=False)
+    return time.perf_counter() - t, int(sum(done))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--blocks", type=int, default=0, help="override the config's block count")
+    ap.add_argument("--cpu-blocks", type=int, default=3000, help="CPU baseline sample (blocks)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunk-ms", type=int, default=100)
+    args = ap.parse_args()
+
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c, svs, chans = scenario(args.config, CONFIGS[args.config]["seed"] + rank)
+    blocks = args.blocks or c["blocks"]
+    fs = c["fs"]
+    n = int(round(fs / 1000))
+    from paper_1907_00463_b200 import abi
+    cfg = abi.TrackingCfg.default()
+    cfg.lock_fail_limit = 2**31 - 1
+    taps = make_taps(c["taps"])
+    inits = channel_inits(chans, fs)
+    C_ch, T = len(inits), taps.n_counted
+    sample_taps = float(blocks) * n * T * C_ch
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from paper_1907_00463_b200 import simsource as ss
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        per_step = min(blocks, 1000)
+        raw = ss.synth(per_step, fs, svs, fmt=c["fmt"], if_hz=c["if_hz"], seed=c["seed"],
+                       device=dev).cpu().numpy()
+        threads = os.cpu_count() or 1
+        kind = "reference"
+        walls = []
+        for step in range(args.warmup + args.steps):
+            if c["taps"] == "epl":
+                wall, _, ce = cpu_reference_run(raw, c, inits, cfg, per_step, threads)
+            else:
+                import oracle
+                fmtc = abi.FMT_INT16_IQ
+                x = oracle.ingest(raw, fmtc, fs)
+                t0 = time.perf_counter()
+                wall, ce = cpu_port_run(x, inits, cfg, taps, fs, per_step, threads)
+                wall = time.perf_counter() - t0
+                kind = "port"
+            if step >= args.warmup:
+                walls.append(wall)
+        st_per = float(per_step) * n * T * C_ch
+        v = st_per / statistics.mean(walls) / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": c["desc"], "sample_blocks_per_step": per_step,
+                           "parallelism": f"{threads} host threads"},
+                "realtime_channels": C_ch * per_step / statistics.mean(walls) / 1000.0,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                                 "sample": f"{per_step} blocks x {C_ch} channels of the workload per step"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    # ------------------------------------------------------------ GPU arm
+    from paper_1907_00463_b200 import simsource as ss
+    from paper_1907_00463_b200.tracking import Context, Tracker
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    raw = ss.synth(blocks, fs, svs, fmt=c["fmt"], if_hz=c["if_hz"], seed=c["seed"] + rank,
+                   device=str(dev))
+    torch.cuda.synchronize()
+    fmt = {"int8_real_if": abi.FMT_INT8_REAL_IF, "int16_iq": abi.FMT_INT16_IQ}[c["fmt"]]
+    ctx = Context(local)
+    trk = Tracker(ctx, fmt, fs, c["if_hz"], inits, taps=taps, cfg=cfg,
+                  ring_samples=(blocks + 8) * n, max_records=blocks)
+    stream = torch.cuda.ExternalStream(trk.cuda_stream(), device=dev)
+    nbytes = raw.numel()
+
+    def step_device():
+        trk.reset(inits)
+        trk.push_device(0, raw.data_ptr(), nbytes)
+        trk.run()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step_device()
+    trk.sync()
+    trk.timing()
+    clocks = ClockSampler(local)
+    barrier()
+    with clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    dev_ms = e0.elapsed_time(e1)
+    ingest_ms, track_ms, launches = trk.timing()
+    t_max = dev_ms
+    if dist:
+        tt = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_per_step = t_max / args.steps
+    counts = trk.epoch_counts()
+    assert int(counts.min()) >= blocks - 1, counts
+    sample_taps = float(counts.sum()) * n * T  # every channel-epoch actually tracked
+    value = world * sample_taps / (ms_per_step * 1e-3) / 1e9
+
+    # ---- e2e through the public API from pinned host memory
+    pinned = ctx.host_alloc(nbytes)
+    pinned[:] = raw.cpu().numpy()
+    bps = abi.BYTES_PER_SAMPLE[fmt]
+    chunk = args.e2e_chunk_ms * n * bps
+    rec_host = None
+    rec_bytes = trk.records_raw(dst_ptr=None, device=False).nbytes
+
+    def step_e2e():
+        trk.reset(inits)
+        for o in range(0, nbytes, chunk):
+            trk.push(0, pinned[o:o + chunk])
+            trk.run()
+        return trk.records_raw()
+
+    for _ in range(max(1, args.warmup)):
+        step_e2e()
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e2.record(stream)
+    for _ in range(args.steps):
+        rec_host = step_e2e()
+    e3.record(stream)
+    e3.synchronize()
+    wall_e2e = (time.perf_counter() - w0) * 1e3
+    barrier()
+    e2e_ms = max(e2.elapsed_time(e3), wall_e2e) / args.steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world * sample_taps / (e2e_ms * 1e-3) / 1e9
+    _, _, e2e_launches = trk.timing()
+
+    # ---- end-of-run gather of the records to rank 0 over NCCL
+    gathered = None
+    if dist:
+        rec_t = torch.empty(rec_bytes, dtype=torch.uint8, device=dev)
+        trk.records_raw(dst_ptr=rec_t.data_ptr(), device=True)
+        outs = [torch.empty_like(rec_t) for _ in range(world)] if rank == 0 else None
+        dist.gather(rec_t, outs, dst=0)
+        gathered = sum(int(o.numel()) for o in outs) if rank == 0 else None
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (track_kernel, one launch/step)
+    clk = clocks.summary()
+    sm_mhz = clk["sm_mhz"] or 1965.0
+    track_launch_ms = track_ms / args.steps
+    real_if = c["fmt"] == "int8_real_if"
+    alg_flops = sample_taps * 2.0 * ops_per_sample_tap(taps.n_counted, C_ch, False)  # FIR runs in ingest
+    achieved = alg_flops / (track_launch_ms * 1e-3) / 1e12
+    peak = fp32_peak_tflops(sm_mhz)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("track_kernel_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    peaks = {}
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        peaks = json.load(open(mp))
+    hbm_peak = peaks.get("hbm_gbs", 6450.0)
+    bytes_per_sample = {"int8_real_if": 1, "int16_iq": 4}[c["fmt"]]
+    alg_bytes = blocks * n * (8 if real_if else bytes_per_sample)  # track_kernel reads the baseband
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        cb = min(args.cpu_blocks, blocks)
+        raw_np = raw.cpu().numpy()
+        try:
+            if c["taps"] == "epl":
+                wall, trk_s, ce = cpu_reference_run(raw_np, c, inits, cfg, cb, threads)
+                kind = "reference"
+            else:
+                import oracle
+                x = oracle.ingest(raw_np[: cb * n * bytes_per_sample], abi.FMT_INT16_IQ, fs)
+                t0 = time.perf_counter()
+                wall, ce = cpu_port_run(x, inits, cfg, taps, fs, cb, threads)
+                wall = time.perf_counter() - t0
+                kind = "port"
+            cpu = {"value": float(cb) * n * T * C_ch / wall / 1e9, "unit": UNIT, "cores": threads,
+                   "kind": kind, "sample": f"first {cb} of {blocks} blocks x {C_ch} channels "
+                   f"(SampleSource producer + track_epoch pool, batched kernel, {wall:.2f} s wall)"}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded, paper_1907_00463_b200/simsource.py; loops start from truth)",
+        "config": {"workload": c["desc"], "blocks": blocks, "channels": C_ch, "taps_counted": T,
+                   "samples_per_block": n, "parallelism": f"weak: {world} rank(s) x own recording",
+                   "l2": "inputs larger than L2 (raw %.0f MB + baseband ring %.2f GB per step)" % (
+                       nbytes / 1e6, blocks * n * 8 / 1e9),
+                   "lock_fail_limit": "INT_MAX (every channel computes every epoch)"},
+        "realtime_channels": world * float(counts.sum()) / (ms_per_step * 1e-3) / 1000.0,
+        "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock under load "
+                                    "(%.0f MHz); FP32 pipe roof per SURVEY 8d" % sm_mhz,
+                     "alg_ops_per_sample_tap": ops_per_sample_tap(T, C_ch, False),
+                     "hbm": {"achieved_gbs": alg_bytes / (track_launch_ms * 1e-3) / 1e9,
+                             "peak_gbs": hbm_peak}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": rec_bytes,
+                "path": "pinned host -> l1rxg_tracker_push (%d ms chunks, H2D overlapped with "
+                        "tracking) -> run -> records_raw to host" % args.e2e_chunk_ms},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if gathered is not None:
+        line["records_gathered_bytes"] = gathered
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -271,6 +271,13 @@ int l1rxg_tracker_records(l1rxg_tracker* trk, int channel, int64_t e0,
  * device buffer (for an NCCL gather) or host buffer. */
 int l1rxg_tracker_records_raw(l1rxg_tracker* trk, void* dst, int dst_is_device,
                               int64_t* bytes_out);
+/* Restarts every stream at sample 0 (empty ring, zero FIR history, like a
+ * fresh SampleSource) and resets the channels to `channels` with zero epoch
+ * counts: one more pass over a recording without reallocating. */
+int l1rxg_tracker_reset(l1rxg_tracker* trk, const l1rxg_channel* channels);
+/* The CUDA stream (cudaStream_t) the tracker's kernels run on, so a caller
+ * can bracket work with its own events. */
+void* l1rxg_tracker_stream(l1rxg_tracker* trk);
 /* Reads back ingested baseband samples [s0, s0+count) of stream s as
  * interleaved doubles (ingest parity checks against SampleSource). */
 int l1rxg_tracker_read_samples(l1rxg_tracker* trk, int stream, int64_t s0,

@@ -21,7 +21,8 @@ EXPORTS = [
     "l1rxg_host_free", "l1rxg_correlate_epoch", "l1rxg_correlate_batch", "l1rxg_tracker_create",
     "l1rxg_tracker_destroy", "l1rxg_tracker_push", "l1rxg_tracker_push_device", "l1rxg_tracker_run",
     "l1rxg_tracker_sync", "l1rxg_tracker_channels", "l1rxg_tracker_epoch_counts",
-    "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_read_samples",
+    "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_reset",
+    "l1rxg_tracker_stream", "l1rxg_tracker_read_samples",
     "l1rxg_tracker_timing", "l1rxg_search_grid",
 ]
 
@@ -69,6 +70,8 @@ def lib():
     _sig(L, "l1rxg_tracker_epoch_counts", C.c_int, vp, P(i64))
     _sig(L, "l1rxg_tracker_records", C.c_int, vp, C.c_int, i64, i64, P(abi.EpochRecord), dp)
     _sig(L, "l1rxg_tracker_records_raw", C.c_int, vp, vp, C.c_int, P(i64))
+    _sig(L, "l1rxg_tracker_reset", C.c_int, vp, P(abi.Channel))
+    _sig(L, "l1rxg_tracker_stream", vp, vp)
     _sig(L, "l1rxg_tracker_read_samples", C.c_int, vp, C.c_int, i64, i64, dp)
     _sig(L, "l1rxg_tracker_timing", C.c_int, vp, dp, dp, P(i64))
     _sig(L, "l1rxg_search_grid", C.c_int, vp, C.c_int, vp, C.c_int, i64, C.c_double, C.c_double,

@@ -819,6 +819,34 @@ int l1rxg_tracker_records_raw(l1rxg_tracker* t, void* dst, int dst_is_device, in
     return 0;
 }
 
+int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
+    if (!t || (!chans && t->d.n_channels > 0))
+        return set_err(L1RXG_EINVAL, "null argument");
+    CK(cudaSetDevice(t->ctx->device));
+    CK(cudaStreamSynchronize(t->ctx->copy));
+    CK(cudaStreamSynchronize(t->ctx->compute));
+    const size_t C = static_cast<size_t>(std::max(1, t->d.n_channels));
+    cudaStream_t st = t->ctx->compute;
+    CK(cudaMemsetAsync(t->d_avail, 0, 8 * t->streams.size(), st));
+    CK(cudaMemsetAsync(t->d_ecount, 0, 8 * C, st));
+    CK(cudaMemsetAsync(t->d_status, 0, 4 * C, st));
+    for (auto& r : t->streams) {
+        r.pushed = 0;
+        r.hist_cur = 0;
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaMemsetAsync(r.hist8[k], 0, 32, st));
+            CK(cudaMemsetAsync(r.histf[k], 0, 32 * sizeof(float2), st));
+        }
+    }
+    if (t->d.n_channels > 0)
+        CK(cudaMemcpyAsync(t->d_chans, chans, sizeof(l1rxg_channel) * t->d.n_channels,
+                           cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+void* l1rxg_tracker_stream(l1rxg_tracker* t) { return t ? static_cast<void*>(t->ctx->compute) : nullptr; }
+
 int l1rxg_tracker_read_samples(l1rxg_tracker* t, int s, int64_t s0, int64_t count, double* iq_out) {
     if (!t || s < 0 || s >= (int)t->streams.size())
         return set_err(L1RXG_EINVAL, "bad stream");

@@ -260,6 +260,17 @@ class Tracker:
                                                   C.byref(nb)))
         return nb.value
 
+    def reset(self, channels) -> None:
+        """Restart all streams at sample 0 with fresh channel states."""
+        chans = list(channels)
+        arr = (abi.Channel * max(1, len(chans)))(*chans)
+        check(self._lib.l1rxg_tracker_reset(self.handle, arr))
+
+    def cuda_stream(self) -> int:
+        """cudaStream_t of the tracker's kernels (wrap with
+        torch.cuda.ExternalStream to time with events)."""
+        return int(self._lib.l1rxg_tracker_stream(self.handle) or 0)
+
     def read_samples(self, stream: int, s0: int, count: int) -> np.ndarray:
         out = np.zeros(2 * count, np.float64)
         check(self._lib.l1rxg_tracker_read_samples(self.handle, stream, s0, count, out.ctypes.data_as(_dp)))
