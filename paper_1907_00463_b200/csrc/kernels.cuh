@@ -30,7 +30,7 @@ constexpr double PI_D = 3.14159265358979323846;  // constants.hpp:20
 constexpr double TWO_PI_D = 2.0 * PI_D;
 constexpr double F_L1_HZ = 1.57542e9;      // constants.hpp:5
 constexpr double CHIP_RATE_HZ = 1.023e6;   // constants.hpp:6
-constexpr int CODE_TABLE = 1024;           // 1023 chips + pad
+constexpr int MAX_NT = 640;                // correlator CTA size cap (<= 102 regs)
 
 // ---------------------------------------------------------------------
 // per-epoch NCO constants (tracking.hpp:234-239)
@@ -75,10 +75,6 @@ __device__ __forceinline__ int tap_boundary(int m, double d, double cps, double 
     return b;
 }
 
-__device__ __forceinline__ int chip_at(const int8_t* code, int m) {
-    return code[m - 1023 * (m / 1023)];
-}
-
 // fma-free complex multiply x * conj(e^{j a}) with (c, s) = (cos a, sin a):
 // (xr c + xi s, xi c - xr s) -- the reference's wipe-off form
 // (tracking.hpp:248-249).
@@ -91,37 +87,60 @@ __device__ __forceinline__ float2 wipe(float2 x, float c, float s) {
 // run[0..RUN).  Overwrites run[j] with the exclusive prefix of the wiped
 // samples and accumulates the run's contribution of every tap (and of the
 // first-half prompt) into acc[2*T+2] (fp32).
-template <int T>
+// Replica phase at a sample index held as a double (no int->fp64 convert
+// on the hot path): same value as tap_value(int).
+__device__ __forceinline__ double tap_value_d(double i, double cps, double base, double d) {
+    return __dadd_rn(__fma_rn(i, cps, base), d);
+}
+// First b in [lo, hi] with tap_value(b) >= m (exists: tap_index(hi) >= m);
+// fp64 estimate, then exact verification with the reference expression
+// (monotone in b), so the boundary is the reference's to the sample.
+__device__ __forceinline__ int tap_boundary_d(double m, double d, double cps, double inv_cps,
+                                              double base, double lo, double hi) {
+    double b = ceil(((m - d) - base) * inv_cps);
+    b = fmax(lo, fmin(hi, b));
+    while (b > lo && tap_value_d(b - 1.0, cps, base, d) >= m) b -= 1.0;
+    while (b < hi && tap_value_d(b, cps, base, d) < m) b += 1.0;
+    return __double2int_rz(b);
+}
+
+constexpr int CHIP_EXT = 4096;  // chip table extended over m in [0, 4096)
+
+template <int T, bool FULL>
 __device__ __forceinline__ void process_run(const EpochConsts& c, float2* run,
                                             const float2* __restrict__ rot,
-                                            const int8_t* __restrict__ code,
+                                            const float* __restrict__ chipf,
                                             const double* __restrict__ d, int kp,
                                             int i0, int cnt, float* acc) {
     // per-run carrier anchor e^{-j theta(i0)}, theta as the reference
-    // computes it (fma(w, i, phi)), reduced in fp64 then rotated in fp32
-    const double th = __fma_rn(c.w, (double)i0, c.phi);
+    // computes it (fma(w, i, phi)), reduced to [-pi, pi] in fp64; the fp32
+    // phasor's ~4e-7 error is common to the run's 31 samples
+    const double di0 = (double)i0;
+    const double th = __fma_rn(c.w, di0, c.phi);
     const double r = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
     float sa, ca;
-    sincosf((float)r, &sa, &ca);
+    __sincosf((float)r, &sa, &ca);
 
     float pr = 0.f, pi = 0.f;
 #pragma unroll
     for (int j = 0; j < RUN; ++j) {
-        const float2 x = run[j];
+        const float2 x = (FULL || j < cnt) ? run[j] : make_float2(0.f, 0.f);
         const float2 q = rot[j];
         const float2 z = wipe(x, q.x, q.y);
         run[j] = make_float2(pr, pi);
         pr += z.x;
         pi += z.y;
     }
-    const int i_last = i0 + cnt - 1;
+    const int i_last = i0 + (FULL ? RUN : cnt) - 1;
+    const double dlo = di0, dhi = (double)i_last;
+    const double dprev = i0 > 0 ? di0 - 1.0 : 0.0;
     const bool straddle = (i0 < c.nh) && (c.nh <= i_last);
 #pragma unroll
     for (int k = 0; k < T; ++k) {
         const double dk = d[k];
-        const int m_hi = tap_index(i_last, c.cps, c.base, dk);
-        const int m_lo = tap_index(i0 > 0 ? i0 - 1 : 0, c.cps, c.base, dk);
-        const float chi = (float)chip_at(code, m_hi);
+        const int m_hi = __double2int_rz(tap_value_d(dhi, c.cps, c.base, dk));
+        const int m_lo = __double2int_rz(tap_value_d(dprev, c.cps, c.base, dk));
+        const float chi = chipf[m_hi];
         float ur = chi * pr, ui = chi * pi;
         // first-half prompt (tracking.hpp:265-271), only where the run
         // straddles n/2
@@ -130,21 +149,20 @@ __device__ __forceinline__ void process_run(const EpochConsts& c, float2* run,
         float hr = 0.f, hi = 0.f;
         if (want_h) {
             m_h = tap_index(c.nh - 1, c.cps, c.base, dk);
-            const float chh = (float)chip_at(code, m_h);
+            const float chh = chipf[m_h];
             const float2 pn = run[c.nh - i0];
             hr = chh * pn.x;
             hi = chh * pn.y;
         }
-        int prev = chip_at(code, m_lo);
+        float prev = chipf[m_lo];
         for (int m = m_lo + 1; m <= m_hi; ++m) {
-            const int cur = chip_at(code, m);
-            const int delta = cur - prev;
+            const float cur = chipf[m];
+            const float df = cur - prev;
             prev = cur;
-            if (delta != 0) {
-                const int b = tap_boundary(m, dk, c.cps, c.inv_cps, c.base, i0, i_last);
+            if (df != 0.f) {
+                const int b = tap_boundary_d((double)m, dk, c.cps, c.inv_cps, c.base, dlo, dhi);
                 if (b > i0) {
                     const float2 pb = run[b - i0];
-                    const float df = (float)delta;
                     ur = fmaf(-df, pb.x, ur);
                     ui = fmaf(-df, pb.y, ui);
                     if (want_h && m <= m_h) {
@@ -184,6 +202,35 @@ __device__ __forceinline__ void load_tile(float2* tile, const float2* __restrict
                                           int len, int cap) {
     for (int i = threadIdx.x; i < cap; i += blockDim.x)
         tile[i] = (i < len) ? __ldg(src + i) : make_float2(0.f, 0.f);
+}
+
+// ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on bar.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // Warp + block reduction of V fp32 partials into fp64 totals in out[V]
@@ -248,30 +295,91 @@ __device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, dou
     return atan2(cross, dot) / (2.0 * PI_D * dt);
 }
 
+// The transcendental pieces of one loop update (and the fmod-based NCO
+// advance) are independent of each other.  The tracking kernel evaluates
+// them in separate WARPS (divergent lanes of one warp would serialise) via
+// loop_piece(), then one thread applies the reference's sequential logic
+// (loop_update) -- the same operations in the same order as a
+// single-thread update, so the result is identical.
+struct LoopPre {
+    double e, l;        // |E|, |L|            (tracking.hpp:96-97, 545-546)
+    double pll;         // Costas atan         (:104-111)
+    double fc, ff;      // FLL coarse / fine   (:113-138)
+    double mu_s, cn0;   // C/N0 window result  (:472-498), if the window closes
+    double code_phase, carrier_phase, chi;  // NCO advance (:275-280)
+};
+constexpr int LOOP_PIECES = 6;
+
+__device__ __forceinline__ void advance_nco(double& code_phase, double& carrier_phase,
+                                            double& chi, const EpochConsts& c);
+
+__device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_channel& ch,
+                                           const l1rxg_corr& o, const LoopCfg& lc,
+                                           const EpochConsts& c) {
+    const double dt = (double)o.n_samples / lc.fs;
+    if (piece == 0) {
+        p.e = sqrt(o.ie * o.ie + o.qe * o.qe);
+        p.l = sqrt(o.il * o.il + o.ql * o.ql);
+    } else if (piece == 1) {
+        if (o.ip == 0.0)
+            p.pll = (o.qp == 0.0) ? 0.0 : (o.qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
+        else
+            p.pll = atan(o.qp / o.ip);
+    } else if (piece == 2) {
+        p.fc = fll_disc(o.ip_h1, o.qp_h1, o.ip_h2, o.qp_h2, dt / 2.0, false);
+    } else if (piece == 3) {
+        p.ff = fll_disc(ch.last_ip, ch.last_qp, o.ip, o.qp, dt, true);
+    } else if (piece == 5) {
+        double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
+        advance_nco(cp, ph, chi, c);
+        p.code_phase = cp;
+        p.carrier_phase = ph;
+        p.chi = chi;
+    } else if (piece == 4) {
+        const int m = lc.cfg.cn0_window_ms;
+        p.mu_s = ch.mu_smoothed;
+        p.cn0 = ch.cn0_dbhz;
+        if (ch.win_len + 1 >= m) {
+            double nbi = 0, nbq = 0, wbp = 0;
+            for (int k = 0; k < m; ++k) {
+                const double wi = k < ch.win_len ? ch.win_ip[k] : o.ip;
+                const double wq = k < ch.win_len ? ch.win_qp[k] : o.qp;
+                const double sg = wi >= 0 ? 1.0 : -1.0;
+                nbi += sg * wi;
+                nbq += sg * wq;
+                wbp += wi * wi + wq * wq;
+            }
+            const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
+            p.mu_s = ch.metrics_valid ? ch.mu_smoothed + 0.2 * (mu - ch.mu_smoothed) : mu;
+            const double md = (double)m;
+            if (p.mu_s >= md - 1e-9)
+                p.cn0 = 65.0;
+            else if (p.mu_s <= 1.0)
+                p.cn0 = 0.0;
+            else
+                p.cn0 = 10.0 * log10((p.mu_s - 1.0) / (md - p.mu_s) / 1e-3);
+        }
+    }
+}
+
 // ch: channel state (post NCO advance by the correlator); o: sums.
-__device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc) {
+__device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc,
+                            const LoopPre& p) {
     const l1rxg_tracking_cfg& cfg = lc.cfg;
     const bool noop = lc.kernel == L1RXG_KERNEL_NOOP;
     const double dt = (double)o.n_samples / lc.fs;
-    const double e = sqrt(o.ie * o.ie + o.qe * o.qe);
-    const double l = sqrt(o.il * o.il + o.ql * o.ql);
+    const double e = p.e, l = p.l;
     const double e_env = e + l;
     const double dll_err = (e + l == 0.0) ? 0.0 : 0.5 * (e - l) / (e + l);  // :95-101
     if (e_env == 0.0 && !noop)
         ch.lock_fail_count++;
-    double pll_err;  // :104-111
-    if (o.ip == 0.0)
-        pll_err = (o.qp == 0.0) ? 0.0 : (o.qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
-    else
-        pll_err = atan(o.qp / o.ip);
+    const double pll_err = p.pll;  // :104-111
     if (ch.fll_enabled && ch.epochs_since_handoff < (int64_t)cfg.fll_pull_in_ms &&
         ch.carrier_lock_ratio < 0.8 && !noop) {  // :561-576
         if (ch.epochs_since_handoff < (int64_t)cfg.fll_coarse_ms) {
-            const double f = fll_disc(o.ip_h1, o.qp_h1, o.ip_h2, o.qp_h2, dt / 2.0, false);
-            ch.pll_integrator += 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D * f * dt;
+            ch.pll_integrator += 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D * p.fc * dt;
         } else if (ch.have_last_prompt) {
-            const double f = fll_disc(ch.last_ip, ch.last_qp, o.ip, o.qp, dt, true);
-            ch.pll_integrator += 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D * f * dt;
+            ch.pll_integrator += 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D * p.ff * dt;
         }
     }
     const double doppler_cmd = loop_filter(ch.pll_integrator, ch.pll_prev_error, ch.pll_primed,
@@ -296,24 +404,10 @@ __device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCf
     ch.win_qp[ch.win_len] = o.qp;
     ch.win_len++;
     const int m = cfg.cn0_window_ms;
-    if (ch.win_len >= m) {
-        double nbi = 0, nbq = 0, wbp = 0;
-        for (int k = 0; k < m; ++k) {
-            const double sg = ch.win_ip[k] >= 0 ? 1.0 : -1.0;
-            nbi += sg * ch.win_ip[k];
-            nbq += sg * ch.win_qp[k];
-            wbp += ch.win_ip[k] * ch.win_ip[k] + ch.win_qp[k] * ch.win_qp[k];
-        }
+    if (ch.win_len >= m) {  // window sums and the C/N0 map come from lane 4
         ch.win_len = 0;
-        const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
-        ch.mu_smoothed = ch.metrics_valid ? ch.mu_smoothed + 0.2 * (mu - ch.mu_smoothed) : mu;
-        const double md = (double)m;
-        if (ch.mu_smoothed >= md - 1e-9)
-            ch.cn0_dbhz = 65.0;
-        else if (ch.mu_smoothed <= 1.0)
-            ch.cn0_dbhz = 0.0;
-        else
-            ch.cn0_dbhz = 10.0 * log10((ch.mu_smoothed - 1.0) / (md - ch.mu_smoothed) / 1e-3);
+        ch.mu_smoothed = p.mu_s;
+        ch.cn0_dbhz = p.cn0;
         ch.metrics_valid = 1;
     }
     if (ch.metrics_valid &&
@@ -349,9 +443,27 @@ struct CorrSmem {
     double sums[2 * T + 2];
     float red[32 * (2 * T + 2)];
     float2 rot[RUN + 1];
-    int8_t code[CODE_TABLE];
+    float chipf[CHIP_EXT];  // chips[m mod 1023] as +/-1.0f, m < CHIP_EXT
+    LoopPre pre;
     int flags;
 };
+
+// chipf[m] = chips[m mod 1023] (the reference's code_ext idea,
+// tracking.hpp:168-173, extended so no modulo is needed on the hot path)
+__device__ __forceinline__ void fill_chips(float* chipf, const int8_t* codes, int prn) {
+    for (int k = threadIdx.x; k < CHIP_EXT; k += blockDim.x)
+        chipf[k] = (float)codes[prn * 1023 + (k % 1023)];
+}
+
+template <int T>
+__device__ __forceinline__ void run_dispatch(const EpochConsts& c, float2* run, const float2* rot,
+                                             const float* chipf, const double* d, int kp, int i0,
+                                             int cnt, float* acc) {
+    if (cnt == RUN)
+        process_run<T, true>(c, run, rot, chipf, d, kp, i0, cnt, acc);
+    else
+        process_run<T, false>(c, run, rot, chipf, d, kp, i0, cnt, acc);
+}
 
 template <int T>
 __device__ __forceinline__ float2* tile_of(CorrSmem<T>* s) {
@@ -378,7 +490,7 @@ __device__ void correlate_epoch(CorrSmem<T>* s, const float2* __restrict__ src, 
         const int i0 = u0 + threadIdx.x * RUN;
         const int cnt = min(RUN, c.n - i0);
         if (cnt > 0)
-            process_run<T>(c, tile + threadIdx.x * RUN, s->rot, s->code, s->d, kp, i0, cnt, acc);
+            run_dispatch<T>(c, tile + threadIdx.x * RUN, s->rot, s->chipf, s->d, kp, i0, cnt, acc);
         __syncthreads();
     }
     block_reduce<2 * T + 2>(acc, s->red, s->sums);
@@ -406,52 +518,179 @@ struct TrackArgs {
     LoopCfg lc;
 };
 
+// Channel-resident persistent tracking kernel: one CTA per channel loops over
+// its epochs with no host round trip.  The epoch window is brought into
+// shared memory by the TMA engine (cp.async.bulk, two mbarrier-tracked
+// halves); the copy of the next window is issued as soon as the current one
+// has been consumed, so it overlaps the block reduction and the loop update.
+struct TileLoad {
+    int64_t pos;   // ring position of the first sample of the unit
+    int delta;     // samples of alignment slack in front (0/1)
+    int h;         // split point (samples, even) between the two halves
+    int len;       // samples of the unit
+};
+
+__device__ __forceinline__ TileLoad plan_load(int64_t abs_first, int len, int64_t R) {
+    TileLoad u;
+    const int64_t pos = abs_first % R;
+    u.delta = (int)(pos & 1);
+    u.pos = pos - u.delta;
+    u.len = len;
+    u.h = 2 * ((len + u.delta) / 4);
+    return u;
+}
+
+__device__ __forceinline__ void issue_load(const TileLoad& u, float2* tile, const float2* ring,
+                                           uint64_t* bars) {
+    const uint32_t total = (uint32_t)(((u.len + u.delta) * 8 + 15) & ~15);
+    const uint32_t b0 = (uint32_t)u.h * 8u;
+    mbar_expect_tx(&bars[0], b0);
+    tma_load_1d(tile, ring + u.pos, b0, &bars[0]);
+    mbar_expect_tx(&bars[1], total - b0);
+    tma_load_1d(tile + u.h, ring + u.pos + u.h, total - b0, &bars[1]);
+}
+
 template <int T>
-__global__ void __launch_bounds__(768, 1) track_kernel(TrackArgs a) {
+struct TrackSmem {
+    CorrSmem<T> cs;
+    uint64_t bars[2];
+    TileLoad unit;      // the load in flight (or last issued)
+    int inflight;       // a unit is in flight into the tile
+};
+
+template <int T>
+__device__ __forceinline__ float2* track_tile(TrackSmem<T>* s) {
+    return reinterpret_cast<float2*>(reinterpret_cast<char*>(s) +
+                                     ((sizeof(TrackSmem<T>) + 15) & ~size_t(15)));
+}
+
+template <int T>
+__global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
+    TrackSmem<T>* ts = reinterpret_cast<TrackSmem<T>*>(smem_raw);
+    CorrSmem<T>* s = &ts->cs;
+    float2* tile = track_tile(ts);
     const int cidx = blockIdx.x;
     const int strm = a.chan_stream[cidx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    constexpr int V = 2 * T + 2;
+    const int cap = blockDim.x * RUN;
+    const int n = a.n;
+    const int nsub = (n + cap - 1) / cap;
+    const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
+    const int64_t avail = a.avail[strm];
+    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
     if (threadIdx.x == 0) {
         s->ch = a.chans[cidx];
-        s->flags = 0;
+        mbar_init(&ts->bars[0], 1);
+        mbar_init(&ts->bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        ts->inflight = 0;
     }
     for (int k = threadIdx.x; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
     __syncthreads();
-    const int prn = s->ch.prn;
-    for (int k = threadIdx.x; k < CODE_TABLE; k += blockDim.x)
-        s->code[k] = (k < 1023) ? a.codes[prn * 1023 + k] : 0;
-    const int64_t avail = a.avail[strm];
-    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
+    fill_chips(s->chipf, a.codes, s->ch.prn);
+    // first epoch: consts, rotators and the first tile load
+    if (threadIdx.x == 0) {
+        const l1rxg_channel& ch = s->ch;
+        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                    ch.carrier_phase_rad, a.lc.fs, n);
+        const int64_t off = ch.sample_offset_next_epoch;
+        if (!noop && ch.state != L1RXG_IDLE && a.max_epochs > 0 && off + n <= avail && off >= 0 &&
+            off >= avail - a.ring_cap) {
+            ts->unit = plan_load(off, min(cap, n), a.ring_cap);
+            issue_load(ts->unit, tile, ring, ts->bars);
+            ts->inflight = 1;
+        }
+    }
+    __syncthreads();
+    fill_rot(s->rot, s->c.w);
+    __syncthreads();
+
+    uint32_t phase = 0;
     int64_t e = 0;
     int64_t done = a.ecount[cidx];
     for (;;) {
         // epoch admission (uniform: every thread reads the same smem state)
         const int64_t off = s->ch.sample_offset_next_epoch;
-        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + a.n > avail)
+        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
             break;
         if (off < avail - a.ring_cap || off < 0) {  // window already overwritten
             if (threadIdx.x == 0)
                 a.status[cidx] = 1;
             break;
         }
-        if (threadIdx.x == 0)
-            make_consts(s->c, s->ch.code_phase_chips, s->ch.code_freq_hz,
-                        s->ch.carrier_doppler_hz, s->ch.carrier_phase_rad, a.lc.fs, a.n);
-        __syncthreads();
-        fill_rot(s->rot, s->c.w);
-        const int64_t pos = off % a.ring_cap;
-        if (a.lc.kernel != L1RXG_KERNEL_NOOP) {
-            correlate_epoch<T>(s, ring + pos, a.kp);
-        } else {
-            if (threadIdx.x < 2 * T + 2)
-                s->sums[threadIdx.x] = 0.0;
-            __syncthreads();
+        const EpochConsts c = s->c;
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[v] = 0.f;
+        for (int q = 0; q < nsub; ++q) {
+            const int u0 = q * cap;
+            const int i0 = u0 + threadIdx.x * RUN;
+            const int cnt = min(RUN, n - i0);
+            if (!noop) {
+                const TileLoad u = ts->unit;
+                const int r0 = u.delta + threadIdx.x * RUN;
+                if (cnt > 0) {
+                    if (r0 < u.h)
+                        mbar_wait(&ts->bars[0], phase);
+                    if (r0 + RUN > u.h)
+                        mbar_wait(&ts->bars[1], phase);
+                    run_dispatch<T>(c, tile + r0, s->rot, s->chipf, s->d, a.kp, i0, cnt, acc);
+                }
+                if (threadIdx.x == 0) {  // every phase completes before the next issue
+                    mbar_wait(&ts->bars[0], phase);
+                    mbar_wait(&ts->bars[1], phase);
+                }
+                phase ^= 1u;
+            }
+            if (q + 1 == nsub) {  // warp-level part of the block reduction
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    float x = acc[v];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+                        x += __shfl_xor_sync(0xffffffffu, x, o);
+                    if (lane == 0)
+                        s->red[warp * V + v] = x;
+                }
+            }
+            __syncthreads();  // tile consumed
+            if (threadIdx.x == 0) {
+                ts->inflight = 0;
+                if (!noop) {
+                    if (q + 1 < nsub) {
+                        ts->unit = plan_load(off + (q + 1) * cap, min(cap, n - (q + 1) * cap), a.ring_cap);
+                        issue_load(ts->unit, tile, ring, ts->bars);
+                        ts->inflight = 1;
+                    } else if (s->ch.state != L1RXG_IDLE && e + 1 < a.max_epochs &&
+                               off + 2 * (int64_t)n <= avail) {
+                        // speculative prefetch of the next epoch's first unit
+                        ts->unit = plan_load(off + n, min(cap, n), a.ring_cap);
+                        issue_load(ts->unit, tile, ring, ts->bars);
+                        ts->inflight = 1;
+                    }
+                }
+            }
+            if (q + 1 < nsub)
+                __syncthreads();  // publish the next unit
         }
-        if (threadIdx.x == 0) {
-            l1rxg_channel& ch = s->ch;
-            const EpochConsts c = s->c;
+        // ---- loop update: warps 0..PW-1 (PW <= 6) split the independent
+        // transcendental pieces, then warp 0 / lane 0 applies them
+        const int PW = min(nwarps, LOOP_PIECES);
+        if (warp < PW) {
+            if (warp == 0) {  // fp64 cross-warp totals
+                for (int v = lane; v < V; v += 32) {
+                    double sm = 0.0;
+                    for (int w = 0; w < nwarps; ++w)
+                        sm += (double)s->red[w * V + v];
+                    s->sums[v] = sm;
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
             l1rxg_corr o;
             o.ie = s->sums[2 * a.ke];
             o.qe = s->sums[2 * a.ke + 1];
@@ -465,14 +704,26 @@ __global__ void __launch_bounds__(768, 1) track_kernel(TrackArgs a) {
             o.qp_h2 = o.qp - o.qp_h1;
             o.n_samples = c.n;
             o.pad_ = 0;
-            l1rxg_epoch_record r;
-            r.sample_offset_start = off;
-            r.code_phase_in = ch.code_phase_chips;
-            r.code_freq_in = ch.code_freq_hz;
-            r.carrier_doppler_in = ch.carrier_doppler_hz;
-            r.carrier_phase_in = ch.carrier_phase_rad;
-            advance_nco(ch.code_phase_chips, ch.carrier_phase_rad, ch.chi_chips, c);
-            loop_update(ch, o, a.lc);
+            if (lane == 0)
+                for (int piece = warp; piece < LOOP_PIECES; piece += PW)
+                    loop_piece(piece, s->pre, s->ch, o, a.lc, c);
+            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
+            const int64_t slot = (int64_t)cidx * a.max_records + (done % a.max_records);
+            if (warp == 0 && a.tap_sums && lane < 2 * T)
+                a.tap_sums[slot * (2 * T) + lane] = s->sums[lane];
+            if (warp == 0 && lane == 0) {
+                l1rxg_channel& ch = s->ch;
+                const LoopPre pre = s->pre;
+                l1rxg_epoch_record r;
+                r.sample_offset_start = off;
+                r.code_phase_in = ch.code_phase_chips;
+                r.code_freq_in = ch.code_freq_hz;
+                r.carrier_doppler_in = ch.carrier_doppler_hz;
+                r.carrier_phase_in = ch.carrier_phase_rad;
+                ch.code_phase_chips = pre.code_phase;
+                ch.carrier_phase_rad = pre.carrier_phase;
+                ch.chi_chips = pre.chi;
+                loop_update(ch, o, a.lc, pre);
             r.epoch_index = ch.epoch_ms_count - 1;
             r.sample_offset_end = ch.sample_offset_next_epoch;
             r.prn = ch.prn;
@@ -493,18 +744,25 @@ __global__ void __launch_bounds__(768, 1) track_kernel(TrackArgs a) {
             r.mu_smoothed = ch.mu_smoothed;
             r.dll_prev_error = ch.dll_prev_error;
             r.pll_prev_error = ch.pll_prev_error;
-            const int64_t slot = (int64_t)cidx * a.max_records + (done % a.max_records);
-            a.recs[slot] = r;
-        }
-        if (a.tap_sums && threadIdx.x < 2 * T) {
-            const int64_t slot = (int64_t)cidx * a.max_records + (done % a.max_records);
-            a.tap_sums[slot * (2 * T) + threadIdx.x] = s->sums[threadIdx.x];
+                a.recs[slot] = r;
+                // next epoch's NCO constants
+                make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                            ch.carrier_phase_rad, a.lc.fs, n);
+            }
+            if (warp == 0) {
+                __syncwarp();
+                fill_rot(s->rot, s->c.w);
+            }
         }
         ++e;
         ++done;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
+        if (ts->inflight) {  // never leave a bulk copy in flight into freed smem
+            mbar_wait(&ts->bars[0], phase);
+            mbar_wait(&ts->bars[1], phase);
+        }
         a.chans[cidx] = s->ch;
         a.ecount[cidx] = done;
     }
@@ -526,13 +784,12 @@ struct JobArgs {
 };
 
 template <int T>
-__global__ void __launch_bounds__(768, 1) correlate_jobs_kernel(JobArgs a) {
+__global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
     const int j = blockIdx.x;
     const int prn = a.prns[j];
-    for (int k = threadIdx.x; k < CODE_TABLE; k += blockDim.x)
-        s->code[k] = (k < 1023) ? a.codes[prn * 1023 + k] : 0;
+    fill_chips(s->chipf, a.codes, prn);
     for (int k = threadIdx.x; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
     if (threadIdx.x == 0) {

@@ -114,7 +114,7 @@ int pick_T(int K) {
 // Block size: enough RUN-sample runs to cover the epoch in the fewest
 // sub-tiles of at most 768 threads (<= 190 KB of shared tile).
 int pick_threads(int n, int* subtiles) {
-    const int max_nt = 768;
+    const int max_nt = MAX_NT;
     const int k = (n + max_nt * RUN - 1) / (max_nt * RUN);
     const int runs = (n + k * RUN - 1) / (k * RUN);
     int nt = ((runs + 31) / 32) * 32;
@@ -131,7 +131,9 @@ size_t smem_bytes(int nt) {
 
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
-    const size_t sm = smem_bytes<T>(nt);
+    // tile: nt*RUN samples + alignment slack of the 16-byte bulk copies
+    const size_t sm = ((sizeof(TrackSmem<T>) + 15) & ~size_t(15)) +
+                      (static_cast<size_t>(nt) * RUN + 4) * sizeof(float2);
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     track_kernel<T><<<n_ch, nt, sm, s>>>(a);
     CK(cudaGetLastError());
@@ -450,10 +452,11 @@ int l1rxg_correlate_batch(l1rxg_ctx* c, const double* iq, int n, int n_jobs,
         if (prns[j] < 1 || prns[j] > 32)
             return set_err(L1RXG_ERANGE, "PRN must be in 1..32");  // cacode.hpp:38-39
         const l1rxg_nco& st = states[j];
+        // replica chip indices must stay inside the extended chip table
         if (!(st.code_freq_hz > 0) || !(st.code_phase_chips >= 0.0) ||
-            !(st.code_phase_chips + 1023.0 + n * (st.code_freq_hz / fs) + 1.0 < 2147483000.0))
+            !(st.code_phase_chips + 1023.0 + n * (st.code_freq_hz / fs) + 2.0 < (double)CHIP_EXT))
             return set_err(L1RXG_EINVAL, "code NCO state out of the correlator's domain "
-                                         "(code_phase >= 0, code_freq > 0)");
+                                         "(0 <= code_phase, code_freq > 0, replica span < 4096 chips)");
     }
     std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->device));
@@ -557,7 +560,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             return set_err(L1RXG_EINVAL, "channel bound to a missing stream");
         if (chans[k].prn < 1 || chans[k].prn > 32)
             return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
-        if (!(chans[k].code_phase_chips >= 0.0) || !(chans[k].code_freq_hz > 0))
+        if (!(chans[k].code_phase_chips >= 0.0) || !(chans[k].code_phase_chips < 1023.0) ||
+            !(chans[k].code_freq_hz > 0) || !(chans[k].code_freq_hz < 1.1 * CHIP_RATE_HZ))
             return set_err(L1RXG_EINVAL, "channel code NCO out of domain");
         if (chans[k].win_len < 0 || chans[k].win_len >= d->cfg.cn0_window_ms)
             return set_err(L1RXG_EINVAL, "channel C/N0 window length out of range");
@@ -569,7 +573,9 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     t->T = pick_T(d->taps.n_taps);
     t->nt = pick_threads(n, nullptr);
     t->R = d->ring_samples;
-    t->apron = n + 64;
+    // apron >= one epoch (+ bulk-copy slack); R + apron even keeps every
+    // stream's ring 16-byte aligned for the TMA copies
+    t->apron = n + 64 + ((t->R + n) & 1);
     t->streams.resize(static_cast<size_t>(d->n_streams));
     auto fail = [&](cudaError_t e) {
         l1rxg_tracker_destroy(t);
