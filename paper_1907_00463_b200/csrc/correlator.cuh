@@ -1,0 +1,840 @@
+// correlator.cuh -- K2 correlator + K3 loop update, sm_100a device code.
+//
+// Hot path (reference: /root/reference/proj/include/l1rx/tracking.hpp):
+//   K2 correlate  tracking.hpp:226-282  carrier wipe + K-tap code replica MAC
+//   K3 loop       tracking.hpp:520-618 (+ :459-515) DLL/PLL/FLL + metrics
+//
+// Correlator algorithm ("boundary-prefix").  The replica of
+// tap k is a +/-1 staircase whose steps sit where the reference's fp64 chip
+// index trunc(fl(fma(i, cps, base) + d_k)) changes.  For the wiped samples
+// y_i the tap sum over a run [i0, i1] of consecutive samples is
+//     sum_i chip_k(i) y_i = chip_k(i1) * P(i1+1) - sum_b (chip_after - chip_before) * P(b)
+// with P(b) the run-local exclusive prefix sum and b the steps inside the
+// run.  Phase A (per thread: a run of RUN samples) wipes the carrier,
+// stores the prefix sums in place in shared memory and adds each tap's
+// chip(end) * total term.  Phase B (flattened over the code's chip
+// TRANSITIONS, about 512 per code period, so every thread does the same
+// amount of work) locates each step exactly -- fp64 estimate, then the
+// reference expression evaluated at the candidate sample and its
+// neighbour (it is monotone in the sample index) -- and subtracts
+// delta * P(b).  Every chip decision is therefore the reference's, bit for
+// bit, while the per-sample cost no longer grows with the number of taps.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "l1rxg.h"
+
+namespace l1rxg {
+
+constexpr int RUN = 31;     // samples per thread run; odd -> LDS.64 conflict-free
+constexpr int MAX_NT = 640; // correlator CTA size cap (<= 102 registers)
+constexpr double PI_D = 3.14159265358979323846;  // constants.hpp:20
+constexpr double TWO_PI_D = 2.0 * PI_D;
+constexpr double F_L1_HZ = 1.57542e9;      // constants.hpp:5
+constexpr double CHIP_RATE_HZ = 1.023e6;   // constants.hpp:6
+constexpr int CHIP_EXT = 4096;             // chip index domain of one epoch
+constexpr int TRANS_EXT = 4096;            // transition table domain (>= 4 periods)
+
+// ---------------------------------------------------------------------
+// per-epoch NCO constants (tracking.hpp:234-239)
+struct EpochConsts {
+    double w;        // 2*pi*fD/fs   rad/sample
+    double cps;      // code_freq/fs chips/sample
+    double inv_cps;  // boundary estimate only (verified exactly)
+    double base;     // code_phase + 1023
+    double phi;      // carrier phase at epoch start
+    int n, nh;
+};
+
+__device__ __forceinline__ void make_consts(EpochConsts& c, double code_phase,
+                                            double code_freq, double doppler,
+                                            double phase, double fs, int n) {
+    c.w = 2.0 * PI_D * doppler / fs;  // (2*pi*fD)/fs as the reference orders it
+    c.cps = code_freq / fs;
+    c.inv_cps = (double)__frcp_rn((float)c.cps);
+    c.base = code_phase + 1023.0;
+    c.phi = phase;
+    c.n = n;
+    c.nh = n / 2;
+}
+
+// The reference's replica phase of tap d at sample i (tracking.hpp:251-254
+// as compiled: ph = fma(i, cps, base), then ph + d rounded).
+__device__ __forceinline__ double tap_value(double i, double cps, double base, double d) {
+    return __dadd_rn(__fma_rn(i, cps, base), d);
+}
+__device__ __forceinline__ int tap_index(int i, double cps, double base, double d) {
+    return __double2int_rz(tap_value((double)i, cps, base, d));
+}
+// First b in [lo, hi] with tap_value(b) >= m, given that one exists
+// (tap_index(hi) >= m).  The estimate ceil((m - d - base)/cps) is within one
+// sample of the answer (its error, < 1e-2 samples, and the reference's
+// rounding, < 1e-11 samples, are far below one sample), so checking the
+// estimate and its left neighbour with the reference expression pins the
+// exact boundary: tap_value is monotone in the sample index.
+__device__ __forceinline__ int tap_boundary(int m, double d, const EpochConsts& c, int lo, int hi) {
+    const double mm = (double)m;
+    int b = __double2int_ru(((mm - d) - c.base) * c.inv_cps);
+    b = max(lo, min(hi, b));
+    const bool dn = (b > lo) && (tap_value((double)(b - 1), c.cps, c.base, d) >= mm);
+    const bool up = !dn && (b < hi) && (tap_value((double)b, c.cps, c.base, d) < mm);
+    return b - (int)dn + (int)up;
+}
+
+// x * conj(e^{j a}) with (c, s) = (cos a, sin a): (xr c + xi s, xi c - xr s),
+// the reference's wipe-off form (tracking.hpp:248-249).
+__device__ __forceinline__ float2 wipe(float2 x, float c, float s) {
+    return make_float2(fmaf(x.x, c, x.y * s), fmaf(x.y, c, -(x.x * s)));
+}
+
+// ---------------------------------------------------------------------
+// Per-PRN chip tables (built once per CTA).
+//   chipf[m]  = chips[m mod 1023] as +/-1.0f            (m < CHIP_EXT)
+//   tm[g]     = chip index of the g-th chip transition  (g < TRANS_EXT)
+//   td[g]     = chips[tm] - chips[tm - 1] in {-2, +2}
+//   cum[r]    = number of transitions at indices <= r within one period
+// A transition at index m means chips[m mod 1023] != chips[(m-1) mod 1023].
+// F(m) = (m / 1023) * L + cum[m mod 1023] counts the transitions in [0, m].
+struct CodeTables {
+    float chipf[CHIP_EXT];
+    int16_t tm[TRANS_EXT];
+    float td[TRANS_EXT];
+    int16_t cum[1024];
+    int L;
+};
+
+__device__ __forceinline__ int trans_count(const CodeTables& ct, int m) {
+    const int p = m / 1023;
+    return p * ct.L + ct.cum[m - p * 1023];
+}
+
+// Builds the tables for one PRN; all threads participate (ends with a barrier).
+__device__ void build_code_tables(CodeTables& ct, const int8_t* codes, int prn) {
+    const int8_t* c = codes + prn * 1023;
+    for (int k = threadIdx.x; k < CHIP_EXT; k += blockDim.x)
+        ct.chipf[k] = (float)c[k % 1023];
+    if (threadIdx.x < 32) {  // one warp: ballot-scan of the transitions
+        const int lane = threadIdx.x;
+        int running = 0;
+        for (int base = 0; base < 1023; base += 32) {
+            const int r = base + lane;
+            const bool t = r < 1023 && c[r] != c[(r + 1022) % 1023];
+            const unsigned mask = __ballot_sync(0xffffffffu, t);
+            const int before = __popc(mask & ((1u << lane) - 1u));
+            if (r < 1023) {
+                if (t)
+                    ct.tm[running + before] = (int16_t)r;
+                ct.cum[r] = (int16_t)(running + before + (t ? 1 : 0));
+            }
+            running += __popc(mask);
+        }
+        if (lane == 0)
+            ct.L = running;
+    }
+    __syncthreads();
+    const int L = ct.L;
+    // extend tm/td over TRANS_EXT (entries >= L derive from the first period)
+    for (int g = threadIdx.x; g < TRANS_EXT; g += blockDim.x) {
+        const int p = g / L, q = g - p * L;
+        const int r = ct.tm[q];  // q < L: first-period entries are final
+        const int m = p * 1023 + r;
+        const float dlt = (float)c[r] - (float)c[(r + 1022) % 1023];
+        if (g >= L)
+            ct.tm[g] = (int16_t)(m < 32767 ? m : 32767);
+        ct.td[g] = dlt;
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------
+// Phase A: one thread's run of samples [i0, i0+cnt) at run[0..RUN).
+// Overwrites run[j] with the exclusive prefix of the wiped (but not yet
+// anchored) samples, stores the run's carrier anchor e^{-j theta(i0)}, and
+// accumulates chip_k(last) * anchor * total into acc[2k..2k+1] for every
+// tap, plus the first-half prompt into acc[2T..2T+1].
+template <int T, bool FULL>
+__device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
+                                        const float2* __restrict__ rot,
+                                        const float* __restrict__ chipf,
+                                        const double* __restrict__ d, int kp, int i0, int cnt,
+                                        float* acc, float2* anchor_slot) {
+    // theta(i0) exactly as the reference computes it (fma(w, i, phi)),
+    // reduced to [-pi, pi] in fp64; the fp32 phasor's ~4e-7 error is common
+    // to the run's samples
+    const double th = __fma_rn(c.w, (double)i0, c.phi);
+    const double r = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
+    float sa, ca;
+    __sincosf((float)r, &sa, &ca);
+    *anchor_slot = make_float2(ca, sa);
+
+    float pr = 0.f, pi = 0.f;
+#pragma unroll
+    for (int j = 0; j < RUN; ++j) {
+        const float2 x = (FULL || j < cnt) ? run[j] : make_float2(0.f, 0.f);
+        const float2 q = rot[j];
+        const float2 z = wipe(x, q.x, q.y);
+        run[j] = make_float2(pr, pi);
+        pr += z.x;
+        pi += z.y;
+    }
+    const int i_last = i0 + (FULL ? RUN : cnt) - 1;
+    const double dl = (double)i_last;
+    const float zr = fmaf(pr, ca, pi * sa);  // anchored run total
+    const float zi = fmaf(pi, ca, -(pr * sa));
+    float chip_p = 0.f;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const float ch = chipf[__double2int_rz(tap_value(dl, c.cps, c.base, d[k]))];
+        acc[2 * k] = fmaf(ch, zr, acc[2 * k]);
+        acc[2 * k + 1] = fmaf(ch, zi, acc[2 * k + 1]);
+        if (k == kp)
+            chip_p = ch;
+    }
+    // first-half prompt (tracking.hpp:265-271)
+    if (i_last < c.nh) {
+        acc[2 * T] = fmaf(chip_p, zr, acc[2 * T]);
+        acc[2 * T + 1] = fmaf(chip_p, zi, acc[2 * T + 1]);
+    } else if (i0 < c.nh) {  // the run straddling n/2: chip(nh-1) * P(nh)
+        const float ch = chipf[tap_index(c.nh - 1, c.cps, c.base, d[kp])];
+        const float2 pn = run[c.nh - i0];
+        acc[2 * T] = fmaf(ch, fmaf(pn.x, ca, pn.y * sa), acc[2 * T]);
+        acc[2 * T + 1] = fmaf(ch, fmaf(pn.y, ca, -(pn.x * sa)), acc[2 * T + 1]);
+    }
+}
+
+template <int T>
+__device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* run,
+                                                 const float2* rot, const float* chipf,
+                                                 const double* d, int kp, int i0, int cnt,
+                                                 float* acc, float2* anchor_slot) {
+    if (cnt == RUN)
+        phase_a<T, true>(c, run, rot, chipf, d, kp, i0, cnt, acc, anchor_slot);
+    else
+        phase_a<T, false>(c, run, rot, chipf, d, kp, i0, cnt, acc, anchor_slot);
+}
+
+// Phase B: every chip transition of every tap whose step falls in the
+// sub-tile [u0, u0+len): acc_k -= delta * anchor(run(b)) * P(b).
+// tile_d[i - u0] holds P(i) (phase A's in-place prefixes).
+template <int T>
+__device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile_d,
+                                        const float2* anchors, const CodeTables& ct,
+                                        const double* d, int kp, int u0, int len, float* acc) {
+    const int hi = u0 + len - 1;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const double dk = d[k];
+        const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, dk);
+        const int mhi = tap_index(hi, c.cps, c.base, dk);
+        const int g0 = trans_count(ct, mlo);
+        const int cntk = trans_count(ct, mhi) - g0;
+        // rotate the starting thread per tap so the remainders spread out
+        int j = (int)threadIdx.x - (k * 197) % (int)blockDim.x;
+        if (j < 0)
+            j += blockDim.x;
+        for (; j < cntk; j += blockDim.x) {
+            const int g = g0 + j;
+            const int m = ct.tm[g];
+            const float dlt = ct.td[g];
+            const int b = tap_boundary(m, dk, c, u0, hi);
+            const int off = b - u0;
+            const float2 p = tile_d[off];
+            const float2 an = anchors[off / RUN];
+            const float ar = fmaf(p.x, an.x, p.y * an.y);
+            const float ai = fmaf(p.y, an.x, -(p.x * an.y));
+            acc[2 * k] = fmaf(-dlt, ar, acc[2 * k]);
+            acc[2 * k + 1] = fmaf(-dlt, ai, acc[2 * k + 1]);
+            if (k == kp && b < c.nh) {
+                acc[2 * T] = fmaf(-dlt, ar, acc[2 * T]);
+                acc[2 * T + 1] = fmaf(-dlt, ai, acc[2 * T + 1]);
+            }
+        }
+    }
+}
+
+// Per-epoch rotator table rot[j] = (cos wj, sin wj), j < RUN (accurate).
+__device__ __forceinline__ void fill_rot(float2* rot, double w, int tid) {
+    if (tid < RUN) {
+        float s, co;
+        sincosf((float)(w * (double)tid), &s, &co);
+        rot[tid] = make_float2(co, s);
+    }
+}
+
+// ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared on the TMA engine, completion on bar.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------------
+// K3: loop update (tracking.hpp:542-601 + :459-515).
+struct LoopCfg {
+    l1rxg_tracking_cfg cfg;
+    int kernel;
+    double fs;
+    // host-precomputed, same operation order as the reference
+    double dt;                  // n / fs                     (:542)
+    double pll_k1, pll_k2;      // ((wn*wn)*dt)*0.5, (2*zeta)*wn  (:71-84)
+    double dll_k1, dll_k2;
+    double fll_k;               // ((4*B_fll)*2)*pi            (:88-92)
+    double alpha;               // 1 / cn0_window_ms           (:466)
+};
+
+__device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, double cq,
+                                           double dt, bool fold) {  // tracking.hpp:113-138
+    double cross = pi_ * cq - pq * ci;
+    double dot = pi_ * ci + pq * cq;
+    if (fold && dot < 0) {
+        cross = -cross;
+        dot = -dot;
+    }
+    if (cross == 0.0 && dot == 0.0)
+        return 0.0;
+    return atan2(cross, dot) / (2.0 * PI_D * dt);
+}
+
+// NCO advance over n samples (tracking.hpp:275-280, fma as compiled)
+__device__ __forceinline__ void advance_nco(double& code_phase, double& carrier_phase,
+                                            double& chi, const EpochConsts& c) {
+    carrier_phase = fmod(__fma_rn(c.w, (double)c.n, carrier_phase), 2.0 * PI_D);
+    const double adv = __dmul_rn((double)c.n, c.cps);
+    code_phase = fmod(__dadd_rn(code_phase, adv), 1023.0);
+    chi = __dadd_rn(chi, adv);
+}
+
+// The transcendental pieces of one update and the fmod-based NCO advance
+// are independent of each other: the tracking kernel evaluates them in
+// separate WARPS (divergent lanes of one warp would serialise), then one
+// thread applies the reference's sequential logic (loop_update).
+struct LoopPre {
+    double e, l;        // |E|, |L|            (tracking.hpp:96-97, 545-546)
+    double pll;         // Costas atan         (:104-111)
+    double fc, ff;      // FLL coarse / fine   (:113-138)
+    double mu_s, cn0;   // C/N0 window result  (:472-498), if the window closes
+    double code_phase, carrier_phase, chi;  // NCO advance (:275-280)
+};
+constexpr int LOOP_PIECES = 6;
+
+__device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_channel& ch,
+                                           const l1rxg_corr& o, const LoopCfg& lc,
+                                           const EpochConsts& c) {
+    if (piece == 0) {
+        p.e = sqrt(o.ie * o.ie + o.qe * o.qe);
+        p.l = sqrt(o.il * o.il + o.ql * o.ql);
+    } else if (piece == 1) {
+        if (o.ip == 0.0)
+            p.pll = (o.qp == 0.0) ? 0.0 : (o.qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
+        else
+            p.pll = atan(o.qp / o.ip);
+    } else if (piece == 2) {
+        p.fc = fll_disc(o.ip_h1, o.qp_h1, o.ip_h2, o.qp_h2, lc.dt / 2.0, false);
+    } else if (piece == 3) {
+        p.ff = fll_disc(ch.last_ip, ch.last_qp, o.ip, o.qp, lc.dt, true);
+    } else if (piece == 4) {
+        const int m = lc.cfg.cn0_window_ms;
+        p.mu_s = ch.mu_smoothed;
+        p.cn0 = ch.cn0_dbhz;
+        if (ch.win_len + 1 >= m) {
+            double nbi = 0, nbq = 0, wbp = 0;
+            for (int k = 0; k < m; ++k) {
+                const double wi = k < ch.win_len ? ch.win_ip[k] : o.ip;
+                const double wq = k < ch.win_len ? ch.win_qp[k] : o.qp;
+                const double sg = wi >= 0 ? 1.0 : -1.0;
+                nbi += sg * wi;
+                nbq += sg * wq;
+                wbp += wi * wi + wq * wq;
+            }
+            const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
+            p.mu_s = ch.metrics_valid ? ch.mu_smoothed + 0.2 * (mu - ch.mu_smoothed) : mu;
+            const double md = (double)m;
+            if (p.mu_s >= md - 1e-9)
+                p.cn0 = 65.0;
+            else if (p.mu_s <= 1.0)
+                p.cn0 = 0.0;
+            else
+                p.cn0 = 10.0 * log10((p.mu_s - 1.0) / (md - p.mu_s) / 1e-3);
+        }
+    } else {
+        double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
+        advance_nco(cp, ph, chi, c);
+        p.code_phase = cp;
+        p.carrier_phase = ph;
+        p.chi = chi;
+    }
+}
+
+// Sequential part of track_epoch on one thread; the channel's scalars are
+// pulled into registers first (independent shared-memory loads) and written
+// back once.  ch must already hold the advanced NCO (code/carrier/chi).
+__device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc,
+                            const LoopPre& p) {
+    const l1rxg_tracking_cfg& cfg = lc.cfg;
+    const bool noop = lc.kernel == L1RXG_KERNEL_NOOP;
+    int state = ch.state, lfc = ch.lock_fail_count, mvalid = ch.metrics_valid;
+    int win_len = ch.win_len;
+    const int64_t esh = ch.epochs_since_handoff;
+    double clr_s = ch.carrier_lock_ratio;
+    double pll_i = ch.pll_integrator, pll_p = ch.pll_prev_error;
+    double dll_i = ch.dll_integrator, dll_p = ch.dll_prev_error;
+    const int pll_pr = ch.pll_primed, dll_pr = ch.dll_primed;
+    const int have_last = ch.have_last_prompt;
+    const double dt = lc.dt;
+
+    const double e = p.e, l = p.l;
+    const double dll_err = (e + l == 0.0) ? 0.0 : 0.5 * (e - l) / (e + l);  // :95-101
+    if (e + l == 0.0 && !noop)  // :545-549
+        lfc++;
+    if (ch.fll_enabled && esh < (int64_t)cfg.fll_pull_in_ms && clr_s < 0.8 && !noop) {  // :561-576
+        if (esh < (int64_t)cfg.fll_coarse_ms)
+            pll_i = __fma_rn(lc.fll_k * p.fc, dt, pll_i);
+        else if (have_last)
+            pll_i = __fma_rn(lc.fll_k * p.ff, dt, pll_i);
+    }
+    // loop_filter_update (:75-84), PLL then DLL
+    pll_i = __fma_rn(lc.pll_k1, p.pll + (pll_pr ? pll_p : p.pll), pll_i);
+    const double doppler_cmd = __fma_rn(lc.pll_k2, p.pll, pll_i) / (2.0 * PI_D);
+    dll_i = __fma_rn(lc.dll_k1, dll_err + (dll_pr ? dll_p : dll_err), dll_i);
+    const double dll_cmd = __fma_rn(lc.dll_k2, dll_err, dll_i);
+    const double cf = __fma_rn(CHIP_RATE_HZ, 1.0 + doppler_cmd / F_L1_HZ, dll_cmd);  // :142-147
+    if (state == L1RXG_ACQUIRED)
+        state = L1RXG_TRACKING;
+
+    // update_quality_metrics (:459-515)
+    const double pwr = o.ip * o.ip + o.qp * o.qp;
+    const double clr = pwr > 0 ? (o.ip * o.ip - o.qp * o.qp) / pwr : 0.0;
+    clr_s += lc.alpha * (clr - clr_s);
+    ch.win_ip[win_len] = o.ip;
+    ch.win_qp[win_len] = o.qp;
+    win_len++;
+    double cn0 = ch.cn0_dbhz, mu_s = ch.mu_smoothed;
+    if (win_len >= cfg.cn0_window_ms) {  // window sums + C/N0 map: piece 4
+        win_len = 0;
+        mu_s = p.mu_s;
+        cn0 = p.cn0;
+        mvalid = 1;
+    }
+    if (mvalid && esh > cfg.fll_pull_in_ms + cfg.cn0_window_ms) {
+        if (cn0 < cfg.cn0_drop_dbhz || clr_s < cfg.carrier_lock_drop)
+            lfc++;
+        else
+            lfc = 0;
+    }
+    if (lfc > cfg.lock_fail_limit)
+        state = L1RXG_IDLE;
+
+    ch.state = state;
+    ch.lock_fail_count = lfc;
+    ch.metrics_valid = mvalid;
+    ch.win_len = win_len;
+    ch.carrier_lock_ratio = clr_s;
+    ch.pll_integrator = pll_i;
+    ch.pll_prev_error = p.pll;
+    ch.pll_primed = 1;
+    ch.dll_integrator = dll_i;
+    ch.dll_prev_error = dll_err;
+    ch.dll_primed = 1;
+    ch.carrier_doppler_hz = doppler_cmd;
+    ch.code_freq_hz = cf;
+    ch.last_ip = o.ip;
+    ch.last_qp = o.qp;
+    ch.have_last_prompt = 1;
+    ch.cn0_dbhz = cn0;
+    ch.mu_smoothed = mu_s;
+    ch.epoch_ms_count += 1;
+    ch.epochs_since_handoff = esh + 1;
+    ch.sample_offset_next_epoch += o.n_samples;
+}
+
+// ---------------------------------------------------------------------
+// Shared-memory layout of a correlator CTA (the sample tile follows it).
+template <int T>
+struct CorrSmem {
+    l1rxg_channel ch;
+    EpochConsts c;
+    LoopPre pre;
+    double d[T];
+    double sums[2 * T + 2];
+    float red[32 * (2 * T + 2)];
+    float2 rot[RUN + 1];
+    float2 anchors[MAX_NT];
+    uint64_t bars[2];
+    int64_t unit_pos;  // TMA unit in flight: ring position (aligned), slack
+    int unit_delta, unit_h, unit_len, inflight;
+    CodeTables ct;
+};
+
+template <int T>
+__host__ __device__ constexpr size_t corr_smem_header() {
+    return (sizeof(CorrSmem<T>) + 15) & ~size_t(15);
+}
+
+template <int T>
+__device__ __forceinline__ float2* tile_of(CorrSmem<T>* s) {
+    return reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + corr_smem_header<T>());
+}
+
+// o (CorrelatorOutputs) from the fp64 sums
+template <int T>
+__device__ __forceinline__ l1rxg_corr corr_from_sums(const double* sums, int ke, int kp, int kl, int n) {
+    l1rxg_corr o;
+    o.ie = sums[2 * ke];
+    o.qe = sums[2 * ke + 1];
+    o.ip = sums[2 * kp];
+    o.qp = sums[2 * kp + 1];
+    o.il = sums[2 * kl];
+    o.ql = sums[2 * kl + 1];
+    o.ip_h1 = sums[2 * T];
+    o.qp_h1 = sums[2 * T + 1];
+    o.ip_h2 = o.ip - o.ip_h1;
+    o.qp_h2 = o.qp - o.qp_h1;
+    o.n_samples = n;
+    o.pad_ = 0;
+    return o;
+}
+
+// warp shuffles of the V partials -> red[warp][v]
+template <int V>
+__device__ __forceinline__ void warp_partials(const float* acc, float* red, int lane, int warp) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        float x = acc[v];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0)
+            red[warp * V + v] = x;
+    }
+}
+
+// fp64 cross-warp totals (by warp 0)
+template <int V>
+__device__ __forceinline__ void warp0_totals(const float* red, double* sums, int lane, int nwarps) {
+    for (int v = lane; v < V; v += 32) {
+        double sm = 0.0;
+        for (int w = 0; w < nwarps; ++w)
+            sm += (double)red[w * V + v];
+        sums[v] = sm;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Kernel arguments for closed-loop tracking.
+struct TrackArgs {
+    const float2* ring;       // [n_streams][ring_stride]
+    int64_t ring_stride;      // R + apron
+    int64_t ring_cap;         // R
+    const int64_t* avail;     // [n_streams] samples ingested
+    l1rxg_channel* chans;     // [C]
+    const int32_t* chan_stream;
+    l1rxg_epoch_record* recs; // [C][max_records]
+    double* tap_sums;         // [C][max_records][2T]
+    int64_t* ecount;          // [C] epochs done
+    int32_t* status;          // [C] 0 ok, 1 ring overrun
+    const int8_t* codes;      // [33][1023]
+    int max_records;
+    int max_epochs;
+    int n;
+    int kp, ke, kl;
+    l1rxg_taps taps;
+    LoopCfg lc;
+};
+
+// TMA unit: samples [abs_first, abs_first + len) of the ring into the tile,
+// copied from the 16-byte aligned position below (delta samples of slack),
+// in two halves on two mbarriers.
+template <int T>
+__device__ __forceinline__ void issue_unit(CorrSmem<T>* s, float2* tile, const float2* ring,
+                                           int64_t abs_first, int len, int64_t R) {
+    const int64_t pos = abs_first % R;
+    const int delta = (int)(pos & 1);
+    const int h = 2 * ((len + delta) / 4);
+    s->unit_pos = pos - delta;
+    s->unit_delta = delta;
+    s->unit_h = h;
+    s->unit_len = len;
+    const uint32_t total = (uint32_t)(((len + delta) * 8 + 15) & ~15);
+    const uint32_t b0 = (uint32_t)h * 8u;
+    mbar_expect_tx(&s->bars[0], b0);
+    tma_load_1d(tile, ring + (pos - delta), b0, &s->bars[0]);
+    mbar_expect_tx(&s->bars[1], total - b0);
+    tma_load_1d(tile + h, ring + (pos - delta) + h, total - b0, &s->bars[1]);
+    s->inflight = 1;
+}
+
+// Channel-resident persistent tracking kernel: one CTA per channel loops
+// over its epochs with no host round trip (replaces the per-channel
+// track_epoch fan-out of Receiver::tracking_round, pipeline.hpp:563-610).
+// The epoch window arrives by TMA; the copy of the next window is issued as
+// soon as the current one has been consumed, overlapping the reduction and
+// the loop update.
+template <int T>
+__global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
+    float2* tile = tile_of(s);
+    const int cidx = blockIdx.x;
+    const int strm = a.chan_stream[cidx];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    constexpr int V = 2 * T + 2;
+    const int cap = blockDim.x * RUN;
+    const int n = a.n;
+    const int nsub = (n + cap - 1) / cap;
+    const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
+    const int64_t avail = a.avail[strm];
+    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
+    if (tid == 0) {
+        s->ch = a.chans[cidx];
+        mbar_init(&s->bars[0], 1);
+        mbar_init(&s->bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s->inflight = 0;
+    }
+    for (int k = tid; k < T; k += blockDim.x)
+        s->d[k] = a.taps.offsets_chips[k];
+    __syncthreads();
+    build_code_tables(s->ct, a.codes, s->ch.prn);
+    if (tid == 0) {  // first epoch: consts and the first tile load
+        const l1rxg_channel& ch = s->ch;
+        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                    ch.carrier_phase_rad, a.lc.fs, n);
+        const int64_t off = ch.sample_offset_next_epoch;
+        if (!noop && ch.state != L1RXG_IDLE && a.max_epochs > 0 && off + n <= avail && off >= 0 &&
+            off >= avail - a.ring_cap)
+            issue_unit(s, tile, ring, off, min(cap, n), a.ring_cap);
+    }
+    __syncthreads();
+    fill_rot(s->rot, s->c.w, tid);
+    __syncthreads();
+
+    uint32_t phase = 0;
+    int64_t e = 0;
+    int64_t done = a.ecount[cidx];
+    for (;;) {
+        // epoch admission (uniform: every thread reads the same smem state)
+        const int64_t off = s->ch.sample_offset_next_epoch;
+        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
+            break;
+        if (off < avail - a.ring_cap || off < 0) {  // window already overwritten
+            if (tid == 0)
+                a.status[cidx] = 1;
+            break;
+        }
+        const EpochConsts c = s->c;
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[v] = 0.f;
+        for (int q = 0; q < nsub; ++q) {
+            const int u0 = q * cap;
+            const int len = min(cap, n - u0);
+            if (!noop) {
+                const int delta = s->unit_delta, h = s->unit_h;
+                const float2* tile_d = tile + delta;
+                const int i0 = u0 + tid * RUN;
+                const int cnt = min(RUN, n - i0);
+                const int r0 = delta + tid * RUN;
+                if (cnt > 0) {
+                    if (r0 < h)
+                        mbar_wait(&s->bars[0], phase);
+                    if (r0 + RUN > h)
+                        mbar_wait(&s->bars[1], phase);
+                    phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt, acc,
+                                        &s->anchors[tid]);
+                }
+                if (tid == 0) {  // every phase completes before the next issue
+                    mbar_wait(&s->bars[0], phase);
+                    mbar_wait(&s->bars[1], phase);
+                }
+                phase ^= 1u;
+                __syncthreads();  // prefixes + anchors visible
+                phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc);
+            }
+            if (q + 1 == nsub)
+                warp_partials<V>(acc, s->red, lane, warp);
+            __syncthreads();  // tile consumed
+            if (tid == 0) {
+                s->inflight = 0;
+                if (!noop) {
+                    if (q + 1 < nsub)
+                        issue_unit(s, tile, ring, off + (q + 1) * cap, min(cap, n - (q + 1) * cap),
+                                   a.ring_cap);
+                    else if (s->ch.state != L1RXG_IDLE && e + 1 < a.max_epochs &&
+                             off + 2 * (int64_t)n <= avail)
+                        issue_unit(s, tile, ring, off + n, min(cap, n), a.ring_cap);  // prefetch
+                }
+            }
+            if (q + 1 < nsub)
+                __syncthreads();  // publish the next unit
+        }
+        // ---- loop update: warps 0..PW-1 split the independent pieces,
+        // then warp 0 / lane 0 applies the sequential logic
+        const int PW = min(nwarps, LOOP_PIECES);
+        if (warp < PW) {
+            if (warp == 0)
+                warp0_totals<V>(s->red, s->sums, lane, nwarps);
+            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
+            const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, c.n);
+            if (lane == 0)
+                for (int piece = warp; piece < LOOP_PIECES; piece += PW)
+                    loop_piece(piece, s->pre, s->ch, o, a.lc, c);
+            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
+            if (warp == 0) {
+                const int64_t slot = (int64_t)cidx * a.max_records + (done % a.max_records);
+                if (a.tap_sums && lane < 2 * T)
+                    a.tap_sums[slot * (2 * T) + lane] = s->sums[lane];
+                if (lane == 0) {
+                    l1rxg_channel& ch = s->ch;
+                    const LoopPre pre = s->pre;
+                    l1rxg_epoch_record r;
+                    r.sample_offset_start = off;
+                    r.code_phase_in = ch.code_phase_chips;
+                    r.code_freq_in = ch.code_freq_hz;
+                    r.carrier_doppler_in = ch.carrier_doppler_hz;
+                    r.carrier_phase_in = ch.carrier_phase_rad;
+                    ch.code_phase_chips = pre.code_phase;
+                    ch.carrier_phase_rad = pre.carrier_phase;
+                    ch.chi_chips = pre.chi;
+                    loop_update(ch, o, a.lc, pre);
+                    // next epoch's NCO constants, then the record
+                    make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                                ch.carrier_phase_rad, a.lc.fs, n);
+                    r.epoch_index = ch.epoch_ms_count - 1;
+                    r.sample_offset_end = ch.sample_offset_next_epoch;
+                    r.prn = ch.prn;
+                    r.state = ch.state;
+                    r.n_samples = c.n;
+                    r.lock_fail_count = ch.lock_fail_count;
+                    r.ie = o.ie; r.qe = o.qe; r.ip = o.ip; r.qp = o.qp; r.il = o.il; r.ql = o.ql;
+                    r.ip_h1 = o.ip_h1; r.qp_h1 = o.qp_h1; r.ip_h2 = o.ip_h2; r.qp_h2 = o.qp_h2;
+                    r.carrier_doppler_hz = ch.carrier_doppler_hz;
+                    r.code_freq_hz = ch.code_freq_hz;
+                    r.code_phase_chips = ch.code_phase_chips;
+                    r.carrier_phase_rad = ch.carrier_phase_rad;
+                    r.chi_chips = ch.chi_chips;
+                    r.cn0_dbhz = ch.cn0_dbhz;
+                    r.carrier_lock_ratio = ch.carrier_lock_ratio;
+                    r.dll_integrator = ch.dll_integrator;
+                    r.pll_integrator = ch.pll_integrator;
+                    r.mu_smoothed = ch.mu_smoothed;
+                    r.dll_prev_error = ch.dll_prev_error;
+                    r.pll_prev_error = ch.pll_prev_error;
+                    a.recs[slot] = r;
+                }
+                __syncwarp();
+                fill_rot(s->rot, s->c.w, lane);
+            }
+        }
+        ++e;
+        ++done;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (s->inflight) {  // never leave a bulk copy in flight into freed smem
+            mbar_wait(&s->bars[0], phase);
+            mbar_wait(&s->bars[1], phase);
+        }
+        a.chans[cidx] = s->ch;
+        a.ecount[cidx] = done;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Open-loop batch (per-call compatibility path and replay tests): job j
+// correlates samples src + j*n with NCO states[j], advances it in place.
+struct JobArgs {
+    const float2* samples;  // [n_jobs][n]
+    l1rxg_nco* states;      // [n_jobs]
+    const int32_t* prns;    // [n_jobs]
+    const int8_t* codes;
+    double* tap_sums;       // [n_jobs][2T]
+    l1rxg_corr* corr;       // [n_jobs]
+    int n, kp, ke, kl, kernel;
+    double fs;
+    l1rxg_taps taps;
+};
+
+template <int T>
+__global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
+    float2* tile = tile_of(s);
+    const int j = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    constexpr int V = 2 * T + 2;
+    const int n = a.n;
+    const int cap = blockDim.x * RUN;
+    for (int k = tid; k < T; k += blockDim.x)
+        s->d[k] = a.taps.offsets_chips[k];
+    if (tid == 0) {
+        const l1rxg_nco st = a.states[j];
+        make_consts(s->c, st.code_phase_chips, st.code_freq_hz, st.carrier_doppler_hz,
+                    st.carrier_phase_rad, a.fs, n);
+    }
+    build_code_tables(s->ct, a.codes, a.prns[j]);  // ends with a barrier
+    fill_rot(s->rot, s->c.w, tid);
+    const EpochConsts c = s->c;
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+        acc[v] = 0.f;
+    const float2* src = a.samples + (int64_t)j * n;
+    if (a.kernel != L1RXG_KERNEL_NOOP) {
+        for (int u0 = 0; u0 < n; u0 += cap) {
+            const int len = min(cap, n - u0);
+            for (int i = tid; i < len; i += blockDim.x)
+                tile[i] = __ldg(src + u0 + i);
+            __syncthreads();
+            const int i0 = u0 + tid * RUN;
+            const int cnt = min(RUN, n - i0);
+            if (cnt > 0)
+                phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
+                                    acc, &s->anchors[tid]);
+            __syncthreads();
+            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc);
+            __syncthreads();
+        }
+    }
+    warp_partials<V>(acc, s->red, lane, warp);
+    __syncthreads();
+    if (warp == 0)
+        warp0_totals<V>(s->red, s->sums, lane, nwarps);
+    __syncthreads();
+    if (tid < 2 * T)
+        a.tap_sums[(int64_t)j * 2 * T + tid] = s->sums[tid];
+    if (tid == 0) {
+        l1rxg_nco st = a.states[j];
+        advance_nco(st.code_phase_chips, st.carrier_phase_rad, st.chi_chips, c);
+        a.states[j] = st;
+        a.corr[j] = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, n);
+    }
+}
+
+}  // namespace l1rxg

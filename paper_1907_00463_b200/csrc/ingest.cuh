@@ -1,0 +1,155 @@
+// ingest.cuh -- K1: raw recording bytes -> complex baseband ring (sm_100a).
+//
+// Reference: SampleSource::read_samples / downconvert (samples.hpp:177-253):
+// int8 / int16 complex decode (/128, /32768) and, for Int8RealIF, the
+// complex mixer at -IF on the global sample index followed by the 23-tap
+// half-band FIR (Hamming-windowed sinc, cutoff fs/4, unit DC gain, x2)
+// with a 22-sample history carried across blocks.  One pass per stream
+// sample, shared by every channel that tracks the stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "l1rxg.h"
+
+namespace l1rxg {
+
+// ---------------------------------------------------------------------
+// K1 ingest.  Ring write: sample g -> ring[g mod R] (+ apron copy).
+__device__ __forceinline__ void ring_put(float2* ring, int64_t R, int64_t apron,
+                                         int64_t pos, float2 v) {
+    ring[pos] = v;
+    if (pos < apron)
+        ring[R + pos] = v;
+}
+
+// Int8RealIF at IF = fs/4: the mixer step is exactly -pi/2, so
+// mixed(g) = v(g)/128 * {1, -j, -1, j}[g mod 4]; the FIR output
+// 2*sum_t h[t] mixed(g-t) (samples.hpp:234-240) is a 23-tap real
+// convolution per output phase with coefficient tables cre/cim[4][23]
+// folded on the host (includes the 2/128 scale).
+__constant__ float c_if4_re[4][23];
+__constant__ float c_if4_im[4][23];
+
+constexpr int ING_TPB = 256;
+constexpr int ING_OUT_PER_THREAD = 4;
+constexpr int ING_TILE = ING_TPB * ING_OUT_PER_THREAD;  // outputs per block
+
+// raw: bytes of samples [g0, g0+count); hist: the 22 bytes before g0
+// (zeros at stream start); writes hist_out = the last 22 bytes of the run.
+__global__ void __launch_bounds__(ING_TPB) ingest_if4_kernel(
+    const int8_t* __restrict__ raw, const int8_t* __restrict__ hist, int8_t* hist_out,
+    int64_t g0, int64_t count, float2* ring, int64_t R, int64_t apron, int64_t pos0,
+    int64_t* avail_slot) {
+    __shared__ float v[ING_TILE + 24];
+    const int64_t t0 = (int64_t)blockIdx.x * ING_TILE;  // run-relative first output
+    // inputs t0-22 .. t0+ING_TILE-1
+    for (int k = threadIdx.x; k < ING_TILE + 22; k += ING_TPB) {
+        const int64_t idx = t0 - 22 + k;
+        int8_t b = 0;
+        if (idx < 0)
+            b = hist[22 + idx];
+        else if (idx < count)
+            b = raw[idx];
+        v[k] = (float)b;
+    }
+    __syncthreads();
+    const int q = threadIdx.x * ING_OUT_PER_THREAD;
+#pragma unroll
+    for (int u = 0; u < ING_OUT_PER_THREAD; ++u) {
+        const int64_t idx = t0 + q + u;
+        if (idx >= count)
+            break;
+        const int ph = (int)((g0 + idx) & 3);
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int t = 0; t < 23; ++t) {
+            const float x = v[q + u + 22 - t];
+            re = fmaf(c_if4_re[ph][t], x, re);
+            im = fmaf(c_if4_im[ph][t], x, im);
+        }
+        int64_t pos = pos0 + idx;
+        if (pos >= R)
+            pos -= R;
+        ring_put(ring, R, apron, pos, make_float2(re, im));
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 22) {
+        const int64_t idx = count - 22 + threadIdx.x;
+        hist_out[threadIdx.x] = idx >= 0 ? raw[idx] : hist[22 + idx];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
+        *avail_slot = g0 + count;
+}
+
+// Generic real IF: pass 1, mixer at the global index in fp64
+// (samples.hpp:217-226) into mixed[22 + i]; mixed[0..22) holds history.
+__global__ void mix_generic_kernel(const int8_t* __restrict__ raw, int64_t g0, int64_t count,
+                                   double w, float2* mixed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count)
+        return;
+    const double vv = (double)raw[i] / 128.0;
+    double s, c;
+    sincos(w * (double)(g0 + i), &s, &c);
+    mixed[22 + i] = make_float2((float)(vv * c), (float)(vv * s));
+}
+
+// pass 2: out(g) = 2 sum_t h[t] mixed(g - t)
+__constant__ float c_halfband2[23];
+__global__ void fir_generic_kernel(const float2* __restrict__ mixed, int64_t count, float2* ring,
+                                   int64_t R, int64_t apron, int64_t pos0, float2* hist_out,
+                                   int64_t* avail_slot, int64_t avail_value) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int t = 0; t < 23; ++t) {
+            const float2 m = mixed[22 + i - t];
+            re = fmaf(c_halfband2[t], m.x, re);
+            im = fmaf(c_halfband2[t], m.y, im);
+        }
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        ring_put(ring, R, apron, pos, make_float2(re, im));
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 22)
+        hist_out[threadIdx.x] = mixed[count + threadIdx.x];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
+        *avail_slot = avail_value;
+}
+
+// Complex int8 / int16 decode (samples.hpp:188-205).
+__global__ void decode_iq_kernel(const void* __restrict__ raw, int fmt, int64_t count,
+                                 float2* ring, int64_t R, int64_t apron, int64_t pos0,
+                                 int64_t* avail_slot, int64_t avail_value) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        float2 v;
+        if (fmt == L1RXG_FMT_INT8_IQ) {
+            const char2 b = reinterpret_cast<const char2*>(raw)[i];
+            v = make_float2((float)b.x * (1.0f / 128.0f), (float)b.y * (1.0f / 128.0f));
+        } else {
+            const short2 b = reinterpret_cast<const short2*>(raw)[i];
+            v = make_float2((float)b.x * (1.0f / 32768.0f), (float)b.y * (1.0f / 32768.0f));
+        }
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        ring_put(ring, R, apron, pos, v);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
+        *avail_slot = avail_value;
+}
+
+// complex<double> -> float2 (per-call path)
+__global__ void cf64_to_f32_kernel(const double2* __restrict__ in, float2* out, int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        const double2 x = in[i];
+        out[i] = make_float2((float)x.x, (float)x.y);
+    }
+}
+
+}  // namespace l1rxg

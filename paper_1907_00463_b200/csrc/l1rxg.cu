@@ -16,7 +16,8 @@
 #include <string>
 #include <vector>
 
-#include "kernels.cuh"
+#include "correlator.cuh"
+#include "ingest.cuh"
 #include "l1rxg.h"
 
 using namespace l1rxg;
@@ -124,16 +125,35 @@ int pick_threads(int n, int* subtiles) {
     return nt;
 }
 
+// tile: nt*RUN samples + alignment slack of the 16-byte bulk copies
 template <int T>
 size_t smem_bytes(int nt) {
-    return ((sizeof(CorrSmem<T>) + 15) & ~size_t(15)) + static_cast<size_t>(nt) * RUN * sizeof(float2);
+    return corr_smem_header<T>() + (static_cast<size_t>(nt) * RUN + 4) * sizeof(float2);
+}
+
+// Loop-filter constants precomputed with the reference's operation order
+// (tracking.hpp:71-92, 466, 542).
+LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int n) {
+    LoopCfg lc{};
+    lc.cfg = cfg;
+    lc.kernel = kernel;
+    lc.fs = fs;
+    lc.dt = static_cast<double>(n) / fs;
+    auto wn = [](double bw, double z) { return 8.0 * z * bw / (4.0 * z * z + 1.0); };
+    const double wp = wn(cfg.pll_bandwidth_hz, cfg.pll_damping);
+    const double wd = wn(cfg.dll_bandwidth_hz, cfg.dll_damping);
+    lc.pll_k1 = wp * wp * lc.dt * 0.5;
+    lc.pll_k2 = 2.0 * cfg.pll_damping * wp;
+    lc.dll_k1 = wd * wd * lc.dt * 0.5;
+    lc.dll_k2 = 2.0 * cfg.dll_damping * wd;
+    lc.fll_k = 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D;
+    lc.alpha = 1.0 / static_cast<double>(cfg.cn0_window_ms);
+    return lc;
 }
 
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
-    // tile: nt*RUN samples + alignment slack of the 16-byte bulk copies
-    const size_t sm = ((sizeof(TrackSmem<T>) + 15) & ~size_t(15)) +
-                      (static_cast<size_t>(nt) * RUN + 4) * sizeof(float2);
+    const size_t sm = smem_bytes<T>(nt);
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     track_kernel<T><<<n_ch, nt, sm, s>>>(a);
     CK(cudaGetLastError());
@@ -727,9 +747,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.ke = t->d.taps.early;
     a.kl = t->d.taps.late;
     a.taps = padded_taps(t->d.taps, t->T);
-    a.lc.cfg = t->d.cfg;
-    a.lc.kernel = t->d.kernel;
-    a.lc.fs = t->d.sample_rate_hz;
+    a.lc = make_loop_cfg(t->d.cfg, t->d.kernel, t->d.sample_rate_hz, a.n);
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
