@@ -221,7 +221,8 @@ __device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* r
 template <int T>
 __device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile_d,
                                         const float2* anchors, const CodeTables& ct,
-                                        const double* d, int kp, int u0, int len, float* acc) {
+                                        const double* d, int kp, int u0, int len, float* acc,
+                                        int nthreads) {
     const int hi = u0 + len - 1;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
@@ -231,10 +232,10 @@ __device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile
         const int g0 = trans_count(ct, mlo);
         const int cntk = trans_count(ct, mhi) - g0;
         // rotate the starting thread per tap so the remainders spread out
-        int j = (int)threadIdx.x - (k * 197) % (int)blockDim.x;
-        if (j < 0)
-            j += blockDim.x;
-        for (; j < cntk; j += blockDim.x) {
+        int j = (int)threadIdx.x - ((k * 64) & 511);
+        while (j < 0)
+            j += nthreads;
+        for (; j < cntk; j += nthreads) {
             const int g = g0 + j;
             const int m = ct.tm[g];
             const float dlt = ct.td[g];
@@ -319,12 +320,30 @@ __device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, dou
     return atan2(cross, dot) / (2.0 * PI_D * dt);
 }
 
+// C fmod(x, y) for y > 0 and |x| < 2^40 y, exactly: the remainder
+// x - k*y (k = trunc(x/y)) is representable, so one fma computes it
+// without rounding; the quotient estimate is corrected by +-1 so the result
+// lands in [0, y) for x >= 0 and (-y, 0] for x < 0, as fmod defines.
+__device__ __forceinline__ double fmod_exact(double x, double y, double inv_y) {
+    double k = trunc(x * inv_y);
+    double r = __fma_rn(-k, y, x);
+    if (x >= 0.0) {
+        if (r < 0.0) { k -= 1.0; r = __fma_rn(-k, y, x); }
+        else if (r >= y) { k += 1.0; r = __fma_rn(-k, y, x); }
+    } else {
+        if (r > 0.0) { k += 1.0; r = __fma_rn(-k, y, x); }
+        else if (r <= -y) { k -= 1.0; r = __fma_rn(-k, y, x); }
+    }
+    return r;
+}
+
 // NCO advance over n samples (tracking.hpp:275-280, fma as compiled)
 __device__ __forceinline__ void advance_nco(double& code_phase, double& carrier_phase,
                                             double& chi, const EpochConsts& c) {
-    carrier_phase = fmod(__fma_rn(c.w, (double)c.n, carrier_phase), 2.0 * PI_D);
+    carrier_phase = fmod_exact(__fma_rn(c.w, (double)c.n, carrier_phase), 2.0 * PI_D,
+                               1.0 / (2.0 * PI_D));
     const double adv = __dmul_rn((double)c.n, c.cps);
-    code_phase = fmod(__dadd_rn(code_phase, adv), 1023.0);
+    code_phase = fmod_exact(__dadd_rn(code_phase, adv), 1023.0, 1.0 / 1023.0);
     chi = __dadd_rn(chi, adv);
 }
 
@@ -334,12 +353,12 @@ __device__ __forceinline__ void advance_nco(double& code_phase, double& carrier_
 // thread applies the reference's sequential logic (loop_update).
 struct LoopPre {
     double e, l;        // |E|, |L|            (tracking.hpp:96-97, 545-546)
+    double dll;         // DLL discriminator   (:95-101)
     double pll;         // Costas atan         (:104-111)
     double fc, ff;      // FLL coarse / fine   (:113-138)
-    double mu_s, cn0;   // C/N0 window result  (:472-498), if the window closes
     double code_phase, carrier_phase, chi;  // NCO advance (:275-280)
 };
-constexpr int LOOP_PIECES = 6;
+constexpr int LOOP_PIECES = 5;
 
 __device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_channel& ch,
                                            const l1rxg_corr& o, const LoopCfg& lc,
@@ -347,6 +366,7 @@ __device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_ch
     if (piece == 0) {
         p.e = sqrt(o.ie * o.ie + o.qe * o.qe);
         p.l = sqrt(o.il * o.il + o.ql * o.ql);
+        p.dll = (p.e + p.l == 0.0) ? 0.0 : 0.5 * (p.e - p.l) / (p.e + p.l);  // :95-101
     } else if (piece == 1) {
         if (o.ip == 0.0)
             p.pll = (o.qp == 0.0) ? 0.0 : (o.qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
@@ -356,30 +376,6 @@ __device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_ch
         p.fc = fll_disc(o.ip_h1, o.qp_h1, o.ip_h2, o.qp_h2, lc.dt / 2.0, false);
     } else if (piece == 3) {
         p.ff = fll_disc(ch.last_ip, ch.last_qp, o.ip, o.qp, lc.dt, true);
-    } else if (piece == 4) {
-        const int m = lc.cfg.cn0_window_ms;
-        p.mu_s = ch.mu_smoothed;
-        p.cn0 = ch.cn0_dbhz;
-        if (ch.win_len + 1 >= m) {
-            double nbi = 0, nbq = 0, wbp = 0;
-            for (int k = 0; k < m; ++k) {
-                const double wi = k < ch.win_len ? ch.win_ip[k] : o.ip;
-                const double wq = k < ch.win_len ? ch.win_qp[k] : o.qp;
-                const double sg = wi >= 0 ? 1.0 : -1.0;
-                nbi += sg * wi;
-                nbq += sg * wq;
-                wbp += wi * wi + wq * wq;
-            }
-            const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
-            p.mu_s = ch.metrics_valid ? ch.mu_smoothed + 0.2 * (mu - ch.mu_smoothed) : mu;
-            const double md = (double)m;
-            if (p.mu_s >= md - 1e-9)
-                p.cn0 = 65.0;
-            else if (p.mu_s <= 1.0)
-                p.cn0 = 0.0;
-            else
-                p.cn0 = 10.0 * log10((p.mu_s - 1.0) / (md - p.mu_s) / 1e-3);
-        }
     } else {
         double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
         advance_nco(cp, ph, chi, c);
@@ -389,27 +385,32 @@ __device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_ch
     }
 }
 
-// Sequential part of track_epoch on one thread; the channel's scalars are
-// pulled into registers first (independent shared-memory loads) and written
-// back once.  ch must already hold the advanced NCO (code/carrier/chi).
-__device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc,
-                            const LoopPre& p) {
+// track_epoch is split along its data dependences:
+//  * loop_fast -- everything the NEXT epoch's correlation needs: FLL
+//    assist, PLL/DLL filters, carrier-aided code frequency, NCO advance,
+//    counters (tracking.hpp:552-601).  On the per-epoch critical path.
+//  * loop_metrics -- lock-fail rule, run state, update_quality_metrics
+//    (lock ratio, C/N0 window, drop to Idle; :545-549, 591-592, 459-515).
+//    Nothing in the next correlation depends on it, so the tracking kernel
+//    runs it on a control warp while the next epoch is being correlated.
+// Together they perform the reference's operations in its order; the only
+// cross-dependence (the FLL gate reads the previous epoch's lock ratio) is
+// honoured because loop_metrics(e) completes before loop_fast(e+1).
+// The channel's scalars are pulled into registers (independent shared-
+// memory loads) and written back once.
+__device__ void loop_fast(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc,
+                          const LoopPre& p) {
     const l1rxg_tracking_cfg& cfg = lc.cfg;
     const bool noop = lc.kernel == L1RXG_KERNEL_NOOP;
-    int state = ch.state, lfc = ch.lock_fail_count, mvalid = ch.metrics_valid;
-    int win_len = ch.win_len;
     const int64_t esh = ch.epochs_since_handoff;
-    double clr_s = ch.carrier_lock_ratio;
+    const double clr_s = ch.carrier_lock_ratio;
     double pll_i = ch.pll_integrator, pll_p = ch.pll_prev_error;
     double dll_i = ch.dll_integrator, dll_p = ch.dll_prev_error;
     const int pll_pr = ch.pll_primed, dll_pr = ch.dll_primed;
     const int have_last = ch.have_last_prompt;
     const double dt = lc.dt;
 
-    const double e = p.e, l = p.l;
-    const double dll_err = (e + l == 0.0) ? 0.0 : 0.5 * (e - l) / (e + l);  // :95-101
-    if (e + l == 0.0 && !noop)  // :545-549
-        lfc++;
+    const double dll_err = p.dll;  // :95-101 (piece 0)
     if (ch.fll_enabled && esh < (int64_t)cfg.fll_pull_in_ms && clr_s < 0.8 && !noop) {  // :561-576
         if (esh < (int64_t)cfg.fll_coarse_ms)
             pll_i = __fma_rn(lc.fll_k * p.fc, dt, pll_i);
@@ -418,41 +419,16 @@ __device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCf
     }
     // loop_filter_update (:75-84), PLL then DLL
     pll_i = __fma_rn(lc.pll_k1, p.pll + (pll_pr ? pll_p : p.pll), pll_i);
-    const double doppler_cmd = __fma_rn(lc.pll_k2, p.pll, pll_i) / (2.0 * PI_D);
+    // the two divisions of the reference (/ 2pi, / f_L1) as multiplications
+    // by the reciprocals: a last-bit difference, far inside the 1e-5 bar
+    const double doppler_cmd = __fma_rn(lc.pll_k2, p.pll, pll_i) * (1.0 / (2.0 * PI_D));
     dll_i = __fma_rn(lc.dll_k1, dll_err + (dll_pr ? dll_p : dll_err), dll_i);
     const double dll_cmd = __fma_rn(lc.dll_k2, dll_err, dll_i);
-    const double cf = __fma_rn(CHIP_RATE_HZ, 1.0 + doppler_cmd / F_L1_HZ, dll_cmd);  // :142-147
-    if (state == L1RXG_ACQUIRED)
-        state = L1RXG_TRACKING;
+    const double cf = __fma_rn(CHIP_RATE_HZ, fma(doppler_cmd, 1.0 / F_L1_HZ, 1.0), dll_cmd);  // :142-147
 
-    // update_quality_metrics (:459-515)
-    const double pwr = o.ip * o.ip + o.qp * o.qp;
-    const double clr = pwr > 0 ? (o.ip * o.ip - o.qp * o.qp) / pwr : 0.0;
-    clr_s += lc.alpha * (clr - clr_s);
-    ch.win_ip[win_len] = o.ip;
-    ch.win_qp[win_len] = o.qp;
-    win_len++;
-    double cn0 = ch.cn0_dbhz, mu_s = ch.mu_smoothed;
-    if (win_len >= cfg.cn0_window_ms) {  // window sums + C/N0 map: piece 4
-        win_len = 0;
-        mu_s = p.mu_s;
-        cn0 = p.cn0;
-        mvalid = 1;
-    }
-    if (mvalid && esh > cfg.fll_pull_in_ms + cfg.cn0_window_ms) {
-        if (cn0 < cfg.cn0_drop_dbhz || clr_s < cfg.carrier_lock_drop)
-            lfc++;
-        else
-            lfc = 0;
-    }
-    if (lfc > cfg.lock_fail_limit)
-        state = L1RXG_IDLE;
-
-    ch.state = state;
-    ch.lock_fail_count = lfc;
-    ch.metrics_valid = mvalid;
-    ch.win_len = win_len;
-    ch.carrier_lock_ratio = clr_s;
+    ch.code_phase_chips = p.code_phase;
+    ch.carrier_phase_rad = p.carrier_phase;
+    ch.chi_chips = p.chi;
     ch.pll_integrator = pll_i;
     ch.pll_prev_error = p.pll;
     ch.pll_primed = 1;
@@ -464,11 +440,67 @@ __device__ void loop_update(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCf
     ch.last_ip = o.ip;
     ch.last_qp = o.qp;
     ch.have_last_prompt = 1;
-    ch.cn0_dbhz = cn0;
-    ch.mu_smoothed = mu_s;
     ch.epoch_ms_count += 1;
     ch.epochs_since_handoff = esh + 1;
     ch.sample_offset_next_epoch += o.n_samples;
+}
+
+// esh: epochs_since_handoff as it was before this epoch's increment.
+__device__ void loop_metrics(l1rxg_channel& ch, const l1rxg_corr& o, const LoopCfg& lc,
+                             double e_env, int64_t esh) {
+    const l1rxg_tracking_cfg& cfg = lc.cfg;
+    const bool noop = lc.kernel == L1RXG_KERNEL_NOOP;
+    int state = ch.state, lfc = ch.lock_fail_count, mvalid = ch.metrics_valid;
+    int win_len = ch.win_len;
+    double clr_s = ch.carrier_lock_ratio, cn0 = ch.cn0_dbhz, mu_s = ch.mu_smoothed;
+    if (e_env == 0.0 && !noop)  // :545-549
+        lfc++;
+    if (state == L1RXG_ACQUIRED)  // :591-592
+        state = L1RXG_TRACKING;
+    // update_quality_metrics (:459-515)
+    const double pwr = o.ip * o.ip + o.qp * o.qp;
+    const double clr = pwr > 0 ? (o.ip * o.ip - o.qp * o.qp) / pwr : 0.0;
+    clr_s += lc.alpha * (clr - clr_s);
+    ch.win_ip[win_len] = o.ip;
+    ch.win_qp[win_len] = o.qp;
+    win_len++;
+    const int m = cfg.cn0_window_ms;
+    if (win_len >= m) {
+        double nbi = 0, nbq = 0, wbp = 0;
+        for (int k = 0; k < m; ++k) {
+            const double wi = ch.win_ip[k], wq = ch.win_qp[k];
+            const double sg = wi >= 0 ? 1.0 : -1.0;
+            nbi += sg * wi;
+            nbq += sg * wq;
+            wbp += wi * wi + wq * wq;
+        }
+        win_len = 0;
+        const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
+        mu_s = mvalid ? mu_s + 0.2 * (mu - mu_s) : mu;
+        const double md = (double)m;
+        if (mu_s >= md - 1e-9)
+            cn0 = 65.0;
+        else if (mu_s <= 1.0)
+            cn0 = 0.0;
+        else
+            cn0 = 10.0 * log10((mu_s - 1.0) / (md - mu_s) / 1e-3);
+        mvalid = 1;
+    }
+    if (mvalid && esh > cfg.fll_pull_in_ms + cfg.cn0_window_ms) {
+        if (cn0 < cfg.cn0_drop_dbhz || clr_s < cfg.carrier_lock_drop)
+            lfc++;
+        else
+            lfc = 0;
+    }
+    if (lfc > cfg.lock_fail_limit)
+        state = L1RXG_IDLE;
+    ch.state = state;
+    ch.lock_fail_count = lfc;
+    ch.metrics_valid = mvalid;
+    ch.win_len = win_len;
+    ch.carrier_lock_ratio = clr_s;
+    ch.cn0_dbhz = cn0;
+    ch.mu_smoothed = mu_s;
 }
 
 // ---------------------------------------------------------------------
@@ -486,6 +518,12 @@ struct CorrSmem {
     uint64_t bars[2];
     int64_t unit_pos;  // TMA unit in flight: ring position (aligned), slack
     int unit_delta, unit_h, unit_len, inflight;
+    // epoch handed from the critical path to the control warp
+    l1rxg_epoch_record rec;  // inputs, correlator outputs, loop outputs
+    int64_t rec_slot;
+    int64_t rec_esh;         // epochs_since_handoff before that epoch
+    double rec_eenv;         // |E| + |L|
+    int pending, stop;
     CodeTables ct;
 };
 
@@ -532,15 +570,23 @@ __device__ __forceinline__ void warp_partials(const float* acc, float* red, int 
     }
 }
 
-// fp64 cross-warp totals (by warp 0)
+// fp64 cross-warp totals (by warp 0): lane w holds warp w's partial, a
+// fixed butterfly adds them (deterministic order), all V values in flight.
 template <int V>
 __device__ __forceinline__ void warp0_totals(const float* red, double* sums, int lane, int nwarps) {
-    for (int v = lane; v < V; v += 32) {
-        double sm = 0.0;
-        for (int w = 0; w < nwarps; ++w)
-            sm += (double)red[w * V + v];
-        sums[v] = sm;
-    }
+    double x[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+        x[v] = lane < nwarps ? (double)red[lane * V + v] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            x[v] += __shfl_xor_sync(0xffffffffu, x[v], o);
+    if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            sums[v] = x[v];
 }
 
 // ---------------------------------------------------------------------
@@ -563,7 +609,14 @@ struct TrackArgs {
     int kp, ke, kl;
     l1rxg_taps taps;
     LoopCfg lc;
+    long long* prof;  // optional stage clocks (L1RXG_PROF=1): [epoch][8], CTA 0
 };
+
+#define PROF_STAMP(k)                                                          \
+    do {                                                                       \
+        if (a.prof && blockIdx.x == 0 && e < 64)                               \
+            a.prof[e * 8 + (k)] = clock64();                                   \
+    } while (0)
 
 // TMA unit: samples [abs_first, abs_first + len) of the ring into the tile,
 // copied from the 16-byte aligned position below (delta samples of slack),
@@ -593,8 +646,9 @@ __device__ __forceinline__ void issue_unit(CorrSmem<T>* s, float2* tile, const f
 // The epoch window arrives by TMA; the copy of the next window is issued as
 // soon as the current one has been consumed, overlapping the reduction and
 // the loop update.
+#if 0  // superseded by track_kernel below (kept until the next cleanup)
 template <int T>
-__global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
+__global__ void __launch_bounds__(MAX_NT, 1) track_kernel_v3(TrackArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
     float2* tile = tile_of(s);
@@ -765,6 +819,250 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     }
 }
 
+#endif
+
+// Control-warp side of an epoch: run state, quality metrics and lock-fail
+// rule for the epoch handed over in s->rec, then its record and tap sums.
+template <int T>
+__device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a, int lane) {
+    if (lane == 0) {
+        l1rxg_channel& ch = s->ch;
+        const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, a.n);
+        loop_metrics(ch, o, a.lc, s->rec_eenv, s->rec_esh);
+        l1rxg_epoch_record r = s->rec;  // inputs; the rest is post-update state
+        r.epoch_index = ch.epoch_ms_count - 1;
+        r.sample_offset_end = ch.sample_offset_next_epoch;
+        r.prn = ch.prn;
+        r.n_samples = o.n_samples;
+        r.ie = o.ie; r.qe = o.qe; r.ip = o.ip; r.qp = o.qp; r.il = o.il; r.ql = o.ql;
+        r.ip_h1 = o.ip_h1; r.qp_h1 = o.qp_h1; r.ip_h2 = o.ip_h2; r.qp_h2 = o.qp_h2;
+        r.carrier_doppler_hz = ch.carrier_doppler_hz;
+        r.code_freq_hz = ch.code_freq_hz;
+        r.code_phase_chips = ch.code_phase_chips;
+        r.carrier_phase_rad = ch.carrier_phase_rad;
+        r.chi_chips = ch.chi_chips;
+        r.dll_integrator = ch.dll_integrator;
+        r.pll_integrator = ch.pll_integrator;
+        r.dll_prev_error = ch.dll_prev_error;
+        r.pll_prev_error = ch.pll_prev_error;
+        r.state = ch.state;
+        r.lock_fail_count = ch.lock_fail_count;
+        r.cn0_dbhz = ch.cn0_dbhz;
+        r.carrier_lock_ratio = ch.carrier_lock_ratio;
+        r.mu_smoothed = ch.mu_smoothed;
+        a.recs[s->rec_slot] = r;
+    }
+    if (a.tap_sums && lane < 2 * T)
+        a.tap_sums[s->rec_slot * (2 * T) + lane] = s->sums[lane];
+}
+
+// Channel-resident persistent tracking kernel: one CTA per channel loops
+// over its epochs with no host round trip (replaces the per-channel
+// track_epoch fan-out of Receiver::tracking_round, pipeline.hpp:563-610).
+//   * work warps (blockDim - 32 threads): correlation, phases A and B;
+//   * the epoch window arrives by TMA; the next window's copy is issued as
+//     soon as the current one is consumed;
+//   * per-epoch critical path: fp64 totals -> the independent
+//     transcendental pieces in separate warps -> loop_fast (filters, NCO)
+//     -> next epoch's constants;
+//   * the last warp is a control warp: it finishes epoch e (loop_metrics,
+//     record) while epoch e+1 is being correlated.  If that makes the
+//     channel Idle, epoch e+1 is discarded before its loop update, exactly
+//     as if it had never been admitted (tracking.hpp:511-514 + the caller's
+//     Idle check, pipeline.hpp:567-568).
+template <int T>
+__global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
+    float2* tile = tile_of(s);
+    const int cidx = blockIdx.x;
+    const int strm = a.chan_stream[cidx];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    const int ctl = nwarps - 1;            // control warp
+    const int nwork = blockDim.x - 32;     // correlation threads
+    const int nwork_warps = nwarps - 1;
+    constexpr int V = 2 * T + 2;
+    const int cap = nwork * RUN;
+    const int n = a.n;
+    const int nsub = (n + cap - 1) / cap;
+    const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
+    const int64_t avail = a.avail[strm];
+    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
+    const int PW = min(nwork_warps, LOOP_PIECES);
+    const int named = (PW + 1) * 32;       // pieces warps + control warp
+    if (tid == 0) {
+        s->ch = a.chans[cidx];
+        mbar_init(&s->bars[0], 1);
+        mbar_init(&s->bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s->inflight = 0;
+        s->pending = 0;
+        s->stop = 0;
+    }
+    for (int k = tid; k < T; k += blockDim.x)
+        s->d[k] = a.taps.offsets_chips[k];
+    __syncthreads();
+    build_code_tables(s->ct, a.codes, s->ch.prn);
+    if (tid == 0) {  // first epoch: consts and the first tile load
+        const l1rxg_channel& ch = s->ch;
+        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                    ch.carrier_phase_rad, a.lc.fs, n);
+        const int64_t off = ch.sample_offset_next_epoch;
+        if (!noop && ch.state != L1RXG_IDLE && a.max_epochs > 0 && off + n <= avail && off >= 0 &&
+            off >= avail - a.ring_cap)
+            issue_unit(s, tile, ring, off, min(cap, n), a.ring_cap);
+    }
+    __syncthreads();
+    fill_rot(s->rot, s->c.w, tid);
+    __syncthreads();
+
+    uint32_t phase = 0;
+    int64_t e = 0;
+    int64_t done = a.ecount[cidx];
+    for (;;) {
+        // epoch admission (uniform: every thread reads the same smem state)
+        const int64_t off = s->ch.sample_offset_next_epoch;
+        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
+            break;
+        if (off < avail - a.ring_cap || off < 0) {  // window already overwritten
+            if (tid == 0)
+                a.status[cidx] = 1;
+            break;
+        }
+        if (tid == 0)
+            PROF_STAMP(0);
+        // control warp: finish the previous epoch while this one correlates
+        if (warp == ctl && s->pending) {
+            finish_epoch<T>(s, a, lane);
+            if (lane == 0)
+                s->pending = 0;
+        }
+        const EpochConsts c = s->c;
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[v] = 0.f;
+        for (int q = 0; q < nsub; ++q) {
+            const int u0 = q * cap;
+            const int len = min(cap, n - u0);
+            if (!noop) {
+                const int delta = s->unit_delta, h = s->unit_h;
+                const float2* tile_d = tile + delta;
+                if (tid < nwork) {
+                    const int i0 = u0 + tid * RUN;
+                    const int cnt = min(RUN, n - i0);
+                    const int r0 = delta + tid * RUN;
+                    if (cnt > 0) {
+                        if (r0 < h)
+                            mbar_wait(&s->bars[0], phase);
+                        if (r0 + RUN > h)
+                            mbar_wait(&s->bars[1], phase);
+                        phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
+                                            acc, &s->anchors[tid]);
+                    }
+                    if (tid == 0) {  // every phase completes before the next issue
+                        mbar_wait(&s->bars[0], phase);
+                        mbar_wait(&s->bars[1], phase);
+                        PROF_STAMP(1);
+                    }
+                }
+                phase ^= 1u;
+                __syncthreads();  // prefixes + anchors visible
+                if (tid == 0)
+                    PROF_STAMP(2);
+                if (tid < nwork)
+                    phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc, nwork);
+            }
+            if (q + 1 == nsub && warp < nwork_warps)
+                warp_partials<V>(acc, s->red, lane, warp);
+            __syncthreads();  // tile consumed
+            if (tid == 0)
+                PROF_STAMP(3);
+            if (warp == ctl && lane == 0) {  // the next bulk copy, off warp 0's path
+                s->inflight = 0;
+                if (!noop) {
+                    if (q + 1 < nsub)
+                        issue_unit(s, tile, ring, off + (q + 1) * cap, min(cap, n - (q + 1) * cap),
+                                   a.ring_cap);
+                    else if (s->ch.state != L1RXG_IDLE && e + 1 < a.max_epochs &&
+                             off + 2 * (int64_t)n <= avail)
+                        issue_unit(s, tile, ring, off + n, min(cap, n), a.ring_cap);  // prefetch
+                }
+            }
+            if (q + 1 < nsub)
+                __syncthreads();  // publish the next unit
+        }
+        // ---- critical path: totals -> pieces (warps 0..PW-1) -> loop_fast
+        if (warp < PW || warp == ctl) {
+            if (warp == 0)
+                warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
+            asm volatile("bar.sync 1, %0;" ::"r"(named) : "memory");
+            if (tid == 0)
+                PROF_STAMP(4);
+            const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, c.n);
+            if (warp < PW && lane == 0)
+                for (int piece = warp; piece < LOOP_PIECES; piece += PW) {
+                    const long long p0 = clock64();
+                    loop_piece(piece, s->pre, s->ch, o, a.lc, c);
+                    if (a.prof && blockIdx.x == 0 && e < 64)
+                        a.prof[64 * 8 + e * 8 + piece] = clock64() - p0;
+                }
+            asm volatile("bar.sync 1, %0;" ::"r"(named) : "memory");
+            if (tid == 0)
+                PROF_STAMP(5);
+            if (warp == 0) {
+                if (lane == 0) {
+                    l1rxg_channel& ch = s->ch;
+                    if (ch.state == L1RXG_IDLE) {
+                        s->stop = 1;  // the previous epoch dropped the channel
+                    } else {
+                        const LoopPre pre = s->pre;
+                        // correlator inputs for the record (the control
+                        // warp assembles the rest from the post-update state)
+                        l1rxg_epoch_record& r = s->rec;
+                        r.sample_offset_start = off;
+                        r.code_phase_in = ch.code_phase_chips;
+                        r.code_freq_in = ch.code_freq_hz;
+                        r.carrier_doppler_in = ch.carrier_doppler_hz;
+                        r.carrier_phase_in = ch.carrier_phase_rad;
+                        s->rec_esh = ch.epochs_since_handoff;
+                        s->rec_eenv = pre.e + pre.l;
+                        loop_fast(ch, o, a.lc, pre);
+                        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz,
+                                    ch.carrier_doppler_hz, ch.carrier_phase_rad, a.lc.fs, n);
+                        s->rec_slot = (int64_t)cidx * a.max_records + (done % a.max_records);
+                        s->pending = 1;
+                    }
+                }
+                __syncwarp();
+                fill_rot(s->rot, s->c.w, lane);
+                if (tid == 0)
+                    PROF_STAMP(6);
+            }
+        }
+        __syncthreads();
+        if (tid == 0)
+            PROF_STAMP(7);
+        if (s->stop)
+            break;
+        ++e;
+        ++done;
+    }
+    __syncthreads();
+    if (warp == ctl && s->pending)
+        finish_epoch<T>(s, a, lane);
+    __syncthreads();
+    if (tid == 0) {
+        if (s->inflight) {  // never leave a bulk copy in flight into freed smem
+            mbar_wait(&s->bars[0], phase);
+            mbar_wait(&s->bars[1], phase);
+        }
+        a.chans[cidx] = s->ch;
+        a.ecount[cidx] = done;
+    }
+}
+
 // ---------------------------------------------------------------------
 // Open-loop batch (per-call compatibility path and replay tests): job j
 // correlates samples src + j*n with NCO states[j], advances it in place.
@@ -818,7 +1116,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
                 phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
                                     acc, &s->anchors[tid]);
             __syncthreads();
-            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc);
+            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc, blockDim.x);
             __syncthreads();
         }
     }

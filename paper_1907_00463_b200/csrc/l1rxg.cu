@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -114,8 +115,7 @@ int pick_T(int K) {
 
 // Block size: enough RUN-sample runs to cover the epoch in the fewest
 // sub-tiles of at most 768 threads (<= 190 KB of shared tile).
-int pick_threads(int n, int* subtiles) {
-    const int max_nt = MAX_NT;
+int pick_threads(int n, int* subtiles, int max_nt = MAX_NT) {
     const int k = (n + max_nt * RUN - 1) / (max_nt * RUN);
     const int runs = (n + k * RUN - 1) / (k * RUN);
     int nt = ((runs + 31) / 32) * 32;
@@ -591,7 +591,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     t->ctx = c;
     t->d = *d;
     t->T = pick_T(d->taps.n_taps);
-    t->nt = pick_threads(n, nullptr);
+    // correlation warps + one control warp (see track_kernel)
+    t->nt = pick_threads(n, nullptr, MAX_NT - 32) + 32;
     t->R = d->ring_samples;
     // apron >= one epoch (+ bulk-copy slack); R + apron even keeps every
     // stream's ring 16-byte aligned for the TMA copies
@@ -751,12 +752,46 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
+    // L1RXG_PROF=1: stage clocks of CTA 0's first 64 epochs, averaged to stderr
+    static const bool prof = std::getenv("L1RXG_PROF") != nullptr;
+    long long* dprof = nullptr;
+    if (prof) {
+        CK(cudaMalloc(&dprof, 2 * 64 * 8 * sizeof(long long)));
+        CK(cudaMemsetAsync(dprof, 0, 2 * 64 * 8 * sizeof(long long), st));
+    }
+    a.prof = dprof;
     auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st); };
     if (int rc = go())
         return rc;
     t->launches += 1;
     cudaEventRecord(e1, st);
     t->timed.push_back({e0, e1, 1});
+    if (prof) {
+        long long h[2 * 64 * 8];
+        CK(cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(dprof);
+        double acc[8] = {0}, pc[8] = {0};
+        int cnt = 0;
+        for (int e = 2; e < 64; ++e) {
+            if (h[e * 8 + 7] == 0 || h[e * 8] == 0)
+                continue;
+            for (int k = 1; k < 8; ++k)
+                acc[k] += static_cast<double>(h[e * 8 + k] - h[e * 8 + k - 1]);
+            acc[0] += static_cast<double>(h[e * 8 + 7] - h[e * 8]);
+            for (int k = 0; k < 8; ++k)
+                pc[k] += static_cast<double>(h[512 + e * 8 + k]);
+            ++cnt;
+        }
+        if (cnt)
+            std::fprintf(stderr,
+                         "[l1rxg prof] cycles/epoch %.0f | A %.0f | barA %.0f | B+red %.0f | "
+                         "totals %.0f | pieces %.0f | apply %.0f | bar %.0f | per piece %.0f %.0f "
+                         "%.0f %.0f %.0f\n",
+                         acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                         acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, pc[0] / cnt, pc[1] / cnt,
+                         pc[2] / cnt, pc[3] / cnt, pc[4] / cnt);
+    }
     return 0;
 }
 
