@@ -379,10 +379,10 @@ def main():
     # ---- end-of-run gather of the records to rank 0 over NCCL
     gathered = None
     if dist:
+        from paper_1907_00463_b200.shard import gather_bytes
         rec_t = torch.empty(rec_bytes, dtype=torch.uint8, device=dev)
         trk.records_raw(dst_ptr=rec_t.data_ptr(), device=True)
-        outs = [torch.empty_like(rec_t) for _ in range(world)] if rank == 0 else None
-        dist.gather(rec_t, outs, dst=0)
+        outs = gather_bytes(rec_t, dist, dst=0)
         gathered = sum(int(o.numel()) for o in outs) if rank == 0 else None
 
     if rank != 0:

@@ -1,0 +1,146 @@
+// tests/cpp/test_adapter.cpp -- the reference's own tracking tests
+// (proj/tests/test_tracking.cpp) re-targeted at the GPU correlator through
+// the drop-in adapter (include/l1rx_gpu.hpp), compiled against the
+// UNMODIFIED reference headers.  Built by tests/cpp/Makefile where
+// /root/reference exists; the binary runs on the GPU box
+// (tests/test_gpu_adapter.py).  Tolerances are the GPU path's 1e-5 bar
+// where the reference uses 1e-9 for its fp64 kernels.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "l1rx/simsource.hpp"
+#include "l1rx/tracking.hpp"
+#include "l1rx_gpu.hpp"
+
+using namespace l1rx;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                          \
+    do {                                                                  \
+        ++g_checks;                                                       \
+        if (!(c)) {                                                       \
+            ++g_fail;                                                     \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+        }                                                                 \
+    } while (0)
+
+static std::vector<cplx> sim_signal(double cn0, double doppler, double delay, double fs,
+                                    double dur, bool noise, std::uint64_t seed) {
+    SimScenario sc;
+    SimSatellite sv;
+    sv.prn = 7;
+    sv.cn0_dbhz = cn0;
+    sv.doppler_hz = doppler;
+    sv.code_delay_chips = delay;
+    sc.satellites.push_back(sv);
+    sc.duration_s = dur;
+    sc.sample_rate_hz = fs;
+    sc.noise_enabled = noise;
+    sc.seed = seed;
+    SimStream stream(sc);
+    std::vector<cplx> buf;
+    while (auto blk = stream.next_block())
+        buf.insert(buf.end(), blk->begin(), blk->end());
+    return buf;
+}
+
+static ChannelState aligned(int prn) {
+    ChannelState ch;
+    ch.prn = prn;
+    ch.state = ChannelRunState::Tracking;
+    return ch;
+}
+
+int main() {
+    const double fs = 5e6;
+    TrackingConfig cfg;
+    // test_tracking.cpp:81-95 aligned noiseless replica
+    {
+        const auto sig = sim_signal(48, 0, 0, fs, 0.001, false, 1);
+        auto ch = aligned(7);
+        const auto out = gpu::correlate_epoch_gpu(sig, ch, ca_code_table()[7], cfg, fs);
+        const double amp = std::sqrt(std::pow(10.0, 4.8) / fs);
+        CHECK(std::abs(out.ip - 5000.0 * amp) <= 1e-5 * 5000.0 * amp);
+        CHECK(std::abs(out.qp) < 1e-5 * out.ip);
+        const double e = std::hypot(out.ie, out.qe), l = std::hypot(out.il, out.ql);
+        CHECK(std::abs(e - l) <= 1e-2 * l);
+        CHECK(out.ip > e);
+    }
+    // test_tracking.cpp:166-204: GPU = scalar kernel within the bar, same state advance
+    {
+        std::mt19937_64 rng(12);
+        auto urand = [&](double lo, double hi) {
+            return lo + (hi - lo) * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+        };
+        for (int trial = 0; trial < 200; ++trial) {
+            std::vector<cplx> view(5000);
+            for (auto& v : view)
+                v = cplx(urand(-1, 1), urand(-1, 1));
+            ChannelState ch;
+            ch.prn = 1 + static_cast<int>(rng() % 32);
+            ch.state = ChannelRunState::Tracking;
+            ch.carrier_doppler_hz = urand(-5000, 5000);
+            ch.carrier_phase_rad = urand(0, 2 * constants::pi);
+            ch.code_phase_chips = urand(0, 1023);
+            ch.code_freq_hz = 1.023e6 + urand(-3, 3);
+            auto ch2 = ch;
+            const auto& code = ca_code_table()[static_cast<std::size_t>(ch.prn)];
+            const auto a = correlate_epoch_scalar(view, ch, code, cfg, fs);
+            const auto b = gpu::correlate_epoch_gpu(view, ch2, code, cfg, fs);
+            const double scale = std::max({std::abs(a.ie), std::abs(a.qe), std::abs(a.ip),
+                                           std::abs(a.qp), std::abs(a.il), std::abs(a.ql), 1e-9});
+            CHECK(std::abs(a.ie - b.ie) <= 1e-5 * scale);
+            CHECK(std::abs(a.qe - b.qe) <= 1e-5 * scale);
+            CHECK(std::abs(a.ip - b.ip) <= 1e-5 * scale);
+            CHECK(std::abs(a.qp - b.qp) <= 1e-5 * scale);
+            CHECK(std::abs(a.il - b.il) <= 1e-5 * scale);
+            CHECK(std::abs(a.ql - b.ql) <= 1e-5 * scale);
+            CHECK(ch.code_phase_chips == ch2.code_phase_chips);
+            CHECK(ch.carrier_phase_rad == ch2.carrier_phase_rad);
+            CHECK(ch.chi_chips == ch2.chi_chips);
+        }
+    }
+    // test_tracking.cpp:238-248: empty view is an error
+    {
+        auto ch = aligned(7);
+        std::vector<cplx> empty;
+        bool threw = false;
+        try {
+            gpu::correlate_epoch_gpu(empty, ch, ca_code_table()[7], cfg, fs);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // closed loop through the GpuTracker (test_tracking.cpp:403-417 scenario,
+    // int8 I/Q recording of the reference simulator)
+    {
+        const double fs2 = 2.048e6;
+        const auto sig = sim_signal(45.0, 320.0, 100.25, fs2, 1.5, true, 77);
+        std::vector<int8_t> raw(2 * sig.size());
+        for (std::size_t i = 0; i < sig.size(); ++i) {
+            auto q = [](double v) {
+                return static_cast<int8_t>(std::max(-127L, std::min(127L, std::lround(v * 128.0))));
+            };
+            raw[2 * i] = q(sig[i].real());
+            raw[2 * i + 1] = q(sig[i].imag());
+        }
+        const auto boundary = static_cast<int>(std::lround(100.25 / constants::chip_rate_hz * fs2));
+        ChannelState ch;
+        init_channel_from_acquisition(ch, 7, 0.0, 0, boundary - 1, 0, fs2);
+        gpu::GpuTracker trk(SampleKind::Int8ComplexInterleaved, fs2, 0.0, {ch}, cfg, 1600 * 2048, 2000);
+        trk.push(raw.data(), static_cast<int64_t>(raw.size()));
+        trk.run();
+        std::vector<ChannelState> out;
+        trk.channels(out);
+        CHECK(out[0].state == ChannelRunState::Tracking);
+        const auto r = trk.records(0, 1000, 1);
+        CHECK(r[0].carrier_lock_ratio > 0.9);
+        CHECK(std::abs(r[0].carrier_doppler_hz - 320.0) < 5.0);
+        CHECK(std::abs(r[0].cn0_dbhz - 45.0) < 2.0);
+    }
+    std::printf("%s: %d checks, %d failures\n", g_fail ? "FAILED" : "OK", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}
