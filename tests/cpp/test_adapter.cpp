@@ -97,9 +97,14 @@ int main() {
             CHECK(std::abs(a.qp - b.qp) <= 1e-5 * scale);
             CHECK(std::abs(a.il - b.il) <= 1e-5 * scale);
             CHECK(std::abs(a.ql - b.ql) <= 1e-5 * scale);
-            CHECK(ch.code_phase_chips == ch2.code_phase_chips);
-            CHECK(ch.carrier_phase_rad == ch2.carrier_phase_rad);
-            CHECK(ch.chi_chips == ch2.chi_chips);
+            // same state advance; margin as test_tracking.cpp:199-202 (inside
+            // this TU g++ may contract the reference's code_phase + n*cps into
+            // an FMA or not, so the reference itself is only ulp-defined here;
+            // against the reference library build the GPU is bit-exact,
+            // tests/test_gpu_correlator.py)
+            CHECK(std::abs(ch.code_phase_chips - ch2.code_phase_chips) <= 1e-9);
+            CHECK(std::abs(ch.carrier_phase_rad - ch2.carrier_phase_rad) <= 1e-9);
+            CHECK(std::abs(ch.chi_chips - ch2.chi_chips) <= 1e-9);
         }
     }
     // test_tracking.cpp:238-248: empty view is an error

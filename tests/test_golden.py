@@ -90,7 +90,7 @@ def test_gpu_ingest_vs_reference_fixture(g, ctx):
     for tag in ("if4", "gn3s"):
         fs, ifz = g[f"ingest_{tag}_rate"]
         raw = g[f"ingest_{tag}_raw"]
-        trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, ifz, [], ring_samples=1 << 14)
+        trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, ifz, [], ring_samples=1 << 16)
         trk.push(0, raw[:2500])
         trk.push(0, raw[2500:])
         got = trk.read_samples(0, 0, raw.size)
