@@ -53,7 +53,7 @@ __device__ __forceinline__ void make_consts(EpochConsts& c, double code_phase,
                                             double phase, double fs, int n) {
     c.w = 2.0 * PI_D * doppler / fs;  // (2*pi*fD)/fs as the reference orders it
     c.cps = code_freq / fs;
-    c.inv_cps = (double)__frcp_rn((float)c.cps);
+    c.inv_cps = __drcp_rn(c.cps);  // correctly rounded (tap_boundary's fast path)
     c.base = code_phase + 1023.0;
     c.phi = phase;
     c.n = n;
@@ -74,10 +74,18 @@ __device__ __forceinline__ int tap_index(int i, double cps, double base, double 
 // rounding, < 1e-11 samples, are far below one sample), so checking the
 // estimate and its left neighbour with the reference expression pins the
 // exact boundary: tap_value is monotone in the sample index.
+//
+// Fast path: with inv_cps correctly rounded, |e - x*| < 2e-11 samples for
+// the exact crossing x* = (m - d - base)/cps, and the reference's own
+// rounding moves its crossing by < 5e-11 samples; so when e is farther than
+// 1e-9 from an integer the boundary is ceil(e) with certainty.  Only near
+// ties (exact ties occur at commensurate rates) take the exact check.
 __device__ __forceinline__ int tap_boundary(int m, double d, const EpochConsts& c, int lo, int hi) {
     const double mm = (double)m;
-    int b = __double2int_ru(((mm - d) - c.base) * c.inv_cps);
-    b = max(lo, min(hi, b));
+    const double e = ((mm - d) - c.base) * c.inv_cps;
+    int b = max(lo, min(hi, __double2int_ru(e)));
+    if (fabs(e - rint(e)) > 1e-9)
+        return b;
     const bool dn = (b > lo) && (tap_value((double)(b - 1), c.cps, c.base, d) >= mm);
     const bool up = !dn && (b < hi) && (tap_value((double)b, c.cps, c.base, d) < mm);
     return b - (int)dn + (int)up;
@@ -218,19 +226,38 @@ __device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* r
 // Phase B: every chip transition of every tap whose step falls in the
 // sub-tile [u0, u0+len): acc_k -= delta * anchor(run(b)) * P(b).
 // tile_d[i - u0] holds P(i) (phase A's in-place prefixes).
+constexpr int MAXSUB = 8;  // sub-tiles per epoch (n <= 8 * 608 * 31)
+
+// Per (sub-tile, tap): first global transition index and count of the
+// transitions whose step falls in the sub-tile -- the same for every
+// thread, so computed once per epoch by one warp (lanes over (q, k)).
+template <int T>
+__device__ __forceinline__ void fill_tap_ranges(int2* tr /*[MAXSUB][T]*/, const EpochConsts& c,
+                                                const CodeTables& ct, const double* d, int cap,
+                                                int nsub, int lane) {
+    for (int idx = lane; idx < nsub * T; idx += 32) {
+        const int q = idx / T, k = idx - q * T;
+        const int u0 = q * cap;
+        const int hi = u0 + min(cap, c.n - u0) - 1;
+        const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, d[k]);
+        const int mhi = tap_index(hi, c.cps, c.base, d[k]);
+        const int g0 = trans_count(ct, mlo);
+        tr[q * T + k] = make_int2(g0, trans_count(ct, mhi) - g0);
+    }
+}
+
 template <int T>
 __device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile_d,
                                         const float2* anchors, const CodeTables& ct,
                                         const double* d, int kp, int u0, int len, float* acc,
-                                        int nthreads) {
+                                        int nthreads, const int2* tr /*[T] of this sub-tile*/) {
     const int hi = u0 + len - 1;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
         const double dk = d[k];
-        const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, dk);
-        const int mhi = tap_index(hi, c.cps, c.base, dk);
-        const int g0 = trans_count(ct, mlo);
-        const int cntk = trans_count(ct, mhi) - g0;
+        const int2 rk = tr[k];
+        const int g0 = rk.x;
+        const int cntk = rk.y;
         // rotate the starting thread per tap so the remainders spread out
         int j = (int)threadIdx.x - ((k * 64) & 511);
         while (j < 0)
@@ -360,28 +387,63 @@ struct LoopPre {
 };
 constexpr int LOOP_PIECES = 5;
 
+// Each piece is its own non-inlined function: inlined into one body the
+// compiler merges and hoists their shared subexpressions above the dispatch,
+// and every piece warp then pays for several pieces.
+__device__ __noinline__ void piece_dll(LoopPre& p, const double* sums, int ke, int kl) {
+    const double ie = sums[2 * ke], qe = sums[2 * ke + 1];
+    const double il = sums[2 * kl], ql = sums[2 * kl + 1];
+    p.e = sqrt(ie * ie + qe * qe);
+    p.l = sqrt(il * il + ql * ql);
+    p.dll = (p.e + p.l == 0.0) ? 0.0 : 0.5 * (p.e - p.l) / (p.e + p.l);  // :95-101
+}
+__device__ __noinline__ void piece_pll(LoopPre& p, const double* sums, int kp) {
+    const double ip = sums[2 * kp], qp = sums[2 * kp + 1];
+    if (ip == 0.0)
+        p.pll = (qp == 0.0) ? 0.0 : (qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
+    else
+        p.pll = atan(qp / ip);
+}
+__device__ __noinline__ void piece_fll(double& out, double a, double b, double c2, double d2,
+                                       double dt, bool fold) {
+    out = fll_disc(a, b, c2, d2, dt, fold);
+}
+__device__ __noinline__ void piece_nco(LoopPre& p, const l1rxg_channel& ch, const EpochConsts& c) {
+    double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
+    advance_nco(cp, ph, chi, c);
+    p.code_phase = cp;
+    p.carrier_phase = ph;
+    p.chi = chi;
+}
+
+// sums: [2T + 2] fp64 totals; the first-half prompt sits at 2T
 __device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_channel& ch,
-                                           const l1rxg_corr& o, const LoopCfg& lc,
-                                           const EpochConsts& c) {
-    if (piece == 0) {
-        p.e = sqrt(o.ie * o.ie + o.qe * o.qe);
-        p.l = sqrt(o.il * o.il + o.ql * o.ql);
-        p.dll = (p.e + p.l == 0.0) ? 0.0 : 0.5 * (p.e - p.l) / (p.e + p.l);  // :95-101
-    } else if (piece == 1) {
-        if (o.ip == 0.0)
-            p.pll = (o.qp == 0.0) ? 0.0 : (o.qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
-        else
-            p.pll = atan(o.qp / o.ip);
-    } else if (piece == 2) {
-        p.fc = fll_disc(o.ip_h1, o.qp_h1, o.ip_h2, o.qp_h2, lc.dt / 2.0, false);
-    } else if (piece == 3) {
-        p.ff = fll_disc(ch.last_ip, ch.last_qp, o.ip, o.qp, lc.dt, true);
-    } else {
-        double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
-        advance_nco(cp, ph, chi, c);
-        p.code_phase = cp;
-        p.carrier_phase = ph;
-        p.chi = chi;
+                                           const double* sums, int T, int ke, int kp, int kl,
+                                           const LoopCfg& lc, const EpochConsts& c) {
+    const int64_t esh = ch.epochs_since_handoff;
+    switch (piece) {
+    case 0:
+        piece_dll(p, sums, ke, kl);
+        break;
+    case 1:
+        piece_pll(p, sums, kp);
+        break;
+    case 2:  // only read during the coarse pull-in stage
+        p.fc = 0.0;
+        if (esh < (int64_t)lc.cfg.fll_coarse_ms) {
+            const double ip = sums[2 * kp], qp = sums[2 * kp + 1];
+            const double h1i = sums[2 * T], h1q = sums[2 * T + 1];
+            piece_fll(p.fc, h1i, h1q, ip - h1i, qp - h1q, lc.dt / 2.0, false);
+        }
+        break;
+    case 3:  // only read during the fine pull-in stage
+        p.ff = 0.0;
+        if (esh < (int64_t)lc.cfg.fll_pull_in_ms && esh >= (int64_t)lc.cfg.fll_coarse_ms)
+            piece_fll(p.ff, ch.last_ip, ch.last_qp, sums[2 * kp], sums[2 * kp + 1], lc.dt, true);
+        break;
+    default:
+        piece_nco(p, ch, c);
+        break;
     }
 }
 
@@ -524,6 +586,7 @@ struct CorrSmem {
     int64_t rec_esh;         // epochs_since_handoff before that epoch
     double rec_eenv;         // |E| + |L|
     int pending, stop;
+    int2 trange[MAXSUB * T];  // phase-B transition ranges per (sub-tile, tap)
     CodeTables ct;
 };
 
@@ -556,37 +619,69 @@ __device__ __forceinline__ l1rxg_corr corr_from_sums(const double* sums, int ke,
     return o;
 }
 
-// warp shuffles of the V partials -> red[warp][v]
+// Warp reduction of the V partials -> red[warp][v] as a reduce-scatter
+// butterfly: at each level a lane keeps half of its values and receives the
+// partner's matching half, so V values need ~V + 5 shuffles instead of 5V.
 template <int V>
 __device__ __forceinline__ void warp_partials(const float* acc, float* red, int lane, int warp) {
+    constexpr int P = (V <= 8) ? 8 : (V <= 16) ? 16 : (V <= 32) ? 32 : 64;
+    if constexpr (P > 32) {
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-        float x = acc[v];
+        for (int v = 0; v < V; ++v) {
+            float x = acc[v];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0)
-            red[warp * V + v] = x;
+            for (int o = 16; o > 0; o >>= 1)
+                x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (lane == 0)
+                red[warp * V + v] = x;
+        }
+    } else {
+        float x[P];
+#pragma unroll
+        for (int v = 0; v < P; ++v)
+            x[v] = v < V ? acc[v] : 0.f;
+        int base = 0;
+#pragma unroll
+        for (int lv = 0, o = 16; lv < 5; ++lv, o >>= 1) {
+            const int c = P >> lv;  // values held before this level
+            if (c > 1) {
+                const int h = c / 2;
+                const bool upper = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < h; ++i) {
+                    const float send = upper ? x[i] : x[i + h];
+                    const float keep = upper ? x[i + h] : x[i];
+                    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+                if (upper)
+                    base += h;
+            } else {
+                x[0] += __shfl_xor_sync(0xffffffffu, x[0], o);
+            }
+        }
+        if (base < V && (lane & (32 / P - 1)) == 0)
+            red[warp * V + base] = x[0];
     }
 }
 
-// fp64 cross-warp totals (by warp 0): lane w holds warp w's partial, a
-// fixed butterfly adds them (deterministic order), all V values in flight.
+// fp64 cross-warp totals (by warp 0): lane v loads the nwarps partials of
+// value v with independent loads and adds them as a fixed pairwise tree
+// (deterministic order, depth log2(nwarps)).
 template <int V>
 __device__ __forceinline__ void warp0_totals(const float* red, double* sums, int lane, int nwarps) {
-    double x[V];
+    constexpr int WMAX = MAX_NT / 32;
+    for (int v = lane; v < V; v += 32) {
+        double x[WMAX];
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-        x[v] = lane < nwarps ? (double)red[lane * V + v] : 0.0;
+        for (int w = 0; w < WMAX; ++w)
+            x[w] = w < nwarps ? (double)red[w * V + v] : 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+        for (int step = 1; step < WMAX; step <<= 1)
 #pragma unroll
-        for (int v = 0; v < V; ++v)
-            x[v] += __shfl_xor_sync(0xffffffffu, x[v], o);
-    if (lane == 0)
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            sums[v] = x[v];
+            for (int w = 0; w + step < WMAX; w += 2 * step)
+                x[w] += x[w + step];
+        sums[v] = x[0];
+    }
 }
 
 // ---------------------------------------------------------------------
@@ -640,187 +735,6 @@ __device__ __forceinline__ void issue_unit(CorrSmem<T>* s, float2* tile, const f
     s->inflight = 1;
 }
 
-// Channel-resident persistent tracking kernel: one CTA per channel loops
-// over its epochs with no host round trip (replaces the per-channel
-// track_epoch fan-out of Receiver::tracking_round, pipeline.hpp:563-610).
-// The epoch window arrives by TMA; the copy of the next window is issued as
-// soon as the current one has been consumed, overlapping the reduction and
-// the loop update.
-#if 0  // superseded by track_kernel below (kept until the next cleanup)
-template <int T>
-__global__ void __launch_bounds__(MAX_NT, 1) track_kernel_v3(TrackArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
-    float2* tile = tile_of(s);
-    const int cidx = blockIdx.x;
-    const int strm = a.chan_stream[cidx];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = (blockDim.x + 31) >> 5;
-    constexpr int V = 2 * T + 2;
-    const int cap = blockDim.x * RUN;
-    const int n = a.n;
-    const int nsub = (n + cap - 1) / cap;
-    const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
-    const int64_t avail = a.avail[strm];
-    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
-    if (tid == 0) {
-        s->ch = a.chans[cidx];
-        mbar_init(&s->bars[0], 1);
-        mbar_init(&s->bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s->inflight = 0;
-    }
-    for (int k = tid; k < T; k += blockDim.x)
-        s->d[k] = a.taps.offsets_chips[k];
-    __syncthreads();
-    build_code_tables(s->ct, a.codes, s->ch.prn);
-    if (tid == 0) {  // first epoch: consts and the first tile load
-        const l1rxg_channel& ch = s->ch;
-        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
-                    ch.carrier_phase_rad, a.lc.fs, n);
-        const int64_t off = ch.sample_offset_next_epoch;
-        if (!noop && ch.state != L1RXG_IDLE && a.max_epochs > 0 && off + n <= avail && off >= 0 &&
-            off >= avail - a.ring_cap)
-            issue_unit(s, tile, ring, off, min(cap, n), a.ring_cap);
-    }
-    __syncthreads();
-    fill_rot(s->rot, s->c.w, tid);
-    __syncthreads();
-
-    uint32_t phase = 0;
-    int64_t e = 0;
-    int64_t done = a.ecount[cidx];
-    for (;;) {
-        // epoch admission (uniform: every thread reads the same smem state)
-        const int64_t off = s->ch.sample_offset_next_epoch;
-        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
-            break;
-        if (off < avail - a.ring_cap || off < 0) {  // window already overwritten
-            if (tid == 0)
-                a.status[cidx] = 1;
-            break;
-        }
-        const EpochConsts c = s->c;
-        float acc[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            acc[v] = 0.f;
-        for (int q = 0; q < nsub; ++q) {
-            const int u0 = q * cap;
-            const int len = min(cap, n - u0);
-            if (!noop) {
-                const int delta = s->unit_delta, h = s->unit_h;
-                const float2* tile_d = tile + delta;
-                const int i0 = u0 + tid * RUN;
-                const int cnt = min(RUN, n - i0);
-                const int r0 = delta + tid * RUN;
-                if (cnt > 0) {
-                    if (r0 < h)
-                        mbar_wait(&s->bars[0], phase);
-                    if (r0 + RUN > h)
-                        mbar_wait(&s->bars[1], phase);
-                    phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt, acc,
-                                        &s->anchors[tid]);
-                }
-                if (tid == 0) {  // every phase completes before the next issue
-                    mbar_wait(&s->bars[0], phase);
-                    mbar_wait(&s->bars[1], phase);
-                }
-                phase ^= 1u;
-                __syncthreads();  // prefixes + anchors visible
-                phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc);
-            }
-            if (q + 1 == nsub)
-                warp_partials<V>(acc, s->red, lane, warp);
-            __syncthreads();  // tile consumed
-            if (tid == 0) {
-                s->inflight = 0;
-                if (!noop) {
-                    if (q + 1 < nsub)
-                        issue_unit(s, tile, ring, off + (q + 1) * cap, min(cap, n - (q + 1) * cap),
-                                   a.ring_cap);
-                    else if (s->ch.state != L1RXG_IDLE && e + 1 < a.max_epochs &&
-                             off + 2 * (int64_t)n <= avail)
-                        issue_unit(s, tile, ring, off + n, min(cap, n), a.ring_cap);  // prefetch
-                }
-            }
-            if (q + 1 < nsub)
-                __syncthreads();  // publish the next unit
-        }
-        // ---- loop update: warps 0..PW-1 split the independent pieces,
-        // then warp 0 / lane 0 applies the sequential logic
-        const int PW = min(nwarps, LOOP_PIECES);
-        if (warp < PW) {
-            if (warp == 0)
-                warp0_totals<V>(s->red, s->sums, lane, nwarps);
-            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
-            const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, c.n);
-            if (lane == 0)
-                for (int piece = warp; piece < LOOP_PIECES; piece += PW)
-                    loop_piece(piece, s->pre, s->ch, o, a.lc, c);
-            asm volatile("bar.sync 1, %0;" ::"r"(PW * 32) : "memory");
-            if (warp == 0) {
-                const int64_t slot = (int64_t)cidx * a.max_records + (done % a.max_records);
-                if (a.tap_sums && lane < 2 * T)
-                    a.tap_sums[slot * (2 * T) + lane] = s->sums[lane];
-                if (lane == 0) {
-                    l1rxg_channel& ch = s->ch;
-                    const LoopPre pre = s->pre;
-                    l1rxg_epoch_record r;
-                    r.sample_offset_start = off;
-                    r.code_phase_in = ch.code_phase_chips;
-                    r.code_freq_in = ch.code_freq_hz;
-                    r.carrier_doppler_in = ch.carrier_doppler_hz;
-                    r.carrier_phase_in = ch.carrier_phase_rad;
-                    ch.code_phase_chips = pre.code_phase;
-                    ch.carrier_phase_rad = pre.carrier_phase;
-                    ch.chi_chips = pre.chi;
-                    loop_update(ch, o, a.lc, pre);
-                    // next epoch's NCO constants, then the record
-                    make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
-                                ch.carrier_phase_rad, a.lc.fs, n);
-                    r.epoch_index = ch.epoch_ms_count - 1;
-                    r.sample_offset_end = ch.sample_offset_next_epoch;
-                    r.prn = ch.prn;
-                    r.state = ch.state;
-                    r.n_samples = c.n;
-                    r.lock_fail_count = ch.lock_fail_count;
-                    r.ie = o.ie; r.qe = o.qe; r.ip = o.ip; r.qp = o.qp; r.il = o.il; r.ql = o.ql;
-                    r.ip_h1 = o.ip_h1; r.qp_h1 = o.qp_h1; r.ip_h2 = o.ip_h2; r.qp_h2 = o.qp_h2;
-                    r.carrier_doppler_hz = ch.carrier_doppler_hz;
-                    r.code_freq_hz = ch.code_freq_hz;
-                    r.code_phase_chips = ch.code_phase_chips;
-                    r.carrier_phase_rad = ch.carrier_phase_rad;
-                    r.chi_chips = ch.chi_chips;
-                    r.cn0_dbhz = ch.cn0_dbhz;
-                    r.carrier_lock_ratio = ch.carrier_lock_ratio;
-                    r.dll_integrator = ch.dll_integrator;
-                    r.pll_integrator = ch.pll_integrator;
-                    r.mu_smoothed = ch.mu_smoothed;
-                    r.dll_prev_error = ch.dll_prev_error;
-                    r.pll_prev_error = ch.pll_prev_error;
-                    a.recs[slot] = r;
-                }
-                __syncwarp();
-                fill_rot(s->rot, s->c.w, lane);
-            }
-        }
-        ++e;
-        ++done;
-        __syncthreads();
-    }
-    if (tid == 0) {
-        if (s->inflight) {  // never leave a bulk copy in flight into freed smem
-            mbar_wait(&s->bars[0], phase);
-            mbar_wait(&s->bars[1], phase);
-        }
-        a.chans[cidx] = s->ch;
-        a.ecount[cidx] = done;
-    }
-}
-
-#endif
-
 // Control-warp side of an epoch: run state, quality metrics and lock-fail
 // rule for the epoch handed over in s->rec, then its record and tap sums.
 template <int T>
@@ -854,6 +768,121 @@ __device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a,
     }
     if (a.tap_sums && lane < 2 * T)
         a.tap_sums[s->rec_slot * (2 * T) + lane] = s->sums[lane];
+}
+
+// The per-epoch critical path on warp 0, SIMT: the transcendental pieces of
+// track_epoch are evaluated as ONE instruction stream over lanes with
+// different inputs (no divergence, no cross-warp hand-off):
+//   atan2 on lanes 0..2: PLL  atan(qp/ip) = atan2(qp*sgn(ip), |ip|)
+//                        (tracking.hpp:104-111), FLL coarse and fine
+//                        (:113-138; the fine one folded to dot >= 0);
+//   sqrt  on lanes 3..4: |E|, |L| (:96-97);
+//   fmod  on lanes 5..6: carrier and code NCO advance (:275-280, exact);
+// lane 0 then runs loop_fast, and lanes 0..1 divide the next epoch's w and
+// cps (:234-236).  All values equal the reference's up to last-bit
+// rounding of atan vs atan2; the state advance is bit-exact.
+template <int T>
+__device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a, const EpochConsts& c,
+                                             int64_t off, int cidx, int64_t done, int nwork_warps,
+                                             int lane) {
+    constexpr int V = 2 * T + 2;
+    warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
+    __syncwarp();
+    l1rxg_channel& ch = s->ch;
+    if (ch.state == L1RXG_IDLE) {  // the previous epoch dropped the channel
+        if (lane == 0)
+            s->stop = 1;
+        return;
+    }
+    const double ie = s->sums[2 * a.ke], qe = s->sums[2 * a.ke + 1];
+    const double il = s->sums[2 * a.kl], ql = s->sums[2 * a.kl + 1];
+    const double ip = s->sums[2 * a.kp], qp = s->sums[2 * a.kp + 1];
+    const double h1i = s->sums[2 * T], h1q = s->sums[2 * T + 1];
+    const double cp0 = ch.code_phase_chips, ph0 = ch.carrier_phase_rad, chi0 = ch.chi_chips;
+    const double adv = __dmul_rn((double)c.n, c.cps);
+    // atan2 lanes
+    double y = 0.0, x = 1.0;
+    bool zero = false;
+    if (lane == 0) {
+        y = ip < 0 ? -qp : qp;
+        x = fabs(ip);
+    } else if (lane == 1 || lane == 2) {
+        const double pi_ = lane == 1 ? h1i : ch.last_ip, pq = lane == 1 ? h1q : ch.last_qp;
+        const double ci = lane == 1 ? ip - h1i : ip, cq = lane == 1 ? qp - h1q : qp;
+        double cross = pi_ * cq - pq * ci;
+        double dot = pi_ * ci + pq * cq;
+        if (lane == 2 && dot < 0) {
+            cross = -cross;
+            dot = -dot;
+        }
+        y = cross;
+        x = dot;
+        zero = cross == 0.0 && dot == 0.0;
+    }
+    const double ang = atan2(y, x);
+    // sqrt lanes
+    const double sq = sqrt(lane == 3 ? ie * ie + qe * qe : il * il + ql * ql);
+    // fmod lanes (exact)
+    const bool carrier = lane == 5;
+    const double fm = fmod_exact(carrier ? __fma_rn(c.w, (double)c.n, ph0) : __dadd_rn(cp0, adv),
+                                 carrier ? 2.0 * PI_D : 1023.0,
+                                 carrier ? 1.0 / (2.0 * PI_D) : 1.0 / 1023.0);
+    const double a_pll = __shfl_sync(0xffffffffu, ang, 0);
+    const double a_fc = __shfl_sync(0xffffffffu, ang, 1);
+    const double a_ff = __shfl_sync(0xffffffffu, ang, 2);
+    const bool z_fc = __shfl_sync(0xffffffffu, zero, 1);
+    const bool z_ff = __shfl_sync(0xffffffffu, zero, 2);
+    const double e = __shfl_sync(0xffffffffu, sq, 3);
+    const double l = __shfl_sync(0xffffffffu, sq, 4);
+    const double ph1 = __shfl_sync(0xffffffffu, fm, 5);
+    const double cp1 = __shfl_sync(0xffffffffu, fm, 6);
+    double fd = 0.0, cf = 0.0;
+    if (lane == 0) {
+        LoopPre pre;
+        pre.e = e;
+        pre.l = l;
+        pre.dll = (e + l == 0.0) ? 0.0 : 0.5 * (e - l) / (e + l);  // :95-101
+        pre.pll = ip == 0.0 ? (qp == 0.0 ? 0.0 : (qp > 0 ? PI_D / 2.0 : -PI_D / 2.0)) : a_pll;
+        pre.fc = z_fc ? 0.0 : a_fc / (2.0 * PI_D * (a.lc.dt / 2.0));
+        pre.ff = z_ff ? 0.0 : a_ff / (2.0 * PI_D * a.lc.dt);
+        pre.carrier_phase = ph1;
+        pre.code_phase = cp1;
+        pre.chi = __dadd_rn(chi0, adv);
+        l1rxg_epoch_record& r = s->rec;  // correlator inputs for the record
+        r.sample_offset_start = off;
+        r.code_phase_in = cp0;
+        r.code_freq_in = ch.code_freq_hz;
+        r.carrier_doppler_in = ch.carrier_doppler_hz;
+        r.carrier_phase_in = ph0;
+        s->rec_esh = ch.epochs_since_handoff;
+        s->rec_eenv = e + l;
+        l1rxg_corr o;
+        o.ip = ip;
+        o.qp = qp;
+        o.n_samples = c.n;
+        loop_fast(ch, o, a.lc, pre);
+        fd = ch.carrier_doppler_hz;
+        cf = ch.code_freq_hz;
+        s->rec_slot = (int64_t)cidx * a.max_records + (done % a.max_records);
+        s->pending = 1;
+    }
+    // next epoch's w = (2 pi fD)/fs and cps = cf/fs, one division per lane
+    fd = __shfl_sync(0xffffffffu, fd, 0);
+    cf = __shfl_sync(0xffffffffu, cf, 0);
+    const double quo = (lane == 0 ? 2.0 * PI_D * fd : cf) / a.lc.fs;
+    const double w = __shfl_sync(0xffffffffu, quo, 0);
+    const double cps = __shfl_sync(0xffffffffu, quo, 1);
+    if (lane == 0) {
+        EpochConsts& nc = s->c;
+        nc.w = w;
+        nc.cps = cps;
+        nc.inv_cps = __drcp_rn(cps);
+        nc.base = cp1 + 1023.0;
+        nc.phi = ph1;
+        nc.n = c.n;
+        nc.nh = c.nh;
+    }
+    __syncwarp();
 }
 
 // Channel-resident persistent tracking kernel: one CTA per channel loops
@@ -915,6 +944,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     }
     __syncthreads();
     fill_rot(s->rot, s->c.w, tid);
+    if (warp == 0)
+        fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, nsub, lane);
     __syncthreads();
 
     uint32_t phase = 0;
@@ -972,7 +1003,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                 if (tid == 0)
                     PROF_STAMP(2);
                 if (tid < nwork)
-                    phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc, nwork);
+                    phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc, nwork,
+                               s->trange + q * T);
             }
             if (q + 1 == nsub && warp < nwork_warps)
                 warp_partials<V>(acc, s->red, lane, warp);
@@ -993,53 +1025,19 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             if (q + 1 < nsub)
                 __syncthreads();  // publish the next unit
         }
-        // ---- critical path: totals -> pieces (warps 0..PW-1) -> loop_fast
-        if (warp < PW || warp == ctl) {
-            if (warp == 0)
-                warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
-            asm volatile("bar.sync 1, %0;" ::"r"(named) : "memory");
+        // ---- critical path, all on warp 0 in SIMT form (no cross-warp
+        // hand-off): totals -> one atan2 / sqrt / fmod / division per lane
+        // -> loop_fast on lane 0 -> next epoch's constants, rotators, ranges
+        if (warp == 0) {
             if (tid == 0)
                 PROF_STAMP(4);
-            const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, c.n);
-            if (warp < PW && lane == 0)
-                for (int piece = warp; piece < LOOP_PIECES; piece += PW) {
-                    const long long p0 = clock64();
-                    loop_piece(piece, s->pre, s->ch, o, a.lc, c);
-                    if (a.prof && blockIdx.x == 0 && e < 64)
-                        a.prof[64 * 8 + e * 8 + piece] = clock64() - p0;
-                }
-            asm volatile("bar.sync 1, %0;" ::"r"(named) : "memory");
+            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane);
             if (tid == 0)
                 PROF_STAMP(5);
-            if (warp == 0) {
-                if (lane == 0) {
-                    l1rxg_channel& ch = s->ch;
-                    if (ch.state == L1RXG_IDLE) {
-                        s->stop = 1;  // the previous epoch dropped the channel
-                    } else {
-                        const LoopPre pre = s->pre;
-                        // correlator inputs for the record (the control
-                        // warp assembles the rest from the post-update state)
-                        l1rxg_epoch_record& r = s->rec;
-                        r.sample_offset_start = off;
-                        r.code_phase_in = ch.code_phase_chips;
-                        r.code_freq_in = ch.code_freq_hz;
-                        r.carrier_doppler_in = ch.carrier_doppler_hz;
-                        r.carrier_phase_in = ch.carrier_phase_rad;
-                        s->rec_esh = ch.epochs_since_handoff;
-                        s->rec_eenv = pre.e + pre.l;
-                        loop_fast(ch, o, a.lc, pre);
-                        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz,
-                                    ch.carrier_doppler_hz, ch.carrier_phase_rad, a.lc.fs, n);
-                        s->rec_slot = (int64_t)cidx * a.max_records + (done % a.max_records);
-                        s->pending = 1;
-                    }
-                }
-                __syncwarp();
-                fill_rot(s->rot, s->c.w, lane);
-                if (tid == 0)
-                    PROF_STAMP(6);
-            }
+            fill_rot(s->rot, s->c.w, lane);
+            fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, nsub, lane);
+            if (tid == 0)
+                PROF_STAMP(6);
         }
         __syncthreads();
         if (tid == 0)
@@ -1098,6 +1096,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
     }
     build_code_tables(s->ct, a.codes, a.prns[j]);  // ends with a barrier
     fill_rot(s->rot, s->c.w, tid);
+    if (warp == 0)
+        fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, (n + cap - 1) / cap, lane);
     const EpochConsts c = s->c;
     float acc[V];
 #pragma unroll
@@ -1116,7 +1116,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
                 phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
                                     acc, &s->anchors[tid]);
             __syncthreads();
-            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc, blockDim.x);
+            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc, blockDim.x,
+                       s->trange + (u0 / cap) * T);
             __syncthreads();
         }
     }

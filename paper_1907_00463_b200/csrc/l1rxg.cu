@@ -462,6 +462,8 @@ int l1rxg_correlate_batch(l1rxg_ctx* c, const double* iq, int n, int n_jobs,
         return set_err(L1RXG_EINVAL, "null context");
     if (n <= 0)
         return set_err(L1RXG_EINVAL, "empty epoch view");  // tracking.hpp:232-233
+    if (n > MAXSUB * (MAX_NT - 32) * RUN)
+        return set_err(L1RXG_EINVAL, "epoch longer than the correlator supports (fs <= 150 MHz)");
     if (n_jobs <= 0)
         return 0;
     if (int rc = validate_taps(taps))
@@ -575,6 +577,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     const int n = static_cast<int>(std::llround(d->sample_rate_hz / 1000.0));
     if (d->ring_samples < 2 * (int64_t)n)
         return set_err(L1RXG_EINVAL, "ring_samples must hold at least two epochs");
+    if (n > MAXSUB * (MAX_NT - 32) * RUN)
+        return set_err(L1RXG_EINVAL, "epoch longer than the correlator supports (fs <= 150 MHz)");
     for (int k = 0; k < d->n_channels; ++k) {
         if (chan_stream[k] < 0 || chan_stream[k] >= d->n_streams)
             return set_err(L1RXG_EINVAL, "channel bound to a missing stream");
@@ -756,8 +760,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     static const bool prof = std::getenv("L1RXG_PROF") != nullptr;
     long long* dprof = nullptr;
     if (prof) {
-        CK(cudaMalloc(&dprof, 2 * 64 * 8 * sizeof(long long)));
-        CK(cudaMemsetAsync(dprof, 0, 2 * 64 * 8 * sizeof(long long), st));
+        CK(cudaMalloc(&dprof, 3 * 64 * 8 * sizeof(long long)));
+        CK(cudaMemsetAsync(dprof, 0, 3 * 64 * 8 * sizeof(long long), st));
     }
     a.prof = dprof;
     auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st); };
@@ -767,11 +771,11 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     cudaEventRecord(e1, st);
     t->timed.push_back({e0, e1, 1});
     if (prof) {
-        long long h[2 * 64 * 8];
+        long long h[3 * 64 * 8];
         CK(cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         cudaFree(dprof);
-        double acc[8] = {0}, pc[8] = {0};
+        double acc[8] = {0}, pc[8] = {0}, arr[8] = {0};
         int cnt = 0;
         for (int e = 2; e < 64; ++e) {
             if (h[e * 8 + 7] == 0 || h[e * 8] == 0)
@@ -781,16 +785,23 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             acc[0] += static_cast<double>(h[e * 8 + 7] - h[e * 8]);
             for (int k = 0; k < 8; ++k)
                 pc[k] += static_cast<double>(h[512 + e * 8 + k]);
+            for (int k = 0; k < 8; ++k)
+                arr[k] += static_cast<double>(h[1024 + e * 8 + k]);
             ++cnt;
         }
         if (cnt)
             std::fprintf(stderr,
                          "[l1rxg prof] cycles/epoch %.0f | A %.0f | barA %.0f | B+red %.0f | "
                          "totals %.0f | pieces %.0f | apply %.0f | bar %.0f | per piece %.0f %.0f "
-                         "%.0f %.0f %.0f\n",
+                         "%.0f %.0f %.0f | loop_fast %.0f consts %.0f warp0_totals %.0f\n",
                          acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
                          acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, pc[0] / cnt, pc[1] / cnt,
-                         pc[2] / cnt, pc[3] / cnt, pc[4] / cnt);
+                         pc[2] / cnt, pc[3] / cnt, pc[4] / cnt, pc[5] / cnt, pc[6] / cnt,
+                         pc[7] / cnt);
+        if (cnt)
+            std::fprintf(stderr, "[l1rxg prof] B1->B2-arrive per warp 0..4: %.0f %.0f %.0f %.0f %.0f ctl %.0f\n",
+                         arr[0] / cnt, arr[1] / cnt, arr[2] / cnt, arr[3] / cnt, arr[4] / cnt,
+                         arr[7] / cnt);
     }
     return 0;
 }
