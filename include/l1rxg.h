@@ -299,6 +299,9 @@ int l1rxg_search_grid(l1rxg_ctx* ctx, int format, const void* bytes,
                       int n_blocks, const int32_t* prns, int n_prns,
                       const double* doppler_bins_hz, int n_bins,
                       int delay_step, int n_delays, double* plane_out);
+/* Device time of the last l1rxg_search_grid: ingest + fold, correlation. */
+int l1rxg_search_grid_timing(l1rxg_ctx* ctx, double* ingest_fold_ms,
+                             double* corr_ms);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@
 
 #include "correlator.cuh"
 #include "ingest.cuh"
+#include "search.cuh"
 #include "l1rxg.h"
 
 using namespace l1rxg;
@@ -244,6 +245,9 @@ struct l1rxg_ctx {
     cudaStream_t compute = nullptr, copy = nullptr;
     int8_t* d_codes = nullptr;
     DevBuf iq64, iq32, states, prns, sums, corr;
+    DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
+    cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
+    double grid_ms[2] = {0, 0};
     std::mutex mu;  // serialises the per-call path
     int64_t launches = 0;
 };
@@ -432,7 +436,11 @@ int l1rxg_destroy(l1rxg_ctx* c) {
         return 0;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    for (DevBuf* b : {&c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr})
+    for (auto e : c->gev)
+        if (e)
+            cudaEventDestroy(e);
+    for (DevBuf* b : {&c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
+                      &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist})
         b->release();
     cudaFree(c->d_codes);
     cudaStreamDestroy(c->compute);
@@ -960,9 +968,118 @@ int l1rxg_tracker_timing(l1rxg_tracker* t, double* ingest_ms, double* track_ms, 
     return 0;
 }
 
-int l1rxg_search_grid(l1rxg_ctx*, int, const void*, int, int64_t, double, double, int,
-                      const int32_t*, int, const double*, int, int, int, double*) {
-    return set_err(L1RXG_EINVAL, "search grid: not built in this version");
+int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_device,
+                      int64_t nbytes, double fs, double if_hz, int n_blocks, const int32_t* prns,
+                      int n_prns, const double* bins, int n_bins, int delay_step, int n_delays,
+                      double* plane_out) {
+    if (!c || !bytes || !prns || !bins || !plane_out)
+        return set_err(L1RXG_EINVAL, "null argument");
+    const int bps = bytes_per_sample(format);
+    if (bps == 0)
+        return set_err(L1RXG_EINVAL, "format must be int8_iq, int16_iq or int8_real_if");
+    // the direct half-chip identity needs an integer number of samples per
+    // half chip, and delays on that grid (config 5: 8 samples at 16.368 MHz)
+    const double spc_d = fs / CHIP_RATE_HZ / 2.0;
+    const int spc = static_cast<int>(std::llround(spc_d));
+    if (spc < 1 || std::fabs(spc_d - spc) > 1e-9)
+        return set_err(L1RXG_EINVAL, "search grid needs fs = 2*k*1.023 MHz (integer samples per half chip)");
+    if (delay_step != spc)
+        return set_err(L1RXG_EINVAL, "search grid delay_step must be half a chip (fs/2.046 MHz samples)");
+    const int N = 2 * GRID_CHIPS * spc;
+    if (n_delays < 1 || n_delays > 2 * GRID_CHIPS)
+        return set_err(L1RXG_EINVAL, "n_delays must be in 1..2046");
+    if (n_blocks < 1 || n_blocks > 24)
+        return set_err(L1RXG_EINVAL, "n_blocks must be in 1..24");
+    if (n_prns < 1 || n_bins < 1)
+        return set_err(L1RXG_EINVAL, "need at least one PRN and one Doppler bin");
+    for (int k = 0; k < n_prns; ++k)
+        if (prns[k] < 1 || prns[k] > 32)
+            return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
+    const bool is_if = format == L1RXG_FMT_INT8_REAL_IF;
+    if (is_if && !(if_hz > 0.0 && if_hz < fs / 2.0))
+        return set_err(L1RXG_EINVAL, "if_frequency_hz required in (0, fs/2) for Int8RealIF");
+    const int64_t nsamp = static_cast<int64_t>(n_blocks) * N;
+    if (nbytes < nsamp * bps)
+        return set_err(L1RXG_EINVAL, "not enough bytes for n_blocks 1-ms blocks");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->compute;
+    if (!c->gev[0])
+        for (auto& e : c->gev)
+            CK(cudaEventCreate(&e));
+    if (c->gbase.ensure(sizeof(float2) * (nsamp + 64)) || c->gF.ensure(sizeof(float2) * 2 * GRID_CHIPS * n_bins * n_blocks) ||
+        c->gplane.ensure(sizeof(float) * 2 * GRID_CHIPS * n_bins * n_prns) || c->gbins.ensure(8 * n_bins) ||
+        c->gprns.ensure(4 * n_prns) || c->ghist.ensure(64 * sizeof(float2)))
+        return L1RXG_ENOMEM;
+    const void* raw = bytes;
+    if (!bytes_on_device) {
+        if (c->graw.ensure(static_cast<size_t>(nsamp * bps)))
+            return L1RXG_ENOMEM;
+        CK(cudaMemcpyAsync(c->graw.p, bytes, nsamp * bps, cudaMemcpyHostToDevice, st));
+        raw = c->graw.p;
+    }
+    CK(cudaMemcpyAsync(c->gbins.p, bins, 8 * n_bins, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->gprns.p, prns, 4 * n_prns, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(c->ghist.p, 0, 64 * sizeof(float2), st));
+    float2* base = static_cast<float2*>(c->gbase.p);
+    CK(cudaEventRecord(c->gev[0], st));
+    // K1 ingest of the n_blocks blocks (a flat ring: R = nsamp, no apron)
+    if (is_if) {
+        const double w = -2.0 * PI_D * if_hz / fs;
+        if (w == -PI_D / 2.0) {
+            const unsigned blocks = static_cast<unsigned>((nsamp + ING_TILE - 1) / ING_TILE);
+            ingest_if4_kernel<<<blocks, ING_TPB, 0, st>>>(
+                static_cast<const int8_t*>(raw), static_cast<const int8_t*>(c->ghist.p),
+                static_cast<int8_t*>(c->ghist.p) + 32, 0, nsamp, base, nsamp, 0, 0, nullptr);
+        } else {
+            DevBuf& mixed = c->iq32;  // reuse as float2 scratch
+            if (mixed.ensure(sizeof(float2) * (nsamp + 22)))
+                return L1RXG_ENOMEM;
+            float2* mx = static_cast<float2*>(mixed.p);
+            CK(cudaMemsetAsync(mx, 0, 22 * sizeof(float2), st));
+            const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
+            mix_generic_kernel<<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(raw), 0, nsamp, w, mx);
+            fir_generic_kernel<<<blocks, 256, 0, st>>>(mx, nsamp, base, nsamp, 0, 0,
+                                                       static_cast<float2*>(c->ghist.p), nullptr, 0);
+        }
+    } else {
+        const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
+        decode_iq_kernel<<<blocks, 256, 0, st>>>(raw, format, nsamp, base, nsamp, 0, 0, nullptr, 0);
+    }
+    CK(cudaGetLastError());
+    grid_fold_kernel<<<n_bins * n_blocks, 256, 2 * GRID_CHIPS * sizeof(float2), st>>>(
+        base, N, spc, static_cast<const double*>(c->gbins.p), fs, n_blocks,
+        static_cast<float2*>(c->gF.p));
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->gev[1], st));
+    const size_t sm = 2 * 1024 * sizeof(float) + sizeof(float2) * GRID_CHIPS * n_blocks;
+    CK(cudaFuncSetAttribute(grid_corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    grid_corr_kernel<<<n_prns * n_bins * 2, GRID_TPB, sm, st>>>(
+        static_cast<const float2*>(c->gF.p), c->d_codes, static_cast<const int32_t*>(c->gprns.p), n_bins,
+        n_blocks, static_cast<float>(N), static_cast<float*>(c->gplane.p));
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->gev[2], st));
+    std::vector<float> pl(static_cast<size_t>(2 * GRID_CHIPS) * n_bins * n_prns);
+    CK(cudaMemcpyAsync(pl.data(), c->gplane.p, pl.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms0 = 0, ms1 = 0;
+    cudaEventElapsedTime(&ms0, c->gev[0], c->gev[1]);
+    cudaEventElapsedTime(&ms1, c->gev[1], c->gev[2]);
+    c->grid_ms[0] = ms0;
+    c->grid_ms[1] = ms1;
+    c->launches += 3;
+    for (int64_t r = 0; r < static_cast<int64_t>(n_bins) * n_prns; ++r)
+        for (int k = 0; k < n_delays; ++k)
+            plane_out[r * n_delays + k] = pl[static_cast<size_t>(r * 2 * GRID_CHIPS + k)];
+    return 0;
+}
+
+int l1rxg_search_grid_timing(l1rxg_ctx* c, double* ingest_fold_ms, double* corr_ms) {
+    if (!c)
+        return set_err(L1RXG_EINVAL, "null context");
+    if (ingest_fold_ms) *ingest_fold_ms = c->grid_ms[0];
+    if (corr_ms) *corr_ms = c->grid_ms[1];
+    return 0;
 }
 
 }  // extern "C"

@@ -1,0 +1,143 @@
+// search.cuh -- K4: correlator-bank search grid (BASELINE config 5), sm_100a.
+//
+// Semantics: acquire_pcs's plane (acquisition.hpp:189-222): for PRN p,
+// Doppler bin f and 1-ms segment s, the carrier is wiped with
+// e^{-j 2 pi f n / fs} anchored at the global sample index n
+// (wipe_carrier, :170-182), circularly correlated with the zero-order-hold
+// code, and |.| is accumulated over segments; FFTW's inverse is
+// unnormalised (fft.hpp:17-19), so a cell is N * |sum_n wiped[n] code[(n-d) mod N]|.
+//
+// Evaluated directly at the half-chip delays d = k * spc (spc = samples per
+// half chip, an integer at the config rates, e.g. 8 at 16.368 MHz) through an
+// exact identity: the ZOH code is constant over each chip, so with
+//   F0[c] = sum of the wiped samples of chip c,
+//   F1[c] = the same shifted by half a chip,
+// corr[d = 2j*spc]     = sum_c F0[c] chip[(c - j) mod 1023]
+// corr[d = (2j+1)*spc] = sum_c F1[c] chip[(c - j) mod 1023]
+// i.e. two 1023-point circular correlations per (PRN, bin, segment) instead of
+// N x 2046 multiply-adds.  K4a folds (per bin and segment, shared by all PRNs);
+// K4b is a register-tiled circulant +-1 correlation on the FP32 pipes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace l1rxg {
+
+constexpr int GRID_CHIPS = 1023;
+
+// K4a: one CTA per (bin, segment).  x: baseband [n_seg][N]; F out:
+// [bin][seg][2][1023] float2.  spc = samples per half chip.
+__global__ void __launch_bounds__(256) grid_fold_kernel(const float2* __restrict__ x, int N, int spc,
+                                                        const double* __restrict__ bins, double fs,
+                                                        int n_seg, float2* F) {
+    extern __shared__ float2 hsum[];  // [2 * 1023] half-chip sums
+    const int bin = blockIdx.x / n_seg, seg = blockIdx.x % n_seg;
+    const double w = -2.0 * 3.14159265358979323846 * bins[bin] / fs;  // wipe_carrier :172
+    const int nh = 2 * GRID_CHIPS;
+    const float2* xs = x + (int64_t)seg * N;
+    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+        // anchor at the half chip's first sample (global index), fp64 reduced
+        const int64_t n0 = (int64_t)seg * N + (int64_t)h * spc;
+        const double th = w * (double)n0;
+        const double r = fma(-rint(th * (1.0 / (2.0 * 3.14159265358979323846))),
+                             2.0 * 3.14159265358979323846, th);
+        float sa, ca;
+        sincosf((float)r, &sa, &ca);
+        float ws, wc;
+        sincosf((float)w, &ws, &wc);
+        float cr = ca, ci = sa, accr = 0.f, acci = 0.f;
+        for (int k = 0; k < spc; ++k) {  // x * e^{j(th + w k)}
+            const float2 v = xs[h * spc + k];
+            accr = fmaf(v.x, cr, fmaf(-v.y, ci, accr));
+            acci = fmaf(v.x, ci, fmaf(v.y, cr, acci));
+            const float nr = cr * wc - ci * ws;
+            ci = cr * ws + ci * wc;
+            cr = nr;
+        }
+        hsum[h] = make_float2(accr, acci);
+    }
+    __syncthreads();
+    float2* Fo = F + ((int64_t)bin * n_seg + seg) * 2 * GRID_CHIPS;
+    for (int c = threadIdx.x; c < GRID_CHIPS; c += blockDim.x) {
+        const float2 a = hsum[2 * c], b = hsum[2 * c + 1], d = hsum[(2 * c + 2) % nh];
+        Fo[c] = make_float2(a.x + b.x, a.y + b.y);                      // F0
+        Fo[GRID_CHIPS + c] = make_float2(b.x + d.x, b.y + d.y);         // F1
+    }
+}
+
+// K4b: one CTA per (PRN, bin, parity); the n_seg vectors of that (bin,
+// parity) sit in shared memory; thread t owns shifts j = t + 256 q (q < 4),
+// vectors in groups of VG; cells accumulate N * |corr| over segments.
+constexpr int GRID_TPB = 256;
+constexpr int GRID_SH = 4;   // shifts per thread (4 * 256 >= 1023)
+constexpr int GRID_VG = 5;   // vectors per register group
+
+__global__ void __launch_bounds__(GRID_TPB) grid_corr_kernel(const float2* __restrict__ F,
+                                                             const int8_t* __restrict__ codes,
+                                                             const int32_t* __restrict__ prns,
+                                                             int n_bins, int n_seg, float scale,
+                                                             float* plane /*[prn][bin][2046]*/) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    float* cd = reinterpret_cast<float*>(sm);                 // chips doubled [2 * 1024]
+    float2* fv = reinterpret_cast<float2*>(sm + 2 * 1024 * 4);  // [n_seg][1023]
+    const int par = blockIdx.x & 1;
+    const int bin = (blockIdx.x >> 1) % n_bins;
+    const int pi = (blockIdx.x >> 1) / n_bins;
+    const int8_t* code = codes + prns[pi] * GRID_CHIPS;
+    // cd[u] = chip[(u - 1023) mod 1023] for u in [0, 2046): chip[(c - j) mod 1023] = cd[c - j + 1023]
+    for (int u = threadIdx.x; u < 2 * GRID_CHIPS; u += blockDim.x)
+        cd[u] = (float)code[u % GRID_CHIPS];
+    for (int s = 0; s < n_seg; ++s)
+        for (int c = threadIdx.x; c < GRID_CHIPS; c += blockDim.x)
+            fv[s * GRID_CHIPS + c] =
+                F[(((int64_t)bin * n_seg + s) * 2 + par) * GRID_CHIPS + c];
+    __syncthreads();
+    float mag[GRID_SH];
+#pragma unroll
+    for (int q = 0; q < GRID_SH; ++q)
+        mag[q] = 0.f;
+    const int j0 = threadIdx.x;
+    for (int s0 = 0; s0 < n_seg; s0 += GRID_VG) {
+        float ar[GRID_SH][GRID_VG], ai[GRID_SH][GRID_VG];
+#pragma unroll
+        for (int q = 0; q < GRID_SH; ++q)
+#pragma unroll
+            for (int v = 0; v < GRID_VG; ++v)
+                ar[q][v] = ai[q][v] = 0.f;
+        const int nv = min(GRID_VG, n_seg - s0);
+#pragma unroll 2
+        for (int c = 0; c < GRID_CHIPS; ++c) {
+            float ch[GRID_SH];
+#pragma unroll
+            for (int q = 0; q < GRID_SH; ++q) {
+                const int j = j0 + q * GRID_TPB;
+                ch[q] = j < GRID_CHIPS ? cd[c - j + GRID_CHIPS] : 0.f;
+            }
+#pragma unroll
+            for (int v = 0; v < GRID_VG; ++v) {
+                const float2 f = v < nv ? fv[(s0 + v) * GRID_CHIPS + c] : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < GRID_SH; ++q) {
+                    ar[q][v] = fmaf(ch[q], f.x, ar[q][v]);
+                    ai[q][v] = fmaf(ch[q], f.y, ai[q][v]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < GRID_SH; ++q)
+#pragma unroll
+            for (int v = 0; v < GRID_VG; ++v)
+                if (v < nv)
+                    mag[q] += scale * sqrtf(fmaf(ar[q][v], ar[q][v], ai[q][v] * ai[q][v]));
+    }
+    float* row = plane + ((int64_t)pi * n_bins + bin) * (2 * GRID_CHIPS);
+#pragma unroll
+    for (int q = 0; q < GRID_SH; ++q) {
+        const int j = j0 + q * GRID_TPB;
+        if (j < GRID_CHIPS)
+            row[2 * j + par] = mag[q];
+    }
+}
+
+}  // namespace l1rxg

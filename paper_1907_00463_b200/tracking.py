@@ -136,6 +136,50 @@ class Context:
         return sums, [corr[k] for k in range(nj)]
 
 
+def search_grid(ctx: "Context", raw, fmt: int, fs: float, if_hz: float, n_blocks: int, prns, bins,
+                n_delays: int | None = None, device_ptr: int | None = None) -> np.ndarray:
+    """acquire_pcs plane semantics (acquisition.hpp:170-222) on the GPU:
+    returns plane[prn][bin][delay] for delays d = k * (samples per half chip),
+    cells N * |sum_n wiped[n] code[(n - d) mod N]| summed over n_blocks
+    1-ms segments.  raw: host bytes, or device_ptr for bytes in HBM."""
+    spc = int(round(fs / 1.023e6 / 2.0))
+    nd = n_delays or 2046
+    prns = np.ascontiguousarray(prns, np.int32)
+    bins = np.ascontiguousarray(bins, np.float64)
+    plane = np.zeros((prns.size, bins.size, nd), np.float64)
+    if device_ptr is not None:
+        ptr, on_dev, nbytes = C.c_void_p(device_ptr), 1, int(raw)
+    else:
+        a = np.ascontiguousarray(raw).view(np.uint8)
+        ptr, on_dev, nbytes = a.ctypes.data_as(C.c_void_p), 0, a.nbytes
+    check(ctx._lib.l1rxg_search_grid(ctx.handle, fmt, ptr, on_dev, nbytes, fs, if_hz, n_blocks,
+                                     prns.ctypes.data_as(C.POINTER(C.c_int32)), prns.size,
+                                     bins.ctypes.data_as(_dp), bins.size, spc, nd,
+                                     plane.ctypes.data_as(_dp)))
+    return plane
+
+
+def search_grid_timing(ctx: "Context"):
+    a, b = C.c_double(), C.c_double()
+    check(ctx._lib.l1rxg_search_grid_timing(ctx.handle, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def pick_peak(plane_row: np.ndarray, bins, fs: float):
+    """detail::pick_peak (acquisition.hpp:114-149) over one PRN's plane
+    [bin][delay] on the half-chip delay grid: (bin, delay index, ratio) with
+    the runner-up taken outside +-1 chip of the peak's code phase."""
+    nb, nd = plane_row.shape
+    best = int(np.argmax(plane_row))
+    pb, pd = divmod(best, nd)
+    d = np.arange(nd)
+    dist = np.minimum(np.abs(d - pd), nd - np.abs(d - pd))
+    mask = dist > 2  # half-chip grid: +-1 chip = 2 delay steps
+    runner = plane_row[:, mask].max() if mask.any() else 0.0
+    ratio = plane_row[pb, pd] / runner if runner > 0 else float("inf")
+    return pb, pd, ratio
+
+
 def _store_nco(ch, nco: abi.Nco) -> None:
     ch.code_phase_chips = nco.code_phase_chips
     ch.code_freq_hz = nco.code_freq_hz

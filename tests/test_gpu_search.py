@@ -1,0 +1,50 @@
+"""Config 5 search grid (K4) on the GPU against the oracle's direct
+time-domain restatement of acquire_pcs's plane (acquisition.hpp:170-222,
+oracle/l1rx_oracle.c orc_search_grid)."""
+import numpy as np
+import pytest
+
+from paper_1907_00463_b200 import abi, simsource as ss
+from paper_1907_00463_b200.tracking import pick_peak, search_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _plane_oracle(oracle_mod, x, N, n_seg, prns, fs, bins, spc):
+    return np.stack([oracle_mod.search_grid(x, N, n_seg, p, fs, bins, spc, 2 * N // (2 * spc))
+                     for p in prns])
+
+
+@pytest.mark.parametrize("fs,fmt,ifz", [(2.046e6, abi.FMT_INT16_IQ, 0.0),
+                                        (16.368e6, abi.FMT_INT8_REAL_IF, 4.092e6)])
+def test_grid_matches_oracle(ctx, oracle_mod, fs, fmt, ifz):
+    spc = int(round(fs / 2.046e6))
+    N = int(round(fs / 1000))
+    svs = [ss.Sv(prn=13, cn0_dbhz=48.0, doppler_hz=1500.0, delay_chips=200.3),
+           ss.Sv(prn=4, cn0_dbhz=44.0, doppler_hz=-2500.0, delay_chips=771.0)]
+    n_seg = 3
+    tag = "int16_iq" if fmt == abi.FMT_INT16_IQ else "int8_real_if"
+    raw = ss.synth(n_seg, fs, svs, fmt=tag, if_hz=ifz, seed=5, device="cuda").cpu().numpy()
+    prns = [13, 4, 9] if fs < 5e6 else [13]
+    bins = np.arange(-5000.0, 5000.1, 500.0) if fs < 5e6 else np.array([1000.0, 1500.0, 2000.0])
+    gpu = search_grid(ctx, raw, fmt, fs, ifz, n_seg, prns, bins)
+    x = oracle_mod.ingest(raw, fmt, fs, ifz)
+    want = _plane_oracle(oracle_mod, x, N, n_seg, prns, fs, bins, spc)
+    scale = want.max()
+    err = np.abs(gpu - want).max() / scale
+    print("grid max err / max cell %.3g" % err)
+    assert err < 1e-5
+    # the detection itself (peak cell, test_acquisition.cpp:145-160)
+    for i, p in enumerate(prns):
+        assert np.unravel_index(np.argmax(gpu[i]), gpu[i].shape) == \
+            np.unravel_index(np.argmax(want[i]), want[i].shape)
+    pb, pd, ratio = pick_peak(gpu[0], bins, fs)
+    assert bins[pb] == 1500.0 and abs(pd * 0.5 - 200.3) < 0.6 and ratio > 2.0
+
+
+def test_grid_rejects_unsupported_rates(ctx):
+    raw = np.zeros(5000 * 2, np.int8)
+    with pytest.raises(ValueError):
+        search_grid(ctx, raw, abi.FMT_INT8_IQ, 5e6, 0.0, 1, [1], [0.0])
+    with pytest.raises(IndexError):
+        search_grid(ctx, np.zeros(2046 * 4, np.int8), abi.FMT_INT16_IQ, 2.046e6, 0.0, 1, [33], [0.0])
