@@ -235,10 +235,19 @@ typedef struct {
     int32_t n_channels;
     int64_t ring_samples;      /* per-stream device ring capacity       */
     int32_t max_records;       /* per-channel record ring capacity      */
-    int32_t pad_;
+    /* CTA shape: 0 = auto.  L1RXG_CTA_LATENCY: one wide CTA per channel
+     * (few channels: the per-epoch critical path is what matters);
+     * L1RXG_CTA_THROUGHPUT: narrower CTAs, two resident per SM so one
+     * channel's serial loop update overlaps another's correlation (many
+     * channels).  auto picks throughput when n_channels >= 2 x SMs. */
+    int32_t cta_mode;
     l1rxg_taps taps;
     l1rxg_tracking_cfg cfg;
 } l1rxg_tracker_desc;
+
+#define L1RXG_CTA_AUTO 0
+#define L1RXG_CTA_LATENCY 1
+#define L1RXG_CTA_THROUGHPUT 2
 
 int l1rxg_tracker_create(l1rxg_ctx* ctx, const l1rxg_tracker_desc* desc,
                          const l1rxg_channel* channels,
@@ -255,6 +264,18 @@ int l1rxg_tracker_push(l1rxg_tracker* trk, int stream, const void* bytes,
 /* Same, from bytes already resident in device memory. */
 int l1rxg_tracker_push_device(l1rxg_tracker* trk, int stream,
                               const void* dev_bytes, int64_t nbytes);
+/* Host-memory variant: one pitched H2D copy (host stream s at
+ * bytes + s * stride_bytes) into the staging block, then the strided
+ * device push.  Asynchronous like l1rxg_tracker_push. */
+int l1rxg_tracker_push_strided(l1rxg_tracker* trk, const void* bytes,
+                               int64_t nbytes_per_stream, int64_t stride_bytes);
+/* Appends nbytes_per_stream to EVERY stream in one launch: stream s reads
+ * dev_bytes + s * stride_bytes (device memory).  All streams must be at the
+ * same sample count (the batched-recordings case, BASELINE config 4: one
+ * SampleSource per recording, samples.hpp:136-211, fed in lock step). */
+int l1rxg_tracker_push_device_strided(l1rxg_tracker* trk, const void* dev_bytes,
+                                      int64_t nbytes_per_stream,
+                                      int64_t stride_bytes);
 /* Runs every channel over every epoch whose 1-ms window is fully
  * ingested (at most max_epochs per channel; <0 = unbounded).  Async. */
 int l1rxg_tracker_run(l1rxg_tracker* trk, int max_epochs);

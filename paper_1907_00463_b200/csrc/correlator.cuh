@@ -108,7 +108,7 @@ __device__ __forceinline__ float2 wipe(float2 x, float c, float s) {
 struct CodeTables {
     float chipf[CHIP_EXT];
     int16_t tm[TRANS_EXT];
-    float td[TRANS_EXT];
+    int8_t td[TRANS_EXT];
     int16_t cum[1024];
     int L;
 };
@@ -148,7 +148,7 @@ __device__ void build_code_tables(CodeTables& ct, const int8_t* codes, int prn) 
         const int p = g / L, q = g - p * L;
         const int r = ct.tm[q];  // q < L: first-period entries are final
         const int m = p * 1023 + r;
-        const float dlt = (float)c[r] - (float)c[(r + 1022) % 1023];
+        const int8_t dlt = (int8_t)(c[r] - c[(r + 1022) % 1023]);
         if (g >= L)
             ct.tm[g] = (int16_t)(m < 32767 ? m : 32767);
         ct.td[g] = dlt;
@@ -265,7 +265,7 @@ __device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile
         for (; j < cntk; j += nthreads) {
             const int g = g0 + j;
             const int m = ct.tm[g];
-            const float dlt = ct.td[g];
+            const float dlt = (float)ct.td[g];
             const int b = tap_boundary(m, dk, c, u0, hi);
             const int off = b - u0;
             const float2 p = tile_d[off];

@@ -143,6 +143,34 @@ __global__ void decode_iq_kernel(const void* __restrict__ raw, int fmt, int64_t 
         *avail_slot = avail_value;
 }
 
+// The same decode for many streams in one launch (blockIdx.y = stream):
+// stream s reads raw + s * raw_stride bytes and writes ring + s * ring_stride.
+__global__ void decode_iq_strided_kernel(const uint8_t* __restrict__ raw, int64_t raw_stride, int fmt,
+                                         int64_t count, float2* ring, int64_t ring_stride, int64_t R,
+                                         int64_t apron, int64_t pos0, int64_t* avail,
+                                         int64_t avail_value) {
+    const int s = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint8_t* rs = raw + (int64_t)s * raw_stride;
+    float2* rg = ring + (int64_t)s * ring_stride;
+    if (i < count) {
+        float2 v;
+        if (fmt == L1RXG_FMT_INT8_IQ) {
+            const char2 b = reinterpret_cast<const char2*>(rs)[i];
+            v = make_float2((float)b.x * (1.0f / 128.0f), (float)b.y * (1.0f / 128.0f));
+        } else {
+            const short2 b = reinterpret_cast<const short2*>(rs)[i];
+            v = make_float2((float)b.x * (1.0f / 32768.0f), (float)b.y * (1.0f / 32768.0f));
+        }
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        ring_put(rg, R, apron, pos, v);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        avail[s] = avail_value;
+}
+
 // complex<double> -> float2 (per-call path)
 __global__ void cf64_to_f32_kernel(const double2* __restrict__ in, float2* out, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -154,7 +154,7 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
 
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
-    const size_t sm = smem_bytes<T>(nt);
+    const size_t sm = smem_bytes<T>(nt - 32);  // the control warp owns no tile runs
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     track_kernel<T><<<n_ch, nt, sm, s>>>(a);
     CK(cudaGetLastError());
@@ -604,7 +604,16 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     t->d = *d;
     t->T = pick_T(d->taps.n_taps);
     // correlation warps + one control warp (see track_kernel)
-    t->nt = pick_threads(n, nullptr, MAX_NT - 32) + 32;
+    {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+        const bool thr = d->cta_mode == L1RXG_CTA_THROUGHPUT ||
+                         (d->cta_mode == L1RXG_CTA_AUTO && d->n_channels >= 2 * nsm);
+        // throughput: 9 correlation warps + control warp, ~112 KB of shared
+        // memory at 7 taps -> two CTAs per SM; latency: up to 19 warps, one
+        // CTA per SM
+        t->nt = pick_threads(n, nullptr, thr ? 288 : MAX_NT - 32) + 32;
+    }
     t->R = d->ring_samples;
     // apron >= one epoch (+ bulk-copy slack); R + apron even keeps every
     // stream's ring 16-byte aligned for the TMA copies
@@ -706,6 +715,86 @@ int l1rxg_tracker_push_device(l1rxg_tracker* t, int s, const void* dev_bytes, in
         return set_err(L1RXG_EINVAL, "push larger than the device ring");
     CK(cudaSetDevice(t->ctx->device));
     return ingest_launch(t, s, dev_bytes, nsamp, t->ctx->compute);
+}
+
+int l1rxg_tracker_push_device_strided(l1rxg_tracker* t, const void* dev_bytes,
+                                      int64_t nbytes_per_stream, int64_t stride_bytes) {
+    if (!t || !dev_bytes)
+        return set_err(L1RXG_EINVAL, "null argument");
+    const int bps = bytes_per_sample(t->d.format);
+    if (nbytes_per_stream <= 0)
+        return 0;
+    if (nbytes_per_stream % bps || stride_bytes % bps)
+        return set_err(L1RXG_EINVAL, "byte count or stride is not a whole number of samples");
+    if (stride_bytes < nbytes_per_stream)
+        return set_err(L1RXG_EINVAL, "stride shorter than the per-stream chunk");
+    const int64_t nsamp = nbytes_per_stream / bps;
+    if (nsamp > t->R - t->nt)
+        return set_err(L1RXG_EINVAL, "push larger than the device ring");
+    CK(cudaSetDevice(t->ctx->device));
+    if (t->d.format == L1RXG_FMT_INT8_REAL_IF) {  // FIR history per stream: one launch each
+        for (size_t s = 0; s < t->streams.size(); ++s)
+            if (int rc = ingest_launch(t, static_cast<int>(s),
+                                       static_cast<const uint8_t*>(dev_bytes) + s * stride_bytes,
+                                       nsamp, t->ctx->compute))
+                return rc;
+        return 0;
+    }
+    const int64_t g0 = t->streams[0].pushed;
+    for (const auto& r : t->streams)
+        if (r.pushed != g0)
+            return set_err(L1RXG_EINVAL, "strided push needs every stream at the same sample count");
+    cudaStream_t st = t->ctx->compute;
+    cudaEvent_t a = get_event(t), b = get_event(t);
+    cudaEventRecord(a, st);
+    const dim3 grid(static_cast<unsigned>((nsamp + 255) / 256), static_cast<unsigned>(t->streams.size()));
+    decode_iq_strided_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(dev_bytes), stride_bytes,
+                                                   t->d.format, nsamp, t->d_ring, t->R + t->apron, t->R,
+                                                   t->apron, g0 % t->R, t->d_avail, g0 + nsamp);
+    CK(cudaGetLastError());
+    cudaEventRecord(b, st);
+    t->timed.push_back({a, b, 0});
+    t->launches += 1;
+    for (auto& r : t->streams)
+        r.pushed += nsamp;
+    return 0;
+}
+
+int l1rxg_tracker_push_strided(l1rxg_tracker* t, const void* bytes, int64_t nbytes_per_stream,
+                               int64_t stride_bytes) {
+    if (!t || !bytes)
+        return set_err(L1RXG_EINVAL, "null argument");
+    if (nbytes_per_stream <= 0)
+        return 0;
+    const int bps = bytes_per_sample(t->d.format);
+    if (nbytes_per_stream % bps || stride_bytes % bps)
+        return set_err(L1RXG_EINVAL, "byte count or stride is not a whole number of samples");
+    if (stride_bytes < nbytes_per_stream)
+        return set_err(L1RXG_EINVAL, "stride shorter than the per-stream chunk");
+    if (nbytes_per_stream / bps > t->R - t->nt)
+        return set_err(L1RXG_EINVAL, "push larger than the device ring");
+    if (t->d.format != L1RXG_FMT_INT8_REAL_IF)
+        for (const auto& r : t->streams)
+            if (r.pushed != t->streams[0].pushed)
+                return set_err(L1RXG_EINVAL, "strided push needs every stream at the same sample count");
+    CK(cudaSetDevice(t->ctx->device));
+    const size_t ns = t->streams.size();
+    const int k = t->stage_cur;
+    t->stage_cur ^= 1;
+    if (t->staging[k].ensure(static_cast<size_t>(nbytes_per_stream) * ns))
+        return L1RXG_ENOMEM;
+    CK(cudaStreamWaitEvent(t->ctx->copy, t->ev_used[k], 0));
+    // one pitched copy gathers every stream's chunk into a dense staging block
+    CK(cudaMemcpy2DAsync(t->staging[k].p, static_cast<size_t>(nbytes_per_stream), bytes,
+                         static_cast<size_t>(stride_bytes), static_cast<size_t>(nbytes_per_stream), ns,
+                         cudaMemcpyHostToDevice, t->ctx->copy));
+    CK(cudaEventRecord(t->ev_copy[k], t->ctx->copy));
+    CK(cudaStreamWaitEvent(t->ctx->compute, t->ev_copy[k], 0));
+    if (int rc = l1rxg_tracker_push_device_strided(t, t->staging[k].p, nbytes_per_stream,
+                                                   nbytes_per_stream))
+        return rc;
+    CK(cudaEventRecord(t->ev_used[k], t->ctx->compute));
+    return 0;
 }
 
 int l1rxg_tracker_push(l1rxg_tracker* t, int s, const void* bytes, int64_t nbytes) {

@@ -220,7 +220,8 @@ class Tracker:
     def __init__(self, ctx: Context, fmt: int, fs: float, if_hz: float, channels,
                  chan_stream=None, n_streams: int = 1, taps: abi.Taps | None = None,
                  cfg: abi.TrackingCfg | None = None, kernel: int = KERNEL_SCALAR,
-                 ring_samples: int | None = None, max_records: int = 1024):
+                 ring_samples: int | None = None, max_records: int = 1024,
+                 cta_mode: int = abi.CTA_AUTO):
         self.ctx = ctx
         self._lib = ctx._lib
         self.fmt, self.fs, self.if_hz = fmt, fs, if_hz
@@ -235,6 +236,7 @@ class Tracker:
         d.n_streams, d.n_channels = n_streams, len(chans)
         d.ring_samples = ring_samples or 64 * self.n
         d.max_records = max_records
+        d.cta_mode = cta_mode
         d.taps, d.cfg = self.taps, self.cfg
         self.desc = d
         cs = chan_stream if chan_stream is not None else [0] * len(chans)
@@ -264,6 +266,20 @@ class Tracker:
 
     def push_device(self, stream: int, dev_ptr: int, nbytes: int) -> None:
         check(self._lib.l1rxg_tracker_push_device(self.handle, stream, C.c_void_p(dev_ptr), nbytes))
+
+    def push_strided(self, data: np.ndarray) -> None:
+        """Host array [n_streams, k] (rows may be a column slice of a wider
+        array): chunk k of every stream, one pitched copy + one launch."""
+        if data.ndim != 2 or data.shape[0] != self.desc.n_streams or data.strides[1] != data.itemsize:
+            raise ValueError("expected a [n_streams, k] array with contiguous rows")
+        check(self._lib.l1rxg_tracker_push_strided(self.handle, C.c_void_p(data.ctypes.data),
+                                                   data.shape[1] * data.itemsize, data.strides[0]))
+        self._keep = data
+
+    def push_device_strided(self, dev_ptr: int, nbytes_per_stream: int, stride_bytes: int) -> None:
+        """Same-length chunk for every stream in one launch (batched recordings)."""
+        check(self._lib.l1rxg_tracker_push_device_strided(self.handle, C.c_void_p(dev_ptr),
+                                                          nbytes_per_stream, stride_bytes))
 
     def run(self, max_epochs: int = -1) -> None:
         check(self._lib.l1rxg_tracker_run(self.handle, max_epochs))
