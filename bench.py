@@ -431,7 +431,7 @@ def run_batch(args, rank, world, local, dist):
     e2e_blocks = blocks
     while e2e_blocks > chunk_b and len(recs) * e2e_blocks * n * 4 * 3 > room:
         e2e_blocks //= 2
-    if len(recs) * e2e_blocks * n * 4 * 3 <= room:
+    if not args.no_e2e and len(recs) * e2e_blocks * n * 4 * 3 <= room:
         eb = e2e_blocks * n * 4
         pinned = ctx.host_alloc(len(recs) * eb).reshape(len(recs), eb)
         pinned[:] = raw[:, :eb].cpu().numpy()
@@ -526,6 +526,7 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override the config's block count")
     ap.add_argument("--cpu-blocks", type=int, default=3000, help="CPU baseline sample (blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="config 4: skip the host-memory e2e leg")
     ap.add_argument("--e2e-chunk-ms", type=int, default=100)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
     ap.add_argument("--cta", default="throughput", choices=["throughput", "latency"])

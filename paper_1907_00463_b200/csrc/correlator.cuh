@@ -35,7 +35,11 @@ constexpr double TWO_PI_D = 2.0 * PI_D;
 constexpr double F_L1_HZ = 1.57542e9;      // constants.hpp:5
 constexpr double CHIP_RATE_HZ = 1.023e6;   // constants.hpp:6
 constexpr int CHIP_EXT = 4096;             // chip index domain of one epoch
-constexpr int TRANS_EXT = 4096;            // transition table domain (>= 4 periods)
+// transition table domain: the largest chip index of an epoch is below
+// 2046 + 1.1 * 1023 + 1 = 3172 (code phase + 1023, code rate < 1.1 x chip
+// rate, |tap| <= 1 chip), i.e. below 3 * L + 104 <= 1736 transitions for
+// every GPS C/A code (L <= 544 per period)
+constexpr int TRANS_EXT = 2048;
 
 // ---------------------------------------------------------------------
 // per-epoch NCO constants (tracking.hpp:234-239)
@@ -91,22 +95,45 @@ __device__ __forceinline__ int tap_boundary(int m, double d, const EpochConsts& 
     return b - (int)dn + (int)up;
 }
 
-// x * conj(e^{j a}) with (c, s) = (cos a, sin a): (xr c + xi s, xi c - xr s),
-// the reference's wipe-off form (tracking.hpp:248-249).
-__device__ __forceinline__ float2 wipe(float2 x, float c, float s) {
-    return make_float2(fmaf(x.x, c, x.y * s), fmaf(x.y, c, -(x.x * s)));
+// Packed FP32x2 arithmetic (FFMA2 on sm_100): a complex value lives in one
+// 64-bit register pair, and a scalar operand broadcasts to both halves.
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk2(float a, float b) {
+    f2x r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(f2x v) {
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
 }
 
 // ---------------------------------------------------------------------
 // Per-PRN chip tables (built once per CTA).
-//   chipf[m]  = chips[m mod 1023] as +/-1.0f            (m < CHIP_EXT)
+//   chip[m]   = chips[m mod 1023] (+/-1)                (m < CHIP_EXT)
 //   tm[g]     = chip index of the g-th chip transition  (g < TRANS_EXT)
 //   td[g]     = chips[tm] - chips[tm - 1] in {-2, +2}
 //   cum[r]    = number of transitions at indices <= r within one period
 // A transition at index m means chips[m mod 1023] != chips[(m-1) mod 1023].
 // F(m) = (m / 1023) * L + cum[m mod 1023] counts the transitions in [0, m].
 struct CodeTables {
-    float chipf[CHIP_EXT];
+    int8_t chip[CHIP_EXT];
     int16_t tm[TRANS_EXT];
     int8_t td[TRANS_EXT];
     int16_t cum[1024];
@@ -122,7 +149,7 @@ __device__ __forceinline__ int trans_count(const CodeTables& ct, int m) {
 __device__ void build_code_tables(CodeTables& ct, const int8_t* codes, int prn) {
     const int8_t* c = codes + prn * 1023;
     for (int k = threadIdx.x; k < CHIP_EXT; k += blockDim.x)
-        ct.chipf[k] = (float)c[k % 1023];
+        ct.chip[k] = c[k % 1023];
     if (threadIdx.x < 32) {  // one warp: ballot-scan of the transitions
         const int lane = threadIdx.x;
         int running = 0;
@@ -165,7 +192,7 @@ __device__ void build_code_tables(CodeTables& ct, const int8_t* codes, int prn) 
 template <int T, bool FULL>
 __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
                                         const float2* __restrict__ rot,
-                                        const float* __restrict__ chipf,
+                                        const int8_t* __restrict__ chip,
                                         const double* __restrict__ d, int kp, int i0, int cnt,
                                         float* acc, float2* anchor_slot) {
     // theta(i0) exactly as the reference computes it (fma(w, i, phi)),
@@ -177,16 +204,35 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     __sincosf((float)r, &sa, &ca);
     *anchor_slot = make_float2(ca, sa);
 
-    float pr = 0.f, pi = 0.f;
+    // z_j = x_j * conj(rot_j), rot[j] = (c, s): FMUL2 xi * (s, c) (the
+    // swapped pair is a free operand swizzle) then FFMA2 xr * (c, -s) give
+    // (xr c + xi s, xi c - xr s), the reference's wipe-off form
+    // (tracking.hpp:248-249), off the dependency chain; the prefix itself is
+    // one FADD2 per sample.  Samples and rotators are loaded PF ahead.
+    constexpr int PF = 4;
+    f2x* runp = reinterpret_cast<f2x*>(run);
+    f2x xw[PF];
+    float2 qw[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        xw[j] = (FULL || j < cnt) ? runp[j] : 0ull;
+        qw[j] = rot[j];
+    }
+    f2x P = 0ull;
 #pragma unroll
     for (int j = 0; j < RUN; ++j) {
-        const float2 x = (FULL || j < cnt) ? run[j] : make_float2(0.f, 0.f);
-        const float2 q = rot[j];
-        const float2 z = wipe(x, q.x, q.y);
-        run[j] = make_float2(pr, pi);
-        pr += z.x;
-        pi += z.y;
+        const float2 x = upk2(xw[j % PF]);
+        const float2 q = qw[j % PF];
+        if (j + PF < RUN) {
+            xw[j % PF] = (FULL || j + PF < cnt) ? runp[j + PF] : 0ull;
+            qw[j % PF] = rot[j + PF];
+        }
+        const f2x z = ffma2(pk2(x.x, x.x), pk2(q.x, -q.y), fmul2(pk2(x.y, x.y), pk2(q.y, q.x)));
+        runp[j] = P;
+        P = fadd2(P, z);
     }
+    const float2 Pt = upk2(P);
+    const float pr = Pt.x, pi = Pt.y;
     const int i_last = i0 + (FULL ? RUN : cnt) - 1;
     const double dl = (double)i_last;
     const float zr = fmaf(pr, ca, pi * sa);  // anchored run total
@@ -194,7 +240,7 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     float chip_p = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
-        const float ch = chipf[__double2int_rz(tap_value(dl, c.cps, c.base, d[k]))];
+        const float ch = (float)chip[__double2int_rz(tap_value(dl, c.cps, c.base, d[k]))];
         acc[2 * k] = fmaf(ch, zr, acc[2 * k]);
         acc[2 * k + 1] = fmaf(ch, zi, acc[2 * k + 1]);
         if (k == kp)
@@ -205,7 +251,7 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
         acc[2 * T] = fmaf(chip_p, zr, acc[2 * T]);
         acc[2 * T + 1] = fmaf(chip_p, zi, acc[2 * T + 1]);
     } else if (i0 < c.nh) {  // the run straddling n/2: chip(nh-1) * P(nh)
-        const float ch = chipf[tap_index(c.nh - 1, c.cps, c.base, d[kp])];
+        const float ch = (float)chip[tap_index(c.nh - 1, c.cps, c.base, d[kp])];
         const float2 pn = run[c.nh - i0];
         acc[2 * T] = fmaf(ch, fmaf(pn.x, ca, pn.y * sa), acc[2 * T]);
         acc[2 * T + 1] = fmaf(ch, fmaf(pn.y, ca, -(pn.x * sa)), acc[2 * T + 1]);
@@ -214,19 +260,19 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
 
 template <int T>
 __device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* run,
-                                                 const float2* rot, const float* chipf,
+                                                 const float2* rot, const int8_t* chip,
                                                  const double* d, int kp, int i0, int cnt,
                                                  float* acc, float2* anchor_slot) {
     if (cnt == RUN)
-        phase_a<T, true>(c, run, rot, chipf, d, kp, i0, cnt, acc, anchor_slot);
+        phase_a<T, true>(c, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
     else
-        phase_a<T, false>(c, run, rot, chipf, d, kp, i0, cnt, acc, anchor_slot);
+        phase_a<T, false>(c, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
 }
 
 // Phase B: every chip transition of every tap whose step falls in the
 // sub-tile [u0, u0+len): acc_k -= delta * anchor(run(b)) * P(b).
 // tile_d[i - u0] holds P(i) (phase A's in-place prefixes).
-constexpr int MAXSUB = 8;  // sub-tiles per epoch (n <= 8 * 608 * 31)
+constexpr int MAXSUB = 24;  // sub-tiles per epoch (n <= 24 * nwork * 31)
 
 // Per (sub-tile, tap): first global transition index and count of the
 // transitions whose step falls in the sub-tile -- the same for every
@@ -246,49 +292,96 @@ __device__ __forceinline__ void fill_tap_ranges(int2* tr /*[MAXSUB][T]*/, const 
     }
 }
 
+// Phase B thread roles: threads are dealt to taps in fixed groups of
+// gsz = nthreads / T (thread t -> tap t / gsz, rank t % gsz; leftover
+// threads idle), so a thread's tap offset and its accumulators stay in
+// registers; a group walks its tap's transitions with stride gsz.
+struct PhaseB {
+    int kt, jt, gsz;  // tap, rank in the tap's group, group size
+    double dk;        // tap offset
+    bool prompt;      // kt is the prompt tap (first-half prompt too)
+    float re, im, hre, him;  // this thread's tap sum and first-half prompt
+};
+
 template <int T>
-__device__ __forceinline__ void phase_b(const EpochConsts& c, const float2* tile_d,
-                                        const float2* anchors, const CodeTables& ct,
-                                        const double* d, int kp, int u0, int len, float* acc,
-                                        int nthreads, const int2* tr /*[T] of this sub-tile*/) {
-    const int hi = u0 + len - 1;
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-        const double dk = d[k];
-        const int2 rk = tr[k];
-        const int g0 = rk.x;
-        const int cntk = rk.y;
-        // rotate the starting thread per tap so the remainders spread out
-        int j = (int)threadIdx.x - ((k * 64) & 511);
-        while (j < 0)
-            j += nthreads;
-        for (; j < cntk; j += nthreads) {
-            const int g = g0 + j;
-            const int m = ct.tm[g];
-            const float dlt = (float)ct.td[g];
-            const int b = tap_boundary(m, dk, c, u0, hi);
-            const int off = b - u0;
-            const float2 p = tile_d[off];
-            const float2 an = anchors[off / RUN];
-            const float ar = fmaf(p.x, an.x, p.y * an.y);
-            const float ai = fmaf(p.y, an.x, -(p.x * an.y));
-            acc[2 * k] = fmaf(-dlt, ar, acc[2 * k]);
-            acc[2 * k + 1] = fmaf(-dlt, ai, acc[2 * k + 1]);
-            if (k == kp && b < c.nh) {
-                acc[2 * T] = fmaf(-dlt, ar, acc[2 * T]);
-                acc[2 * T + 1] = fmaf(-dlt, ai, acc[2 * T + 1]);
-            }
-        }
+__device__ __forceinline__ void phase_b_init(PhaseB& pb, const double* d, int kp, int tid,
+                                             int nthreads) {
+    pb.gsz = max(1, nthreads / T);
+    pb.kt = tid / pb.gsz;
+    pb.jt = tid - pb.kt * pb.gsz;
+    pb.dk = pb.kt < T ? d[pb.kt] : 0.0;
+    pb.prompt = pb.kt == kp;
+    pb.re = pb.im = pb.hre = pb.him = 0.f;
+}
+
+// One transition at step b of delta dlt: acc -= dlt * anchor(run(b)) * P(b).
+__device__ __forceinline__ void phase_b_one(PhaseB& pb, const float2* tile_d, const float2* anchors,
+                                            int u0, int nh, int b, float dlt) {
+    const int off = b - u0;
+    const float2 p = tile_d[off];
+    const float2 an = anchors[off / RUN];
+    const float ar = fmaf(p.x, an.x, p.y * an.y);
+    const float ai = fmaf(p.y, an.x, -(p.x * an.y));
+    pb.re = fmaf(-dlt, ar, pb.re);
+    pb.im = fmaf(-dlt, ai, pb.im);
+    if (pb.prompt && b < nh) {
+        pb.hre = fmaf(-dlt, ar, pb.hre);
+        pb.him = fmaf(-dlt, ai, pb.him);
     }
 }
 
-// Per-epoch rotator table rot[j] = (cos wj, sin wj), j < RUN (accurate).
+// The transitions of this thread's tap in the sub-tile [u0, u0+len), two at
+// a time so the fp64 boundary searches of the pair overlap.
+template <int T>
+__device__ __forceinline__ void phase_b(PhaseB& pb, const EpochConsts& c, const float2* tile_d,
+                                        const float2* anchors, const CodeTables& ct, int u0,
+                                        int len, const int2* tr /*[T] of this sub-tile*/) {
+    if (pb.kt >= T)
+        return;
+    const int hi = u0 + len - 1;
+    const int2 rk = tr[pb.kt];
+    const int g0 = rk.x, cnt = rk.y;
+    for (int j = pb.jt; j < cnt; j += 2 * pb.gsz) {
+        const int j2 = j + pb.gsz;
+        const bool two = j2 < cnt;
+        const int ga = g0 + j, gb = g0 + (two ? j2 : j);
+        const int ma = ct.tm[ga], mb = ct.tm[gb];
+        const float da = (float)ct.td[ga], db = (float)ct.td[gb];
+        const int ba = tap_boundary(ma, pb.dk, c, u0, hi);
+        const int bb = tap_boundary(mb, pb.dk, c, u0, hi);
+        phase_b_one(pb, tile_d, anchors, u0, c.nh, ba, da);
+        if (two)
+            phase_b_one(pb, tile_d, anchors, u0, c.nh, bb, db);
+    }
+}
+
+// Folds a thread's phase-B sums into its V = 2T+2 partials (once per epoch).
+template <int T>
+__device__ __forceinline__ void phase_b_fold(PhaseB& pb, float* acc) {
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+        if (k == pb.kt) {
+            acc[2 * k] += pb.re;
+            acc[2 * k + 1] += pb.im;
+        }
+    acc[2 * T] += pb.hre;
+    acc[2 * T + 1] += pb.him;
+    pb.re = pb.im = pb.hre = pb.him = 0.f;
+}
+
+// Per-epoch rotator table rot[j] = (cos wj, sin wj), j < RUN (accurate
+// sincosf); 8 bytes so phase A's broadcast read is one shared wavefront.
 __device__ __forceinline__ void fill_rot(float2* rot, double w, int tid) {
     if (tid < RUN) {
         float s, co;
         sincosf((float)(w * (double)tid), &s, &co);
         rot[tid] = make_float2(co, s);
     }
+}
+
+// Named barrier over the first `count` threads (a multiple of 32).
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers ---------------------------
@@ -576,10 +669,9 @@ struct CorrSmem {
     double sums[2 * T + 2];
     float red[32 * (2 * T + 2)];
     float2 rot[RUN + 1];
-    float2 anchors[MAX_NT];
-    uint64_t bars[2];
-    int64_t unit_pos;  // TMA unit in flight: ring position (aligned), slack
-    int unit_delta, unit_h, unit_len, inflight;
+    uint64_t bars[2][2];  // per tile buffer: the two halves of its bulk copy
+    int inflight[2];      // per tile buffer: a bulk copy is outstanding
+    int64_t issue_pos;    // ring position of the next unit to copy
     // epoch handed from the critical path to the control warp
     l1rxg_epoch_record rec;  // inputs, correlator outputs, loop outputs
     int64_t rec_slot;
@@ -595,9 +687,17 @@ __host__ __device__ constexpr size_t corr_smem_header() {
     return (sizeof(CorrSmem<T>) + 15) & ~size_t(15);
 }
 
+// Dynamic shared memory after the header: anchors[nwork] (one carrier
+// anchor per run of the current unit), then nbuf sample tiles of cap + 4
+// float2 each (cap = nwork * RUN; +4: bulk-copy alignment slack).
 template <int T>
-__device__ __forceinline__ float2* tile_of(CorrSmem<T>* s) {
+__device__ __forceinline__ float2* anchors_of(CorrSmem<T>* s) {
     return reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + corr_smem_header<T>());
+}
+__host__ __device__ constexpr int anchors_len(int nwork) { return (nwork + 1) & ~1; }
+template <int T>
+__device__ __forceinline__ float2* tile_of(CorrSmem<T>* s, int nwork, int b) {
+    return anchors_of(s) + anchors_len(nwork) + (size_t)b * (nwork * RUN + 4);
 }
 
 // o (CorrelatorOutputs) from the fp64 sums
@@ -705,6 +805,7 @@ struct TrackArgs {
     l1rxg_taps taps;
     LoopCfg lc;
     long long* prof;  // optional stage clocks (L1RXG_PROF=1): [epoch][8], CTA 0
+    int nbuf;         // sample tiles per CTA: 1 (latency shape) or 2 (double-buffered)
 };
 
 #define PROF_STAMP(k)                                                          \
@@ -712,27 +813,32 @@ struct TrackArgs {
         if (a.prof && blockIdx.x == 0 && e < 64)                               \
             a.prof[e * 8 + (k)] = clock64();                                   \
     } while (0)
+// per-unit stage sums of CTA 0, kept in registers and flushed once per
+// epoch (bank 1 of the profile buffer)
+#define PROF_UNIT(k, t0)                                                       \
+    do {                                                                       \
+        if (a.prof) {                                                          \
+            const long long t_ = clock64();                                    \
+            pu[k] += t_ - (t0);                                                \
+            (t0) = t_;                                                         \
+        }                                                                      \
+    } while (0)
 
-// TMA unit: samples [abs_first, abs_first + len) of the ring into the tile,
+// TMA unit: len samples from ring position pos (< R) into the tile,
 // copied from the 16-byte aligned position below (delta samples of slack),
 // in two halves on two mbarriers.
 template <int T>
-__device__ __forceinline__ void issue_unit(CorrSmem<T>* s, float2* tile, const float2* ring,
-                                           int64_t abs_first, int len, int64_t R) {
-    const int64_t pos = abs_first % R;
+__device__ __forceinline__ void issue_unit(CorrSmem<T>* s, int b, float2* tile, const float2* ring,
+                                           int64_t pos, int len) {
     const int delta = (int)(pos & 1);
     const int h = 2 * ((len + delta) / 4);
-    s->unit_pos = pos - delta;
-    s->unit_delta = delta;
-    s->unit_h = h;
-    s->unit_len = len;
     const uint32_t total = (uint32_t)(((len + delta) * 8 + 15) & ~15);
     const uint32_t b0 = (uint32_t)h * 8u;
-    mbar_expect_tx(&s->bars[0], b0);
-    tma_load_1d(tile, ring + (pos - delta), b0, &s->bars[0]);
-    mbar_expect_tx(&s->bars[1], total - b0);
-    tma_load_1d(tile + h, ring + (pos - delta) + h, total - b0, &s->bars[1]);
-    s->inflight = 1;
+    mbar_expect_tx(&s->bars[b][0], b0);
+    tma_load_1d(tile, ring + (pos - delta), b0, &s->bars[b][0]);
+    mbar_expect_tx(&s->bars[b][1], total - b0);
+    tma_load_1d(tile + h, ring + (pos - delta) + h, total - b0, &s->bars[b][1]);
+    s->inflight[b] = 1;
 }
 
 // Control-warp side of an epoch: run state, quality metrics and lock-fail
@@ -888,22 +994,26 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
 // Channel-resident persistent tracking kernel: one CTA per channel loops
 // over its epochs with no host round trip (replaces the per-channel
 // track_epoch fan-out of Receiver::tracking_round, pipeline.hpp:563-610).
-//   * work warps (blockDim - 32 threads): correlation, phases A and B;
-//   * the epoch window arrives by TMA; the next window's copy is issued as
-//     soon as the current one is consumed;
-//   * per-epoch critical path: fp64 totals -> the independent
-//     transcendental pieces in separate warps -> loop_fast (filters, NCO)
-//     -> next epoch's constants;
-//   * the last warp is a control warp: it finishes epoch e (loop_metrics,
-//     record) while epoch e+1 is being correlated.  If that makes the
-//     channel Idle, epoch e+1 is discarded before its loop update, exactly
-//     as if it had never been admitted (tracking.hpp:511-514 + the caller's
-//     Idle check, pipeline.hpp:567-568).
+//   * work warps (blockDim - 32 threads): correlation, phases A and B, one
+//     sub-tile ("unit", cap = nwork * RUN samples) at a time;
+//   * units arrive by TMA bulk copy into nbuf tiles: with one tile the next
+//     unit is copied once the current one is consumed (latency shape: one
+//     unit per epoch, the copy overlaps the loop update); with two tiles
+//     the copy of unit u+2 is issued as soon as unit u is consumed, so it
+//     overlaps unit u+1's correlation (throughput shape, many units per
+//     epoch);
+//   * per-epoch critical path on warp 0: fp64 totals -> the transcendental
+//     pieces in SIMT lanes -> loop_fast (filters, NCO) -> next epoch's
+//     constants;
+//   * the last warp is a control warp: it issues the copies and finishes
+//     epoch e (loop_metrics, record) while epoch e+1 is being correlated.
+//     If that makes the channel Idle, epoch e+1 is discarded before its
+//     loop update, exactly as if it had never been admitted
+//     (tracking.hpp:511-514 + the caller's Idle check, pipeline.hpp:567-568).
 template <int T>
 __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
-    float2* tile = tile_of(s);
     const int cidx = blockIdx.x;
     const int strm = a.chan_stream[cidx];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -915,32 +1025,56 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     const int cap = nwork * RUN;
     const int n = a.n;
     const int nsub = (n + cap - 1) / cap;
+    const int nbuf = a.nbuf;
     const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
     const int64_t avail = a.avail[strm];
     const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
-    const int PW = min(nwork_warps, LOOP_PIECES);
-    const int named = (PW + 1) * 32;       // pieces warps + control warp
+    float2* anchors = anchors_of(s);
+    const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
+    // unit v of this launch: epoch v / nsub, sub-tile v % nsub, into tile
+    // v % nbuf.  Units of the epoch being correlated (ev <= ecur) are always
+    // copied; a later epoch's only if the admission test will accept it as
+    // things stand (not Idle, in range, fully ingested).
+    auto try_issue = [&](int v, int ecur) {
+        const int ev = v / nsub;
+        const int q = v - ev * nsub;
+        const int64_t offv = off0 + (int64_t)ev * n;
+        if (noop || ev >= a.max_epochs || offv + n > avail || off0 < 0 ||
+            off0 < avail - a.ring_cap || (ev > ecur && s->ch.state == L1RXG_IDLE))
+            return;
+        const int b = v & (nbuf - 1);
+        const int len = min(cap, n - q * cap);
+        // units tile the epochs contiguously and are issued in order without
+        // gaps, so the ring position advances by each unit's length
+        const int64_t pos = s->issue_pos;
+        issue_unit(s, b, tile_of(s, nwork, b), ring, pos, len);
+        const int64_t nxt = pos + len;
+        s->issue_pos = nxt >= a.ring_cap ? nxt - a.ring_cap : nxt;
+    };
     if (tid == 0) {
         s->ch = a.chans[cidx];
-        mbar_init(&s->bars[0], 1);
-        mbar_init(&s->bars[1], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s->bars[b][0], 1);
+            mbar_init(&s->bars[b][1], 1);
+            s->inflight[b] = 0;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s->inflight = 0;
         s->pending = 0;
         s->stop = 0;
     }
     for (int k = tid; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
     __syncthreads();
+    PhaseB pb;
+    phase_b_init<T>(pb, s->d, a.kp, tid, nwork);
     build_code_tables(s->ct, a.codes, s->ch.prn);
-    if (tid == 0) {  // first epoch: consts and the first tile load
+    if (tid == 0) {  // first epoch: consts and the first units
+        s->issue_pos = off0 >= 0 ? off0 % a.ring_cap : 0;
         const l1rxg_channel& ch = s->ch;
         make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
                     ch.carrier_phase_rad, a.lc.fs, n);
-        const int64_t off = ch.sample_offset_next_epoch;
-        if (!noop && ch.state != L1RXG_IDLE && a.max_epochs > 0 && off + n <= avail && off >= 0 &&
-            off >= avail - a.ring_cap)
-            issue_unit(s, tile, ring, off, min(cap, n), a.ring_cap);
+        for (int v = 0; v < nbuf; ++v)
+            try_issue(v, -1);
     }
     __syncthreads();
     fill_rot(s->rot, s->c.w, tid);
@@ -948,8 +1082,12 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, nsub, lane);
     __syncthreads();
 
-    uint32_t phase = 0;
-    int64_t e = 0;
+    uint32_t phase = 0;  // bit b: parity of tile b's next completion
+    int e = 0;
+    int u = 0;           // next unit to consume
+    // ring position of unit u, tracked by every thread (the copy's 16-byte
+    // alignment slack follows from it) so no hand-off from the issuer is needed
+    int64_t upos = off0 >= 0 ? off0 % a.ring_cap : 0;
     int64_t done = a.ecount[cidx];
     for (;;) {
         // epoch admission (uniform: every thread reads the same smem state)
@@ -974,11 +1112,20 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
 #pragma unroll
         for (int v = 0; v < V; ++v)
             acc[v] = 0.f;
-        for (int q = 0; q < nsub; ++q) {
+        long long tu = a.prof ? clock64() : 0;
+        long long pu[5] = {0, 0, 0, 0, 0};
+        for (int q = 0; q < nsub; ++q, ++u) {
+            const int b = nbuf == 1 ? 0 : (int)(u & 1);
+            const uint32_t par = (phase >> b) & 1u;
             const int u0 = q * cap;
             const int len = min(cap, n - u0);
+            const int delta = (int)(upos & 1);
+            const int h = 2 * ((len + delta) / 4);
+            upos += len;
+            if (upos >= a.ring_cap)
+                upos -= a.ring_cap;
             if (!noop) {
-                const int delta = s->unit_delta, h = s->unit_h;
+                float2* tile = tile_of(s, nwork, b);
                 const float2* tile_d = tile + delta;
                 if (tid < nwork) {
                     const int i0 = u0 + tid * RUN;
@@ -986,51 +1133,59 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                     const int r0 = delta + tid * RUN;
                     if (cnt > 0) {
                         if (r0 < h)
-                            mbar_wait(&s->bars[0], phase);
+                            mbar_wait(&s->bars[b][0], par);
                         if (r0 + RUN > h)
-                            mbar_wait(&s->bars[1], phase);
-                        phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
-                                            acc, &s->anchors[tid]);
+                            mbar_wait(&s->bars[b][1], par);
+                        phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
+                                            acc, &anchors[tid]);
                     }
-                    if (tid == 0) {  // every phase completes before the next issue
-                        mbar_wait(&s->bars[0], phase);
-                        mbar_wait(&s->bars[1], phase);
+                    if (tid == 0) {  // every copy completes before its tile is reused
+                        mbar_wait(&s->bars[b][0], par);
+                        mbar_wait(&s->bars[b][1], par);
                         PROF_STAMP(1);
+                        PROF_UNIT(0, tu);
                     }
                 }
-                phase ^= 1u;
-                __syncthreads();  // prefixes + anchors visible
-                if (tid == 0)
-                    PROF_STAMP(2);
-                if (tid < nwork)
-                    phase_b<T>(c, tile_d, s->anchors, s->ct, s->d, a.kp, u0, len, acc, nwork,
-                               s->trange + q * T);
-            }
-            if (q + 1 == nsub && warp < nwork_warps)
-                warp_partials<V>(acc, s->red, lane, warp);
-            __syncthreads();  // tile consumed
-            if (tid == 0)
-                PROF_STAMP(3);
-            if (warp == ctl && lane == 0) {  // the next bulk copy, off warp 0's path
-                s->inflight = 0;
-                if (!noop) {
-                    if (q + 1 < nsub)
-                        issue_unit(s, tile, ring, off + (q + 1) * cap, min(cap, n - (q + 1) * cap),
-                                   a.ring_cap);
-                    else if (s->ch.state != L1RXG_IDLE && e + 1 < a.max_epochs &&
-                             off + 2 * (int64_t)n <= avail)
-                        issue_unit(s, tile, ring, off + n, min(cap, n), a.ring_cap);  // prefetch
+                phase ^= 1u << b;
+                if (tid < nwork) {
+                    // prefixes + anchors visible: the work warps only, so the
+                    // control warp's epoch finish does not hold phase B
+                    named_bar_sync(1, nwork);
+                    if (tid == 0) {
+                        PROF_STAMP(2);
+                        PROF_UNIT(1, tu);
+                    }
+                    phase_b<T>(pb, c, tile_d, anchors, s->ct, u0, len, s->trange + q * T);
                 }
             }
-            if (q + 1 < nsub)
-                __syncthreads();  // publish the next unit
+            if (q + 1 == nsub && warp < nwork_warps) {
+                phase_b_fold<T>(pb, acc);
+                warp_partials<V>(acc, s->red, lane, warp);
+            }
+            if (tid == 0)
+                PROF_UNIT(2, tu);
+            __syncthreads();  // tile consumed
+            if (tid == 0) {
+                PROF_STAMP(3);
+                PROF_UNIT(3, tu);
+            }
+            if (warp == ctl && lane == 0) {  // the next bulk copy, off warp 0's path
+                s->inflight[b] = 0;
+                try_issue(u + nbuf, e);
+            }
+            if (tid == 0)
+                PROF_UNIT(4, tu);
         }
         // ---- critical path, all on warp 0 in SIMT form (no cross-warp
         // hand-off): totals -> one atan2 / sqrt / fmod / division per lane
         // -> loop_fast on lane 0 -> next epoch's constants, rotators, ranges
         if (warp == 0) {
-            if (tid == 0)
+            if (tid == 0) {
                 PROF_STAMP(4);
+                if (a.prof && blockIdx.x == 0 && e < 64)
+                    for (int k = 0; k < 5; ++k)
+                        a.prof[512 + e * 8 + k] = pu[k];
+            }
             warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane);
             if (tid == 0)
                 PROF_STAMP(5);
@@ -1052,10 +1207,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         finish_epoch<T>(s, a, lane);
     __syncthreads();
     if (tid == 0) {
-        if (s->inflight) {  // never leave a bulk copy in flight into freed smem
-            mbar_wait(&s->bars[0], phase);
-            mbar_wait(&s->bars[1], phase);
-        }
+        for (int b = 0; b < nbuf; ++b)
+            if (s->inflight[b]) {  // never leave a bulk copy in flight into freed smem
+                mbar_wait(&s->bars[b][0], (phase >> b) & 1u);
+                mbar_wait(&s->bars[b][1], (phase >> b) & 1u);
+            }
         a.chans[cidx] = s->ch;
         a.ecount[cidx] = done;
     }
@@ -1080,7 +1236,8 @@ template <int T>
 __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
-    float2* tile = tile_of(s);
+    float2* anchors = anchors_of(s);
+    float2* tile = tile_of(s, blockDim.x, 0);
     const int j = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = (blockDim.x + 31) >> 5;
@@ -1095,6 +1252,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
                     st.carrier_phase_rad, a.fs, n);
     }
     build_code_tables(s->ct, a.codes, a.prns[j]);  // ends with a barrier
+    PhaseB pb;
+    phase_b_init<T>(pb, s->d, a.kp, tid, blockDim.x);
     fill_rot(s->rot, s->c.w, tid);
     if (warp == 0)
         fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, (n + cap - 1) / cap, lane);
@@ -1113,14 +1272,14 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
             const int i0 = u0 + tid * RUN;
             const int cnt = min(RUN, n - i0);
             if (cnt > 0)
-                phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chipf, s->d, a.kp, i0, cnt,
-                                    acc, &s->anchors[tid]);
+                phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
+                                    acc, &anchors[tid]);
             __syncthreads();
-            phase_b<T>(c, tile, s->anchors, s->ct, s->d, a.kp, u0, len, acc, blockDim.x,
-                       s->trange + (u0 / cap) * T);
+            phase_b<T>(pb, c, tile, anchors, s->ct, u0, len, s->trange + (u0 / cap) * T);
             __syncthreads();
         }
     }
+    phase_b_fold<T>(pb, acc);
     warp_partials<V>(acc, s->red, lane, warp);
     __syncthreads();
     if (warp == 0)

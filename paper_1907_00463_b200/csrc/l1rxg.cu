@@ -126,10 +126,12 @@ int pick_threads(int n, int* subtiles, int max_nt = MAX_NT) {
     return nt;
 }
 
-// tile: nt*RUN samples + alignment slack of the 16-byte bulk copies
+// header + anchors[nwork] + nbuf tiles of nwork*RUN samples (+ alignment
+// slack of the 16-byte bulk copies)
 template <int T>
-size_t smem_bytes(int nt) {
-    return corr_smem_header<T>() + (static_cast<size_t>(nt) * RUN + 4) * sizeof(float2);
+size_t smem_bytes(int nwork, int nbuf = 1) {
+    return corr_smem_header<T>() + static_cast<size_t>(anchors_len(nwork)) * sizeof(float2) +
+           static_cast<size_t>(nbuf) * (static_cast<size_t>(nwork) * RUN + 4) * sizeof(float2);
 }
 
 // Loop-filter constants precomputed with the reference's operation order
@@ -154,8 +156,10 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
 
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
-    const size_t sm = smem_bytes<T>(nt - 32);  // the control warp owns no tile runs
+    const size_t sm = smem_bytes<T>(nt - 32, a.nbuf);  // the control warp owns no tile runs
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
     track_kernel<T><<<n_ch, nt, sm, s>>>(a);
     CK(cudaGetLastError());
     return 0;
@@ -265,6 +269,7 @@ struct l1rxg_tracker {
     l1rxg_tracker_desc d{};
     int T = 3;
     int nt = 64;
+    int nbuf = 1;
     int64_t R = 0, apron = 0;
     std::vector<StreamRing> streams;
     float2* d_ring = nullptr;
@@ -609,10 +614,24 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
         const bool thr = d->cta_mode == L1RXG_CTA_THROUGHPUT ||
                          (d->cta_mode == L1RXG_CTA_AUTO && d->n_channels >= 2 * nsm);
-        // throughput: 9 correlation warps + control warp, ~112 KB of shared
-        // memory at 7 taps -> two CTAs per SM; latency: up to 19 warps, one
-        // CTA per SM
-        t->nt = pick_threads(n, nullptr, thr ? 288 : MAX_NT - 32) + 32;
+        // latency: up to 19 correlation warps + the control warp, one CTA
+        // per SM, one tile (the copy overlaps the loop update).
+        // throughput: 5 correlation warps + the control warp and two tiles
+        // (copy of unit u+2 overlaps unit u+1), ~110 KB of shared memory ->
+        // two CTAs per SM, so one CTA's serial loop update overlaps the
+        // other's correlation
+        if (thr) {
+            static const char* ev_nw = std::getenv("L1RXG_THR_NWORK");
+            static const char* ev_nb = std::getenv("L1RXG_THR_NBUF");
+            int mx = ev_nw ? std::atoi(ev_nw) : 128;
+            while ((n + mx * RUN - 1) / (mx * RUN) > MAXSUB)
+                mx += 32;
+            t->nt = pick_threads(n, nullptr, mx) + 32;
+            t->nbuf = ev_nb ? std::atoi(ev_nb) : 1;
+        } else {
+            t->nt = pick_threads(n, nullptr, MAX_NT - 32) + 32;
+            t->nbuf = 1;
+        }
     }
     t->R = d->ring_samples;
     // apron >= one epoch (+ bulk-copy slack); R + apron even keeps every
@@ -850,6 +869,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.kl = t->d.taps.late;
     a.taps = padded_taps(t->d.taps, t->T);
     a.lc = make_loop_cfg(t->d.cfg, t->d.kernel, t->d.sample_rate_hz, a.n);
+    a.nbuf = t->nbuf;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
@@ -889,16 +909,16 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
         if (cnt)
             std::fprintf(stderr,
                          "[l1rxg prof] cycles/epoch %.0f | A %.0f | barA %.0f | B+red %.0f | "
-                         "totals %.0f | pieces %.0f | apply %.0f | bar %.0f | per piece %.0f %.0f "
-                         "%.0f %.0f %.0f | loop_fast %.0f consts %.0f warp0_totals %.0f\n",
+                         "totals %.0f | pieces %.0f | apply %.0f | bar %.0f\n",
                          acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-                         acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, pc[0] / cnt, pc[1] / cnt,
-                         pc[2] / cnt, pc[3] / cnt, pc[4] / cnt, pc[5] / cnt, pc[6] / cnt,
-                         pc[7] / cnt);
+                         acc[5] / cnt, acc[6] / cnt, acc[7] / cnt);
         if (cnt)
-            std::fprintf(stderr, "[l1rxg prof] B1->B2-arrive per warp 0..4: %.0f %.0f %.0f %.0f %.0f ctl %.0f\n",
-                         arr[0] / cnt, arr[1] / cnt, arr[2] / cnt, arr[3] / cnt, arr[4] / cnt,
-                         arr[7] / cnt);
+            std::fprintf(stderr,
+                         "[l1rxg prof] per epoch, summed over units (thread 0): A+wait %.0f | "
+                         "barrier A %.0f | B+partials %.0f | consumed barrier %.0f | "
+                         "issue+publish %.0f\n",
+                         pc[0] / cnt, pc[1] / cnt, pc[2] / cnt, pc[3] / cnt, pc[4] / cnt);
+        (void)arr;
     }
     return 0;
 }
