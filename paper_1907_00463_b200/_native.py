@@ -11,7 +11,7 @@ from functools import lru_cache
 from . import abi
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "_lib", "libl1rxg.so")
+SO = os.environ.get("L1RXG_SO") or os.path.join(PKG, "_lib", "libl1rxg.so")  # override: experiments
 
 # every symbol include/l1rxg.h declares (tests/test_abi.py checks the header
 # against this list and the .so against both)

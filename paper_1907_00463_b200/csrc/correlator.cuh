@@ -95,8 +95,7 @@ __device__ __forceinline__ int tap_boundary(int m, double d, const EpochConsts& 
     return b - (int)dn + (int)up;
 }
 
-// Packed FP32x2 arithmetic (FFMA2 on sm_100): a complex value lives in one
-// 64-bit register pair, and a scalar operand broadcasts to both halves.
+// A complex sample as one 64-bit value (one LDS.64 / STS.64).
 typedef unsigned long long f2x;
 __device__ __forceinline__ f2x pk2(float a, float b) {
     f2x r;
@@ -107,21 +106,6 @@ __device__ __forceinline__ float2 upk2(f2x v) {
     float2 r;
     asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
     return r;
-}
-__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
-    f2x d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
-    f2x d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
-    f2x d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
 }
 
 // ---------------------------------------------------------------------
@@ -204,11 +188,11 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     __sincosf((float)r, &sa, &ca);
     *anchor_slot = make_float2(ca, sa);
 
-    // z_j = x_j * conj(rot_j), rot[j] = (c, s): FMUL2 xi * (s, c) (the
-    // swapped pair is a free operand swizzle) then FFMA2 xr * (c, -s) give
-    // (xr c + xi s, xi c - xr s), the reference's wipe-off form
-    // (tracking.hpp:248-249), off the dependency chain; the prefix itself is
-    // one FADD2 per sample.  Samples and rotators are loaded PF ahead.
+    // z_j = x_j * conj(rot_j), rot[j] = (c, s): (xr c + xi s, xi c - xr s),
+    // the reference's wipe-off form (tracking.hpp:248-249), off the
+    // dependency chain; the prefix itself is two FADDs per sample.  Samples
+    // and rotators are loaded PF ahead.  (A packed FFMA2 form needs a
+    // negated pair per sample plus register-pair moves and measured slower.)
     constexpr int PF = 4;
     f2x* runp = reinterpret_cast<f2x*>(run);
     f2x xw[PF];
@@ -227,9 +211,10 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
             xw[j % PF] = (FULL || j + PF < cnt) ? runp[j + PF] : 0ull;
             qw[j % PF] = rot[j + PF];
         }
-        const f2x z = ffma2(pk2(x.x, x.x), pk2(q.x, -q.y), fmul2(pk2(x.y, x.y), pk2(q.y, q.x)));
+        const float zr = fmaf(x.x, q.x, x.y * q.y), zi = fmaf(x.y, q.x, -(x.x * q.y));
         runp[j] = P;
-        P = fadd2(P, z);
+        const float2 Pf = upk2(P);
+        P = pk2(Pf.x + zr, Pf.y + zi);
     }
     const float2 Pt = upk2(P);
     const float pr = Pt.x, pi = Pt.y;
@@ -352,6 +337,40 @@ __device__ __forceinline__ void phase_b(PhaseB& pb, const EpochConsts& c, const 
         phase_b_one(pb, tile_d, anchors, u0, c.nh, ba, da);
         if (two)
             phase_b_one(pb, tile_d, anchors, u0, c.nh, bb, db);
+    }
+}
+
+// Variant: all taps per thread, transitions dealt round-robin per tap.
+template <int T>
+__device__ __forceinline__ void phase_b_pertap(const EpochConsts& c, const float2* tile_d,
+                                               const float2* anchors, const CodeTables& ct,
+                                               const double* d, int kp, int u0, int len, float* acc,
+                                               int nthreads, const int2* tr) {
+    const int hi = u0 + len - 1;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const double dk = d[k];
+        const int2 rk = tr[k];
+        int j = (int)threadIdx.x - ((k * 64) & 511);
+        while (j < 0)
+            j += nthreads;
+        for (; j < rk.y; j += nthreads) {
+            const int g = rk.x + j;
+            const int m = ct.tm[g];
+            const float dlt = (float)ct.td[g];
+            const int b = tap_boundary(m, dk, c, u0, hi);
+            const int off = b - u0;
+            const float2 p = tile_d[off];
+            const float2 an = anchors[off / RUN];
+            const float ar = fmaf(p.x, an.x, p.y * an.y);
+            const float ai = fmaf(p.y, an.x, -(p.x * an.y));
+            acc[2 * k] = fmaf(-dlt, ar, acc[2 * k]);
+            acc[2 * k + 1] = fmaf(-dlt, ai, acc[2 * k + 1]);
+            if (k == kp && b < c.nh) {
+                acc[2 * T] = fmaf(-dlt, ar, acc[2 * T]);
+                acc[2 * T + 1] = fmaf(-dlt, ai, acc[2 * T + 1]);
+            }
+        }
     }
 }
 
@@ -808,6 +827,10 @@ struct TrackArgs {
     int nbuf;         // sample tiles per CTA: 1 (latency shape) or 2 (double-buffered)
 };
 
+// Stage clocks (profiling builds only: -DL1RXG_PROFILE, run with
+// L1RXG_PROF=1): CTA 0's first 64 epochs, bank 0 per-epoch stamps, bank 1
+// per-unit stage sums kept in registers and flushed once per epoch.
+#ifdef L1RXG_PROFILE
 #define PROF_STAMP(k)                                                          \
     do {                                                                       \
         if (a.prof && blockIdx.x == 0 && e < 64)                               \
@@ -823,6 +846,14 @@ struct TrackArgs {
             (t0) = t_;                                                         \
         }                                                                      \
     } while (0)
+#else
+#define PROF_STAMP(k) \
+    do {              \
+    } while (0)
+#define PROF_UNIT(k, t0) \
+    do {                 \
+    } while (0)
+#endif
 
 // TMA unit: len samples from ring position pos (< R) into the tile,
 // copied from the 16-byte aligned position below (delta samples of slack),
@@ -1112,8 +1143,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
 #pragma unroll
         for (int v = 0; v < V; ++v)
             acc[v] = 0.f;
+#ifdef L1RXG_PROFILE
         long long tu = a.prof ? clock64() : 0;
         long long pu[5] = {0, 0, 0, 0, 0};
+#endif
         for (int q = 0; q < nsub; ++q, ++u) {
             const int b = nbuf == 1 ? 0 : (int)(u & 1);
             const uint32_t par = (phase >> b) & 1u;
@@ -1155,7 +1188,12 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         PROF_STAMP(2);
                         PROF_UNIT(1, tu);
                     }
+#ifdef L1RXG_PHB_PERTAP
+                    phase_b_pertap<T>(c, tile_d, anchors, s->ct, s->d, a.kp, u0, len, acc, nwork,
+                                      s->trange + q * T);
+#else
                     phase_b<T>(pb, c, tile_d, anchors, s->ct, u0, len, s->trange + q * T);
+#endif
                 }
             }
             if (q + 1 == nsub && warp < nwork_warps) {
@@ -1182,9 +1220,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         if (warp == 0) {
             if (tid == 0) {
                 PROF_STAMP(4);
+#ifdef L1RXG_PROFILE
                 if (a.prof && blockIdx.x == 0 && e < 64)
                     for (int k = 0; k < 5; ++k)
                         a.prof[512 + e * 8 + k] = pu[k];
+#endif
             }
             warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane);
             if (tid == 0)
