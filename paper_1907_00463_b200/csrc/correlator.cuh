@@ -188,11 +188,11 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     __sincosf((float)r, &sa, &ca);
     *anchor_slot = make_float2(ca, sa);
 
-    // z_j = x_j * conj(rot_j), rot[j] = (c, s): (xr c + xi s, xi c - xr s),
-    // the reference's wipe-off form (tracking.hpp:248-249), off the
-    // dependency chain; the prefix itself is two FADDs per sample.  Samples
-    // and rotators are loaded PF ahead.  (A packed FFMA2 form needs a
-    // negated pair per sample plus register-pair moves and measured slower.)
+    // P += x_j * conj(rot_j), rot[j] = (c, s): (xr c + xi s, xi c - xr s),
+    // the reference's wipe-off form (tracking.hpp:248-249), as four FFMAs
+    // straight into the prefix.  Samples and rotators are loaded PF ahead.
+    // (A packed FFMA2 form needs a negated pair per sample plus
+    // register-pair moves and measured slower.)
     constexpr int PF = 4;
     f2x* runp = reinterpret_cast<f2x*>(run);
     f2x xw[PF];
@@ -211,10 +211,9 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
             xw[j % PF] = (FULL || j + PF < cnt) ? runp[j + PF] : 0ull;
             qw[j % PF] = rot[j + PF];
         }
-        const float zr = fmaf(x.x, q.x, x.y * q.y), zi = fmaf(x.y, q.x, -(x.x * q.y));
         runp[j] = P;
         const float2 Pf = upk2(P);
-        P = pk2(Pf.x + zr, Pf.y + zi);
+        P = pk2(fmaf(x.y, q.y, fmaf(x.x, q.x, Pf.x)), fmaf(-x.x, q.y, fmaf(x.y, q.x, Pf.y)));
     }
     const float2 Pt = upk2(P);
     const float pr = Pt.x, pi = Pt.y;
