@@ -474,8 +474,10 @@ def run_batch(args, rank, world, local, dist):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic_config4.json")
-    if os.path.exists(prof):
-        traffic = json.load(open(prof)).get("track_kernel_dram_bytes_per_launch")
+    launches_per_step = -(-blocks // chunk_b)
+    if os.path.exists(prof):  # measured DRAM bytes per channel-epoch x channel-epochs per launch
+        per = json.load(open(prof)).get("dram_bytes_per_channel_epoch")
+        traffic = per * epochs_local / launches_per_step if per else None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle
@@ -504,6 +506,8 @@ def run_batch(args, rank, world, local, dist):
         "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": "DRAM bytes per track_kernel launch (one %d-block chunk of every "
+                                     "recording), profiles/ncu_traffic_config4.json" % chunk_b,
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock under load "
                                     "(%.0f MHz); FP32 pipe roof per SURVEY 8d" % sm_mhz,
                      "alg_ops_per_sample_tap": ops_per_sample_tap(T, 12, False),
