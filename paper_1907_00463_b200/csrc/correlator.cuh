@@ -79,7 +79,7 @@ __device__ __forceinline__ int tap_index(int i, double cps, double base, double 
 // estimate and its left neighbour with the reference expression pins the
 // exact boundary: tap_value is monotone in the sample index.
 //
-// Fast path: with inv_cps correctly rounded, |e - x*| < 2e-11 samples for
+// Fast path: with inv_cps within 2 ulp of 1/cps, |e - x*| < 4e-11 samples for
 // the exact crossing x* = (m - d - base)/cps, and the reference's own
 // rounding moves its crossing by < 5e-11 samples; so when e is farther than
 // 1e-9 from an integer the boundary is ceil(e) with certainty.  Only near
@@ -258,23 +258,6 @@ __device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* r
 // tile_d[i - u0] holds P(i) (phase A's in-place prefixes).
 constexpr int MAXSUB = 24;  // sub-tiles per epoch (n <= 24 * nwork * 31)
 
-// Per (sub-tile, tap): first global transition index and count of the
-// transitions whose step falls in the sub-tile -- the same for every
-// thread, so computed once per epoch by one warp (lanes over (q, k)).
-template <int T>
-__device__ __forceinline__ void fill_tap_ranges(int2* tr /*[MAXSUB][T]*/, const EpochConsts& c,
-                                                const CodeTables& ct, const double* d, int cap,
-                                                int nsub, int lane) {
-    for (int idx = lane; idx < nsub * T; idx += 32) {
-        const int q = idx / T, k = idx - q * T;
-        const int u0 = q * cap;
-        const int hi = u0 + min(cap, c.n - u0) - 1;
-        const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, d[k]);
-        const int mhi = tap_index(hi, c.cps, c.base, d[k]);
-        const int g0 = trans_count(ct, mlo);
-        tr[q * T + k] = make_int2(g0, trans_count(ct, mhi) - g0);
-    }
-}
 
 // Phase B thread roles: threads are dealt to taps in fixed groups of
 // gsz = nthreads / T (thread t -> tap t / gsz, rank t % gsz; leftover
@@ -282,6 +265,7 @@ __device__ __forceinline__ void fill_tap_ranges(int2* tr /*[MAXSUB][T]*/, const 
 // registers; a group walks its tap's transitions with stride gsz.
 struct PhaseB {
     int kt, jt, gsz;  // tap, rank in the tap's group, group size
+    int g0, cnt;      // this unit: first global transition index of the tap, count
     double dk;        // tap offset
     bool prompt;      // kt is the prompt tap (first-half prompt too)
     float re, im, hre, him;  // this thread's tap sum and first-half prompt
@@ -314,17 +298,33 @@ __device__ __forceinline__ void phase_b_one(PhaseB& pb, const float2* tile_d, co
     }
 }
 
+// The range of this thread's tap's transitions whose step falls in the unit
+// [u0, u0+len): computed by every thread of the tap group at the start of
+// the unit (it depends only on the epoch constants), so it overlaps phase A
+// instead of sitting on the per-epoch serial path.
+template <int T>
+__device__ __forceinline__ void phase_b_range(PhaseB& pb, const EpochConsts& c, const CodeTables& ct,
+                                              int u0, int len) {
+    if (pb.kt >= T) {
+        pb.g0 = pb.cnt = 0;
+        return;
+    }
+    const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, pb.dk);
+    const int mhi = tap_index(u0 + len - 1, c.cps, c.base, pb.dk);
+    pb.g0 = trans_count(ct, mlo);
+    pb.cnt = trans_count(ct, mhi) - pb.g0;
+}
+
 // The transitions of this thread's tap in the sub-tile [u0, u0+len), two at
 // a time so the fp64 boundary searches of the pair overlap.
 template <int T>
 __device__ __forceinline__ void phase_b(PhaseB& pb, const EpochConsts& c, const float2* tile_d,
                                         const float2* anchors, const CodeTables& ct, int u0,
-                                        int len, const int2* tr /*[T] of this sub-tile*/) {
+                                        int len) {
     if (pb.kt >= T)
         return;
     const int hi = u0 + len - 1;
-    const int2 rk = tr[pb.kt];
-    const int g0 = rk.x, cnt = rk.y;
+    const int g0 = pb.g0, cnt = pb.cnt;
     for (int j = pb.jt; j < cnt; j += 2 * pb.gsz) {
         const int j2 = j + pb.gsz;
         const bool two = j2 < cnt;
@@ -431,6 +431,34 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
+// ---- thread-block cluster helpers (distributed shared memory) ----------
+__device__ __forceinline__ uint32_t cluster_map(const void* local, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+    return r;
+}
+// Asynchronous remote store that completes `8` transaction bytes on the
+// remote CTA's mbarrier (no fence / separate arrive needed).
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double x, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                     remote_addr),
+                 "d"(x), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
 // ---------------------------------------------------------------------
 // K3: loop update (tracking.hpp:542-601 + :459-515).
 struct LoopCfg {
@@ -443,7 +471,80 @@ struct LoopCfg {
     double dll_k1, dll_k2;
     double fll_k;               // ((4*B_fll)*2)*pi            (:88-92)
     double alpha;               // 1 / cn0_window_ms           (:466)
+    double inv_fs;              // 1 / fs (division by fs: div_fs)
+    double inv_fll_c, inv_fll_f;  // 1 / (2 pi (dt/2)), 1 / (2 pi dt) (:113-138)
 };
+
+// ---- branch-free fp64 helpers for the per-epoch critical path ----------
+// (SIMT lanes evaluate different pieces of the update with the same
+// instruction stream; without branches the pieces interleave.)
+// Reciprocal to ~1 ulp: hardware seed + two Newton steps.
+__device__ __forceinline__ double fast_rcp(double b) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    r = __fma_rn(r, __fma_rn(-b, r, 1.0), r);
+    return __fma_rn(r, __fma_rn(-b, r, 1.0), r);
+}
+// a / b to ~1 ulp (loop-filter internals, 1e-5 bar)
+__device__ __forceinline__ double fast_div(double a, double b) {
+    const double r = fast_rcp(b);
+    const double q = a * r;
+    return __fma_rn(__fma_rn(-b, q, a), r, q);
+}
+// sqrt to ~1 ulp, x >= 0
+__device__ __forceinline__ double fast_sqrt(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * __fma_rn(-0.5 * x * r, r, 1.5);
+    r = r * __fma_rn(-0.5 * x * r, r, 1.5);
+    const double s = x * r;
+    const double t = __fma_rn(0.5 * r, __fma_rn(-s, s, x), s);
+    return x > 0.0 ? t : 0.0;
+}
+// atan2(y, x), branch-free, relative error < 1e-13 (minimax polynomial of
+// atan(t)/t in t^2 on |t| <= tan(pi/8) after octant reduction, evaluated by
+// Estrin's scheme; t from a one-Newton-step reciprocal): the loop filters'
+// bar is 1e-5, and the short dependency chain is what matters here.
+__device__ __forceinline__ double atan2_bf(double y, double x) {
+    const double ax = fabs(x), ay = fabs(y);
+    const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+    const bool big = mn > 0.41421356237309503 * mx;
+    const double num = big ? mn - mx : mn;
+    const double den = big ? mn + mx : mx;
+    double r0;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(den));
+    const double rc = __fma_rn(r0, __fma_rn(-den, r0, 1.0), r0);
+    const double t = den > 0.0 ? num * rc : 0.0;
+    const double u = t * t, u2 = u * u, u4 = u2 * u2, u8 = u4 * u4;
+    const double p01 = __fma_rn(-0.33333333333328574, u, 1.0);
+    const double p23 = __fma_rn(-0.14285714182900408, u, 0.1999999999888112);
+    const double p45 = __fma_rn(-0.09090774637548268, u, 0.11111106252782828);
+    const double p67 = __fma_rn(-0.06640401512223144, u, 0.07689974062542373);
+    const double p89 = __fma_rn(-0.04350303905541161, u, 0.05689174687479212);
+    const double q0 = __fma_rn(p23, u2, p01);
+    const double q1 = __fma_rn(p67, u2, p45);
+    const double q2 = __fma_rn(0.021161483326090677, u2, p89);
+    const double p = __fma_rn(__fma_rn(q2, u4, q1), u4, q0);
+    (void)u8;
+    double r = __fma_rn(t, p, 0.0) + (big ? PI_D / 4.0 : 0.0);
+    r = ay > ax ? PI_D / 2.0 - r : r;
+    r = x < 0.0 ? PI_D - r : r;
+    return copysign(r, y);
+}
+// a / b correctly rounded for the NCO rates (w = 2 pi fD / fs, cps = cf / fs
+// must be the reference's IEEE quotients): reciprocal estimate + one exact
+// FMA correction, checked against the half-ulp bound; IEEE division only
+// when the check cannot decide.
+__device__ __forceinline__ double div_exact(double a, double b, double inv_b) {
+    const double q0 = a * inv_b;
+    const double q = __fma_rn(__fma_rn(-q0, b, a), inv_b, q0);
+    const double r = __fma_rn(-q, b, a);  // exact remainder
+    const double ulp = __longlong_as_double(__double_as_longlong(fabs(q)) & 0x7ff0000000000000ll) *
+                       2.220446049250313e-16;
+    if (!(fabs(r) < 0.49 * ulp * fabs(b)))
+        return a / b;
+    return q;
+}
 
 __device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, double cq,
                                            double dt, bool fold) {  // tracking.hpp:113-138
@@ -464,15 +565,12 @@ __device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, dou
 // lands in [0, y) for x >= 0 and (-y, 0] for x < 0, as fmod defines.
 __device__ __forceinline__ double fmod_exact(double x, double y, double inv_y) {
     double k = trunc(x * inv_y);
-    double r = __fma_rn(-k, y, x);
-    if (x >= 0.0) {
-        if (r < 0.0) { k -= 1.0; r = __fma_rn(-k, y, x); }
-        else if (r >= y) { k += 1.0; r = __fma_rn(-k, y, x); }
-    } else {
-        if (r > 0.0) { k += 1.0; r = __fma_rn(-k, y, x); }
-        else if (r <= -y) { k -= 1.0; r = __fma_rn(-k, y, x); }
-    }
-    return r;
+    const double r = __fma_rn(-k, y, x);
+    // branch-free +-1 correction of the quotient estimate
+    const double adj = x >= 0.0 ? (r < 0.0 ? -1.0 : (r >= y ? 1.0 : 0.0))
+                                : (r > 0.0 ? 1.0 : (r <= -y ? -1.0 : 0.0));
+    k += adj;
+    return __fma_rn(-k, y, x);
 }
 
 // NCO advance over n samples (tracking.hpp:275-280, fma as compiled)
@@ -688,6 +786,7 @@ struct CorrSmem {
     float red[32 * (2 * T + 2)];
     float2 rot[RUN + 1];
     uint64_t bars[2][2];  // per tile buffer: the two halves of its bulk copy
+    uint64_t pbar[2];     // cluster: partial totals of epoch e landed (e & 1)
     int inflight[2];      // per tile buffer: a bulk copy is outstanding
     int64_t issue_pos;    // ring position of the next unit to copy
     // epoch handed from the critical path to the control warp
@@ -696,7 +795,7 @@ struct CorrSmem {
     int64_t rec_esh;         // epochs_since_handoff before that epoch
     double rec_eenv;         // |E| + |L|
     int pending, stop;
-    int2 trange[MAXSUB * T];  // phase-B transition ranges per (sub-tile, tap)
+    double nco_ph1, nco_cp1;  // this epoch's NCO advance (control warp, off the critical path)
     CodeTables ct;
 };
 
@@ -716,6 +815,12 @@ __host__ __device__ constexpr int anchors_len(int nwork) { return (nwork + 1) & 
 template <int T>
 __device__ __forceinline__ float2* tile_of(CorrSmem<T>* s, int nwork, int b) {
     return anchors_of(s) + anchors_len(nwork) + (size_t)b * (nwork * RUN + 4);
+}
+// Cluster exchange slots after the tiles: [2 (epoch parity)][csize][2T+2]
+// fp64 partial totals, written by every CTA of the cluster into every CTA.
+template <int T>
+__device__ __forceinline__ double* xslots_of(CorrSmem<T>* s, int nwork, int nbuf) {
+    return reinterpret_cast<double*>(tile_of(s, nwork, nbuf));
 }
 
 // o (CorrelatorOutputs) from the fp64 sums
@@ -782,23 +887,27 @@ __device__ __forceinline__ void warp_partials(const float* acc, float* red, int 
     }
 }
 
-// fp64 cross-warp totals (by warp 0): lane v loads the nwarps partials of
-// value v with independent loads and adds them as a fixed pairwise tree
-// (deterministic order, depth log2(nwarps)).
+// fp64 cross-warp totals (by warp 0): lane v adds the nwarps partials of
+// value v into four interleaved fp64 chains, then pairs them -- a fixed,
+// deterministic order; only the live warps are converted and added.
 template <int V>
 __device__ __forceinline__ void warp0_totals(const float* red, double* sums, int lane, int nwarps) {
-    constexpr int WMAX = MAX_NT / 32;
     for (int v = lane; v < V; v += 32) {
-        double x[WMAX];
-#pragma unroll
-        for (int w = 0; w < WMAX; ++w)
-            x[w] = w < nwarps ? (double)red[w * V + v] : 0.0;
-#pragma unroll
-        for (int step = 1; step < WMAX; step <<= 1)
-#pragma unroll
-            for (int w = 0; w + step < WMAX; w += 2 * step)
-                x[w] += x[w + step];
-        sums[v] = x[0];
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+        int w = 0;
+        for (; w + 4 <= nwarps; w += 4) {
+            x0 += (double)red[w * V + v];
+            x1 += (double)red[(w + 1) * V + v];
+            x2 += (double)red[(w + 2) * V + v];
+            x3 += (double)red[(w + 3) * V + v];
+        }
+        if (w < nwarps)
+            x0 += (double)red[w * V + v];
+        if (w + 1 < nwarps)
+            x1 += (double)red[(w + 1) * V + v];
+        if (w + 2 < nwarps)
+            x2 += (double)red[(w + 2) * V + v];
+        sums[v] = (x0 + x1) + (x2 + x3);
     }
 }
 
@@ -824,6 +933,8 @@ struct TrackArgs {
     LoopCfg lc;
     long long* prof;  // optional stage clocks (L1RXG_PROF=1): [epoch][8], CTA 0
     int nbuf;         // sample tiles per CTA: 1 (latency shape) or 2 (double-buffered)
+    int csize;        // CTAs per channel (a thread-block cluster when > 1)
+    int share;        // samples of each epoch per cluster CTA (multiple of RUN)
 };
 
 // Stage clocks (profiling builds only: -DL1RXG_PROFILE, run with
@@ -845,7 +956,25 @@ struct TrackArgs {
             (t0) = t_;                                                         \
         }                                                                      \
     } while (0)
+// thread 0's phase A sub-steps (bank 3)
+#define PROF_A(k)                                                              \
+    do {                                                                       \
+        if (a.prof && blockIdx.x == 0 && e < 64 && tid == 0)                  \
+            a.prof[1536 + e * 8 + (k)] = clock64();                            \
+    } while (0)
+// warp-0 update sub-steps (bank 2)
+#define PROF_W(k)                                                              \
+    do {                                                                       \
+        if (a.prof && blockIdx.x == 0 && ep < 64 && lane == 0)                 \
+            a.prof[1024 + ep * 8 + (k)] = clock64();                           \
+    } while (0)
 #else
+#define PROF_A(k) \
+    do {          \
+    } while (0)
+#define PROF_W(k) \
+    do {          \
+    } while (0)
 #define PROF_STAMP(k) \
     do {              \
     } while (0)
@@ -871,10 +1000,28 @@ __device__ __forceinline__ void issue_unit(CorrSmem<T>* s, int b, float2* tile, 
     s->inflight[b] = 1;
 }
 
+// NCO advance of the epoch being correlated (tracking.hpp:275-280, exact
+// fmod): depends only on the pre-epoch state, so the control warp computes it
+// (lanes 0/1) while the work warps correlate.
+__device__ __forceinline__ void nco_advance_lanes(double& ph1, double& cp1, const EpochConsts& c,
+                                                  const l1rxg_channel& ch, int lane) {
+    const bool carrier = lane == 0;
+    const double adv = __dmul_rn((double)c.n, c.cps);
+    const double fm = fmod_exact(carrier ? __fma_rn(c.w, (double)c.n, ch.carrier_phase_rad)
+                                         : __dadd_rn(ch.code_phase_chips, adv),
+                                 carrier ? 2.0 * PI_D : 1023.0,
+                                 carrier ? 1.0 / (2.0 * PI_D) : 1.0 / 1023.0);
+    if (lane == 0)
+        ph1 = fm;
+    else if (lane == 1)
+        cp1 = fm;
+}
+
 // Control-warp side of an epoch: run state, quality metrics and lock-fail
 // rule for the epoch handed over in s->rec, then its record and tap sums.
 template <int T>
-__device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a, int lane) {
+__device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a, int lane,
+                                             bool writer) {
     if (lane == 0) {
         l1rxg_channel& ch = s->ch;
         const l1rxg_corr o = corr_from_sums<T>(s->sums, a.ke, a.kp, a.kl, a.n);
@@ -900,9 +1047,10 @@ __device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a,
         r.cn0_dbhz = ch.cn0_dbhz;
         r.carrier_lock_ratio = ch.carrier_lock_ratio;
         r.mu_smoothed = ch.mu_smoothed;
-        a.recs[s->rec_slot] = r;
+        if (writer)
+            a.recs[s->rec_slot] = r;
     }
-    if (a.tap_sums && lane < 2 * T)
+    if (writer && a.tap_sums && lane < 2 * T)
         a.tap_sums[s->rec_slot * (2 * T) + lane] = s->sums[lane];
 }
 
@@ -920,10 +1068,36 @@ __device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a,
 template <int T>
 __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a, const EpochConsts& c,
                                              int64_t off, int cidx, int64_t done, int nwork_warps,
-                                             int lane) {
+                                             int lane, int crank, int ep, double* xs, int rec_i) {
     constexpr int V = 2 * T + 2;
+    PROF_W(0);
     warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
     __syncwarp();
+    PROF_W(1);
+    if (a.csize > 1) {
+        // every CTA of the cluster sends its fp64 totals to every CTA
+        // (st.async completing bytes on the receiver's mbarrier), then each
+        // sums the csize slots in rank order: identical cluster totals (and
+        // so identical loop updates) in every CTA, one round trip
+        const int par = ep & 1;
+        const int K = a.csize;
+        for (int it = lane; it < V * K; it += 32) {
+            const int q = it / V, v = it - q * V;
+            st_async_f64(cluster_map(xs + (par * K + crank) * V + v, q), s->sums[v],
+                         cluster_map(&s->pbar[par], q));
+        }
+        if (lane == 0)
+            mbar_expect_tx(&s->pbar[par], (uint32_t)(K * V * 8));
+        mbar_wait_cluster(&s->pbar[par], (uint32_t)(ep >> 1) & 1u);
+        for (int v = lane; v < V; v += 32) {
+            double t = 0.0;
+            for (int q = 0; q < K; ++q)
+                t += xs[(par * K + q) * V + v];
+            s->sums[v] = t;
+        }
+        __syncwarp();
+    }
+    PROF_W(2);
     l1rxg_channel& ch = s->ch;
     if (ch.state == L1RXG_IDLE) {  // the previous epoch dropped the channel
         if (lane == 0)
@@ -955,14 +1129,10 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
         x = dot;
         zero = cross == 0.0 && dot == 0.0;
     }
-    const double ang = atan2(y, x);
+    const double ang = atan2_bf(y, x);
     // sqrt lanes
-    const double sq = sqrt(lane == 3 ? ie * ie + qe * qe : il * il + ql * ql);
-    // fmod lanes (exact)
-    const bool carrier = lane == 5;
-    const double fm = fmod_exact(carrier ? __fma_rn(c.w, (double)c.n, ph0) : __dadd_rn(cp0, adv),
-                                 carrier ? 2.0 * PI_D : 1023.0,
-                                 carrier ? 1.0 / (2.0 * PI_D) : 1.0 / 1023.0);
+    const double sq = fast_sqrt(lane == 3 ? ie * ie + qe * qe : il * il + ql * ql);
+    PROF_W(3);
     const double a_pll = __shfl_sync(0xffffffffu, ang, 0);
     const double a_fc = __shfl_sync(0xffffffffu, ang, 1);
     const double a_ff = __shfl_sync(0xffffffffu, ang, 2);
@@ -970,17 +1140,17 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
     const bool z_ff = __shfl_sync(0xffffffffu, zero, 2);
     const double e = __shfl_sync(0xffffffffu, sq, 3);
     const double l = __shfl_sync(0xffffffffu, sq, 4);
-    const double ph1 = __shfl_sync(0xffffffffu, fm, 5);
-    const double cp1 = __shfl_sync(0xffffffffu, fm, 6);
+    const double ph1 = s->nco_ph1;  // NCO advance, computed by the control warp
+    const double cp1 = s->nco_cp1;
     double fd = 0.0, cf = 0.0;
     if (lane == 0) {
         LoopPre pre;
         pre.e = e;
         pre.l = l;
-        pre.dll = (e + l == 0.0) ? 0.0 : 0.5 * (e - l) / (e + l);  // :95-101
+        pre.dll = (e + l == 0.0) ? 0.0 : 0.5 * fast_div(e - l, e + l);  // :95-101
         pre.pll = ip == 0.0 ? (qp == 0.0 ? 0.0 : (qp > 0 ? PI_D / 2.0 : -PI_D / 2.0)) : a_pll;
-        pre.fc = z_fc ? 0.0 : a_fc / (2.0 * PI_D * (a.lc.dt / 2.0));
-        pre.ff = z_ff ? 0.0 : a_ff / (2.0 * PI_D * a.lc.dt);
+        pre.fc = z_fc ? 0.0 : a_fc * a.lc.inv_fll_c;
+        pre.ff = z_ff ? 0.0 : a_ff * a.lc.inv_fll_f;
         pre.carrier_phase = ph1;
         pre.code_phase = cp1;
         pre.chi = __dadd_rn(chi0, adv);
@@ -996,29 +1166,31 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
         o.ip = ip;
         o.qp = qp;
         o.n_samples = c.n;
+        PROF_W(4);
         loop_fast(ch, o, a.lc, pre);
+        PROF_W(5);
         fd = ch.carrier_doppler_hz;
         cf = ch.code_freq_hz;
-        s->rec_slot = (int64_t)cidx * a.max_records + (done % a.max_records);
+        s->rec_slot = (int64_t)cidx * a.max_records + rec_i;
         s->pending = 1;
     }
-    // next epoch's w = (2 pi fD)/fs and cps = cf/fs, one division per lane
-    fd = __shfl_sync(0xffffffffu, fd, 0);
-    cf = __shfl_sync(0xffffffffu, cf, 0);
-    const double quo = (lane == 0 ? 2.0 * PI_D * fd : cf) / a.lc.fs;
-    const double w = __shfl_sync(0xffffffffu, quo, 0);
-    const double cps = __shfl_sync(0xffffffffu, quo, 1);
+    // next epoch's w = (2 pi fD)/fs and cps = cf/fs (IEEE quotients, both on
+    // lane 0: independent, so they overlap); inv_cps is formed by each thread
+    // at the start of the next epoch, off this path
+    PROF_W(6);
     if (lane == 0) {
+        const double w = div_exact(2.0 * PI_D * fd, a.lc.fs, a.lc.inv_fs);
+        const double cps = div_exact(cf, a.lc.fs, a.lc.inv_fs);
         EpochConsts& nc = s->c;
         nc.w = w;
         nc.cps = cps;
-        nc.inv_cps = __drcp_rn(cps);
         nc.base = cp1 + 1023.0;
         nc.phi = ph1;
         nc.n = c.n;
         nc.nh = c.nh;
     }
     __syncwarp();
+    PROF_W(7);
 }
 
 // Channel-resident persistent tracking kernel: one CTA per channel loops
@@ -1044,7 +1216,12 @@ template <int T>
 __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
-    const int cidx = blockIdx.x;
+    // cluster split: csize consecutive CTAs (one cluster) share a channel,
+    // CTA crank correlating samples [r0, rend) of every epoch
+    const int csize = a.csize;
+    const int crank = csize > 1 ? (int)(blockIdx.x % csize) : 0;
+    const int cidx = blockIdx.x / csize;
+    const bool writer = crank == 0;
     const int strm = a.chan_stream[cidx];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = (blockDim.x + 31) >> 5;
@@ -1054,12 +1231,17 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     constexpr int V = 2 * T + 2;
     const int cap = nwork * RUN;
     const int n = a.n;
-    const int nsub = (n + cap - 1) / cap;
+    const int r0 = csize > 1 ? crank * a.share : 0;
+    const int rend = csize > 1 ? min(n, r0 + a.share) : n;
+    const int my_n = rend - r0;
+    const int nsub = (my_n + cap - 1) / cap;
+    const int skip = n - my_n;             // ring samples between this CTA's epochs
     const int nbuf = a.nbuf;
     const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
     const int64_t avail = a.avail[strm];
     const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
     float2* anchors = anchors_of(s);
+    double* xs = xslots_of(s, nwork, nbuf);
     const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
     // unit v of this launch: epoch v / nsub, sub-tile v % nsub, into tile
     // v % nbuf.  Units of the epoch being correlated (ev <= ecur) are always
@@ -1073,19 +1255,23 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             off0 < avail - a.ring_cap || (ev > ecur && s->ch.state == L1RXG_IDLE))
             return;
         const int b = v & (nbuf - 1);
-        const int len = min(cap, n - q * cap);
-        // units tile the epochs contiguously and are issued in order without
-        // gaps, so the ring position advances by each unit's length
+        const int len = min(cap, rend - (r0 + q * cap));
+        // units are issued in order without gaps: the ring position advances
+        // by each unit's length (+ the other cluster CTAs' samples at the end
+        // of an epoch)
         const int64_t pos = s->issue_pos;
         issue_unit(s, b, tile_of(s, nwork, b), ring, pos, len);
-        const int64_t nxt = pos + len;
-        s->issue_pos = nxt >= a.ring_cap ? nxt - a.ring_cap : nxt;
+        int64_t nxt = pos + len + (q + 1 == nsub ? skip : 0);
+        while (nxt >= a.ring_cap)
+            nxt -= a.ring_cap;
+        s->issue_pos = nxt;
     };
     if (tid == 0) {
         s->ch = a.chans[cidx];
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s->bars[b][0], 1);
             mbar_init(&s->bars[b][1], 1);
+            mbar_init(&s->pbar[b], 1);  // the local expect_tx arrive + K*V*8 bytes
             s->inflight[b] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1094,12 +1280,15 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     }
     for (int k = tid; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
+    if (csize > 1)
+        cluster_sync_all();  // barriers initialised before any remote arrive
     __syncthreads();
     PhaseB pb;
     phase_b_init<T>(pb, s->d, a.kp, tid, nwork);
     build_code_tables(s->ct, a.codes, s->ch.prn);
+    const int64_t pos0 = off0 >= 0 ? (off0 + r0) % a.ring_cap : 0;
     if (tid == 0) {  // first epoch: consts and the first units
-        s->issue_pos = off0 >= 0 ? off0 % a.ring_cap : 0;
+        s->issue_pos = pos0;
         const l1rxg_channel& ch = s->ch;
         make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
                     ch.carrier_phase_rad, a.lc.fs, n);
@@ -1108,8 +1297,6 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     }
     __syncthreads();
     fill_rot(s->rot, s->c.w, tid);
-    if (warp == 0)
-        fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, nsub, lane);
     __syncthreads();
 
     uint32_t phase = 0;  // bit b: parity of tile b's next completion
@@ -1117,10 +1304,12 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     int u = 0;           // next unit to consume
     // ring position of unit u, tracked by every thread (the copy's 16-byte
     // alignment slack follows from it) so no hand-off from the issuer is needed
-    int64_t upos = off0 >= 0 ? off0 % a.ring_cap : 0;
+    int64_t upos = pos0;
     int64_t done = a.ecount[cidx];
+    int rec_i = (int)(done % a.max_records);  // record slot of the current epoch
     for (;;) {
-        // epoch admission (uniform: every thread reads the same smem state)
+        // epoch admission (uniform: every thread -- and every CTA of a
+        // cluster -- reads the same state)
         const int64_t off = s->ch.sample_offset_next_epoch;
         if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
             break;
@@ -1131,13 +1320,18 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         }
         if (tid == 0)
             PROF_STAMP(0);
-        // control warp: finish the previous epoch while this one correlates
-        if (warp == ctl && s->pending) {
-            finish_epoch<T>(s, a, lane);
-            if (lane == 0)
-                s->pending = 0;
+        PROF_A(0);
+        EpochConsts c = s->c;
+        // control warp: this epoch's NCO advance, then finish the previous
+        // epoch, while this one correlates
+        if (warp == ctl) {
+            nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
+            if (s->pending) {
+                finish_epoch<T>(s, a, lane, writer);
+                if (lane == 0)
+                    s->pending = 0;
+            }
         }
-        const EpochConsts c = s->c;
         float acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v)
@@ -1149,31 +1343,42 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         for (int q = 0; q < nsub; ++q, ++u) {
             const int b = nbuf == 1 ? 0 : (int)(u & 1);
             const uint32_t par = (phase >> b) & 1u;
-            const int u0 = q * cap;
-            const int len = min(cap, n - u0);
+            const int u0 = r0 + q * cap;
+            const int len = min(cap, rend - u0);
             const int delta = (int)(upos & 1);
             const int h = 2 * ((len + delta) / 4);
-            upos += len;
-            if (upos >= a.ring_cap)
+            upos += len + (q + 1 == nsub ? skip : 0);
+            while (upos >= a.ring_cap)
                 upos -= a.ring_cap;
             if (!noop) {
                 float2* tile = tile_of(s, nwork, b);
                 const float2* tile_d = tile + delta;
                 if (tid < nwork) {
+                    PROF_A(1);
                     const int i0 = u0 + tid * RUN;
-                    const int cnt = min(RUN, n - i0);
-                    const int r0 = delta + tid * RUN;
+                    const int cnt = min(RUN, rend - i0);
+                    const int r0t = delta + tid * RUN;
+                    PROF_A(2);
+                    // each half of the copy has waiters (thread 0's run starts
+                    // in the first, the last run ends in the second), so after
+                    // the work-warp barrier below both copies are complete
                     if (cnt > 0) {
-                        if (r0 < h)
+                        if (r0t < h)
                             mbar_wait(&s->bars[b][0], par);
-                        if (r0 + RUN > h)
+                        if (r0t + RUN > h)
                             mbar_wait(&s->bars[b][1], par);
-                        phase_a_dispatch<T>(c, tile + r0, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
-                                            acc, &anchors[tid]);
                     }
-                    if (tid == 0) {  // every copy completes before its tile is reused
-                        mbar_wait(&s->bars[b][0], par);
-                        mbar_wait(&s->bars[b][1], par);
+                    PROF_A(3);
+                    // phase B's constants and transition range depend only on
+                    // the epoch constants: computed here so they interleave
+                    // with phase A
+                    c.inv_cps = fast_rcp(c.cps);  // tap_boundary's estimate (within 2 ulp)
+                    phase_b_range<T>(pb, c, s->ct, u0, len);
+                    if (cnt > 0)
+                        phase_a_dispatch<T>(c, tile + r0t, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
+                                            acc, &anchors[tid]);
+                    PROF_A(4);
+                    if (tid == 0) {
                         PROF_STAMP(1);
                         PROF_UNIT(0, tu);
                     }
@@ -1187,12 +1392,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         PROF_STAMP(2);
                         PROF_UNIT(1, tu);
                     }
-#ifdef L1RXG_PHB_PERTAP
-                    phase_b_pertap<T>(c, tile_d, anchors, s->ct, s->d, a.kp, u0, len, acc, nwork,
-                                      s->trange + q * T);
-#else
-                    phase_b<T>(pb, c, tile_d, anchors, s->ct, u0, len, s->trange + q * T);
-#endif
+                    phase_b<T>(pb, c, tile_d, anchors, s->ct, u0, len);
                 }
             }
             if (q + 1 == nsub && warp < nwork_warps) {
@@ -1214,8 +1414,9 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                 PROF_UNIT(4, tu);
         }
         // ---- critical path, all on warp 0 in SIMT form (no cross-warp
-        // hand-off): totals -> one atan2 / sqrt / fmod / division per lane
-        // -> loop_fast on lane 0 -> next epoch's constants, rotators, ranges
+        // hand-off): totals (+ the cluster exchange) -> one atan2 / sqrt /
+        // fmod / division per lane -> loop_fast on lane 0 -> next epoch's
+        // constants, rotators, ranges
         if (warp == 0) {
             if (tid == 0) {
                 PROF_STAMP(4);
@@ -1225,11 +1426,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         a.prof[512 + e * 8 + k] = pu[k];
 #endif
             }
-            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane);
+            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
             if (tid == 0)
                 PROF_STAMP(5);
             fill_rot(s->rot, s->c.w, lane);
-            fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, nsub, lane);
             if (tid == 0)
                 PROF_STAMP(6);
         }
@@ -1240,10 +1440,12 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             break;
         ++e;
         ++done;
+        if (++rec_i == a.max_records)
+            rec_i = 0;
     }
     __syncthreads();
     if (warp == ctl && s->pending)
-        finish_epoch<T>(s, a, lane);
+        finish_epoch<T>(s, a, lane, writer);
     __syncthreads();
     if (tid == 0) {
         for (int b = 0; b < nbuf; ++b)
@@ -1251,9 +1453,13 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                 mbar_wait(&s->bars[b][0], (phase >> b) & 1u);
                 mbar_wait(&s->bars[b][1], (phase >> b) & 1u);
             }
-        a.chans[cidx] = s->ch;
-        a.ecount[cidx] = done;
+        if (writer) {
+            a.chans[cidx] = s->ch;
+            a.ecount[cidx] = done;
+        }
     }
+    if (csize > 1)
+        cluster_sync_all();  // no CTA leaves while a peer may still write into it
 }
 
 // ---------------------------------------------------------------------
@@ -1294,8 +1500,6 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
     PhaseB pb;
     phase_b_init<T>(pb, s->d, a.kp, tid, blockDim.x);
     fill_rot(s->rot, s->c.w, tid);
-    if (warp == 0)
-        fill_tap_ranges<T>(s->trange, s->c, s->ct, s->d, cap, (n + cap - 1) / cap, lane);
     const EpochConsts c = s->c;
     float acc[V];
 #pragma unroll
@@ -1314,7 +1518,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
                 phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
                                     acc, &anchors[tid]);
             __syncthreads();
-            phase_b<T>(pb, c, tile, anchors, s->ct, u0, len, s->trange + (u0 / cap) * T);
+            phase_b_range<T>(pb, c, s->ct, u0, len);
+            phase_b<T>(pb, c, tile, anchors, s->ct, u0, len);
             __syncthreads();
         }
     }

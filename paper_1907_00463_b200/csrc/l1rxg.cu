@@ -151,16 +151,39 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
     lc.dll_k2 = 2.0 * cfg.dll_damping * wd;
     lc.fll_k = 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D;
     lc.alpha = 1.0 / static_cast<double>(cfg.cn0_window_ms);
+    lc.inv_fs = 1.0 / fs;
+    lc.inv_fll_c = 1.0 / (2.0 * PI_D * (lc.dt / 2.0));
+    lc.inv_fll_f = 1.0 / (2.0 * PI_D * lc.dt);
     return lc;
 }
 
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
-    const size_t sm = smem_bytes<T>(nt - 32, a.nbuf);  // the control warp owns no tile runs
+    // the control warp owns no tile runs; + the cluster exchange slots
+    const size_t sm = smem_bytes<T>(nt - 32, a.nbuf) +
+                      (a.csize > 1 ? 2u * a.csize * (2 * T + 2) * sizeof(double) : 0);
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
-    track_kernel<T><<<n_ch, nt, sm, s>>>(a);
+    if (a.csize <= 1) {
+        track_kernel<T><<<n_ch, nt, sm, s>>>(a);
+    } else {  // one thread-block cluster of csize CTAs per channel
+        if (a.csize > 8)
+            CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(n_ch * a.csize));
+        cfg.blockDim = dim3(static_cast<unsigned>(nt));
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(a.csize);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, track_kernel<T>, a));
+    }
     CK(cudaGetLastError());
     return 0;
 }
@@ -270,6 +293,8 @@ struct l1rxg_tracker {
     int T = 3;
     int nt = 64;
     int nbuf = 1;
+    int csize = 1;   // CTAs per channel (cluster) in the latency shape
+    int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
     std::vector<StreamRing> streams;
     float2* d_ring = nullptr;
@@ -629,8 +654,28 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             t->nt = pick_threads(n, nullptr, mx) + 32;
             t->nbuf = ev_nb ? std::atoi(ev_nb) : 1;
         } else {
-            t->nt = pick_threads(n, nullptr, MAX_NT - 32) + 32;
-            t->nbuf = 1;
+            // latency shape: split each channel's epoch over a cluster of K
+            // CTAs (one per SM) while the channels x K fit the SMs and each
+            // CTA keeps >= 1024 samples; K = 1 is the single-CTA path
+            static const char* ev_cl = std::getenv("L1RXG_CLUSTER");
+            int K = 1;
+            if (ev_cl) {
+                K = std::max(1, std::min(16, std::atoi(ev_cl)));
+            } else {
+                while (K < 16 && d->n_channels * K * 2 <= nsm && n / (K * 2) >= 1024)
+                    K *= 2;
+            }
+            const int share = ((n + K * RUN - 1) / (K * RUN)) * RUN;
+            while (K > 1 && (K - 1) * share >= n)
+                --K;
+            t->csize = K;
+            t->share = K > 1 ? share : n;
+            t->nt = pick_threads(t->share, nullptr, MAX_NT - 32) + 32;
+            // a second tile when it fits: the copy of epoch e+1 is then issued
+            // while epoch e is still being correlated (a full epoch ahead)
+            static const char* ev_nb1 = std::getenv("L1RXG_LAT_NBUF");
+            const size_t two = static_cast<size_t>(t->nt - 32) * RUN * 2 * sizeof(float2) + 40000;
+            t->nbuf = ev_nb1 ? std::atoi(ev_nb1) : (two <= 200000 ? 2 : 1);
         }
     }
     t->R = d->ring_samples;
@@ -870,6 +915,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.taps = padded_taps(t->d.taps, t->T);
     a.lc = make_loop_cfg(t->d.cfg, t->d.kernel, t->d.sample_rate_hz, a.n);
     a.nbuf = t->nbuf;
+    a.csize = t->csize;
+    a.share = t->share;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
@@ -877,8 +924,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     static const bool prof = std::getenv("L1RXG_PROF") != nullptr;
     long long* dprof = nullptr;
     if (prof) {
-        CK(cudaMalloc(&dprof, 3 * 64 * 8 * sizeof(long long)));
-        CK(cudaMemsetAsync(dprof, 0, 3 * 64 * 8 * sizeof(long long), st));
+        CK(cudaMalloc(&dprof, 4 * 64 * 8 * sizeof(long long)));
+        CK(cudaMemsetAsync(dprof, 0, 4 * 64 * 8 * sizeof(long long), st));
     }
     a.prof = dprof;
     auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st); };
@@ -888,7 +935,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     cudaEventRecord(e1, st);
     t->timed.push_back({e0, e1, 1});
     if (prof) {
-        long long h[3 * 64 * 8];
+        long long h[4 * 64 * 8];
         CK(cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         cudaFree(dprof);
@@ -902,8 +949,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             acc[0] += static_cast<double>(h[e * 8 + 7] - h[e * 8]);
             for (int k = 0; k < 8; ++k)
                 pc[k] += static_cast<double>(h[512 + e * 8 + k]);
-            for (int k = 0; k < 8; ++k)
-                arr[k] += static_cast<double>(h[1024 + e * 8 + k]);
+            for (int k = 1; k < 8; ++k)
+                arr[k] += static_cast<double>(h[1024 + e * 8 + k] - h[1024 + e * 8 + k - 1]);
             ++cnt;
         }
         if (cnt)
@@ -918,7 +965,30 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
                          "barrier A %.0f | B+partials %.0f | consumed barrier %.0f | "
                          "issue+publish %.0f\n",
                          pc[0] / cnt, pc[1] / cnt, pc[2] / cnt, pc[3] / cnt, pc[4] / cnt);
-        (void)arr;
+        if (cnt)
+            std::fprintf(stderr,
+                         "[l1rxg prof] warp-0 update: totals %.0f | cluster exchange %.0f | "
+                         "operands %.0f | atan2/sqrt/fmod %.0f | shuffles+pre %.0f | loop_fast %.0f "
+                         "| division %.0f | consts %.0f\n",
+                         arr[1] / cnt, arr[2] / cnt, 0.0, arr[3] / cnt, arr[4] / cnt, arr[5] / cnt,
+                         arr[6] / cnt, arr[7] / cnt);
+        {
+            double ph[8] = {0};
+            int c2 = 0;
+            for (int e = 2; e < 64; ++e) {
+                if (h[1536 + e * 8] == 0)
+                    continue;
+                for (int k = 1; k < 8; ++k)
+                    if (h[1536 + e * 8 + k])
+                        ph[k] += static_cast<double>(h[1536 + e * 8 + k] - h[1536 + e * 8 + k - 1]);
+                ++c2;
+            }
+            if (c2)
+                std::fprintf(stderr,
+                             "[l1rxg prof] phase A (thread 0, last unit): consts %.0f | range %.0f | "
+                             "tile wait %.0f | phase A %.0f | own-copy wait %.0f\n",
+                             ph[1] / c2, ph[2] / c2, ph[3] / c2, ph[4] / c2, ph[5] / c2);
+        }
     }
     return 0;
 }
