@@ -95,6 +95,29 @@ __device__ __forceinline__ int tap_boundary(int m, double d, const EpochConsts& 
     return b - (int)dn + (int)up;
 }
 
+// Sample kinds of a tracker ring: SK_F32 (float2: decoded/filtered real IF),
+// SK_I16 (raw cint16, 4 B) and SK_I8 (raw cint8, 2 B); raw samples are
+// converted while they are wiped (the /32768 or /128 scale is a power of two,
+// folded exactly into the rotator table).
+constexpr int SK_F32 = 0, SK_I16 = 1, SK_I8 = 2;
+template <int SK>
+struct Samp;
+template <>
+struct Samp<SK_F32> {
+    typedef unsigned long long raw_t;
+    static constexpr int esz = 8;
+};
+template <>
+struct Samp<SK_I16> {
+    typedef uint32_t raw_t;
+    static constexpr int esz = 4;
+};
+template <>
+struct Samp<SK_I8> {
+    typedef uint16_t raw_t;
+    static constexpr int esz = 2;
+};
+
 // A complex sample as one 64-bit value (one LDS.64 / STS.64).
 typedef unsigned long long f2x;
 __device__ __forceinline__ f2x pk2(float a, float b) {
@@ -106,6 +129,23 @@ __device__ __forceinline__ float2 upk2(f2x v) {
     float2 r;
     asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
     return r;
+}
+__device__ __forceinline__ float2 cvt_sample(f2x v) { return upk2(v); }
+// Raw complex ints -> exact floats without the (quarter-rate) I2F: flipping
+// the sign bit biases each component to an unsigned value u = v + 2^(b-1);
+// 0x4B400000 | u is the float 1.5 * 2^23 + u, so one FADD removes the
+// bias exactly (|v| < 2^22).  Little endian: the real part is the low half.
+__device__ __forceinline__ float2 cvt_sample(uint32_t w) {  // cint16
+    const uint32_t u = w ^ 0x80008000u;
+    const float re = __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7610));
+    const float im = __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7632));
+    return make_float2(re - 12615680.0f, im - 12615680.0f);  // 1.5 * 2^23 + 2^15
+}
+__device__ __forceinline__ float2 cvt_sample(uint16_t h) {  // cint8
+    const uint32_t u = (uint32_t)h ^ 0x8080u;
+    const float re = __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7640));
+    const float im = __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7641));
+    return make_float2(re - 12583040.0f, im - 12583040.0f);  // 1.5 * 2^23 + 2^7
 }
 
 // ---------------------------------------------------------------------
@@ -173,8 +213,10 @@ __device__ void build_code_tables(CodeTables& ct, const int8_t* codes, int prn) 
 // anchored) samples, stores the run's carrier anchor e^{-j theta(i0)}, and
 // accumulates chip_k(last) * anchor * total into acc[2k..2k+1] for every
 // tap, plus the first-half prompt into acc[2T..2T+1].
-template <int T, bool FULL>
-__device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
+// raw: the run's samples (any sample kind); run: where its exclusive prefix
+// sums go (the same memory for float2 rings: in place).
+template <int T, bool FULL, typename R>
+__device__ __forceinline__ void phase_a(const EpochConsts& c, const R* raw, float2* run,
                                         const float2* __restrict__ rot,
                                         const int8_t* __restrict__ chip,
                                         const double* __restrict__ d, int kp, int i0, int cnt,
@@ -195,20 +237,20 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     // register-pair moves and measured slower.)
     constexpr int PF = 4;
     f2x* runp = reinterpret_cast<f2x*>(run);
-    f2x xw[PF];
+    R xw[PF];
     float2 qw[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
-        xw[j] = (FULL || j < cnt) ? runp[j] : 0ull;
+        xw[j] = (FULL || j < cnt) ? raw[j] : R(0);
         qw[j] = rot[j];
     }
     f2x P = 0ull;
 #pragma unroll
     for (int j = 0; j < RUN; ++j) {
-        const float2 x = upk2(xw[j % PF]);
+        const float2 x = cvt_sample(xw[j % PF]);
         const float2 q = qw[j % PF];
         if (j + PF < RUN) {
-            xw[j % PF] = (FULL || j + PF < cnt) ? runp[j + PF] : 0ull;
+            xw[j % PF] = (FULL || j + PF < cnt) ? raw[j + PF] : R(0);
             qw[j % PF] = rot[j + PF];
         }
         runp[j] = P;
@@ -242,15 +284,15 @@ __device__ __forceinline__ void phase_a(const EpochConsts& c, float2* run,
     }
 }
 
-template <int T>
-__device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, float2* run,
+template <int T, typename R>
+__device__ __forceinline__ void phase_a_dispatch(const EpochConsts& c, const R* raw, float2* run,
                                                  const float2* rot, const int8_t* chip,
                                                  const double* d, int kp, int i0, int cnt,
                                                  float* acc, float2* anchor_slot) {
     if (cnt == RUN)
-        phase_a<T, true>(c, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
+        phase_a<T, true>(c, raw, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
     else
-        phase_a<T, false>(c, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
+        phase_a<T, false>(c, raw, run, rot, chip, d, kp, i0, cnt, acc, anchor_slot);
 }
 
 // Phase B: every chip transition of every tap whose step falls in the
@@ -387,13 +429,15 @@ __device__ __forceinline__ void phase_b_fold(PhaseB& pb, float* acc) {
     pb.re = pb.im = pb.hre = pb.him = 0.f;
 }
 
-// Per-epoch rotator table rot[j] = (cos wj, sin wj), j < RUN (accurate
-// sincosf); 8 bytes so phase A's broadcast read is one shared wavefront.
-__device__ __forceinline__ void fill_rot(float2* rot, double w, int tid) {
+// Per-epoch rotator table rot[j] = scale * (cos wj, sin wj), j < RUN
+// (accurate sincosf; scale = the raw samples' power-of-two decode factor, so
+// the products equal decode-then-wipe exactly); 8 bytes so phase A's
+// broadcast read is one shared wavefront.
+__device__ __forceinline__ void fill_rot(float2* rot, double w, int tid, float scale = 1.f) {
     if (tid < RUN) {
         float s, co;
         sincosf((float)(w * (double)tid), &s, &co);
-        rot[tid] = make_float2(co, s);
+        rot[tid] = make_float2(co * scale, s * scale);
     }
 }
 
@@ -812,15 +856,28 @@ __device__ __forceinline__ float2* anchors_of(CorrSmem<T>* s) {
     return reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + corr_smem_header<T>());
 }
 __host__ __device__ constexpr int anchors_len(int nwork) { return (nwork + 1) & ~1; }
+// Sample tile b: nwork*RUN samples of esz bytes + 16 B of bulk-copy
+// alignment slack on each side, rounded to 16 B.
+__host__ __device__ constexpr size_t tile_bytes(int nwork, int esz) {
+    return ((static_cast<size_t>(nwork) * RUN * esz + 32) + 15) & ~size_t(15);
+}
 template <int T>
-__device__ __forceinline__ float2* tile_of(CorrSmem<T>* s, int nwork, int b) {
-    return anchors_of(s) + anchors_len(nwork) + (size_t)b * (nwork * RUN + 4);
+__device__ __forceinline__ unsigned char* tile_of(CorrSmem<T>* s, int nwork, int b, int esz) {
+    return reinterpret_cast<unsigned char*>(anchors_of(s) + anchors_len(nwork)) +
+           (size_t)b * tile_bytes(nwork, esz);
+}
+// Raw sample kinds: the prefix sums go to their own float2 tile after the
+// sample tiles (float2 rings keep them in place).
+template <int T>
+__device__ __forceinline__ float2* prefix_of(CorrSmem<T>* s, int nwork, int nbuf, int esz) {
+    return reinterpret_cast<float2*>(tile_of(s, nwork, nbuf, esz));
 }
 // Cluster exchange slots after the tiles: [2 (epoch parity)][csize][2T+2]
 // fp64 partial totals, written by every CTA of the cluster into every CTA.
 template <int T>
-__device__ __forceinline__ double* xslots_of(CorrSmem<T>* s, int nwork, int nbuf) {
-    return reinterpret_cast<double*>(tile_of(s, nwork, nbuf));
+__device__ __forceinline__ double* xslots_of(CorrSmem<T>* s, int nwork, int nbuf, int esz) {
+    return reinterpret_cast<double*>(prefix_of(s, nwork, nbuf, esz) +
+                                     (esz == 8 ? 0 : (size_t)nwork * RUN));
 }
 
 // o (CorrelatorOutputs) from the fp64 sums
@@ -914,7 +971,7 @@ __device__ __forceinline__ void warp0_totals(const float* red, double* sums, int
 // ---------------------------------------------------------------------
 // Kernel arguments for closed-loop tracking.
 struct TrackArgs {
-    const float2* ring;       // [n_streams][ring_stride]
+    const unsigned char* ring;  // [n_streams][ring_stride] samples of esz bytes
     int64_t ring_stride;      // R + apron
     int64_t ring_cap;         // R
     const int64_t* avail;     // [n_streams] samples ingested
@@ -983,20 +1040,23 @@ struct TrackArgs {
     } while (0)
 #endif
 
-// TMA unit: len samples from ring position pos (< R) into the tile,
-// copied from the 16-byte aligned position below (delta samples of slack),
-// in two halves on two mbarriers.
+// TMA unit: len samples (esz bytes each) from ring position pos (< R) into
+// the tile, copied from the 16-byte aligned position below (delta samples of
+// slack), in two halves on two mbarriers.
 template <int T>
-__device__ __forceinline__ void issue_unit(CorrSmem<T>* s, int b, float2* tile, const float2* ring,
-                                           int64_t pos, int len) {
-    const int delta = (int)(pos & 1);
-    const int h = 2 * ((len + delta) / 4);
-    const uint32_t total = (uint32_t)(((len + delta) * 8 + 15) & ~15);
-    const uint32_t b0 = (uint32_t)h * 8u;
+__device__ __forceinline__ void issue_unit(CorrSmem<T>* s, int b, unsigned char* tile,
+                                           const unsigned char* ring, int64_t pos, int len, int esz) {
+    const int A = 16 / esz;  // samples per 16 bytes
+    const int delta = (int)(pos & (A - 1));
+    const int h = A * ((len + delta) / (2 * A));
+    const uint32_t total = (uint32_t)(((len + delta) * esz + 15) & ~15);
+    const uint32_t b0 = (uint32_t)(h * esz);
+    const unsigned char* src = ring + (pos - delta) * esz;
     mbar_expect_tx(&s->bars[b][0], b0);
-    tma_load_1d(tile, ring + (pos - delta), b0, &s->bars[b][0]);
+    if (b0)
+        tma_load_1d(tile, src, b0, &s->bars[b][0]);
     mbar_expect_tx(&s->bars[b][1], total - b0);
-    tma_load_1d(tile + h, ring + (pos - delta) + h, total - b0, &s->bars[b][1]);
+    tma_load_1d(tile + b0, src + b0, total - b0, &s->bars[b][1]);
     s->inflight[b] = 1;
 }
 
@@ -1212,8 +1272,11 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
 //     If that makes the channel Idle, epoch e+1 is discarded before its
 //     loop update, exactly as if it had never been admitted
 //     (tracking.hpp:511-514 + the caller's Idle check, pipeline.hpp:567-568).
-template <int T>
+template <int T, int SK>
 __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
+    typedef typename Samp<SK>::raw_t R;
+    constexpr int esz = Samp<SK>::esz;
+    constexpr int A = 16 / esz;  // samples per 16-byte bulk-copy granule
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
     // cluster split: csize consecutive CTAs (one cluster) share a channel,
@@ -1239,9 +1302,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     const int nbuf = a.nbuf;
     const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
     const int64_t avail = a.avail[strm];
-    const float2* ring = a.ring + (int64_t)strm * a.ring_stride;
+    const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * esz;
     float2* anchors = anchors_of(s);
-    double* xs = xslots_of(s, nwork, nbuf);
+    double* xs = xslots_of(s, nwork, nbuf, esz);
+    const float scale = SK == SK_I16 ? 1.f / 32768.f : SK == SK_I8 ? 1.f / 128.f : 1.f;
     const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
     // unit v of this launch: epoch v / nsub, sub-tile v % nsub, into tile
     // v % nbuf.  Units of the epoch being correlated (ev <= ecur) are always
@@ -1260,7 +1324,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
         // by each unit's length (+ the other cluster CTAs' samples at the end
         // of an epoch)
         const int64_t pos = s->issue_pos;
-        issue_unit(s, b, tile_of(s, nwork, b), ring, pos, len);
+        issue_unit(s, b, tile_of(s, nwork, b, esz), ring, pos, len, esz);
         int64_t nxt = pos + len + (q + 1 == nsub ? skip : 0);
         while (nxt >= a.ring_cap)
             nxt -= a.ring_cap;
@@ -1296,7 +1360,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             try_issue(v, -1);
     }
     __syncthreads();
-    fill_rot(s->rot, s->c.w, tid);
+    fill_rot(s->rot, s->c.w, tid, scale);
     __syncthreads();
 
     uint32_t phase = 0;  // bit b: parity of tile b's next completion
@@ -1345,14 +1409,17 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             const uint32_t par = (phase >> b) & 1u;
             const int u0 = r0 + q * cap;
             const int len = min(cap, rend - u0);
-            const int delta = (int)(upos & 1);
-            const int h = 2 * ((len + delta) / 4);
+            const int delta = (int)(upos & (A - 1));
+            const int h = A * ((len + delta) / (2 * A));
             upos += len + (q + 1 == nsub ? skip : 0);
             while (upos >= a.ring_cap)
                 upos -= a.ring_cap;
             if (!noop) {
-                float2* tile = tile_of(s, nwork, b);
-                const float2* tile_d = tile + delta;
+                const R* rawt = reinterpret_cast<const R*>(tile_of(s, nwork, b, esz)) + delta;
+                // prefix sums: in place for float2 rings, else their own tile
+                float2* pre = SK == SK_F32 ? reinterpret_cast<float2*>(tile_of(s, nwork, b, esz)) + delta
+                                           : prefix_of(s, nwork, nbuf, esz);
+                const float2* tile_d = pre;
                 if (tid < nwork) {
                     PROF_A(1);
                     const int i0 = u0 + tid * RUN;
@@ -1375,8 +1442,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                     c.inv_cps = fast_rcp(c.cps);  // tap_boundary's estimate (within 2 ulp)
                     phase_b_range<T>(pb, c, s->ct, u0, len);
                     if (cnt > 0)
-                        phase_a_dispatch<T>(c, tile + r0t, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
-                                            acc, &anchors[tid]);
+                        phase_a_dispatch<T>(c, rawt + tid * RUN, pre + tid * RUN, s->rot, s->ct.chip,
+                                            s->d, a.kp, i0, cnt, acc, &anchors[tid]);
                     PROF_A(4);
                     if (tid == 0) {
                         PROF_STAMP(1);
@@ -1429,7 +1496,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
             warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
             if (tid == 0)
                 PROF_STAMP(5);
-            fill_rot(s->rot, s->c.w, lane);
+            fill_rot(s->rot, s->c.w, lane, scale);
             if (tid == 0)
                 PROF_STAMP(6);
         }
@@ -1482,7 +1549,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
     float2* anchors = anchors_of(s);
-    float2* tile = tile_of(s, blockDim.x, 0);
+    float2* tile = reinterpret_cast<float2*>(tile_of(s, blockDim.x, 0, 8));
     const int j = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = (blockDim.x + 31) >> 5;
@@ -1515,8 +1582,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
             const int i0 = u0 + tid * RUN;
             const int cnt = min(RUN, n - i0);
             if (cnt > 0)
-                phase_a_dispatch<T>(c, tile + tid * RUN, s->rot, s->ct.chip, s->d, a.kp, i0, cnt,
-                                    acc, &anchors[tid]);
+                phase_a_dispatch<T>(c, reinterpret_cast<const f2x*>(tile + tid * RUN), tile + tid * RUN,
+                                    s->rot, s->ct.chip, s->d, a.kp, i0, cnt, acc, &anchors[tid]);
             __syncthreads();
             phase_b_range<T>(pb, c, s->ct, u0, len);
             phase_b<T>(pb, c, tile, anchors, s->ct, u0, len);

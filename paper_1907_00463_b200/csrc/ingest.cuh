@@ -171,6 +171,50 @@ __global__ void decode_iq_strided_kernel(const uint8_t* __restrict__ raw, int64_
         avail[s] = avail_value;
 }
 
+// Complex int8 / int16 recordings are kept RAW in the tracker's ring (E =
+// uint16_t or uint32_t per sample; the correlator converts while it wipes,
+// with the /128 or /32768 scale folded exactly into its rotator table): the
+// push is a copy into ring position pos (+ the apron mirror).
+template <typename E>
+__global__ void copy_raw_kernel(const E* __restrict__ src, int64_t count, E* ring, int64_t R,
+                                int64_t apron, int64_t pos0, int64_t* avail_slot,
+                                int64_t avail_value) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        const E v = src[i];
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        ring[pos] = v;
+        if (pos < apron)
+            ring[R + pos] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
+        *avail_slot = avail_value;
+}
+// The same for every stream of a tracker in one launch (blockIdx.y = stream).
+template <typename E>
+__global__ void copy_raw_strided_kernel(const uint8_t* __restrict__ src, int64_t src_stride_bytes,
+                                        int64_t count, E* ring, int64_t ring_stride, int64_t R,
+                                        int64_t apron, int64_t pos0, int64_t* avail,
+                                        int64_t avail_value) {
+    const int s = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const E* sp = reinterpret_cast<const E*>(src + (int64_t)s * src_stride_bytes);
+    E* rg = ring + (int64_t)s * ring_stride;
+    if (i < count) {
+        const E v = sp[i];
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        rg[pos] = v;
+        if (pos < apron)
+            rg[R + pos] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        avail[s] = avail_value;
+}
+
 // complex<double> -> float2 (per-call path)
 __global__ void cf64_to_f32_kernel(const double2* __restrict__ in, float2* out, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

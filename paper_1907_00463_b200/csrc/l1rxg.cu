@@ -126,12 +126,25 @@ int pick_threads(int n, int* subtiles, int max_nt = MAX_NT) {
     return nt;
 }
 
-// header + anchors[nwork] + nbuf tiles of nwork*RUN samples (+ alignment
-// slack of the 16-byte bulk copies)
+// header + anchors[nwork] + nbuf sample tiles of nwork*RUN samples of esz
+// bytes (+ bulk-copy slack) + for raw sample kinds the float2 prefix tile
 template <int T>
-size_t smem_bytes(int nwork, int nbuf = 1) {
+size_t smem_bytes(int nwork, int nbuf = 1, int esz = 8) {
     return corr_smem_header<T>() + static_cast<size_t>(anchors_len(nwork)) * sizeof(float2) +
-           static_cast<size_t>(nbuf) * (static_cast<size_t>(nwork) * RUN + 4) * sizeof(float2);
+           static_cast<size_t>(nbuf) * tile_bytes(nwork, esz) +
+           (esz == 8 ? 0 : static_cast<size_t>(nwork) * RUN * sizeof(float2));
+}
+
+// ring element size per recording format: real IF is filtered to float2;
+// complex int recordings are decoded to float2 too unless L1RXG_RAW_RING=1
+// keeps them raw (2/4 B per sample, converted in the correlator: fewer ring
+// and shared-memory bytes, but the separate prefix tile costs shared-memory
+// capacity -- measured slower for the throughput shape)
+int ring_esz(int fmt) {
+    static const char* ev = std::getenv("L1RXG_RAW_RING");
+    if (!(ev && std::atoi(ev)))
+        return 8;
+    return fmt == L1RXG_FMT_INT16_IQ ? 4 : fmt == L1RXG_FMT_INT8_IQ ? 2 : 8;
 }
 
 // Loop-filter constants precomputed with the reference's operation order
@@ -157,19 +170,19 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
     return lc;
 }
 
-template <int T>
-int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
+template <int T, int SK>
+int launch_track_sk(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
     // the control warp owns no tile runs; + the cluster exchange slots
-    const size_t sm = smem_bytes<T>(nt - 32, a.nbuf) +
+    const size_t sm = smem_bytes<T>(nt - 32, a.nbuf, Samp<SK>::esz) +
                       (a.csize > 1 ? 2u * a.csize * (2 * T + 2) * sizeof(double) : 0);
-    CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     if (a.csize <= 1) {
-        track_kernel<T><<<n_ch, nt, sm, s>>>(a);
+        track_kernel<T, SK><<<n_ch, nt, sm, s>>>(a);
     } else {  // one thread-block cluster of csize CTAs per channel
         if (a.csize > 8)
-            CK(cudaFuncSetAttribute(track_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(n_ch * a.csize));
         cfg.blockDim = dim3(static_cast<unsigned>(nt));
@@ -182,15 +195,24 @@ int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, track_kernel<T>, a));
+        CK(cudaLaunchKernelEx(&cfg, track_kernel<T, SK>, a));
     }
     CK(cudaGetLastError());
     return 0;
 }
 
 template <int T>
+int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
+    switch (sk) {
+    case SK_I16: return launch_track_sk<T, SK_I16>(a, n_ch, nt, s);
+    case SK_I8: return launch_track_sk<T, SK_I8>(a, n_ch, nt, s);
+    default: return launch_track_sk<T, SK_F32>(a, n_ch, nt, s);
+    }
+}
+
+template <int T>
 int launch_jobs(const JobArgs& a, int n_jobs, int nt, cudaStream_t s) {
-    const size_t sm = smem_bytes<T>(nt);
+    const size_t sm = smem_bytes<T>(nt, 1, 8);
     CK(cudaFuncSetAttribute(correlate_jobs_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     correlate_jobs_kernel<T><<<n_jobs, nt, sm, s>>>(a);
     CK(cudaGetLastError());
@@ -280,7 +302,7 @@ struct l1rxg_ctx {
 };
 
 struct StreamRing {
-    float2* ring = nullptr;  // R + apron
+    unsigned char* ring = nullptr;  // R + apron samples of esz bytes
     int64_t pushed = 0;      // samples ingested
     int8_t* hist8[2] = {nullptr, nullptr};
     float2* histf[2] = {nullptr, nullptr};
@@ -296,8 +318,9 @@ struct l1rxg_tracker {
     int csize = 1;   // CTAs per channel (cluster) in the latency shape
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
+    int esz = 8;     // ring element bytes (ring_esz)
     std::vector<StreamRing> streams;
-    float2* d_ring = nullptr;
+    unsigned char* d_ring = nullptr;
     int64_t* d_avail = nullptr;
     l1rxg_channel* d_chans = nullptr;
     int32_t* d_chan_stream = nullptr;
@@ -347,7 +370,7 @@ int ingest_launch(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nsamp,
             const int64_t blocks = (nsamp + ING_TILE - 1) / ING_TILE;
             ingest_if4_kernel<<<(unsigned)blocks, ING_TPB, 0, st>>>(
                 static_cast<const int8_t*>(dev_bytes), r.hist8[cur], r.hist8[cur ^ 1], g0, nsamp,
-                r.ring, t->R, t->apron, pos0, slot);
+                reinterpret_cast<float2*>(r.ring), t->R, t->apron, pos0, slot);
             r.hist_cur ^= 1;
             t->launches += 1;
         } else {
@@ -359,15 +382,26 @@ int ingest_launch(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nsamp,
             const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
             mix_generic_kernel<<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(dev_bytes), g0,
                                                        nsamp, w, mixed);
-            fir_generic_kernel<<<blocks, 256, 0, st>>>(mixed, nsamp, r.ring, t->R, t->apron, pos0,
-                                                       r.histf[cur ^ 1], slot, g0 + nsamp);
+            fir_generic_kernel<<<blocks, 256, 0, st>>>(mixed, nsamp, reinterpret_cast<float2*>(r.ring),
+                                                       t->R, t->apron, pos0, r.histf[cur ^ 1], slot,
+                                                       g0 + nsamp);
             r.hist_cur ^= 1;
             t->launches += 2;
         }
     } else {
         const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
-        decode_iq_kernel<<<blocks, 256, 0, st>>>(dev_bytes, fmt, nsamp, r.ring, t->R, t->apron,
-                                                 pos0, slot, g0 + nsamp);
+        if (t->esz == 8)
+            decode_iq_kernel<<<blocks, 256, 0, st>>>(dev_bytes, fmt, nsamp,
+                                                     reinterpret_cast<float2*>(r.ring), t->R, t->apron,
+                                                     pos0, slot, g0 + nsamp);
+        else if (fmt == L1RXG_FMT_INT16_IQ)
+            copy_raw_kernel<uint32_t><<<blocks, 256, 0, st>>>(
+                static_cast<const uint32_t*>(dev_bytes), nsamp, reinterpret_cast<uint32_t*>(r.ring),
+                t->R, t->apron, pos0, slot, g0 + nsamp);
+        else
+            copy_raw_kernel<uint16_t><<<blocks, 256, 0, st>>>(
+                static_cast<const uint16_t*>(dev_bytes), nsamp, reinterpret_cast<uint16_t*>(r.ring),
+                t->R, t->apron, pos0, slot, g0 + nsamp);
         t->launches += 1;
     }
     CK(cudaGetLastError());
@@ -648,7 +682,9 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         if (thr) {
             static const char* ev_nw = std::getenv("L1RXG_THR_NWORK");
             static const char* ev_nb = std::getenv("L1RXG_THR_NBUF");
-            int mx = ev_nw ? std::atoi(ev_nw) : 128;
+            // 128 correlation threads (float2 ring: ~51 KB) or 96 (raw samples
+            // + prefix tile: ~55 KB) keep four CTAs per SM
+            int mx = ev_nw ? std::atoi(ev_nw) : (ring_esz(d->format) == 8 ? 128 : 96);
             while ((n + mx * RUN - 1) / (mx * RUN) > MAXSUB)
                 mx += 32;
             t->nt = pick_threads(n, nullptr, mx) + 32;
@@ -679,9 +715,14 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         }
     }
     t->R = d->ring_samples;
-    // apron >= one epoch (+ bulk-copy slack); R + apron even keeps every
-    // stream's ring 16-byte aligned for the TMA copies
-    t->apron = n + 64 + ((t->R + n) & 1);
+    t->esz = ring_esz(d->format);
+    // apron >= one epoch (+ bulk-copy slack); R + apron a multiple of the
+    // samples per 16 bytes keeps every stream's ring 16-byte aligned for TMA
+    {
+        const int64_t A = 16 / t->esz;
+        t->apron = n + 64;
+        t->apron += (A - (t->R + t->apron) % A) % A;
+    }
     t->streams.resize(static_cast<size_t>(d->n_streams));
     auto fail = [&](cudaError_t e) {
         l1rxg_tracker_destroy(t);
@@ -690,11 +731,11 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     };
     cudaError_t e;
     const int64_t stride = t->R + t->apron;
-    if ((e = cudaMalloc(&t->d_ring, sizeof(float2) * static_cast<size_t>(stride) * t->streams.size())) !=
+    if ((e = cudaMalloc(&t->d_ring, static_cast<size_t>(t->esz) * static_cast<size_t>(stride) * t->streams.size())) !=
         cudaSuccess)
         return fail(e);
     for (size_t k = 0; k < t->streams.size(); ++k)
-        t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride;
+        t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride * t->esz;
     for (auto& r : t->streams) {
         for (int k = 0; k < 2; ++k) {
             if ((e = cudaMalloc(&r.hist8[k], 32)) != cudaSuccess ||
@@ -812,9 +853,22 @@ int l1rxg_tracker_push_device_strided(l1rxg_tracker* t, const void* dev_bytes,
     cudaEvent_t a = get_event(t), b = get_event(t);
     cudaEventRecord(a, st);
     const dim3 grid(static_cast<unsigned>((nsamp + 255) / 256), static_cast<unsigned>(t->streams.size()));
-    decode_iq_strided_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(dev_bytes), stride_bytes,
-                                                   t->d.format, nsamp, t->d_ring, t->R + t->apron, t->R,
-                                                   t->apron, g0 % t->R, t->d_avail, g0 + nsamp);
+    if (t->esz == 8)
+        decode_iq_strided_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(dev_bytes), stride_bytes,
+                                                       t->d.format, nsamp,
+                                                       reinterpret_cast<float2*>(t->d_ring),
+                                                       t->R + t->apron, t->R, t->apron, g0 % t->R,
+                                                       t->d_avail, g0 + nsamp);
+    else if (t->d.format == L1RXG_FMT_INT16_IQ)
+        copy_raw_strided_kernel<uint32_t><<<grid, 256, 0, st>>>(
+            static_cast<const uint8_t*>(dev_bytes), stride_bytes, nsamp,
+            reinterpret_cast<uint32_t*>(t->d_ring), t->R + t->apron, t->R, t->apron, g0 % t->R,
+            t->d_avail, g0 + nsamp);
+    else
+        copy_raw_strided_kernel<uint16_t><<<grid, 256, 0, st>>>(
+            static_cast<const uint8_t*>(dev_bytes), stride_bytes, nsamp,
+            reinterpret_cast<uint16_t*>(t->d_ring), t->R + t->apron, t->R, t->apron, g0 % t->R,
+            t->d_avail, g0 + nsamp);
     CK(cudaGetLastError());
     cudaEventRecord(b, st);
     t->timed.push_back({a, b, 0});
@@ -928,7 +982,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
         CK(cudaMemsetAsync(dprof, 0, 4 * 64 * 8 * sizeof(long long), st));
     }
     a.prof = dprof;
-    auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st); };
+    const int sk = t->esz == 4 ? SK_I16 : t->esz == 2 ? SK_I8 : SK_F32;
+    auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st, sk); };
     if (int rc = go())
         return rc;
     t->launches += 1;
@@ -1112,16 +1167,34 @@ int l1rxg_tracker_read_samples(l1rxg_tracker* t, int s, int64_t s0, int64_t coun
     const StreamRing& r = t->streams[static_cast<size_t>(s)];
     if (s0 < 0 || count < 0 || s0 + count > r.pushed || s0 < r.pushed - t->R)
         return set_err(L1RXG_EINVAL, "samples not in the ring");
-    std::vector<float2> tmp(static_cast<size_t>(count));
+    const int esz = t->esz;
+    std::vector<unsigned char> tmp(static_cast<size_t>(count) * esz);
     for (int64_t k = 0; k < count;) {
         const int64_t pos = (s0 + k) % t->R;
         const int64_t run = std::min(count - k, t->R - pos);
-        CK(cudaMemcpy(tmp.data() + k, r.ring + pos, sizeof(float2) * run, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tmp.data() + k * esz, r.ring + pos * esz, static_cast<size_t>(esz) * run,
+                      cudaMemcpyDeviceToHost));
         k += run;
     }
+    // the ring holds the SampleSource outputs (samples.hpp:188-253): float2
+    // after the IF front end, raw complex ints otherwise (decoded here)
     for (int64_t k = 0; k < count; ++k) {
-        iq_out[2 * k] = tmp[static_cast<size_t>(k)].x;
-        iq_out[2 * k + 1] = tmp[static_cast<size_t>(k)].y;
+        const unsigned char* p = tmp.data() + k * esz;
+        if (esz == 8) {
+            float v[2];
+            std::memcpy(v, p, 8);
+            iq_out[2 * k] = v[0];
+            iq_out[2 * k + 1] = v[1];
+        } else if (esz == 4) {
+            int16_t v[2];
+            std::memcpy(v, p, 4);
+            iq_out[2 * k] = static_cast<double>(static_cast<float>(v[0]) * (1.0f / 32768.0f));
+            iq_out[2 * k + 1] = static_cast<double>(static_cast<float>(v[1]) * (1.0f / 32768.0f));
+        } else {
+            const int8_t v0 = static_cast<int8_t>(p[0]), v1 = static_cast<int8_t>(p[1]);
+            iq_out[2 * k] = static_cast<double>(static_cast<float>(v0) * (1.0f / 128.0f));
+            iq_out[2 * k + 1] = static_cast<double>(static_cast<float>(v1) * (1.0f / 128.0f));
+        }
     }
     return 0;
 }
