@@ -171,6 +171,33 @@ __global__ void decode_iq_strided_kernel(const uint8_t* __restrict__ raw, int64_
         avail[s] = avail_value;
 }
 
+// Fast path of the strided cint16 decode: two samples per thread (one 8-byte
+// load, one 16-byte store), for even ring positions, even R and an even
+// apron (then a pair never straddles the wrap or the apron edge).
+__global__ void decode_i16x2_strided_kernel(const uint8_t* __restrict__ raw, int64_t raw_stride,
+                                            int64_t npairs, float2* ring, int64_t ring_stride,
+                                            int64_t R, int64_t apron, int64_t pos0, int64_t* avail,
+                                            int64_t avail_value) {
+    const int s = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint2* rs = reinterpret_cast<const uint2*>(raw + (int64_t)s * raw_stride);
+    float2* rg = ring + (int64_t)s * ring_stride;
+    if (i < npairs) {
+        const uint2 w = __ldcs(rs + i);  // streamed once
+        const float k = 1.0f / 32768.0f;
+        const float4 v = make_float4((float)(short)(w.x & 0xffffu) * k, (float)((int)w.x >> 16) * k,
+                                     (float)(short)(w.y & 0xffffu) * k, (float)((int)w.y >> 16) * k);
+        int64_t pos = pos0 + 2 * i;
+        if (pos >= R)
+            pos -= R;
+        *reinterpret_cast<float4*>(rg + pos) = v;
+        if (pos < apron)
+            *reinterpret_cast<float4*>(rg + R + pos) = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        avail[s] = avail_value;
+}
+
 // Complex int8 / int16 recordings are kept RAW in the tracker's ring (E =
 // uint16_t or uint32_t per sample; the correlator converts while it wipes,
 // with the /128 or /32768 scale folded exactly into its rotator table): the

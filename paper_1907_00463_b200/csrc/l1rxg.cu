@@ -853,7 +853,16 @@ int l1rxg_tracker_push_device_strided(l1rxg_tracker* t, const void* dev_bytes,
     cudaEvent_t a = get_event(t), b = get_event(t);
     cudaEventRecord(a, st);
     const dim3 grid(static_cast<unsigned>((nsamp + 255) / 256), static_cast<unsigned>(t->streams.size()));
-    if (t->esz == 8)
+    const int64_t pos0 = g0 % t->R;
+    if (t->esz == 8 && t->d.format == L1RXG_FMT_INT16_IQ && (pos0 & 1) == 0 && (t->R & 1) == 0 &&
+        (t->apron & 1) == 0 && (nsamp & 1) == 0 && (stride_bytes & 7) == 0 &&
+        (reinterpret_cast<uintptr_t>(dev_bytes) & 7) == 0) {
+        const dim3 g2(static_cast<unsigned>((nsamp / 2 + 255) / 256), static_cast<unsigned>(t->streams.size()));
+        decode_i16x2_strided_kernel<<<g2, 256, 0, st>>>(static_cast<const uint8_t*>(dev_bytes), stride_bytes,
+                                                        nsamp / 2, reinterpret_cast<float2*>(t->d_ring),
+                                                        t->R + t->apron, t->R, t->apron, pos0, t->d_avail,
+                                                        g0 + nsamp);
+    } else if (t->esz == 8)
         decode_iq_strided_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(dev_bytes), stride_bytes,
                                                        t->d.format, nsamp,
                                                        reinterpret_cast<float2*>(t->d_ring),
