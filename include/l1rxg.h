@@ -235,11 +235,14 @@ typedef struct {
     int32_t n_channels;
     int64_t ring_samples;      /* per-stream device ring capacity       */
     int32_t max_records;       /* per-channel record ring capacity      */
-    /* CTA shape: 0 = auto.  L1RXG_CTA_LATENCY: one wide CTA per channel
-     * (few channels: the per-epoch critical path is what matters);
-     * L1RXG_CTA_THROUGHPUT: narrower CTAs, two resident per SM so one
-     * channel's serial loop update overlaps another's correlation (many
-     * channels).  auto picks throughput when n_channels >= 2 x SMs. */
+    /* CTA shape: 0 = auto.  L1RXG_CTA_LATENCY: each channel's epoch split
+     * over a thread-block cluster of up to 16 CTAs (one per SM; the CTAs
+     * exchange fp64 partial sums through distributed shared memory and all
+     * run the same loop update) -- few channels, the per-epoch critical path
+     * is what matters; L1RXG_CTA_SINGLE: the latency shape with one CTA per
+     * channel; L1RXG_CTA_THROUGHPUT: narrow CTAs, four resident per SM, so
+     * one channel's serial loop update overlaps the others' correlation
+     * (many channels).  Auto picks throughput when n_channels >= 2 x SMs. */
     int32_t cta_mode;
     l1rxg_taps taps;
     l1rxg_tracking_cfg cfg;
@@ -248,6 +251,7 @@ typedef struct {
 #define L1RXG_CTA_AUTO 0
 #define L1RXG_CTA_LATENCY 1
 #define L1RXG_CTA_THROUGHPUT 2
+#define L1RXG_CTA_SINGLE 3
 
 int l1rxg_tracker_create(l1rxg_ctx* ctx, const l1rxg_tracker_desc* desc,
                          const l1rxg_channel* channels,

@@ -644,6 +644,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return rc;
     if (int rc = validate_cfg(&d->cfg))
         return rc;
+    if (d->cta_mode < L1RXG_CTA_AUTO || d->cta_mode > L1RXG_CTA_SINGLE)
+        return set_err(L1RXG_EINVAL, "unknown cta_mode");
     if (d->n_streams < 1 || d->n_channels < 0 || d->max_records < 1)
         return set_err(L1RXG_EINVAL, "n_streams >= 1, n_channels >= 0, max_records >= 1");
     const int n = static_cast<int>(std::llround(d->sample_rate_hz / 1000.0));
@@ -695,7 +697,9 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             // CTA keeps >= 1024 samples; K = 1 is the single-CTA path
             static const char* ev_cl = std::getenv("L1RXG_CLUSTER");
             int K = 1;
-            if (ev_cl) {
+            if (d->cta_mode == L1RXG_CTA_SINGLE) {
+                K = 1;
+            } else if (ev_cl) {
                 K = std::max(1, std::min(16, std::atoi(ev_cl)));
             } else {
                 while (K < 16 && d->n_channels * K * 2 <= nsm && n / (K * 2) >= 1024)

@@ -119,9 +119,12 @@ def test_trajectory_agrees_with_reference_until_first_tie(ctx, oracle_mod):
     assert d.max() < 0.05 and chi.max() < 1e-3
 
 
-def test_twelve_channel_shared_stream(ctx, oracle_mod):
+@pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SINGLE, abi.CTA_THROUGHPUT])
+def test_twelve_channel_shared_stream(ctx, oracle_mod, cta_mode):
     """Config 2 shape (scaled to 300 blocks): 12 channels, PRNs 1-12, one
-    shared int8 real-IF stream, replay parity for every channel."""
+    shared int8 real-IF stream, replay parity for every channel -- with each
+    channel's epoch split over a cluster (auto), one CTA per channel, and the
+    narrow four-per-SM throughput CTAs (several tiles per epoch)."""
     fs, n = IF_FS, 16368
     rng = np.random.default_rng(2)
     svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(35, 50), doppler_hz=rng.uniform(-5000, 5000),
@@ -130,7 +133,7 @@ def test_twelve_channel_shared_stream(ctx, oracle_mod):
     inits = [_init(sv, fs) for sv in svs]
     cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
     trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, inits, ring_samples=400 * n,
-                  max_records=300)
+                  max_records=300, cta_mode=cta_mode)
     for c0 in range(0, raw.size, 37 * n):  # chunked pushes + runs
         trk.push(0, raw[c0:c0 + 37 * n])
         trk.run()
@@ -281,6 +284,12 @@ def test_batched_recordings_throughput_mode(ctx, oracle_mod):
         assert ra.tobytes() == rb.tobytes()
         x = oracle_mod.ingest(raw[cstream[c]], abi.FMT_INT16_IQ, fs)
         replay_check(oracle_mod, inits[c], ra, x, n, cfg, taps, fs, tap_sums=ta)
+
+
+def test_bad_cta_mode_rejected(ctx):
+    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 2.048e6)
+    with pytest.raises(ValueError):
+        Tracker(ctx, abi.FMT_INT8_IQ, 2.048e6, 0.0, [init], ring_samples=8 * 2048, cta_mode=7)
 
 
 def test_strided_push_rejects(ctx):
