@@ -531,7 +531,7 @@ def main():
     ap.add_argument("--cpu-blocks", type=int, default=3000, help="CPU baseline sample (blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="config 4: skip the host-memory e2e leg")
-    ap.add_argument("--e2e-chunk-ms", type=int, default=100)
+    ap.add_argument("--e2e-chunk-ms", type=int, default=1000)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
     ap.add_argument("--cta", default="throughput", choices=["throughput", "latency"])
     args = ap.parse_args()
