@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define L1RXG_ABI_VERSION 1
+#define L1RXG_ABI_VERSION 2
 #define L1RXG_CODE_LENGTH 1023
 #define L1RXG_MAX_TAPS 16
 #define L1RXG_WIN_MAX 64
@@ -244,6 +244,11 @@ typedef struct {
      * one channel's serial loop update overlaps the others' correlation
      * (many channels).  Auto picks throughput when n_channels >= 2 x SMs. */
     int32_t cta_mode;
+    /* Latency shape: CTAs per channel cluster (0 = auto, 1..16). */
+    int32_t cluster_size;
+    /* 1: keep complex int recordings raw in the ring (2/4 B per sample,
+     * converted in the correlator); 0: decode to float2 (default). */
+    int32_t ring_raw;
     l1rxg_taps taps;
     l1rxg_tracking_cfg cfg;
 } l1rxg_tracker_desc;

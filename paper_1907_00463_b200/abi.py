@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 CODE_LENGTH = 1023
 MAX_TAPS = 16
 WIN_MAX = 64
@@ -157,6 +157,7 @@ class TrackerDesc(C.Structure):
                 ("sample_rate_hz", C.c_double), ("if_frequency_hz", C.c_double),
                 ("n_streams", C.c_int32), ("n_channels", C.c_int32),
                 ("ring_samples", C.c_int64), ("max_records", C.c_int32), ("cta_mode", C.c_int32),
+                ("cluster_size", C.c_int32), ("ring_raw", C.c_int32),
                 ("taps", Taps), ("cfg", TrackingCfg)]
 
 

@@ -136,13 +136,12 @@ size_t smem_bytes(int nwork, int nbuf = 1, int esz = 8) {
 }
 
 // ring element size per recording format: real IF is filtered to float2;
-// complex int recordings are decoded to float2 too unless L1RXG_RAW_RING=1
-// keeps them raw (2/4 B per sample, converted in the correlator: fewer ring
-// and shared-memory bytes, but the separate prefix tile costs shared-memory
-// capacity -- measured slower for the throughput shape)
-int ring_esz(int fmt) {
-    static const char* ev = std::getenv("L1RXG_RAW_RING");
-    if (!(ev && std::atoi(ev)))
+// complex int recordings are decoded to float2 too unless the descriptor's
+// ring_raw keeps them raw (2/4 B per sample, converted in the correlator:
+// fewer ring and shared-memory bytes, but the separate prefix tile costs
+// shared-memory capacity -- measured slower for the throughput shape)
+int ring_esz(int fmt, int raw) {
+    if (!raw)
         return 8;
     return fmt == L1RXG_FMT_INT16_IQ ? 4 : fmt == L1RXG_FMT_INT8_IQ ? 2 : 8;
 }
@@ -646,6 +645,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return rc;
     if (d->cta_mode < L1RXG_CTA_AUTO || d->cta_mode > L1RXG_CTA_SINGLE)
         return set_err(L1RXG_EINVAL, "unknown cta_mode");
+    if (d->cluster_size < 0 || d->cluster_size > 16 || (d->ring_raw != 0 && d->ring_raw != 1))
+        return set_err(L1RXG_EINVAL, "cluster_size must be in 0..16, ring_raw 0 or 1");
     if (d->n_streams < 1 || d->n_channels < 0 || d->max_records < 1)
         return set_err(L1RXG_EINVAL, "n_streams >= 1, n_channels >= 0, max_records >= 1");
     const int n = static_cast<int>(std::llround(d->sample_rate_hz / 1000.0));
@@ -686,7 +687,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             static const char* ev_nb = std::getenv("L1RXG_THR_NBUF");
             // 128 correlation threads (float2 ring: ~51 KB) or 96 (raw samples
             // + prefix tile: ~55 KB) keep four CTAs per SM
-            int mx = ev_nw ? std::atoi(ev_nw) : (ring_esz(d->format) == 8 ? 128 : 96);
+            int mx = ev_nw ? std::atoi(ev_nw) : (ring_esz(d->format, d->ring_raw) == 8 ? 128 : 96);
             while ((n + mx * RUN - 1) / (mx * RUN) > MAXSUB)
                 mx += 32;
             t->nt = pick_threads(n, nullptr, mx) + 32;
@@ -699,6 +700,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             int K = 1;
             if (d->cta_mode == L1RXG_CTA_SINGLE) {
                 K = 1;
+            } else if (d->cluster_size > 0) {
+                K = d->cluster_size;
             } else if (ev_cl) {
                 K = std::max(1, std::min(16, std::atoi(ev_cl)));
             } else {
@@ -719,7 +722,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         }
     }
     t->R = d->ring_samples;
-    t->esz = ring_esz(d->format);
+    t->esz = ring_esz(d->format, d->ring_raw);
     // apron >= one epoch (+ bulk-copy slack); R + apron a multiple of the
     // samples per 16 bytes keeps every stream's ring 16-byte aligned for TMA
     {

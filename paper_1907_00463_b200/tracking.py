@@ -221,7 +221,7 @@ class Tracker:
                  chan_stream=None, n_streams: int = 1, taps: abi.Taps | None = None,
                  cfg: abi.TrackingCfg | None = None, kernel: int = KERNEL_SCALAR,
                  ring_samples: int | None = None, max_records: int = 1024,
-                 cta_mode: int = abi.CTA_AUTO):
+                 cta_mode: int = abi.CTA_AUTO, cluster_size: int = 0, ring_raw: bool = False):
         self.ctx = ctx
         self._lib = ctx._lib
         self.fmt, self.fs, self.if_hz = fmt, fs, if_hz
@@ -237,6 +237,8 @@ class Tracker:
         d.ring_samples = ring_samples or 64 * self.n
         d.max_records = max_records
         d.cta_mode = cta_mode
+        d.cluster_size = cluster_size
+        d.ring_raw = int(ring_raw)
         d.taps, d.cfg = self.taps, self.cfg
         self.desc = d
         cs = chan_stream if chan_stream is not None else [0] * len(chans)

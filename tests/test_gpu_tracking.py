@@ -248,7 +248,8 @@ def _batch_scenario(n_rec, fs, ms, seed):
     return np.stack(raws), inits, cstream
 
 
-def test_batched_recordings_throughput_mode(ctx, oracle_mod):
+@pytest.mark.parametrize("ring_raw", [False, True])
+def test_batched_recordings_throughput_mode(ctx, oracle_mod, ring_raw):
     """Config 4 shape: recordings pushed in lock step (one strided H2D +
     one decode launch per chunk), narrow two-per-SM CTAs; per-epoch replay
     parity for every channel, and the host and device strided pushes give
@@ -264,7 +265,7 @@ def test_batched_recordings_throughput_mode(ctx, oracle_mod):
     def make():
         return Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=nrec,
                        taps=taps, cfg=cfg, ring_samples=24 * n, max_records=ms,
-                       cta_mode=abi.CTA_THROUGHPUT)
+                       cta_mode=abi.CTA_THROUGHPUT, ring_raw=ring_raw)
     a = make()
     for c0 in range(0, raw.shape[1], chunk):
         a.push_strided(raw[:, c0:c0 + chunk])
@@ -306,3 +307,48 @@ def test_strided_push_rejects(ctx):
         trk2 = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=[0, 1], n_streams=2,
                        ring_samples=4 * n)
         trk2.push_strided(np.zeros((2, 2 * 8 * n), np.int16))
+
+
+@pytest.mark.parametrize("K", [2, 3, 5, 12, 16])
+def test_cluster_sizes(ctx, oracle_mod, K):
+    """Each channel's epoch split over K CTAs (any K, not only powers of
+    two): per-epoch replay parity, 4 channels of the config-2 shape."""
+    fs, n = IF_FS, 16368
+    rng = np.random.default_rng(20 + K)
+    svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(38, 50), doppler_hz=rng.uniform(-5000, 5000),
+                 delay_chips=rng.uniform(0, 1023)) for p in (3, 8, 14, 27)]
+    raw = _raw(80, fs, svs, "int8_real_if", IF_HZ, seed=30 + K)
+    inits = [_init(sv, fs) for sv in svs]
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, inits, ring_samples=100 * n,
+                  max_records=80, cta_mode=abi.CTA_LATENCY, cluster_size=K)
+    trk.push(0, raw)
+    trk.run()
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, IF_HZ)
+    for c in range(len(inits)):
+        recs = trk.records(c)
+        assert len(recs) >= 77
+        replay_check(oracle_mod, inits[c], recs, x, n, cfg, taps, fs)
+
+
+@pytest.mark.parametrize("fmt,fs", [(abi.FMT_INT8_IQ, 2.048e6), (abi.FMT_INT16_IQ, 16.368e6)])
+@pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SINGLE])
+def test_raw_ring_matches_decoded_ring(ctx, fmt, fs, cta_mode):
+    """Raw complex-int rings (converted in the correlator with the decode
+    scale folded into the rotators, a power of two) give bit-identical
+    records to decoded float2 rings in the same CTA shape.  (The throughput
+    shape picks a different tile size for raw rings, so its fp32 summation
+    order differs; it is covered by per-epoch replay parity instead.)"""
+    n = int(round(fs / 1000))
+    sv = ss.Sv(prn=7, cn0_dbhz=46.0, doppler_hz=-1500.0, delay_chips=321.7)
+    name = "int8_iq" if fmt == abi.FMT_INT8_IQ else "int16_iq"
+    raw = _raw(60, fs, [sv], name, seed=91)
+    outs = []
+    for rr in (False, True):
+        trk = Tracker(ctx, fmt, fs, 0.0, [_init(sv, fs)], ring_samples=70 * n, max_records=60,
+                      cta_mode=cta_mode, ring_raw=rr)
+        trk.push(0, raw)
+        trk.run()
+        outs.append(trk.records(0))
+    assert len(outs[0]) >= 58
+    assert outs[0].tobytes() == outs[1].tobytes()
