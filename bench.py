@@ -303,9 +303,22 @@ def run_grid(args, rank, world, local, dist):
                     "ratio": round(float(ratio), 2)})
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
-    corr_flops = float(len(prns)) * bins.size * blocks * 2 * 1023 * 1023 * 4  # 2 FFMA x 2 flop
+    fp32_path = os.environ.get("L1RXG_GRID_FP32", "0") not in ("", "0")
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    if fp32_path:  # FP32-pipe circulant kernel: 2 FFMA x 2 flop per cell-chip
+        corr_flops = float(len(prns)) * bins.size * blocks * 2 * 1023 * 1023 * 4
+        peak = fp32_peak_tflops(sm_mhz)
+        bound, note = "fp32", ("executed algorithm: two 1023-point circulant +-1 correlations per "
+                               "(PRN, bin, block) on the FP32 pipes; direct-equivalent rate in value")
+    else:  # bf16x3 tensor-core GEMM: M=1024 delays, N=2*2*bins*blocks rows, K=3*1024
+        corr_flops = 2.0 * 1024 * (4 * bins.size * blocks) * 3072 * len(prns)
+        peak = peaks.get("bf16_tflops", 2250.0)
+        bound, note = "tensor", ("executed algorithm: per PRN one bf16 GEMM (fp32 folds split into "
+                                 "three bf16 terms, +-1 circulant code matrix, fp32 accumulate) via "
+                                 "cuBLAS on tcgen05; peak = MEASURED_PEAKS bf16_tflops (burst); the "
+                                 "corr time also holds the split, circulant-build and |.| kernels")
     achieved = corr_flops / (corr_ms / args.steps * 1e-3) / 1e12
-    peak = fp32_peak_tflops(sm_mhz)
     line = {"metric": METRIC, "value": world * direct_st / (t_max * 1e-3) / 1e9, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -314,14 +327,12 @@ def run_grid(args, rank, world, local, dist):
                        "value_basis": "direct-equivalent sample-taps (PRN x bin x delay x sample)",
                        "parallelism": f"weak: {world} rank(s)"},
             "kernel_ms_per_step": {"ingest_fold": fold_ms / args.steps, "corr": corr_ms / args.steps},
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "note": "executed algorithm: two 1023-point circulant +-1 correlations per "
-                                 "(PRN, bin, block); direct-equivalent rate in value"},
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None, "note": note},
             "e2e": {"value": world * direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes),
                     "d2h_bytes_per_step": int(plane.size * 4)},
-            "detections": det, "gpu_launches": 3 * args.steps, "clocks": clk}
+            "detections": det, "gpu_launches": (3 if fp32_path else 6) * args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

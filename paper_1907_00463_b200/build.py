@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 def nvcc_cmd(verbose: bool = False) -> list:
     cmd = [NVCC, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", SO, *SOURCES, "-lcudart"]
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", SO, *SOURCES, "-lcudart", "-lcublas"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     return cmd

@@ -6,6 +6,7 @@
 // rings of complex baseband (float2) fed by the ingest kernels, the channel
 // states, and per-channel epoch-record rings.  See include/l1rxg.h for the
 // reference interface each entry point replaces.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -294,6 +295,8 @@ struct l1rxg_ctx {
     int8_t* d_codes = nullptr;
     DevBuf iq64, iq32, states, prns, sums, corr;
     DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
+    DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
+    cublasHandle_t blas = nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     double grid_ms[2] = {0, 0};
     std::mutex mu;  // serialises the per-call path
@@ -503,8 +506,11 @@ int l1rxg_destroy(l1rxg_ctx* c) {
         if (e)
             cudaEventDestroy(e);
     for (DevBuf* b : {&c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
-                      &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist})
+                      &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist, &c->gA,
+                      &c->gMt, &c->gC})
         b->release();
+    if (c->blas)
+        cublasDestroy(c->blas);
     cudaFree(c->d_codes);
     cudaStreamDestroy(c->compute);
     cudaStreamDestroy(c->copy);
@@ -1320,12 +1326,46 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         static_cast<float2*>(c->gF.p));
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->gev[1], st));
-    const size_t sm = 2 * 1024 * sizeof(float) + sizeof(float2) * GRID_CHIPS * n_blocks;
-    CK(cudaFuncSetAttribute(grid_corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    grid_corr_kernel<<<n_prns * n_bins * 2, GRID_TPB, sm, st>>>(
-        static_cast<const float2*>(c->gF.p), c->d_codes, static_cast<const int32_t*>(c->gprns.p), n_bins,
-        n_blocks, static_cast<float>(N), static_cast<float*>(c->gplane.p));
-    CK(cudaGetLastError());
+    const char* ev_fp32 = std::getenv("L1RXG_GRID_FP32");  // per call: tests compare both
+    if (ev_fp32 && std::atoi(ev_fp32)) {  // FP32-pipe circulant correlation (reference kernel)
+        const size_t sm = 2 * 1024 * sizeof(float) + sizeof(float2) * GRID_CHIPS * n_blocks;
+        CK(cudaFuncSetAttribute(grid_corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        grid_corr_kernel<<<n_prns * n_bins * 2, GRID_TPB, sm, st>>>(
+            static_cast<const float2*>(c->gF.p), c->d_codes, static_cast<const int32_t*>(c->gprns.p),
+            n_bins, n_blocks, static_cast<float>(N), static_cast<float*>(c->gplane.p));
+        CK(cudaGetLastError());
+    } else {  // tensor cores: one bf16x3 GEMM per PRN (search.cuh K4b)
+        const int n_vec = n_bins * n_blocks * 2;
+        const int rows = 2 * n_vec;
+        if (c->gA.ensure(sizeof(__nv_bfloat16) * static_cast<size_t>(rows) * GRID_KS) ||
+            c->gMt.ensure(sizeof(__nv_bfloat16) * static_cast<size_t>(n_prns) * GRID_K * GRID_KS) ||
+            c->gC.ensure(sizeof(float) * static_cast<size_t>(n_prns) * rows * GRID_K))
+            return L1RXG_ENOMEM;
+        if (!c->blas) {
+            if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
+                return set_err(L1RXG_ECUDA, "cublasCreate failed");
+        }
+        cublasSetStream(c->blas, st);
+        grid_split_kernel<<<n_vec, 256, 0, st>>>(static_cast<const float2*>(c->gF.p), n_vec,
+                                                 static_cast<__nv_bfloat16*>(c->gA.p));
+        grid_circ_kernel<<<dim3(GRID_KS, n_prns), 256, 0, st>>>(
+            c->d_codes, static_cast<const int32_t*>(c->gprns.p), static_cast<__nv_bfloat16*>(c->gMt.p));
+        CK(cudaGetLastError());
+        const float one = 1.f, zero = 0.f;
+        // column-major: C_p (GRID_K x rows) = Mt_p (GRID_K x GRID_KS) * A (GRID_KS x rows)
+        const cublasStatus_t bs = cublasGemmStridedBatchedEx(
+            c->blas, CUBLAS_OP_N, CUBLAS_OP_N, GRID_K, rows, GRID_KS, &one, c->gMt.p, CUDA_R_16BF,
+            GRID_K, static_cast<long long>(GRID_K) * GRID_KS, c->gA.p, CUDA_R_16BF, GRID_KS, 0, &zero,
+            c->gC.p, CUDA_R_32F, GRID_K, static_cast<long long>(rows) * GRID_K, n_prns,
+            CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+        if (bs != CUBLAS_STATUS_SUCCESS)
+            return set_err(L1RXG_ECUDA, "cublasGemmStridedBatchedEx failed");
+        grid_mag_kernel<<<dim3(n_bins * 2, n_prns), 256, 0, st>>>(
+            static_cast<const float*>(c->gC.p), rows, n_bins, n_blocks, static_cast<float>(N),
+            static_cast<float*>(c->gplane.p));
+        CK(cudaGetLastError());
+        c->launches += 3;
+    }
     CK(cudaEventRecord(c->gev[2], st));
     std::vector<float> pl(static_cast<size_t>(2 * GRID_CHIPS) * n_bins * n_prns);
     CK(cudaMemcpyAsync(pl.data(), c->gplane.p, pl.size() * sizeof(float), cudaMemcpyDeviceToHost, st));

@@ -19,6 +19,7 @@
 // K4b is a register-tiled circulant +-1 correlation on the FP32 pipes.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -137,6 +138,77 @@ __global__ void __launch_bounds__(GRID_TPB) grid_corr_kernel(const float2* __res
         const int j = j0 + q * GRID_TPB;
         if (j < GRID_CHIPS)
             row[2 * j + par] = mag[q];
+    }
+}
+
+// ---- K4b on the tensor cores ------------------------------------------
+// The 2 x n_bins x n_seg circular correlations of a PRN are ONE matrix
+// product: with M_p[k][j] = chip_p[(k - j) mod 1023] (a circulant, +-1),
+// corr[v][j] = sum_k F[v][k] M_p[k][j] for every fold vector v (re and im
+// separately).  The fp32 folds are split into three bf16 terms
+// F = F1 + F2 + F3 (24 significant bits, as fp32), and +-1 is exact in bf16,
+// so one bf16 GEMM with K = 3 x 1024 ([F1 F2 F3] against [M; M; M]) and fp32
+// accumulation reproduces the fp32 correlation on the 5th-gen tensor cores.
+constexpr int GRID_K = 1024;      // 1023 chips padded with a zero row/column
+constexpr int GRID_KS = 3 * GRID_K;
+
+// A[r][GRID_KS], r = vector * 2 + (0: re, 1: im); vector = (bin*n_seg+seg)*2+par
+__global__ void grid_split_kernel(const float2* __restrict__ F, int n_vec, __nv_bfloat16* A) {
+    const int v = blockIdx.x;
+    for (int c = threadIdx.x; c < GRID_K; c += blockDim.x) {
+        const float2 f = c < GRID_CHIPS ? F[(int64_t)v * GRID_CHIPS + c] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri) {
+            const float x = ri ? f.y : f.x;
+            const __nv_bfloat16 h1 = __float2bfloat16_rn(x);
+            const float r1 = x - __bfloat162float(h1);
+            const __nv_bfloat16 h2 = __float2bfloat16_rn(r1);
+            const __nv_bfloat16 h3 = __float2bfloat16_rn(r1 - __bfloat162float(h2));
+            __nv_bfloat16* row = A + ((int64_t)v * 2 + ri) * GRID_KS;
+            row[c] = h1;
+            row[GRID_K + c] = h2;
+            row[2 * GRID_K + c] = h3;
+        }
+    }
+}
+
+// Mt_p (column-major GRID_K x GRID_KS for cuBLAS): Mt[j + GRID_K * k'] =
+// chip_p[(k - j) mod 1023] with k = k' mod GRID_K, zero on the padding.
+__global__ void grid_circ_kernel(const int8_t* __restrict__ codes, const int32_t* __restrict__ prns,
+                                 __nv_bfloat16* Mt) {
+    const int pi = blockIdx.y;
+    const int kp = blockIdx.x;  // column k'
+    const int k = kp % GRID_K;
+    const int8_t* code = codes + prns[pi] * GRID_CHIPS;
+    __nv_bfloat16* col = Mt + ((int64_t)pi * GRID_KS + kp) * GRID_K;
+    for (int j = threadIdx.x; j < GRID_K; j += blockDim.x) {
+        float v = 0.f;
+        if (k < GRID_CHIPS && j < GRID_CHIPS) {
+            int m = k - j;
+            if (m < 0)
+                m += GRID_CHIPS;
+            v = (float)code[m];
+        }
+        col[j] = __float2bfloat16_rn(v);
+    }
+}
+
+// plane[p][bin][2j + par] = scale * sum_seg |C_p[re row][j] + i C_p[im row][j]|
+__global__ void grid_mag_kernel(const float* __restrict__ C, int n_rows, int n_bins, int n_seg,
+                                float scale, float* plane) {
+    const int pi = blockIdx.y;
+    const int bp = blockIdx.x;  // bin * 2 + par
+    const int bin = bp >> 1, par = bp & 1;
+    const float* Cp = C + (int64_t)pi * n_rows * GRID_K;
+    float* row = plane + ((int64_t)pi * n_bins + bin) * (2 * GRID_CHIPS);
+    for (int j = threadIdx.x; j < GRID_CHIPS; j += blockDim.x) {
+        float m = 0.f;
+        for (int seg = 0; seg < n_seg; ++seg) {
+            const int64_t v = ((int64_t)bin * n_seg + seg) * 2 + par;
+            const float re = Cp[(v * 2) * GRID_K + j], im = Cp[(v * 2 + 1) * GRID_K + j];
+            m += scale * sqrtf(fmaf(re, re, im * im));
+        }
+        row[2 * j + par] = m;
     }
 }
 

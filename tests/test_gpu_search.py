@@ -15,9 +15,19 @@ def _plane_oracle(oracle_mod, x, N, n_seg, prns, fs, bins, spc):
                      for p in prns])
 
 
+@pytest.fixture(params=["tensor", "fp32"])
+def grid_path(request, monkeypatch):
+    """The bf16x3 tensor-core GEMM (default) and the FP32-pipe kernel."""
+    if request.param == "fp32":
+        monkeypatch.setenv("L1RXG_GRID_FP32", "1")
+    else:
+        monkeypatch.delenv("L1RXG_GRID_FP32", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("fs,fmt,ifz", [(2.046e6, abi.FMT_INT16_IQ, 0.0),
                                         (16.368e6, abi.FMT_INT8_REAL_IF, 4.092e6)])
-def test_grid_matches_oracle(ctx, oracle_mod, fs, fmt, ifz):
+def test_grid_matches_oracle(ctx, oracle_mod, fs, fmt, ifz, grid_path):
     spc = int(round(fs / 2.046e6))
     N = int(round(fs / 1000))
     svs = [ss.Sv(prn=13, cn0_dbhz=48.0, doppler_hz=1500.0, delay_chips=200.3),
