@@ -296,6 +296,7 @@ struct l1rxg_ctx {
     DevBuf iq64, iq32, states, prns, sums, corr;
     DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
     DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
+    std::vector<int32_t> gMt_prns;                        // PRNs whose circulants gMt holds
     cublasHandle_t blas = nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     double grid_ms[2] = {0, 0};
@@ -1337,10 +1338,13 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
     } else {  // tensor cores: one bf16x3 GEMM per PRN (search.cuh K4b)
         const int n_vec = n_bins * n_blocks * 2;
         const int rows = 2 * n_vec;
+        const void* mt_before = c->gMt.p;
         if (c->gA.ensure(sizeof(__nv_bfloat16) * static_cast<size_t>(rows) * GRID_KS) ||
             c->gMt.ensure(sizeof(__nv_bfloat16) * static_cast<size_t>(n_prns) * GRID_K * GRID_KS) ||
             c->gC.ensure(sizeof(float) * static_cast<size_t>(n_prns) * rows * GRID_K))
             return L1RXG_ENOMEM;
+        if (c->gMt.p != mt_before)
+            c->gMt_prns.clear();  // reallocated: contents gone
         if (!c->blas) {
             if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS)
                 return set_err(L1RXG_ECUDA, "cublasCreate failed");
@@ -1348,9 +1352,17 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         cublasSetStream(c->blas, st);
         grid_split_kernel<<<n_vec, 256, 0, st>>>(static_cast<const float2*>(c->gF.p), n_vec,
                                                  static_cast<__nv_bfloat16*>(c->gA.p));
-        grid_circ_kernel<<<dim3(GRID_KS, n_prns), 256, 0, st>>>(
-            c->d_codes, static_cast<const int32_t*>(c->gprns.p), static_cast<__nv_bfloat16*>(c->gMt.p));
-        CK(cudaGetLastError());
+        // the circulant code matrices depend only on the PRN list: built once
+        // per list and kept with the context
+        const std::vector<int32_t> want(prns, prns + n_prns);
+        if (c->gMt_prns != want) {
+            c->gMt_prns.clear();
+            grid_circ_kernel<<<dim3(GRID_KS, n_prns), 256, 0, st>>>(
+                c->d_codes, static_cast<const int32_t*>(c->gprns.p),
+                static_cast<__nv_bfloat16*>(c->gMt.p));
+            CK(cudaGetLastError());
+            c->gMt_prns = want;
+        }
         const float one = 1.f, zero = 0.f;
         // column-major: C_p (GRID_K x rows) = Mt_p (GRID_K x GRID_KS) * A (GRID_KS x rows)
         const cublasStatus_t bs = cublasGemmStridedBatchedEx(

@@ -194,6 +194,8 @@ __global__ void grid_circ_kernel(const int8_t* __restrict__ codes, const int32_t
 }
 
 // plane[p][bin][2j + par] = scale * sum_seg |C_p[re row][j] + i C_p[im row][j]|
+// (four delays per thread: 16-byte loads; the product rows of a (bin, par)
+// are read once, HBM-bound)
 __global__ void grid_mag_kernel(const float* __restrict__ C, int n_rows, int n_bins, int n_seg,
                                 float scale, float* plane) {
     const int pi = blockIdx.y;
@@ -201,14 +203,24 @@ __global__ void grid_mag_kernel(const float* __restrict__ C, int n_rows, int n_b
     const int bin = bp >> 1, par = bp & 1;
     const float* Cp = C + (int64_t)pi * n_rows * GRID_K;
     float* row = plane + ((int64_t)pi * n_bins + bin) * (2 * GRID_CHIPS);
-    for (int j = threadIdx.x; j < GRID_CHIPS; j += blockDim.x) {
-        float m = 0.f;
-        for (int seg = 0; seg < n_seg; ++seg) {
-            const int64_t v = ((int64_t)bin * n_seg + seg) * 2 + par;
-            const float re = Cp[(v * 2) * GRID_K + j], im = Cp[(v * 2 + 1) * GRID_K + j];
-            m += scale * sqrtf(fmaf(re, re, im * im));
-        }
-        row[2 * j + par] = m;
+    const int j4 = threadIdx.x;  // delays 4*j4 .. 4*j4+3 (GRID_K = 4 * 256)
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int seg = 0; seg < n_seg; ++seg) {
+        const int64_t v = ((int64_t)bin * n_seg + seg) * 2 + par;
+        const float4 re = __ldcs(reinterpret_cast<const float4*>(Cp + (v * 2) * GRID_K) + j4);
+        const float4 im = __ldcs(reinterpret_cast<const float4*>(Cp + (v * 2 + 1) * GRID_K) + j4);
+        m.x += scale * sqrtf(fmaf(re.x, re.x, im.x * im.x));
+        m.y += scale * sqrtf(fmaf(re.y, re.y, im.y * im.y));
+        m.z += scale * sqrtf(fmaf(re.z, re.z, im.z * im.z));
+        m.w += scale * sqrtf(fmaf(re.w, re.w, im.w * im.w));
+    }
+    const float mv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = 4 * j4 + q;
+        if (j < GRID_CHIPS)
+            row[2 * j + par] = mv[q];
     }
 }
 
