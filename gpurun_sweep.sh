@@ -2,8 +2,10 @@ cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 summ() { python -c "
 import json,sys
 l=[x for x in open(sys.argv[1]) if x.startswith('{')][-1]; d=json.loads(l); print(sys.argv[2], round(d['value'],1), round(d['ms_per_step'],2), round(d['roofline']['frac'],4), d['kernel_ms_per_step'])" $1 "$2"; }
-for v in default sc; do
-SO=""; [ $v = sc ] && SO=$PWD/_exp/sc/libl1rxg.so
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -1
+for v in head new; do
+SO=""; [ $v = head ] && SO=$PWD/_exp/head/libl1rxg.so
 L1RXG_SO=$SO python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/b2.log 2>&1; summ gpurun_out/b2.log "config2 $v"
 L1RXG_SO=$SO python bench.py --config 4 --recordings 256 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/sw4.log 2>&1; summ gpurun_out/sw4.log "config4-256 $v"
+L1RXG_SO=$SO python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/b3.log 2>&1; summ gpurun_out/b3.log "config3 $v"
 done

@@ -308,6 +308,9 @@ constexpr int MAXSUB = 24;  // sub-tiles per epoch (n <= 24 * nwork * 31)
 struct PhaseB {
     int kt, jt, gsz;  // tap, rank in the tap's group, group size
     int g0, cnt;      // this unit: first global transition index of the tap, count
+    int n1;           // exact steps found before the unit's samples arrived (<= 2)
+    int b1[2];        //   their sample positions
+    float d1[2];      //   and chip deltas
     double dk;        // tap offset
     bool prompt;      // kt is the prompt tap (first-half prompt too)
     float re, im, hre, him;  // this thread's tap sum and first-half prompt
@@ -340,13 +343,13 @@ __device__ __forceinline__ void phase_b_one(PhaseB& pb, const float2* tile_d, co
     }
 }
 
-// The range of this thread's tap's transitions whose step falls in the unit
-// [u0, u0+len): computed by every thread of the tap group at the start of
-// the unit (it depends only on the epoch constants), so it overlaps phase A
-// instead of sitting on the per-epoch serial path.
+// Latency shape (one unit per epoch, its copy long done): the tap's
+// transition range, computed right before phase A so it interleaves with it,
+// and the whole walk after phase A (two steps at a time).
 template <int T>
 __device__ __forceinline__ void phase_b_range(PhaseB& pb, const EpochConsts& c, const CodeTables& ct,
                                               int u0, int len) {
+    pb.n1 = -1;  // no steps precomputed: phase_b walks from the first
     if (pb.kt >= T) {
         pb.g0 = pb.cnt = 0;
         return;
@@ -357,17 +360,52 @@ __device__ __forceinline__ void phase_b_range(PhaseB& pb, const EpochConsts& c, 
     pb.cnt = trans_count(ct, mhi) - pb.g0;
 }
 
-// The transitions of this thread's tap in the sub-tile [u0, u0+len), two at
-// a time so the fp64 boundary searches of the pair overlap.
+// Phase B, part 1 -- before the unit's samples are needed (it depends only
+// on the epoch constants, so it runs while the bulk copy lands): the range
+// of this thread's tap's transitions whose step falls in the unit
+// [u0, u0+len), and the exact steps of the first two of them (the two fp64
+// searches overlap).  Part 2 (after phase A) is then only the prefix reads
+// and FMAs, so the tile is released sooner.
 template <int T>
+__device__ __forceinline__ void phase_b_pre(PhaseB& pb, const EpochConsts& c, const CodeTables& ct,
+                                            int u0, int len) {
+    pb.n1 = 0;
+    if (pb.kt >= T) {
+        pb.g0 = pb.cnt = 0;
+        return;
+    }
+    const int hi = u0 + len - 1;
+    const int mlo = tap_index(u0 > 0 ? u0 - 1 : 0, c.cps, c.base, pb.dk);
+    const int mhi = tap_index(hi, c.cps, c.base, pb.dk);
+    pb.g0 = trans_count(ct, mlo);
+    pb.cnt = trans_count(ct, mhi) - pb.g0;
+    const int j1 = pb.jt, j2 = pb.jt + pb.gsz;
+    pb.n1 = j1 < pb.cnt ? (j2 < pb.cnt ? 2 : 1) : 0;
+    const int ga = pb.g0 + (pb.n1 > 0 ? j1 : 0), gb = pb.g0 + (pb.n1 > 1 ? j2 : 0);
+    const int ma = ct.tm[ga], mb = ct.tm[gb];
+    pb.d1[0] = (float)ct.td[ga];
+    pb.d1[1] = (float)ct.td[gb];
+    pb.b1[0] = pb.n1 > 0 ? tap_boundary(ma, pb.dk, c, u0, hi) : u0;
+    pb.b1[1] = pb.n1 > 1 ? tap_boundary(mb, pb.dk, c, u0, hi) : u0;
+}
+
+// Phase B, part 2: the steps found in part 1, then (low sample rates only)
+// the rest of the tap's transitions, two at a time.
+template <int T, bool PRE = true>
 __device__ __forceinline__ void phase_b(PhaseB& pb, const EpochConsts& c, const float2* tile_d,
                                         const float2* anchors, const CodeTables& ct, int u0,
                                         int len) {
     if (pb.kt >= T)
         return;
+    if constexpr (PRE) {
+        if (pb.n1 > 0)
+            phase_b_one(pb, tile_d, anchors, u0, c.nh, pb.b1[0], pb.d1[0]);
+        if (pb.n1 > 1)
+            phase_b_one(pb, tile_d, anchors, u0, c.nh, pb.b1[1], pb.d1[1]);
+    }
     const int hi = u0 + len - 1;
     const int g0 = pb.g0, cnt = pb.cnt;
-    for (int j = pb.jt; j < cnt; j += 2 * pb.gsz) {
+    for (int j = PRE ? pb.jt + 2 * pb.gsz : pb.jt; j < cnt; j += 2 * pb.gsz) {
         const int j2 = j + pb.gsz;
         const bool two = j2 < cnt;
         const int ga = g0 + j, gb = g0 + (two ? j2 : j);
@@ -378,40 +416,6 @@ __device__ __forceinline__ void phase_b(PhaseB& pb, const EpochConsts& c, const 
         phase_b_one(pb, tile_d, anchors, u0, c.nh, ba, da);
         if (two)
             phase_b_one(pb, tile_d, anchors, u0, c.nh, bb, db);
-    }
-}
-
-// Variant: all taps per thread, transitions dealt round-robin per tap.
-template <int T>
-__device__ __forceinline__ void phase_b_pertap(const EpochConsts& c, const float2* tile_d,
-                                               const float2* anchors, const CodeTables& ct,
-                                               const double* d, int kp, int u0, int len, float* acc,
-                                               int nthreads, const int2* tr) {
-    const int hi = u0 + len - 1;
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-        const double dk = d[k];
-        const int2 rk = tr[k];
-        int j = (int)threadIdx.x - ((k * 64) & 511);
-        while (j < 0)
-            j += nthreads;
-        for (; j < rk.y; j += nthreads) {
-            const int g = rk.x + j;
-            const int m = ct.tm[g];
-            const float dlt = (float)ct.td[g];
-            const int b = tap_boundary(m, dk, c, u0, hi);
-            const int off = b - u0;
-            const float2 p = tile_d[off];
-            const float2 an = anchors[off / RUN];
-            const float ar = fmaf(p.x, an.x, p.y * an.y);
-            const float ai = fmaf(p.y, an.x, -(p.x * an.y));
-            acc[2 * k] = fmaf(-dlt, ar, acc[2 * k]);
-            acc[2 * k + 1] = fmaf(-dlt, ai, acc[2 * k + 1]);
-            if (k == kp && b < c.nh) {
-                acc[2 * T] = fmaf(-dlt, ar, acc[2 * T]);
-                acc[2 * T + 1] = fmaf(-dlt, ai, acc[2 * T + 1]);
-            }
-        }
     }
 }
 
@@ -992,6 +996,7 @@ struct TrackArgs {
     int nbuf;         // sample tiles per CTA: 1 (latency shape) or 2 (double-buffered)
     int csize;        // CTAs per channel (a thread-block cluster when > 1)
     int share;        // samples of each epoch per cluster CTA (multiple of RUN)
+    int thr;          // throughput-shape instantiation (track_kernel<..., true>)
 };
 
 // Stage clocks (profiling builds only: -DL1RXG_PROFILE, run with
@@ -1272,7 +1277,12 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
 //     If that makes the channel Idle, epoch e+1 is discarded before its
 //     loop update, exactly as if it had never been admitted
 //     (tracking.hpp:511-514 + the caller's Idle check, pipeline.hpp:567-568).
-template <int T, int SK>
+// THR: throughput shape (many units per epoch, four CTAs per SM): phase B's
+// steps are searched while each unit's copy lands.  !THR: latency shapes
+// (the copy is long done): the search interleaves with phase A.  Separate
+// instantiations keep each shape's code small (the serial per-epoch path of
+// the latency shape is sensitive to instruction-cache misses).
+template <int T, int SK, bool THR>
 __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
     typedef typename Samp<SK>::raw_t R;
     constexpr int esz = Samp<SK>::esz;
@@ -1425,6 +1435,15 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                     const int i0 = u0 + tid * RUN;
                     const int cnt = min(RUN, rend - i0);
                     const int r0t = delta + tid * RUN;
+                    // phase B's transition range and first exact steps depend
+                    // only on the epoch constants: with several units per
+                    // epoch they are found while this unit's copy lands; with
+                    // one (latency shape, copy long done) they interleave
+                    // with phase A below
+                    if constexpr (THR) {
+                        c.inv_cps = fast_rcp(c.cps);  // tap_boundary's estimate (within 2 ulp)
+                        phase_b_pre<T>(pb, c, s->ct, u0, len);
+                    }
                     PROF_A(2);
                     // each half of the copy has waiters (thread 0's run starts
                     // in the first, the last run ends in the second), so after
@@ -1436,11 +1455,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                             mbar_wait(&s->bars[b][1], par);
                     }
                     PROF_A(3);
-                    // phase B's constants and transition range depend only on
-                    // the epoch constants: computed here so they interleave
-                    // with phase A
-                    c.inv_cps = fast_rcp(c.cps);  // tap_boundary's estimate (within 2 ulp)
-                    phase_b_range<T>(pb, c, s->ct, u0, len);
+                    if constexpr (!THR) {
+                        c.inv_cps = fast_rcp(c.cps);
+                        phase_b_range<T>(pb, c, s->ct, u0, len);
+                    }
                     if (cnt > 0)
                         phase_a_dispatch<T>(c, rawt + tid * RUN, pre + tid * RUN, s->rot, s->ct.chip,
                                             s->d, a.kp, i0, cnt, acc, &anchors[tid]);
@@ -1459,7 +1477,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         PROF_STAMP(2);
                         PROF_UNIT(1, tu);
                     }
-                    phase_b<T>(pb, c, tile_d, anchors, s->ct, u0, len);
+                    phase_b<T, THR>(pb, c, tile_d, anchors, s->ct, u0, len);
                 }
             }
             if (q + 1 == nsub && warp < nwork_warps) {
@@ -1585,7 +1603,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) correlate_jobs_kernel(JobArgs a) {
                 phase_a_dispatch<T>(c, reinterpret_cast<const f2x*>(tile + tid * RUN), tile + tid * RUN,
                                     s->rot, s->ct.chip, s->d, a.kp, i0, cnt, acc, &anchors[tid]);
             __syncthreads();
-            phase_b_range<T>(pb, c, s->ct, u0, len);
+            phase_b_pre<T>(pb, c, s->ct, u0, len);
             phase_b<T>(pb, c, tile, anchors, s->ct, u0, len);
             __syncthreads();
         }

@@ -170,19 +170,19 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
     return lc;
 }
 
-template <int T, int SK>
+template <int T, int SK, bool THR>
 int launch_track_sk(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
     // the control warp owns no tile runs; + the cluster exchange slots
     const size_t sm = smem_bytes<T>(nt - 32, a.nbuf, Samp<SK>::esz) +
                       (a.csize > 1 ? 2u * a.csize * (2 * T + 2) * sizeof(double) : 0);
-    CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    CK(cudaFuncSetAttribute(track_kernel<T, SK, THR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_kernel<T, SK, THR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     if (a.csize <= 1) {
-        track_kernel<T, SK><<<n_ch, nt, sm, s>>>(a);
+        track_kernel<T, SK, THR><<<n_ch, nt, sm, s>>>(a);
     } else {  // one thread-block cluster of csize CTAs per channel
         if (a.csize > 8)
-            CK(cudaFuncSetAttribute(track_kernel<T, SK>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            CK(cudaFuncSetAttribute(track_kernel<T, SK, THR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(n_ch * a.csize));
         cfg.blockDim = dim3(static_cast<unsigned>(nt));
@@ -195,19 +195,24 @@ int launch_track_sk(const TrackArgs& a, int n_ch, int nt, cudaStream_t s) {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, track_kernel<T, SK>, a));
+        CK(cudaLaunchKernelEx(&cfg, track_kernel<T, SK, THR>, a));
     }
     CK(cudaGetLastError());
     return 0;
 }
 
+template <int T, bool THR>
+int launch_track_thr(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
+    switch (sk) {
+    case SK_I16: return launch_track_sk<T, SK_I16, THR>(a, n_ch, nt, s);
+    case SK_I8: return launch_track_sk<T, SK_I8, THR>(a, n_ch, nt, s);
+    default: return launch_track_sk<T, SK_F32, THR>(a, n_ch, nt, s);
+    }
+}
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
-    switch (sk) {
-    case SK_I16: return launch_track_sk<T, SK_I16>(a, n_ch, nt, s);
-    case SK_I8: return launch_track_sk<T, SK_I8>(a, n_ch, nt, s);
-    default: return launch_track_sk<T, SK_F32>(a, n_ch, nt, s);
-    }
+    return a.thr ? launch_track_thr<T, true>(a, n_ch, nt, s, sk)
+                 : launch_track_thr<T, false>(a, n_ch, nt, s, sk);
 }
 
 template <int T>
@@ -319,6 +324,7 @@ struct l1rxg_tracker {
     int nt = 64;
     int nbuf = 1;
     int csize = 1;   // CTAs per channel (cluster) in the latency shape
+    int thr = 0;     // throughput shape
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
     int esz = 8;     // ring element bytes (ring_esz)
@@ -699,6 +705,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
                 mx += 32;
             t->nt = pick_threads(n, nullptr, mx) + 32;
             t->nbuf = ev_nb ? std::atoi(ev_nb) : 1;
+            t->thr = 1;
         } else {
             // latency shape: split each channel's epoch over a cluster of K
             // CTAs (one per SM) while the channels x K fit the SMs and each
@@ -994,6 +1001,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.nbuf = t->nbuf;
     a.csize = t->csize;
     a.share = t->share;
+    a.thr = t->thr;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
