@@ -594,19 +594,6 @@ __device__ __forceinline__ double div_exact(double a, double b, double inv_b) {
     return q;
 }
 
-__device__ __forceinline__ double fll_disc(double pi_, double pq, double ci, double cq,
-                                           double dt, bool fold) {  // tracking.hpp:113-138
-    double cross = pi_ * cq - pq * ci;
-    double dot = pi_ * ci + pq * cq;
-    if (fold && dot < 0) {
-        cross = -cross;
-        dot = -dot;
-    }
-    if (cross == 0.0 && dot == 0.0)
-        return 0.0;
-    return atan2(cross, dot) / (2.0 * PI_D * dt);
-}
-
 // C fmod(x, y) for y > 0 and |x| < 2^40 y, exactly: the remainder
 // x - k*y (k = trunc(x/y)) is representable, so one fma computes it
 // without rounding; the quotient estimate is corrected by +-1 so the result
@@ -631,10 +618,9 @@ __device__ __forceinline__ void advance_nco(double& code_phase, double& carrier_
     chi = __dadd_rn(chi, adv);
 }
 
-// The transcendental pieces of one update and the fmod-based NCO advance
-// are independent of each other: the tracking kernel evaluates them in
-// separate WARPS (divergent lanes of one warp would serialise), then one
-// thread applies the reference's sequential logic (loop_update).
+// The discriminator values and NCO advance of one epoch, the inputs of the
+// reference's sequential loop logic (loop_fast); computed in parallel lanes
+// of warp 0 and by the control warp (see warp0_update).
 struct LoopPre {
     double e, l;        // |E|, |L|            (tracking.hpp:96-97, 545-546)
     double dll;         // DLL discriminator   (:95-101)
@@ -642,67 +628,6 @@ struct LoopPre {
     double fc, ff;      // FLL coarse / fine   (:113-138)
     double code_phase, carrier_phase, chi;  // NCO advance (:275-280)
 };
-constexpr int LOOP_PIECES = 5;
-
-// Each piece is its own non-inlined function: inlined into one body the
-// compiler merges and hoists their shared subexpressions above the dispatch,
-// and every piece warp then pays for several pieces.
-__device__ __noinline__ void piece_dll(LoopPre& p, const double* sums, int ke, int kl) {
-    const double ie = sums[2 * ke], qe = sums[2 * ke + 1];
-    const double il = sums[2 * kl], ql = sums[2 * kl + 1];
-    p.e = sqrt(ie * ie + qe * qe);
-    p.l = sqrt(il * il + ql * ql);
-    p.dll = (p.e + p.l == 0.0) ? 0.0 : 0.5 * (p.e - p.l) / (p.e + p.l);  // :95-101
-}
-__device__ __noinline__ void piece_pll(LoopPre& p, const double* sums, int kp) {
-    const double ip = sums[2 * kp], qp = sums[2 * kp + 1];
-    if (ip == 0.0)
-        p.pll = (qp == 0.0) ? 0.0 : (qp > 0 ? PI_D / 2.0 : -PI_D / 2.0);
-    else
-        p.pll = atan(qp / ip);
-}
-__device__ __noinline__ void piece_fll(double& out, double a, double b, double c2, double d2,
-                                       double dt, bool fold) {
-    out = fll_disc(a, b, c2, d2, dt, fold);
-}
-__device__ __noinline__ void piece_nco(LoopPre& p, const l1rxg_channel& ch, const EpochConsts& c) {
-    double cp = ch.code_phase_chips, ph = ch.carrier_phase_rad, chi = ch.chi_chips;
-    advance_nco(cp, ph, chi, c);
-    p.code_phase = cp;
-    p.carrier_phase = ph;
-    p.chi = chi;
-}
-
-// sums: [2T + 2] fp64 totals; the first-half prompt sits at 2T
-__device__ __forceinline__ void loop_piece(int piece, LoopPre& p, const l1rxg_channel& ch,
-                                           const double* sums, int T, int ke, int kp, int kl,
-                                           const LoopCfg& lc, const EpochConsts& c) {
-    const int64_t esh = ch.epochs_since_handoff;
-    switch (piece) {
-    case 0:
-        piece_dll(p, sums, ke, kl);
-        break;
-    case 1:
-        piece_pll(p, sums, kp);
-        break;
-    case 2:  // only read during the coarse pull-in stage
-        p.fc = 0.0;
-        if (esh < (int64_t)lc.cfg.fll_coarse_ms) {
-            const double ip = sums[2 * kp], qp = sums[2 * kp + 1];
-            const double h1i = sums[2 * T], h1q = sums[2 * T + 1];
-            piece_fll(p.fc, h1i, h1q, ip - h1i, qp - h1q, lc.dt / 2.0, false);
-        }
-        break;
-    case 3:  // only read during the fine pull-in stage
-        p.ff = 0.0;
-        if (esh < (int64_t)lc.cfg.fll_pull_in_ms && esh >= (int64_t)lc.cfg.fll_coarse_ms)
-            piece_fll(p.ff, ch.last_ip, ch.last_qp, sums[2 * kp], sums[2 * kp + 1], lc.dt, true);
-        break;
-    default:
-        piece_nco(p, ch, c);
-        break;
-    }
-}
 
 // track_epoch is split along its data dependences:
 //  * loop_fast -- everything the NEXT epoch's correlation needs: FLL
@@ -1126,10 +1051,11 @@ __device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a,
 //                        (tracking.hpp:104-111), FLL coarse and fine
 //                        (:113-138; the fine one folded to dot >= 0);
 //   sqrt  on lanes 3..4: |E|, |L| (:96-97);
-//   fmod  on lanes 5..6: carrier and code NCO advance (:275-280, exact);
-// lane 0 then runs loop_fast, and lanes 0..1 divide the next epoch's w and
-// cps (:234-236).  All values equal the reference's up to last-bit
-// rounding of atan vs atan2; the state advance is bit-exact.
+// (branch-free fp64 helpers, so the pieces interleave); the exact-fmod NCO
+// advance (:275-280) was computed by the control warp during the epoch.
+// Lane 0 then runs loop_fast and forms the next epoch's w and cps as IEEE
+// quotients (:234-236).  Loop values agree with the reference to ~1e-15
+// relative (the parity bar is 1e-5); the state advance is bit-exact.
 template <int T>
 __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a, const EpochConsts& c,
                                              int64_t off, int cidx, int64_t done, int nwork_warps,
