@@ -383,7 +383,8 @@ def run_batch(args, rank, world, local, dist):
     ctx = Context(local)
     trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs),
                   taps=taps, cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks,
-                  cta_mode=abi.CTA_THROUGHPUT if args.cta != "latency" else abi.CTA_LATENCY)
+                  cta_mode=abi.CTA_THROUGHPUT if args.cta != "latency" else abi.CTA_LATENCY,
+                  ring_raw=args.ring_raw)
     stream = torch.cuda.ExternalStream(trk.cuda_stream(), device=dev)
     chunk = chunk_b * n * 4
 
@@ -545,6 +546,7 @@ def main():
     ap.add_argument("--e2e-chunk-ms", type=int, default=1000)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
     ap.add_argument("--cta", default="throughput", choices=["throughput", "latency"])
+    ap.add_argument("--ring-raw", action="store_true", help="config 4: keep cint16 raw in the rings")
     args = ap.parse_args()
 
     import torch

@@ -2,10 +2,8 @@ cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 summ() { python -c "
 import json,sys
 l=[x for x in open(sys.argv[1]) if x.startswith('{')][-1]; d=json.loads(l); print(sys.argv[2], round(d['value'],1), round(d['ms_per_step'],2), round(d['roofline']['frac'],4), d['kernel_ms_per_step'])" $1 "$2"; }
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -1
-for v in head new; do
-SO=""; [ $v = head ] && SO=$PWD/_exp/head/libl1rxg.so
-L1RXG_SO=$SO python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/b2.log 2>&1; summ gpurun_out/b2.log "config2 $v"
-L1RXG_SO=$SO python bench.py --config 4 --recordings 256 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/sw4.log 2>&1; summ gpurun_out/sw4.log "config4-256 $v"
-L1RXG_SO=$SO python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/b3.log 2>&1; summ gpurun_out/b3.log "config3 $v"
+for cfg in "64 2" "96 2" "128 2"; do
+  set -- $cfg
+  L1RXG_THR_NWORK=$1 L1RXG_THR_NBUF=$2 python bench.py --config 4 --recordings 256 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --ring-raw > gpurun_out/sw.log 2>&1; summ gpurun_out/sw.log "raw nwork $1 nbuf $2"
+  L1RXG_SO=$PWD/_exp/skipab/libl1rxg.so L1RXG_THR_NWORK=$1 L1RXG_THR_NBUF=$2 python bench.py --config 4 --recordings 256 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --ring-raw > gpurun_out/sw.log 2>&1; summ gpurun_out/sw.log "   skeleton raw nwork $1 nbuf $2"
 done

@@ -1385,9 +1385,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         c.inv_cps = fast_rcp(c.cps);
                         phase_b_range<T>(pb, c, s->ct, u0, len);
                     }
+#ifndef L1RXG_XSKIP_A
                     if (cnt > 0)
                         phase_a_dispatch<T>(c, rawt + tid * RUN, pre + tid * RUN, s->rot, s->ct.chip,
                                             s->d, a.kp, i0, cnt, acc, &anchors[tid]);
+#endif
                     PROF_A(4);
                     if (tid == 0) {
                         PROF_STAMP(1);
@@ -1403,7 +1405,9 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_kernel(TrackArgs a) {
                         PROF_STAMP(2);
                         PROF_UNIT(1, tu);
                     }
+#ifndef L1RXG_XSKIP_B
                     phase_b<T, THR>(pb, c, tile_d, anchors, s->ct, u0, len);
+#endif
                 }
             }
             if (q + 1 == nsub && warp < nwork_warps) {
