@@ -352,3 +352,25 @@ def test_raw_ring_matches_decoded_ring(ctx, fmt, fs, cta_mode):
         outs.append(trk.records(0))
     assert len(outs[0]) >= 58
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+@pytest.mark.parametrize("fs", [5.0e6, 3.969e6])
+@pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SINGLE, abi.CTA_THROUGHPUT])
+def test_odd_epoch_lengths(ctx, oracle_mod, fs, cta_mode):
+    """Epoch lengths that are not multiples of the 31-sample run: 5 MHz (the
+    paper's recordings, n = 5000) and n = 3969 (one sample past a full
+    throughput tile: a 1-sample last unit, whose bulk copy has an empty first
+    half), in every CTA shape; cint8 input, per-epoch replay parity."""
+    n = int(round(fs / 1000))
+    sv = ss.Sv(prn=21, cn0_dbhz=47.0, doppler_hz=2100.0, delay_chips=640.4)
+    raw = _raw(50, fs, [sv], "int8_iq", seed=int(fs) % 1000)
+    init = _init(sv, fs)
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    trk = Tracker(ctx, abi.FMT_INT8_IQ, fs, 0.0, [init], ring_samples=60 * n, max_records=50,
+                  cta_mode=cta_mode)
+    trk.push(0, raw.view(np.int8))
+    trk.run()
+    recs, tsums = trk.records(0, tap_sums=True)
+    assert len(recs) >= 48
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_IQ, fs)
+    replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=tsums)
