@@ -775,6 +775,9 @@ def main():
                        nbytes / 1e6, blocks * n * 8 / 1e9),
                    "lock_fail_limit": "INT_MAX (every channel computes every epoch)"},
         "realtime_channels": world * float(counts.sum()) / (ms_per_step * 1e-3) / 1000.0,
+        # the per-epoch critical path of a channel (track launch time / epochs),
+        # the latency view SURVEY 8d asks for on the sequential configs
+        "epoch_latency_us": track_launch_ms * 1e3 / max(1.0, float(counts.max())),
         "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -1,3 +1,4 @@
+# Full measurement pass used for profiles/: gpurun --timeout 2400 -- "bash tools/gpu_full.sh"
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/full
 python bench.py --config 4 > gpurun_out/full/bench_config4.json 2> gpurun_out/full/bench_config4.err
 python bench.py --config 5 > gpurun_out/full/bench_config5.json 2> gpurun_out/full/bench_config5.err

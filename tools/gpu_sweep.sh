@@ -1,3 +1,4 @@
+# Scratch driver for gpurun sweeps (edited per experiment): gpurun --timeout 1500 -- "bash tools/gpu_sweep.sh"
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 summ() { python -c "
 import json,sys
