@@ -344,7 +344,7 @@ BATCH = dict(recordings=512, chunk_blocks=50, blocks_per_step=100,
                   "C/N0 U[30,50] dB-Hz")
 
 
-def run_batch(args, rank, world, local, dist):
+def run_batch(args, rank, world, local, dist, emit=True):
     """Config 4: many independent recordings, sharded by recording over the
     ranks (strong scaling: the 512 recordings are split, no data-path
     collective).  One step = every local recording x `blocks_per_step`
@@ -474,8 +474,9 @@ def run_batch(args, rank, world, local, dist):
                        "H2D + one decode launch per %d-block chunk) -> run -> records_raw to host" % chunk_b}
         del pinned
     if rank != 0:
-        dist.destroy_process_group()
-        return
+        if emit:
+            dist.destroy_process_group()
+        return None
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
     track_launch_ms = track_ms / args.steps
@@ -523,13 +524,40 @@ def run_batch(args, rank, world, local, dist):
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock under load "
                                     "(%.0f MHz); FP32 pipe roof per SURVEY 8d" % sm_mhz,
                      "alg_ops_per_sample_tap": ops_per_sample_tap(T, 12, False),
-                     "hbm": {"achieved_gbs": (epochs_local * n * 8) / (track_launch_ms * 1e-3) / 1e9,
-                             "peak_gbs": peaks.get("hbm_gbs", 6450.0)}},
+                     "hbm": {"achieved_gbs": (len(recs) * blocks * n * 8) / (track_launch_ms * 1e-3) / 1e9,
+                             "peak_gbs": peaks.get("hbm_gbs", 6450.0),
+                             "note": "unique float2 baseband bytes per step (each recording's ring "
+                                     "read once; its 12 channels share it through L2)"}},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
     }
+    if not emit:
+        return line
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    return line
+
+
+def companion_config4(args, rank, world, local, dist):
+    """The throughput shape next to the latency-bound headline: config 4
+    (independent recordings, 12 channels x 7 taps, cint16 at 65.472 MHz) on
+    128 recordings x 100 blocks, its value and roofline fraction (the full
+    512-recording line: `bench.py --config 4`)."""
+    import copy
+    import torch
+    a = copy.copy(args)
+    a.recordings, a.blocks, a.steps, a.warmup = 128, 100, 2, 1
+    a.no_cpu_baseline, a.no_e2e, a.cta, a.ring_raw = True, True, "throughput", False
+    try:
+        ln = run_batch(a, rank, world, local, dist, emit=False)
+        torch.cuda.empty_cache()
+        return {"workload": "config4 shape, 128 recordings x 12 channels x 7 taps x 100 blocks "
+                            "(bench.py --config 4 runs all 512)",
+                "value": ln["value"], "unit": ln["unit"], "ms_per_step": ln["ms_per_step"],
+                "realtime_channels": ln["realtime_channels"], "roofline": ln["roofline"],
+                "clocks": ln["clocks"]}
+    except Exception as ex:  # reported, never fatal for the headline line
+        return {"error": repr(ex)}
 
 
 def main():
@@ -547,6 +575,8 @@ def main():
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
     ap.add_argument("--cta", default="throughput", choices=["throughput", "latency"])
     ap.add_argument("--ring-raw", action="store_true", help="config 4: keep cint16 raw in the rings")
+    ap.add_argument("--no-companion", dest="companion", action="store_false",
+                    help="config 2: skip the config-4 throughput companion measurement")
     args = ap.parse_args()
 
     import torch
@@ -796,6 +826,8 @@ def main():
     }
     if gathered is not None:
         line["records_gathered_bytes"] = gathered
+    if args.config == 2 and args.companion and world == 1:
+        line["companion_throughput"] = companion_config4(args, rank, world, local, dist)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
