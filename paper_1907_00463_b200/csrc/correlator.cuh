@@ -519,7 +519,6 @@ struct LoopCfg {
     double dll_k1, dll_k2;
     double fll_k;               // ((4*B_fll)*2)*pi            (:88-92)
     double alpha;               // 1 / cn0_window_ms           (:466)
-    double inv_fs;              // 1 / fs (division by fs: div_fs)
     double inv_fll_c, inv_fll_f;  // 1 / (2 pi (dt/2)), 1 / (2 pi dt) (:113-138)
 };
 
@@ -578,20 +577,6 @@ __device__ __forceinline__ double atan2_bf(double y, double x) {
     r = ay > ax ? PI_D / 2.0 - r : r;
     r = x < 0.0 ? PI_D - r : r;
     return copysign(r, y);
-}
-// a / b correctly rounded for the NCO rates (w = 2 pi fD / fs, cps = cf / fs
-// must be the reference's IEEE quotients): reciprocal estimate + one exact
-// FMA correction, checked against the half-ulp bound; IEEE division only
-// when the check cannot decide.
-__device__ __forceinline__ double div_exact(double a, double b, double inv_b) {
-    const double q0 = a * inv_b;
-    const double q = __fma_rn(__fma_rn(-q0, b, a), inv_b, q0);
-    const double r = __fma_rn(-q, b, a);  // exact remainder
-    const double ulp = __longlong_as_double(__double_as_longlong(fabs(q)) & 0x7ff0000000000000ll) *
-                       2.220446049250313e-16;
-    if (!(fabs(r) < 0.49 * ulp * fabs(b)))
-        return a / b;
-    return q;
 }
 
 // C fmod(x, y) for y > 0 and |x| < 2^40 y, exactly: the remainder
@@ -701,10 +686,12 @@ __device__ void loop_metrics(l1rxg_channel& ch, const l1rxg_corr& o, const LoopC
         lfc++;
     if (state == L1RXG_ACQUIRED)  // :591-592
         state = L1RXG_TRACKING;
-    // update_quality_metrics (:459-515)
-    const double pwr = o.ip * o.ip + o.qp * o.qp;
-    const double clr = pwr > 0 ? (o.ip * o.ip - o.qp * o.qp) / pwr : 0.0;
-    clr_s += lc.alpha * (clr - clr_s);
+    // update_quality_metrics (:459-515); explicit roundings (no FMA
+    // contraction), so every kernel instantiation computes the same bits
+    const double ii = __dmul_rn(o.ip, o.ip), qq = __dmul_rn(o.qp, o.qp);
+    const double pwr = __dadd_rn(ii, qq);
+    const double clr = pwr > 0 ? __ddiv_rn(__dsub_rn(ii, qq), pwr) : 0.0;
+    clr_s = __dadd_rn(clr_s, __dmul_rn(lc.alpha, __dsub_rn(clr, clr_s)));
     ch.win_ip[win_len] = o.ip;
     ch.win_qp[win_len] = o.qp;
     win_len++;
@@ -714,20 +701,21 @@ __device__ void loop_metrics(l1rxg_channel& ch, const l1rxg_corr& o, const LoopC
         for (int k = 0; k < m; ++k) {
             const double wi = ch.win_ip[k], wq = ch.win_qp[k];
             const double sg = wi >= 0 ? 1.0 : -1.0;
-            nbi += sg * wi;
-            nbq += sg * wq;
-            wbp += wi * wi + wq * wq;
+            nbi = __dadd_rn(nbi, __dmul_rn(sg, wi));
+            nbq = __dadd_rn(nbq, __dmul_rn(sg, wq));
+            wbp = __dadd_rn(wbp, __dadd_rn(__dmul_rn(wi, wi), __dmul_rn(wq, wq)));
         }
         win_len = 0;
-        const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
-        mu_s = mvalid ? mu_s + 0.2 * (mu - mu_s) : mu;
+        const double mu =
+            wbp > 0 ? __ddiv_rn(__dadd_rn(__dmul_rn(nbi, nbi), __dmul_rn(nbq, nbq)), wbp) : 0.0;
+        mu_s = mvalid ? __dadd_rn(mu_s, __dmul_rn(0.2, __dsub_rn(mu, mu_s))) : mu;
         const double md = (double)m;
         if (mu_s >= md - 1e-9)
             cn0 = 65.0;
         else if (mu_s <= 1.0)
             cn0 = 0.0;
         else
-            cn0 = 10.0 * log10((mu_s - 1.0) / (md - mu_s) / 1e-3);
+            cn0 = __dmul_rn(10.0, log10(__ddiv_rn(__ddiv_rn(__dsub_rn(mu_s, 1.0), __dsub_rn(md, mu_s)), 1e-3)));
         mvalid = 1;
     }
     if (mvalid && esh > cfg.fll_pull_in_ms + cfg.cn0_window_ms) {
@@ -1110,8 +1098,8 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
     } else if (lane == 1 || lane == 2) {
         const double pi_ = lane == 1 ? h1i : ch.last_ip, pq = lane == 1 ? h1q : ch.last_qp;
         const double ci = lane == 1 ? ip - h1i : ip, cq = lane == 1 ? qp - h1q : qp;
-        double cross = pi_ * cq - pq * ci;
-        double dot = pi_ * ci + pq * cq;
+        double cross = __dsub_rn(__dmul_rn(pi_, cq), __dmul_rn(pq, ci));
+        double dot = __dadd_rn(__dmul_rn(pi_, ci), __dmul_rn(pq, cq));
         if (lane == 2 && dot < 0) {
             cross = -cross;
             dot = -dot;
@@ -1122,7 +1110,8 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
     }
     const double ang = atan2_bf(y, x);
     // sqrt lanes
-    const double sq = fast_sqrt(lane == 3 ? ie * ie + qe * qe : il * il + ql * ql);
+    const double sq = fast_sqrt(lane == 3 ? __dadd_rn(__dmul_rn(ie, ie), __dmul_rn(qe, qe))
+                                          : __dadd_rn(__dmul_rn(il, il), __dmul_rn(ql, ql)));
     PROF_W(3);
     const double a_pll = __shfl_sync(0xffffffffu, ang, 0);
     const double a_fc = __shfl_sync(0xffffffffu, ang, 1);
@@ -1165,13 +1154,17 @@ __device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a,
         s->rec_slot = (int64_t)cidx * a.max_records + rec_i;
         s->pending = 1;
     }
-    // next epoch's w = (2 pi fD)/fs and cps = cf/fs (IEEE quotients, both on
-    // lane 0: independent, so they overlap); inv_cps is formed by each thread
-    // at the start of the next epoch, off this path
+    // next epoch's w = (2 pi fD)/fs and cps = cf/fs, the reference's IEEE
+    // quotients (lanes 0 and 1); inv_cps is formed by each thread at the start
+    // of the next epoch, off this path
     PROF_W(6);
+    fd = __shfl_sync(0xffffffffu, fd, 0);
+    cf = __shfl_sync(0xffffffffu, cf, 0);
+    // one IEEE division per lane (two on one lane serialise: 2.5x slower)
+    const double quo = (lane == 0 ? 2.0 * PI_D * fd : cf) / a.lc.fs;
+    const double w = __shfl_sync(0xffffffffu, quo, 0);
+    const double cps = __shfl_sync(0xffffffffu, quo, 1);
     if (lane == 0) {
-        const double w = div_exact(2.0 * PI_D * fd, a.lc.fs, a.lc.inv_fs);
-        const double cps = div_exact(cf, a.lc.fs, a.lc.inv_fs);
         EpochConsts& nc = s->c;
         nc.w = w;
         nc.cps = cps;

@@ -164,7 +164,6 @@ LoopCfg make_loop_cfg(const l1rxg_tracking_cfg& cfg, int kernel, double fs, int 
     lc.dll_k2 = 2.0 * cfg.dll_damping * wd;
     lc.fll_k = 4.0 * cfg.fll_bandwidth_hz * 2.0 * PI_D;
     lc.alpha = 1.0 / static_cast<double>(cfg.cn0_window_ms);
-    lc.inv_fs = 1.0 / fs;
     lc.inv_fll_c = 1.0 / (2.0 * PI_D * (lc.dt / 2.0));
     lc.inv_fll_f = 1.0 / (2.0 * PI_D * lc.dt);
     return lc;

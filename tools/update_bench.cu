@@ -35,7 +35,7 @@ static const char* W[] = {"totals", "cluster", "operands", "atan2/sqrt", "pre", 
 int main() {
     TrackArgs a{};
     a.n = 16368; a.kp = 1; a.ke = 0; a.kl = 2; a.max_records = 16; a.csize = 1;
-    a.lc.fs = 16.368e6; a.lc.dt = 1e-3; a.lc.inv_fs = 1.0 / 16.368e6; a.lc.pll_k1 = 0.1; a.lc.pll_k2 = 0.2;
+    a.lc.fs = 16.368e6; a.lc.dt = 1e-3; a.lc.pll_k1 = 0.1; a.lc.pll_k2 = 0.2;
     a.lc.dll_k1 = 0.01; a.lc.dll_k2 = 0.02; a.lc.fll_k = 1.0; a.lc.inv_fll_c = 1.0; a.lc.inv_fll_f = 1.0;
     a.lc.cfg.fll_pull_in_ms = 400; a.lc.cfg.fll_coarse_ms = 100;
     long long* c; cudaMalloc(&c, 8);
