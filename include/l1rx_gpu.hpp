@@ -226,4 +226,21 @@ private:
     std::size_t n_ = 0;
 };
 
+// Host navigation-data consumer over the GPU's epoch records (SURVEY.md 8(f)
+// item 1): the reference's own nav::on_prompt (navdata.hpp:607-625), fed the
+// values track_epoch would have passed it (tracking.hpp:596-597): the epoch's
+// prompt I, its epoch index and chi at the START of the epoch (the previous
+// record's chi, or the hand-off value for the first).  Legal off the device
+// because nav state never feeds the loops; a record with state Idle is where
+// the reference would have reset it (tracking.hpp:511-514).
+inline void replay_nav(NavDecodeState& st, const std::vector<l1rxg_epoch_record>& recs,
+                       double& chi_at_start) {
+    for (const auto& r : recs) {
+        nav::on_prompt(st, r.ip, r.epoch_index, chi_at_start);
+        chi_at_start = r.chi_chips;
+        if (r.state == L1RXG_IDLE)
+            st = NavDecodeState{};
+    }
+}
+
 }  // namespace l1rx::gpu

@@ -13,6 +13,7 @@
 #include "l1rx/simsource.hpp"
 #include "l1rx/tracking.hpp"
 #include "l1rx_gpu.hpp"
+#include "support/test_eph.hpp"  // the reference's test ephemeris (proj/tests/support)
 
 using namespace l1rx;
 
@@ -145,6 +146,81 @@ int main() {
         CHECK(r[0].carrier_lock_ratio > 0.9);
         CHECK(std::abs(r[0].carrier_doppler_hz - 320.0) < 5.0);
         CHECK(std::abs(r[0].cn0_dbhz - 45.0) < 2.0);
+    }
+    // navigation data decoded on the host from the GPU's
+    // records.  The reference simulator modulates an encoded ephemeris
+    // (simsource.hpp:80-125, navdata.hpp pack/encode); the GPU tracks 33 s;
+    // the reference's nav state machine replays the records and must recover
+    // the ephemeris within quantization (test_navdata.cpp:268-300 criteria).
+    {
+        const double fs2 = 2.048e6;
+        const auto eph = testsupport::make_test_ephemeris(21);
+        SimScenario sc;
+        SimSatellite sv;
+        sv.prn = eph.prn;
+        sv.cn0_dbhz = 46.0;
+        sv.doppler_hz = -850.0;
+        sv.code_delay_chips = 400.5;
+        sv.ephemeris = eph;
+        sc.satellites.push_back(sv);
+        sc.duration_s = 63.0;
+        sc.sample_rate_hz = fs2;
+        sc.seed = 99;
+        // start one subframe before subframe 1 (ids cycle with tow/6), so
+        // subframes 1-3 arrive after bit sync and the first preamble
+        sc.tow_start_s = 259224;
+        SimStream stream(sc);
+        const auto boundary = static_cast<int>(std::lround(400.5 / constants::chip_rate_hz * fs2));
+        ChannelState ch;
+        init_channel_from_acquisition(ch, eph.prn, -850.0, 0, boundary, 0, fs2);
+        gpu::GpuTracker trk(SampleKind::Int8ComplexInterleaved, fs2, 0.0, {ch}, cfg, 2200 * 2048, 2000);  // 1-s pushes
+        NavDecodeState st;
+        double chi = ch.chi_chips;
+        int64_t fetched = 0;
+        std::vector<int8_t> raw;
+        auto q = [](double v) {
+            return static_cast<int8_t>(std::max(-127L, std::min(127L, std::lround(v * 128.0))));
+        };
+        auto flush = [&]() {
+            trk.push(raw.data(), static_cast<int64_t>(raw.size()));
+            trk.run();
+            raw.clear();
+            std::vector<ChannelState> now;
+            trk.channels(now);
+            const int64_t have = static_cast<int64_t>(now[0].epoch_ms_count);
+            if (have > fetched) {
+                gpu::replay_nav(st, trk.records(0, fetched, have - fetched), chi);
+                fetched = have;
+            }
+        };
+        while (auto blk = stream.next_block()) {
+            for (const auto& v : *blk) {
+                raw.push_back(q(v.real()));
+                raw.push_back(q(v.imag()));
+            }
+            if (raw.size() >= static_cast<std::size_t>(2 * 1000 * 2048))
+                flush();
+        }
+        if (!raw.empty())
+            flush();
+        CHECK(fetched >= 62900);
+        CHECK(st.nav_state == NavState::Eph);
+        CHECK(st.eph.has_value());
+        if (st.eph) {
+            const auto& d = *st.eph;
+            const double pi = constants::pi;
+            CHECK(d.iode == eph.iode);
+            CHECK(d.week_number == eph.week_number);
+            CHECK(testsupport::within_quantum(d.sqrt_a, eph.sqrt_a, std::pow(2, -19)));
+            CHECK(testsupport::within_quantum(d.ecc, eph.ecc, std::pow(2, -33)));
+            CHECK(testsupport::within_quantum(d.m0_rad, eph.m0_rad, std::pow(2, -31) * pi));
+            CHECK(testsupport::within_quantum(d.omega0_rad, eph.omega0_rad, std::pow(2, -31) * pi));
+            CHECK(testsupport::within_quantum(d.i0_rad, eph.i0_rad, std::pow(2, -31) * pi));
+            CHECK(testsupport::within_quantum(d.af0_s, eph.af0_s, std::pow(2, -31)));
+        }
+        CHECK(st.last_tow_s % 6 == 0);
+        std::printf("nav: state %d, tow %lld, records %lld\n", static_cast<int>(st.nav_state),
+                    static_cast<long long>(st.last_tow_s), static_cast<long long>(fetched));
     }
     std::printf("%s: %d checks, %d failures\n", g_fail ? "FAILED" : "OK", g_checks, g_fail);
     return g_fail ? 1 : 0;
