@@ -202,12 +202,16 @@ def cpu_reference_run(raw_np, c, inits, cfg_struct, blocks, threads):
     return wall.value, trk.value, ce.value
 
 
-def cpu_port_run(x_cplx, inits, cfg_struct, taps, fs, blocks, threads):
-    """Builder K-tap restatement (oracle port) for multi-tap configs."""
+def cpu_port_run(x_cplx, inits, cfg_struct, taps, fs, blocks, threads, chan_stream=None):
+    """Builder K-tap restatement (oracle port) for multi-tap configs.
+    `x_cplx` is one complex stream or a list of them (`chan_stream` binds
+    each channel to its stream)."""
     import oracle
     n = int(round(fs / 1000))
+    xs = x_cplx if isinstance(x_cplx, list) else [x_cplx]
+    cs = chan_stream if chan_stream is not None else [0] * len(inits)
     t = time.perf_counter()
-    _, done, _, _ = oracle.track_run(inits, [0] * len(inits), [x_cplx], n, cfg_struct, taps, fs,
+    _, done, _, _ = oracle.track_run(inits, cs, xs, n, cfg_struct, taps, fs,
                                      blocks, threads=threads, records=False)
     return time.perf_counter() - t, int(sum(done))
 
@@ -338,7 +342,7 @@ def run_grid(args, rank, world, local, dist):
         dist.destroy_process_group()
 
 
-BATCH = dict(recordings=512, chunk_blocks=50, blocks_per_step=100,
+BATCH = dict(recordings=512, chunk_blocks=50, blocks_per_step=1000,
              desc="config4: 512 independent seeded recordings x 12 channels x 7 taps (0.25 chip), "
                   "complex int16 I/Q at 65.472 MHz, 8-12 visible SVs per recording, Doppler U(+-5 kHz), "
                   "C/N0 U[30,50] dB-Hz")
@@ -363,6 +367,16 @@ def run_batch(args, rank, world, local, dist, emit=True):
     recs = shard_range(n_rec_total, world, rank)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    # The whole workload (every recording x every block) is resident in HBM:
+    # raw cint16 + the per-recording float2 ring + records/tap sums.  If the
+    # device cannot hold it, the step shrinks to the largest chunk multiple
+    # that fits and config.blocks_per_step says so.
+    want_blocks = blocks
+    free = torch.cuda.mem_get_info(dev)[0]
+    per_block = len(recs) * (n * 4 + 12 * (248 + 2 * 8 * 8))
+    fixed = len(recs) * (chunk_b + 5) * n * 8 + (6 << 30)
+    if fixed + per_block * blocks > free:
+        blocks = max(chunk_b, (free - fixed) // per_block // chunk_b * chunk_b)
     taps = make_taps("wide7")
     cfg = abi.TrackingCfg.default()
     cfg.lock_fail_limit = 2**31 - 1
@@ -446,7 +460,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
     if not args.no_e2e and len(recs) * e2e_blocks * n * 4 * 3 <= room:
         eb = e2e_blocks * n * 4
         pinned = ctx.host_alloc(len(recs) * eb).reshape(len(recs), eb)
-        pinned[:] = raw[:, :eb].cpu().numpy()
+        for j in range(len(recs)):  # row by row: a strided slice would stage a device copy
+            pinned[j] = raw[j, :eb].cpu().numpy()
         rec_bytes = trk.records_raw(dst_ptr=None, device=False).nbytes
 
         def step_e2e():
@@ -495,13 +510,15 @@ def run_batch(args, rank, world, local, dist, emit=True):
     if world == 1 and not args.no_cpu_baseline:
         import oracle
         threads = os.cpu_count() or 1
-        cb = min(args.cpu_blocks, blocks, 100)
-        x = oracle.ingest(raw[0, : cb * n * 4].cpu().numpy(), abi.FMT_INT16_IQ, fs)
-        ci = inits[: cstream.count(0)]
-        wall, ce = cpu_port_run(x, ci, cfg, taps, fs, cb, threads)
+        cb = min(args.cpu_blocks, blocks, 500)
+        R = min(8, len(recs))  # enough channels to keep every host thread busy
+        xs = [oracle.ingest(raw[j, : cb * n * 4].cpu().numpy(), abi.FMT_INT16_IQ, fs) for j in range(R)]
+        nci = sum(1 for s_ in cstream if s_ < R)
+        wall, ce = cpu_port_run(xs, inits[:nci], cfg, taps, fs, cb, threads, chan_stream=cstream[:nci])
+        del xs
         cpu = {"value": float(ce) * n * T / wall / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"recording 0: {len(ci)} channels x {cb} blocks (oracle K-tap restatement, "
-                         f"{wall:.2f} s wall)"}
+               "sample": f"recordings 0-{R - 1}: {nci} channels x {cb} blocks (oracle K-tap "
+                         f"restatement, {wall:.2f} s wall)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -509,6 +526,7 @@ def run_batch(args, rank, world, local, dist, emit=True):
         "data": "synthetic (seeded per recording, paper_1907_00463_b200/simsource.py; loops start from truth)",
         "config": {"workload": BATCH["desc"], "recordings": n_rec_total, "channels": C_ch * world,
                    "taps_counted": T, "samples_per_block": n, "blocks_per_step": blocks,
+                   "blocks_requested": want_blocks,
                    "chunk_blocks": chunk_b, "cta_mode": args.cta,
                    "parallelism": f"strong: {n_rec_total} recordings over {world} rank(s)",
                    "l2": "inputs larger than L2 (raw %.1f GB + baseband ring %.1f GB per rank)" % (
@@ -535,6 +553,57 @@ def run_batch(args, rank, world, local, dist, emit=True):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    return line
+
+
+def run_batch_reference(args, rank):
+    """`--impl reference` for config 4: the reference's K-tap tracking path
+    (oracle port: the reference's builder has no multi-tap batch driver to
+    compile standalone) on every host thread, over a bounded sample of the
+    workload — the first 8 recordings x 250 blocks per step, same scenarios
+    and seeds as the GPU arm."""
+    import torch
+    from paper_1907_00463_b200 import abi, simsource as ss
+    import oracle
+    if rank != 0:
+        return None
+    c = CONFIGS[4]
+    fs, n = c["fs"], int(round(c["fs"] / 1000))
+    per_step = min(args.blocks or 250, 250)
+    R = 8
+    taps = make_taps("wide7")
+    cfg = abi.TrackingCfg.default()
+    cfg.lock_fail_limit = 2**31 - 1
+    T = taps.n_counted
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    xs, inits, cstream = [], [], []
+    for r in range(R):
+        _, svs, chans = scenario(4, c["seed"] + r)
+        raw = ss.synth(per_step, fs, svs, fmt="int16_iq", seed=c["seed"] + r, device=dev)
+        xs.append(oracle.ingest(raw.cpu().numpy(), abi.FMT_INT16_IQ, fs))
+        ci = channel_inits(chans, fs)
+        inits += ci
+        cstream += [r] * len(ci)
+    threads = os.cpu_count() or 1
+    walls, ces = [], []
+    for step in range(args.warmup + args.steps):
+        wall, ce = cpu_port_run(xs, inits, cfg, taps, fs, per_step, threads, chan_stream=cstream)
+        if step >= args.warmup:
+            walls.append(wall)
+            ces.append(ce)
+    w = statistics.mean(walls)
+    v = statistics.mean(ces) * n * T / w / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": BATCH["desc"], "sample_recordings": R,
+                                            "sample_blocks_per_step": per_step,
+                                            "parallelism": f"{threads} host threads"},
+            "realtime_channels": statistics.mean(ces) / w / 1000.0,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{R} recordings ({len(inits)} channels) x {per_step} blocks per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
     return line
 
 
@@ -593,6 +662,8 @@ def main():
         return run_grid(args, rank, world, local, dist)
     if args.config == 4 and args.impl == "gpu":
         return run_batch(args, rank, world, local, dist)
+    if args.config == 4:
+        return run_batch_reference(args, rank)
     c, svs, chans = scenario(args.config, CONFIGS[args.config]["seed"] + rank)
     blocks = args.blocks or c["blocks"]
     fs = c["fs"]
