@@ -103,6 +103,16 @@ def scenario(cfg_id, seed):
     return c, svs, chans
 
 
+def stream_manifest(raw_row, seed, svs, fmt):
+    """Manifest of a synthetic stream: seed, signal parameters and
+    the SHA-256 of its raw bytes (the CPU checker consumes the same bytes)."""
+    import hashlib
+    h = hashlib.sha256(raw_row.cpu().numpy().tobytes()).hexdigest()
+    return {"seed": int(seed), "fmt": fmt, "bytes": int(raw_row.numel()), "sha256": h,
+            "svs": [{"prn": sv.prn, "cn0_dbhz": round(sv.cn0_dbhz, 3), "doppler_hz": round(sv.doppler_hz, 3),
+                     "delay_chips": round(sv.delay_chips, 4)} for sv in svs]}
+
+
 def channel_inits(chans, fs, lock_fail_limit_inf=True):
     from paper_1907_00463_b200 import simsource as ss
     from paper_1907_00463_b200.tracking import init_channel_from_acquisition
@@ -394,6 +404,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
     torch.cuda.synchronize()
     t_syn = time.perf_counter() - t_syn
     C_ch = len(inits)
+    manifest0 = stream_manifest(raw[0], c["seed"] + recs[0], scenario(4, c["seed"] + recs[0])[1],
+                                "int16_iq") if len(recs) else None
     ctx = Context(local)
     trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs),
                   taps=taps, cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks,
@@ -447,6 +459,16 @@ def run_batch(args, rank, world, local, dist, emit=True):
     sample_taps_all = epochs_all * n * T
     value = sample_taps_all / (ms_per_step * 1e-3) / 1e9
 
+    # ---- end-of-run gather of the records to rank 0, untimed
+    gathered = None
+    if dist:
+        from paper_1907_00463_b200.shard import gather_bytes
+        rec_t = torch.empty(trk.records_nbytes(), dtype=torch.uint8, device=dev)
+        trk.records_raw(dst_ptr=rec_t.data_ptr(), device=True)
+        outs = gather_bytes(rec_t, dist, dst=0)
+        gathered = sum(int(o.numel()) for o in outs) if rank == 0 else None
+        del rec_t, outs
+
     # ---- e2e: the same step from pinned host memory (strided pushes)
     e2e = None
     try:
@@ -462,7 +484,7 @@ def run_batch(args, rank, world, local, dist, emit=True):
         pinned = ctx.host_alloc(len(recs) * eb).reshape(len(recs), eb)
         for j in range(len(recs)):  # row by row: a strided slice would stage a device copy
             pinned[j] = raw[j, :eb].cpu().numpy()
-        rec_bytes = trk.records_raw(dst_ptr=None, device=False).nbytes
+        rec_bytes = trk.records_nbytes()
 
         def step_e2e():
             trk.reset(inits)
@@ -510,8 +532,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
     if world == 1 and not args.no_cpu_baseline:
         import oracle
         threads = os.cpu_count() or 1
-        cb = min(args.cpu_blocks, blocks, 500)
-        R = min(8, len(recs))  # enough channels to keep every host thread busy
+        cb = min(args.cpu_blocks, blocks, 1000)
+        R = min(8, len(recs))  # >= 8 recordings x 1000 blocks, scaled linearly
         xs = [oracle.ingest(raw[j, : cb * n * 4].cpu().numpy(), abi.FMT_INT16_IQ, fs) for j in range(R)]
         nci = sum(1 for s_ in cstream if s_ < R)
         wall, ce = cpu_port_run(xs, inits[:nci], cfg, taps, fs, cb, threads, chan_stream=cstream[:nci])
@@ -532,6 +554,7 @@ def run_batch(args, rank, world, local, dist, emit=True):
                    "l2": "inputs larger than L2 (raw %.1f GB + baseband ring %.1f GB per rank)" % (
                        raw.numel() / 1e9, len(recs) * (chunk_b + 5) * n * 8 / 1e9),
                    "synth_s": round(t_syn, 1),
+                   "manifest_recording0": manifest0,
                    "lock_fail_limit": "INT_MAX (every channel computes every epoch)"},
         "realtime_channels": epochs_all / (ms_per_step * 1e-3) / 1000.0,
         "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
@@ -548,6 +571,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
                                      "read once; its 12 channels share it through L2)"}},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
     }
+    if gathered is not None:
+        line["records_gathered_bytes"] = gathered
     if not emit:
         return line
     print(json.dumps(line), flush=True)
@@ -560,8 +585,8 @@ def run_batch_reference(args, rank):
     """`--impl reference` for config 4: the reference's K-tap tracking path
     (oracle port: the reference's builder has no multi-tap batch driver to
     compile standalone) on every host thread, over a bounded sample of the
-    workload — the first 8 recordings x 250 blocks per step, same scenarios
-    and seeds as the GPU arm."""
+    workload — the first 8 recordings x 1000 blocks per step,
+    same scenarios and seeds as the GPU arm."""
     import torch
     from paper_1907_00463_b200 import abi, simsource as ss
     import oracle
@@ -569,7 +594,7 @@ def run_batch_reference(args, rank):
         return None
     c = CONFIGS[4]
     fs, n = c["fs"], int(round(c["fs"] / 1000))
-    per_step = min(args.blocks or 250, 250)
+    per_step = min(args.blocks or 1000, 1000)
     R = 8
     taps = make_taps("wide7")
     cfg = abi.TrackingCfg.default()
@@ -775,7 +800,7 @@ def main():
     bps = abi.BYTES_PER_SAMPLE[fmt]
     chunk = args.e2e_chunk_ms * n * bps
     rec_host = None
-    rec_bytes = trk.records_raw(dst_ptr=None, device=False).nbytes
+    rec_bytes = trk.records_nbytes()
 
     def step_e2e():
         trk.reset(inits)
@@ -874,7 +899,8 @@ def main():
                    "samples_per_block": n, "parallelism": f"weak: {world} rank(s) x own recording",
                    "l2": "inputs larger than L2 (raw %.0f MB + baseband ring %.2f GB per step)" % (
                        nbytes / 1e6, blocks * n * 8 / 1e9),
-                   "lock_fail_limit": "INT_MAX (every channel computes every epoch)"},
+                   "lock_fail_limit": "INT_MAX (every channel computes every epoch)",
+                   "manifest": stream_manifest(raw, c["seed"] + rank, svs, c["fmt"])},
         "realtime_channels": world * float(counts.sum()) / (ms_per_step * 1e-3) / 1000.0,
         # the per-epoch critical path of a channel (track launch time / epochs),
         # the latency view SURVEY 8d asks for on the sequential configs

@@ -310,6 +310,12 @@ class Tracker:
             sums.ctypes.data_as(_dp) if tap_sums else None))
         return (recs, sums) if tap_sums else recs
 
+    def records_nbytes(self) -> int:
+        """Bytes `records_raw` writes (every channel x max_records)."""
+        nb = C.c_int64()
+        check(self._lib.l1rxg_tracker_records_raw(self.handle, None, 0, C.byref(nb)))
+        return nb.value
+
     def records_raw(self, dst_ptr: int | None = None, device: bool = False):
         nb = C.c_int64()
         check(self._lib.l1rxg_tracker_records_raw(self.handle, None, 0, C.byref(nb)))
