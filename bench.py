@@ -409,7 +409,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
     ctx = Context(local)
     trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs),
                   taps=taps, cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks,
-                  cta_mode=abi.CTA_THROUGHPUT if args.cta != "latency" else abi.CTA_LATENCY,
+                  cta_mode={"segment": abi.CTA_SEGMENT, "throughput": abi.CTA_THROUGHPUT,
+                            "latency": abi.CTA_LATENCY}[args.cta],
                   ring_raw=args.ring_raw)
     stream = torch.cuda.ExternalStream(trk.cuda_stream(), device=dev)
     chunk = chunk_b * n * 4
@@ -667,7 +668,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="config 4: skip the host-memory e2e leg")
     ap.add_argument("--e2e-chunk-ms", type=int, default=1000)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
-    ap.add_argument("--cta", default="throughput", choices=["throughput", "latency"])
+    ap.add_argument("--cta", default="throughput", choices=["segment", "throughput", "latency"],
+                    help="config 4 CTA shape: segment correlator (raw cint16 ring), throughput, latency")
     ap.add_argument("--ring-raw", action="store_true", help="config 4: keep cint16 raw in the rings")
     ap.add_argument("--no-companion", dest="companion", action="store_false",
                     help="config 2: skip the config-4 throughput companion measurement")

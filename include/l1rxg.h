@@ -242,7 +242,13 @@ typedef struct {
      * is what matters; L1RXG_CTA_SINGLE: the latency shape with one CTA per
      * channel; L1RXG_CTA_THROUGHPUT: narrow CTAs, four resident per SM, so
      * one channel's serial loop update overlaps the others' correlation
-     * (many channels).  Auto picks throughput when n_channels >= 2 x SMs. */
+     * (many channels).  Auto picks throughput when n_channels >= 2 x SMs.
+     * L1RXG_CTA_SEGMENT: the throughput shape's segment correlator over a
+     * raw complex-int16 ring (no decode pass; per-warp TMA tensor copies;
+     * the run sums captured in registers instead of a shared-memory prefix
+     * tile); complex int16 only, fs >= 4.096 MHz.  Auto picks it for the
+     * throughput shape on complex int16 recordings whose chips span > 33
+     * samples with tap residues > 15.5 samples apart (BASELINE config 4). */
     int32_t cta_mode;
     /* Latency shape: CTAs per channel cluster (0 = auto, 1..16). */
     int32_t cluster_size;
@@ -257,6 +263,7 @@ typedef struct {
 #define L1RXG_CTA_LATENCY 1
 #define L1RXG_CTA_THROUGHPUT 2
 #define L1RXG_CTA_SINGLE 3
+#define L1RXG_CTA_SEGMENT 4
 
 int l1rxg_tracker_create(l1rxg_ctx* ctx, const l1rxg_tracker_desc* desc,
                          const l1rxg_channel* channels,

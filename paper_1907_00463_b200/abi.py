@@ -19,7 +19,7 @@ OK, EINVAL, ELOGIC, ERANGE, ECUDA, ENOMEM = range(6)
 KERNEL_SCALAR, KERNEL_BATCHED, KERNEL_NOOP = 0, 1, 2          # tracking.hpp:60
 FMT_INT8_IQ, FMT_INT16_IQ, FMT_INT8_REAL_IF, FMT_CF64 = 0, 1, 2, 3  # samples.hpp:22-26
 IDLE, ACQUIRED, TRACKING = 0, 1, 2                             # tracking.hpp:59
-CTA_AUTO, CTA_LATENCY, CTA_THROUGHPUT, CTA_SINGLE = 0, 1, 2, 3
+CTA_AUTO, CTA_LATENCY, CTA_THROUGHPUT, CTA_SINGLE, CTA_SEGMENT = 0, 1, 2, 3, 4
 
 BYTES_PER_SAMPLE = {FMT_INT8_IQ: 2, FMT_INT16_IQ: 4, FMT_INT8_REAL_IF: 1}  # samples.hpp:33-40
 

@@ -997,8 +997,8 @@ __device__ __forceinline__ void nco_advance_lanes(double& ph1, double& cp1, cons
 
 // Control-warp side of an epoch: run state, quality metrics and lock-fail
 // rule for the epoch handed over in s->rec, then its record and tap sums.
-template <int T>
-__device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a, int lane,
+template <int T, typename S>
+__device__ __forceinline__ void finish_epoch(S* s, const TrackArgs& a, int lane,
                                              bool writer) {
     if (lane == 0) {
         l1rxg_channel& ch = s->ch;
@@ -1044,8 +1044,8 @@ __device__ __forceinline__ void finish_epoch(CorrSmem<T>* s, const TrackArgs& a,
 // Lane 0 then runs loop_fast and forms the next epoch's w and cps as IEEE
 // quotients (:234-236).  Loop values agree with the reference to ~1e-15
 // relative (the parity bar is 1e-5); the state advance is bit-exact.
-template <int T>
-__device__ __forceinline__ void warp0_update(CorrSmem<T>* s, const TrackArgs& a, const EpochConsts& c,
+template <int T, typename S>
+__device__ __forceinline__ void warp0_update(S* s, const TrackArgs& a, const EpochConsts& c,
                                              int64_t off, int cidx, int64_t done, int nwork_warps,
                                              int lane, int crank, int ep, double* xs, int rec_i) {
     constexpr int V = 2 * T + 2;

@@ -21,6 +21,7 @@
 #include "correlator.cuh"
 #include "ingest.cuh"
 #include "search.cuh"
+#include "segcorr.cuh"
 #include "l1rxg.h"
 
 using namespace l1rxg;
@@ -214,6 +215,18 @@ int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
                  : launch_track_thr<T, false>(a, n_ch, nt, s, sk);
 }
 
+// Segment correlator: one CTA per channel, four per SM.
+template <int T>
+int launch_seg(const SegArgs& sa, int n_ch, cudaStream_t s) {
+    const size_t sm = seg_smem_bytes<T>(sa.t.n);
+    CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    track_seg_kernel<T><<<n_ch, SEG_NT, sm, s>>>(sa);
+    CK(cudaGetLastError());
+    return 0;
+}
+
 template <int T>
 int launch_jobs(const JobArgs& a, int n_jobs, int nt, cudaStream_t s) {
     const size_t sm = smem_bytes<T>(nt, 1, 8);
@@ -234,6 +247,61 @@ int launch_jobs(const JobArgs& a, int n_jobs, int nt, cudaStream_t s) {
     case 16: return FN<16>(__VA_ARGS__);   \
     default: return set_err(L1RXG_EINVAL, "unsupported tap count"); \
     }
+
+// Segment correlator fast-path geometry (track_seg_kernel is exact for any
+// geometry; outside this one most runs would take its per-sample slow
+// path): a chip spans more than 33 samples (at most one replica step per
+// tap in a 32-sample run) and distinct tap residues (offsets mod 1 chip)
+// are more than 15.5 samples apart (one dynamic capture per half-run).
+bool seg_geometry_ok(const l1rxg_tracker_desc* d) {
+    const double spc = d->sample_rate_hz / CHIP_RATE_HZ;
+    if (spc <= 33.0)
+        return false;
+    std::vector<double> r;
+    for (int k = 0; k < d->taps.n_taps; ++k)
+        r.push_back(d->taps.offsets_chips[k] - std::floor(d->taps.offsets_chips[k]));
+    std::sort(r.begin(), r.end());
+    std::vector<double> u;
+    for (double x : r)
+        if (u.empty() || x - u.back() > 1e-9)
+            u.push_back(x);
+    if (u.size() > 1 && 1.0 + u.front() - u.back() < 1e-9)
+        u.pop_back();  // 0 and 1 - eps are one residue
+    double gap = 1.0;
+    for (size_t k = 0; k < u.size(); ++k)
+        gap = std::min(gap, (k + 1 < u.size() ? u[k + 1] : 1.0 + u[0]) - u[k]);
+    return gap * spc > 15.5;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The seg ring ([stream][R + apron] cint16) as a 3-D tensor of u32 samples:
+// {32 samples, rows of the stream, streams}, box 32 x 32 rows x 1, 128B swizzle.
+int encode_ring_map(CUtensorMap* map, void* ring, int64_t stride_samples, int n_streams) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            return set_err(L1RXG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(stride_samples / 32), static_cast<cuuint64_t>(n_streams)};
+    cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(stride_samples) * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, ring, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return set_err(L1RXG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
 
 int validate_taps(const l1rxg_taps* t) {
     if (!t || t->n_taps < 1 || t->n_taps > L1RXG_MAX_TAPS)
@@ -324,6 +392,8 @@ struct l1rxg_tracker {
     int nbuf = 1;
     int csize = 1;   // CTAs per channel (cluster) in the latency shape
     int thr = 0;     // throughput shape
+    int seg = 0;     // segment correlator (track_seg_kernel) over a raw cint16 ring
+    CUtensorMap tmap{};  // seg: the ring as [stream][row][32 samples] for TMA tensor copies
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
     int esz = 8;     // ring element bytes (ring_esz)
@@ -655,7 +725,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return rc;
     if (int rc = validate_cfg(&d->cfg))
         return rc;
-    if (d->cta_mode < L1RXG_CTA_AUTO || d->cta_mode > L1RXG_CTA_SINGLE)
+    if (d->cta_mode < L1RXG_CTA_AUTO || d->cta_mode > L1RXG_CTA_SEGMENT)
         return set_err(L1RXG_EINVAL, "unknown cta_mode");
     if (d->cluster_size < 0 || d->cluster_size > 16 || (d->ring_raw != 0 && d->ring_raw != 1))
         return set_err(L1RXG_EINVAL, "cluster_size must be in 0..16, ring_raw 0 or 1");
@@ -666,6 +736,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return set_err(L1RXG_EINVAL, "ring_samples must hold at least two epochs");
     if (n > MAXSUB * (MAX_NT - 32) * RUN)
         return set_err(L1RXG_EINVAL, "epoch longer than the correlator supports (fs <= 150 MHz)");
+    if (d->cta_mode == L1RXG_CTA_SEGMENT && (d->format != L1RXG_FMT_INT16_IQ || n < SEG_MIN_N))
+        return set_err(L1RXG_EINVAL, "the segment correlator takes complex int16 at fs >= 4.096 MHz");
     for (int k = 0; k < d->n_channels; ++k) {
         if (chan_stream[k] < 0 || chan_stream[k] >= d->n_streams)
             return set_err(L1RXG_EINVAL, "channel bound to a missing stream");
@@ -688,13 +760,24 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
         const bool thr = d->cta_mode == L1RXG_CTA_THROUGHPUT ||
                          (d->cta_mode == L1RXG_CTA_AUTO && d->n_channels >= 2 * nsm);
+        // segment correlator: on request, or for the auto throughput shape on
+        // complex int16 recordings where its fast path is the common case
+        static const char* ev_seg = std::getenv("L1RXG_SEG");
+        const bool seg = d->cta_mode == L1RXG_CTA_SEGMENT ||
+                         (d->cta_mode == L1RXG_CTA_AUTO && thr && d->format == L1RXG_FMT_INT16_IQ &&
+                          n >= SEG_MIN_N && seg_geometry_ok(d) && !(ev_seg && ev_seg[0] == '0'));
         // latency: up to 19 correlation warps + the control warp, one CTA
         // per SM, one tile (the copy overlaps the loop update).
         // throughput: 5 correlation warps + the control warp and two tiles
         // (copy of unit u+2 overlaps unit u+1), ~110 KB of shared memory ->
         // two CTAs per SM, so one CTA's serial loop update overlaps the
         // other's correlation
-        if (thr) {
+        if (seg) {
+            t->seg = 1;
+            t->thr = 1;
+            t->nt = SEG_NT;
+            t->nbuf = SEG_NBUF;
+        } else if (thr) {
             static const char* ev_nw = std::getenv("L1RXG_THR_NWORK");
             static const char* ev_nb = std::getenv("L1RXG_THR_NBUF");
             // 128 correlation threads (float2 ring: ~51 KB) or 96 (raw samples
@@ -736,9 +819,15 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     }
     t->R = d->ring_samples;
     t->esz = ring_esz(d->format, d->ring_raw);
-    // apron >= one epoch (+ bulk-copy slack); R + apron a multiple of the
-    // samples per 16 bytes keeps every stream's ring 16-byte aligned for TMA
-    {
+    if (t->seg) {
+        // raw cint16 in rows of 32 samples: R and the apron whole rows; the
+        // apron covers an epoch plus the last unit's row overhang
+        t->esz = 4;
+        t->R = (t->R + 31) / 32 * 32;
+        t->apron = (n + 2048 + 31) / 32 * 32;
+    } else {
+        // apron >= one epoch (+ bulk-copy slack); R + apron a multiple of the
+        // samples per 16 bytes keeps every stream's ring 16-byte aligned for TMA
         const int64_t A = 16 / t->esz;
         t->apron = n + 64;
         t->apron += (A - (t->R + t->apron) % A) % A;
@@ -756,6 +845,13 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return fail(e);
     for (size_t k = 0; k < t->streams.size(); ++k)
         t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride * t->esz;
+    if (t->seg) {
+        if (int rc = encode_ring_map(&t->tmap, t->d_ring, stride, d->n_streams)) {
+            const std::string msg = g_err;
+            l1rxg_tracker_destroy(t);
+            return set_err(rc, msg);
+        }
+    }
     for (auto& r : t->streams) {
         for (int k = 0; k < 2; ++k) {
             if ((e = cudaMalloc(&r.hist8[k], 32)) != cudaSuccess ||
@@ -1013,7 +1109,15 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     }
     a.prof = dprof;
     const int sk = t->esz == 4 ? SK_I16 : t->esz == 2 ? SK_I8 : SK_F32;
-    auto go = [&]() -> int { DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st, sk); };
+    SegArgs sa;
+    auto go = [&]() -> int {
+        if (t->seg) {
+            sa.t = a;
+            sa.tmap = t->tmap;
+            DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
+        }
+        DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st, sk);
+    };
     if (int rc = go())
         return rc;
     t->launches += 1;

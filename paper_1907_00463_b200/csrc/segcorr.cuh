@@ -1,0 +1,547 @@
+// segcorr.cuh -- the segment correlator: throughput-shape tracking kernel
+// over raw complex-int16 rings (sm_100a).
+//
+// Same contract as track_kernel (correlator.cuh; reference
+// tracking.hpp:226-282 correlate + :520-618 track_epoch), a different
+// schedule for the many-channel case (BASELINE config 4):
+//
+//   * the ring keeps the recording's raw cint16 samples (4 B, no decode
+//     pass: the K1 ingest is fused into the correlator) in rows of 32
+//     samples (128 B), and each work warp pulls its own 32-row units by TMA
+//     TENSOR copies with the 128-byte swizzle, double-buffered per warp (no
+//     CTA barrier per unit);
+//   * lane l owns row l of a unit: a ring-aligned run of 32 consecutive
+//     samples, read as eight conflict-free LDS.128 (the swizzle puts the 8
+//     lanes of a quarter-warp on 8 different bank groups);
+//   * carrier wipe as in track_kernel (per-epoch rotator table e^{-jwj} +
+//     a per-run fp64-anchored phasor) with four FFMAs per sample into the
+//     run's running sum P, but NO prefix tile: a tap's replica changes at
+//     most once inside a run when a chip spans > 32 samples, and the steps
+//     of all taps inside one half-run share one position when the taps'
+//     residues are > 15 samples apart (config 4: 64 samples per chip,
+//     0.25-chip grid), so P is captured in REGISTERS at the static midpoint
+//     and at one dynamic position per half, and tap k's run sum is
+//         chip_end * P(32) + (chip_start - chip_end) * P(q_k);
+//   * every step position q_k is the reference's exact fp64 chip decision
+//     (tap_boundary: estimate + exact check), and whatever does not fit the
+//     register captures (ties between taps of one residue, more than one
+//     step per run at low sample rates, the run holding the n/2 split of
+//     the half-epoch prompt) takes an exact per-sample slow path over the
+//     same shared-memory row -- correct for every geometry, fast for the
+//     one it is chosen for.
+//
+// Per-epoch critical path, control warp and records: identical to the
+// throughput shape of track_kernel (warp0_update, finish_epoch, loop_fast,
+// loop_metrics are shared).
+#pragma once
+
+#include <cuda.h>  // CUtensorMap (the map itself is encoded on the host)
+
+#include <type_traits>
+
+#include "correlator.cuh"
+
+namespace l1rxg {
+
+constexpr int SEG_NW = 4;                    // work warps per CTA
+constexpr int SEG_NT = 32 * (SEG_NW + 1);    // + the control warp
+constexpr int SEG_NBUF = 2;                  // TMA buffers per work warp
+constexpr int SEG_UNIT_BYTES = 32 * 128;     // 32 rows x 32 cint16 samples
+constexpr int SEG_MIN_N = 32 * 32 * SEG_NW;  // every work warp has >= 1 unit per epoch
+
+struct __align__(64) SegArgs {
+    TrackArgs t;
+    CUtensorMap tmap;  // ring as [stream][row][32 x u32], SWIZZLE_128B, box 32 x 32 x 1
+};
+
+// chipx[m]: bit 0 = chip[m] > 0, bit 1 = chip[m+1] != chip[m]
+template <int T>
+struct SegSmem {
+    l1rxg_channel ch;
+    EpochConsts c;
+    double d[T];
+    double sums[2 * T + 2];
+    float red[SEG_NW * (2 * T + 2)];
+    __align__(16) float2 rot[32];
+    uint64_t fbar[SEG_NW][SEG_NBUF];  // per work warp: its unit buffers' TMA completion
+    uint64_t pbar[2];                 // (cluster exchange: unused, csize == 1)
+    l1rxg_epoch_record rec;
+    int64_t rec_slot;
+    int64_t rec_esh;
+    double rec_eenv;
+    int pending, stop;
+    double nco_ph1, nco_cp1;
+    int8_t chipx[CHIP_EXT];  // bit 0: chip[m] > 0, bit 1: chip[m+1] != chip[m]
+    int16_t tm[TRANS_EXT];   // chip index of the g-th chip transition (as CodeTables)
+    int16_t cum[1024];       // transitions at indices <= r within one period
+    int L;                   // transitions per period
+};
+
+// Per-epoch step table, one entry per 32-sample run of the epoch (runs
+// counted from the ring row holding the epoch's first sample):
+//   bits [0,5)  q0: the first-half capture position (1..15; 0 = none)
+//   bits [5,10) q1: the second-half capture position (17..31; 0 = none)
+//   bits 10+2k..: tap k's step in the run: 0 none, 1 at 16, 2 at q0, 3 at q1
+//   bit 10+2T+k: tap k takes the exact slow path in this run
+template <int T>
+struct SegEntry {
+    typedef typename std::conditional<(3 * T + 10 <= 32), uint32_t, unsigned long long>::type type;
+};
+// runs per epoch table: every row a unit of the epoch can cover
+__host__ __device__ constexpr int seg_table_runs(int n) { return (((n + 62) >> 5) + 31) / 32 * 32; }
+
+template <int T>
+__host__ __device__ constexpr size_t seg_smem_bytes(int n) {
+    // header, step table, then up to 1 KB of padding to the 1024-B aligned unit buffers
+    return ((sizeof(SegSmem<T>) + 15) & ~size_t(15)) +
+           ((static_cast<size_t>(seg_table_runs(n)) * sizeof(typename SegEntry<T>::type) + 15) & ~size_t(15)) +
+           1024 + static_cast<size_t>(SEG_NW) * SEG_NBUF * SEG_UNIT_BYTES;
+}
+
+// 3-D tensor TMA: box {32 u32, 32 rows, 1 stream} at (0, row, stream).
+__device__ __forceinline__ void tma_load_rows(uint32_t dst, const CUtensorMap* map, int row, int strm,
+                                              uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(strm), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// floor(v) for 0 <= v < 2^31: v + 1.5 * 2^52 rounded down leaves floor(v)
+// in the low word (one DADD, no F2I).  With v = fl(fma(i, cps, base) + d)
+// this is the reference's trunc((int64)(ph + d)) chip index exactly.
+__device__ __forceinline__ int floor_idx(double v) {
+    return __double2loint(__dadd_rd(v, 6755399441055744.0));
+}
+
+// cint16 word -> (re, im) * 65536 exactly (full-rate I2FP; the 2^-16 and
+// the format's 1/32768 are folded into the rotator table, exact powers of two)
+__device__ __forceinline__ float seg_re(uint32_t w) { return (float)(int)(w << 16); }
+__device__ __forceinline__ float seg_im(uint32_t w) { return (float)(int)(w & 0xffff0000u); }
+
+// Sample j of the run in row `row` of a 128B-swizzled unit buffer.
+__device__ __forceinline__ uint32_t seg_sample(const unsigned char* buf, int row, int j) {
+    return *reinterpret_cast<const uint32_t*>(buf + row * 128 + ((((j >> 2) ^ row) & 7) << 4) + ((j & 3) << 2));
+}
+
+// Exact per-sample slow path: sum over j in [jlo, jhi) of
+// chip[idx(i0 + j, d)] * x_j * conj(rot_j) (un-anchored), the reference's
+// chip decision per sample.
+__device__ __noinline__ float2 seg_slow_sum(const unsigned char* buf, int row, const float2* rot,
+                                            const int8_t* chipx, double d, int i0, int jlo, int jhi,
+                                            double cps, double base) {
+    float sr = 0.f, si = 0.f;
+    for (int j = jlo; j < jhi; ++j) {
+        const uint32_t w = seg_sample(buf, row, j);
+        const float xr = seg_re(w), xi = seg_im(w);
+        const float2 q = rot[j];
+        const float yr = fmaf(xi, q.y, xr * q.x);
+        const float yi = fmaf(-xr, q.y, xi * q.x);
+        const int m = floor_idx(__dadd_rn(__fma_rn((double)(i0 + j), cps, base), d));
+        const float ch = (chipx[m] & 1) ? 1.f : -1.f;
+        sr = fmaf(ch, yr, sr);
+        si = fmaf(ch, yi, si);
+    }
+    return make_float2(sr, si);
+}
+
+// One run (32 samples of row `lane`), fast path: running sum with the
+// captures P(16) (static), P(q0) for q0 in [1, 16), P(q1) for q1 in (16, 32).
+// MASK: samples outside [jlo, jhi) (epoch edges) count as zero.
+template <bool MASK>
+__device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, const float4* rot4, int q0,
+                                        int q1, int jlo, int jhi, float2& p16, float2& c0, float2& c1,
+                                        float2& tot) {
+    const unsigned char* rowp = buf + lane * 128;
+    const int sw = lane & 7;
+    float pr = 0.f, pi = 0.f;
+    float c0r = 0.f, c0i = 0.f, c1r = 0.f, c1i = 0.f, hr = 0.f, hi = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(rowp + ((ch ^ sw) << 4));
+        const float4 ra = rot4[2 * ch], rb = rot4[2 * ch + 1];
+        const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+        const float rc[4] = {ra.x, ra.z, rb.x, rb.z};
+        const float rs[4] = {ra.y, ra.w, rb.y, rb.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = 4 * ch + t;
+            uint32_t x = ws[t];
+            if (MASK)
+                x = (j >= jlo && j < jhi) ? x : 0u;
+            if (j == 16) {
+                hr = pr;
+                hi = pi;
+            } else if (j < 16) {
+                if (j == q0) {
+                    c0r = pr;
+                    c0i = pi;
+                }
+            } else {
+                if (j == q1) {
+                    c1r = pr;
+                    c1i = pi;
+                }
+            }
+            const float xr = seg_re(x), xi = seg_im(x);
+            pr = fmaf(xi, rs[t], fmaf(xr, rc[t], pr));
+            pi = fmaf(-xr, rs[t], fmaf(xi, rc[t], pi));
+        }
+    }
+    p16 = make_float2(hr, hi);
+    c0 = make_float2(c0r, c0i);
+    c1 = make_float2(c1r, c1i);
+    tot = make_float2(pr, pi);
+}
+
+// anchored value z * conj(anchor), anchor = (cos, sin) of theta(i0)
+__device__ __forceinline__ float2 seg_anchor(float2 z, float ca, float sa) {
+    return make_float2(fmaf(z.x, ca, z.y * sa), fmaf(z.y, ca, -(z.x * sa)));
+}
+
+// Step table fill for one epoch (the work threads, after the loop update):
+// every chip transition m of every tap with its step inside the epoch,
+// located exactly (tap_boundary), entered in the run holding it.  A step at
+// a run's first sample needs no entry (the run's start chip has it).  Two
+// positions competing for one half's capture, or two steps of one tap in
+// one run, send that tap to the slow path for that run.
+template <int T>
+__device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
+    const int p = m / 1023;
+    return p * s->L + s->cum[m - p * 1023];
+}
+
+// Step table fill for one epoch (the work threads, after the loop update):
+// every chip transition m of every tap with its step inside the epoch,
+// located exactly (tap_boundary), entered in the run holding it.  A step at
+// a run's first sample needs no entry (the run's start chip has it).  Two
+// positions competing for one half's capture, or two steps of one tap in
+// one run, send that tap to the slow path for that run.
+template <int T>
+__device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const SegSmem<T>* s,
+                                        const EpochConsts& c, int lead, int tid, int nthr) {
+    typedef typename SegEntry<T>::type E;
+    const int n = c.n;
+#pragma unroll 1
+    for (int k = 0; k < T; ++k) {
+        const double dk = s->d[k];
+        // transitions at chip indices in (idx(0), idx(n-1)]
+        const int g0 = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));
+        const int g1 = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk));
+        for (int g = g0 + tid; g < g1; g += nthr) {
+            const int b = tap_boundary(s->tm[g], dk, c, 1, n - 1);
+            const int pos = b + lead;
+            const int r = pos >> 5, q = pos & 31;
+            if (q == 0)
+                continue;
+            E code = 1;
+            if (q != 16) {
+                const int fsh = q < 16 ? 0 : 5;
+                code = q < 16 ? 2 : 3;
+                E old = tab[r];
+                for (;;) {
+                    const int f = (int)((old >> fsh) & 31);
+                    if (f == q)
+                        break;
+                    if (f != 0) {
+                        code = 0;  // this half already captures another position
+                        break;
+                    }
+                    const E prev = atomicCAS(&tab[r], old, old | ((E)q << fsh));
+                    if (prev == old)
+                        break;
+                    old = prev;
+                }
+            }
+            const int sh = 10 + 2 * k;
+            const E slowbit = (E)1 << (10 + 2 * T + k);
+            if (code) {
+                const E prev = atomicOr(&tab[r], code << sh);
+                if ((prev >> sh) & 3)
+                    atomicOr(&tab[r], slowbit);  // a second step of tap k in this run
+            } else {
+                atomicOr(&tab[r], slowbit);
+            }
+        }
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_constant__ SegArgs sa) {
+    typedef typename SegEntry<T>::type E;
+    const TrackArgs& a = sa.t;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SegSmem<T>* s = reinterpret_cast<SegSmem<T>*>(smem_raw);
+    const int n = a.n;
+    const uint32_t sbase = smem_u32(smem_raw);
+    const uint32_t hdr = (uint32_t)((sizeof(SegSmem<T>) + 15) & ~size_t(15));
+    E* tab = reinterpret_cast<E*>(smem_raw + hdr);
+    const int truns = seg_table_runs(n);
+    const uint32_t tend = hdr + (uint32_t)((truns * sizeof(E) + 15) & ~size_t(15));
+    const uint32_t boff = ((sbase + tend + 1023u) & ~1023u) - sbase;  // unit buffers, 1024-B aligned
+    const float4* rot4 = reinterpret_cast<const float4*>(s->rot);
+
+    const int cidx = blockIdx.x;
+    const int strm = a.chan_stream[cidx];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ctl = SEG_NW;  // control warp
+    constexpr int NWT = 32 * SEG_NW;
+    constexpr int V = 2 * T + 2;
+    const int nh = n / 2;
+    const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
+    const int64_t avail = a.avail[strm];
+    const int64_t R = a.ring_cap;  // multiple of 32
+    const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
+    const float scale = 1.f / (32768.f * 65536.f);
+
+    if (tid == 0) {
+        s->ch = a.chans[cidx];
+        for (int w = 0; w < SEG_NW; ++w)
+            for (int b = 0; b < SEG_NBUF; ++b)
+                mbar_init(&s->fbar[w][b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s->pending = 0;
+        s->stop = 0;
+    }
+    for (int k = tid; k < T; k += blockDim.x)
+        s->d[k] = a.taps.offsets_chips[k];
+    for (int r = tid; r < truns; r += blockDim.x)
+        tab[r] = 0;
+    __syncthreads();
+    {
+        const int8_t* cc = a.codes + s->ch.prn * 1023;
+        for (int m = tid; m < CHIP_EXT; m += blockDim.x) {
+            const int8_t c0 = cc[m % 1023], c1 = cc[(m + 1) % 1023];
+            s->chipx[m] = (int8_t)((c0 > 0 ? 1 : 0) | (c0 != c1 ? 2 : 0));
+        }
+        if (warp == SEG_NW) {  // control warp: ballot-scan of the code's transitions
+            int running = 0;
+            for (int base = 0; base < 1023; base += 32) {
+                const int r = base + lane;
+                const bool t = r < 1023 && cc[r] != cc[(r + 1022) % 1023];
+                const unsigned mask = __ballot_sync(0xffffffffu, t);
+                const int before = __popc(mask & ((1u << lane) - 1u));
+                if (r < 1023) {
+                    if (t)
+                        s->tm[running + before] = (int16_t)r;
+                    s->cum[r] = (int16_t)(running + before + (t ? 1 : 0));
+                }
+                running += __popc(mask);
+            }
+            if (lane == 0)
+                s->L = running;
+            __syncwarp();
+            for (int g = running + lane; g < TRANS_EXT; g += 32) {  // later periods
+                const int p = g / running, q = g - p * running;
+                const int m = p * 1023 + s->tm[q];
+                s->tm[g] = (int16_t)(m < 32767 ? m : 32767);
+            }
+        }
+    }
+    if (tid == 0) {
+        const l1rxg_channel& ch = s->ch;
+        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                    ch.carrier_phase_rad, a.lc.fs, n);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        float sn, co;
+        sincosf((float)(s->c.w * (double)tid), &sn, &co);
+        s->rot[tid] = make_float2(co * scale, sn * scale);
+    }
+
+    // ---- per-work-warp unit stream (uniform across the warp's lanes) ----
+    // unit = (epoch ie, warp-unit ik): rows [32 ik, 32 ik + 32) of epoch ie,
+    // rows counted from the ring row holding the epoch's first sample
+    const bool ring_ok = !noop && off0 >= 0 && off0 >= avail - R;
+    int iss_e = 0, iss_k = warp;
+    int64_t iss_pos = ring_ok ? off0 % R : 0;  // ring position of epoch iss_e's first sample
+    int iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+    int64_t issued = 0, consumed = 0;
+    auto issue_one = [&]() -> bool {
+        if (!ring_ok || iss_e >= a.max_epochs || off0 + (int64_t)iss_e * n + n > avail)
+            return false;
+        const int b = (int)(issued % SEG_NBUF);
+        if (lane == 0) {
+            uint64_t* bar = &s->fbar[warp][b];
+            mbar_expect_tx(bar, SEG_UNIT_BYTES);
+            tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
+                          (int)(iss_pos >> 5) + 32 * iss_k, strm, bar);
+        }
+        ++issued;
+        iss_k += SEG_NW;
+        if (iss_k >= iss_nwu) {
+            ++iss_e;
+            iss_k = warp;
+            iss_pos += n;
+            if (iss_pos >= R)
+                iss_pos -= R;
+            iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+        }
+        return true;
+    };
+    if (warp < SEG_NW)
+        while (issued < SEG_NBUF && issue_one()) {
+        }
+    __syncthreads();
+
+    int e = 0;
+    int64_t done = a.ecount[cidx];
+    int rec_i = (int)(done % a.max_records);
+    for (;;) {
+        const int64_t off = s->ch.sample_offset_next_epoch;
+        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
+            break;
+        if (off < avail - R || off < 0) {  // window already overwritten
+            if (tid == 0)
+                a.status[cidx] = 1;
+            break;
+        }
+        EpochConsts c = s->c;
+        if (warp == ctl) {
+            nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
+            if (s->pending) {
+                finish_epoch<T>(s, a, lane, true);
+                if (lane == 0)
+                    s->pending = 0;
+            }
+        }
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[v] = 0.f;
+        if (warp < SEG_NW) {
+            c.inv_cps = fast_rcp(c.cps);
+            const int lead = (int)(off & 31);
+            const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
+            if (!noop) {
+                seg_fill<T>(tab, s, c, lead, tid, NWT);
+                named_bar_sync(1, NWT);
+            }
+            bool snapped = false;
+            float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
+            for (int k = warp; k < nwu && !noop; k += SEG_NW) {
+                const int r = 32 * k + lane;  // the lane's run: epoch run index
+                const int i0 = 32 * r - lead;  // epoch index of its first sample
+                const int jlo = max(0, -i0);
+                const int jhi = max(jlo, min(32, n - i0));
+                const E w = tab[r];
+                tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
+                const uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
+                // start chips of the taps (the reference's chip index at i0)
+                // (the first run of an epoch starts before sample 0: its
+                // start chip is the one at the first sample it counts)
+                const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
+                float cs[T];
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
+                    cs[t] = ((slow >> t) & 1u) ? 0.f : ((s->chipx[ms] & 1) ? 1.f : -1.f);
+                }
+                // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
+                const double th = __fma_rn(c.w, (double)i0, c.phi);
+                const double rr = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
+                float sa_, ca_;
+                __sincosf((float)rr, &sa_, &ca_);
+                // half-epoch prompt: snapshot of the prompt tap before the
+                // first run that reaches past n/2 (a thread's runs ascend)
+                if (!snapped && i0 + 32 > nh) {
+                    snapped = true;
+#pragma unroll
+                    for (int t = 0; t < T; ++t)
+                        if (t == a.kp) {
+                            hr = acc[2 * t];
+                            hi = acc[2 * t + 1];
+                        }
+                }
+                // ---- the unit's samples
+                const int b = (int)(consumed % SEG_NBUF);
+                mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
+                const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
+                float2 p16, pc0, pc1, tot;
+                const int q0 = (int)(w & 31), q1 = (int)((w >> 5) & 31);
+                if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
+                    seg_run<false>(buf, lane, rot4, q0, q1, 0, 32, p16, pc0, pc1, tot);
+                else
+                    seg_run<true>(buf, lane, rot4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
+                // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
+                // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
+                const float2 v0 = seg_anchor(tot, ca_, sa_);
+                const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
+                const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
+                const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int code = (int)(w >> (10 + 2 * t)) & 3;
+                    const float2 lo = (code & 1) ? v1 : v0;
+                    const float2 hi2 = (code & 1) ? v3 : v2;
+                    const float2 v = (code & 2) ? hi2 : lo;
+                    acc[2 * t] = fmaf(cs[t], v.x, acc[2 * t]);
+                    acc[2 * t + 1] = fmaf(cs[t], v.y, acc[2 * t + 1]);
+                }
+                if (slow) {
+#pragma unroll
+                    for (int t = 0; t < T; ++t)
+                        if ((slow >> t) & 1u) {
+                            const float2 z = seg_anchor(
+                                seg_slow_sum(buf, lane, s->rot, s->chipx, s->d[t], i0, jlo, jhi, c.cps, c.base),
+                                ca_, sa_);
+                            acc[2 * t] += z.x;
+                            acc[2 * t + 1] += z.y;
+                        }
+                }
+                if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
+                    const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipx, s->d[a.kp], i0,
+                                                             jlo, max(jlo, min(jhi, nh - i0)), c.cps, c.base),
+                                                ca_, sa_);
+                    hr += z.x;
+                    hi += z.y;
+                }
+                __syncwarp();
+                ++consumed;
+                while (issued < consumed + SEG_NBUF && issue_one()) {
+                }
+            }
+            if (!snapped) {
+#pragma unroll
+                for (int t = 0; t < T; ++t)
+                    if (t == a.kp) {
+                        hr = acc[2 * t];
+                        hi = acc[2 * t + 1];
+                    }
+            }
+            acc[2 * T] = hr;
+            acc[2 * T + 1] = hi;
+            warp_partials<V>(acc, s->red, lane, warp);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            warp0_update<T>(s, a, c, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
+            float sn, co;
+            sincosf((float)(s->c.w * (double)lane), &sn, &co);
+            s->rot[lane] = make_float2(co * scale, sn * scale);
+        }
+        __syncthreads();
+        if (s->stop)
+            break;
+        ++e;
+        ++done;
+        if (++rec_i == a.max_records)
+            rec_i = 0;
+    }
+    __syncthreads();
+    if (warp == ctl && s->pending)
+        finish_epoch<T>(s, a, lane, true);
+    if (warp < SEG_NW) {  // never leave a bulk copy in flight into freed smem
+        for (int64_t u = consumed; u < issued; ++u)
+            mbar_wait(&s->fbar[warp][u % SEG_NBUF], (uint32_t)((u / SEG_NBUF) & 1));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.chans[cidx] = s->ch;
+        a.ecount[cidx] = done;
+    }
+}
+
+}  // namespace l1rxg

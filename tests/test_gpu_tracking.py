@@ -248,12 +248,14 @@ def _batch_scenario(n_rec, fs, ms, seed):
     return np.stack(raws), inits, cstream
 
 
-@pytest.mark.parametrize("ring_raw", [False, True])
-def test_batched_recordings_throughput_mode(ctx, oracle_mod, ring_raw):
+@pytest.mark.parametrize("mode", ["float2", "raw", "segment"])
+def test_batched_recordings_throughput_mode(ctx, oracle_mod, mode):
     """Config 4 shape: recordings pushed in lock step (one strided H2D +
-    one decode launch per chunk), narrow two-per-SM CTAs; per-epoch replay
-    parity for every channel, and the host and device strided pushes give
-    bit-identical records."""
+    one decode launch per chunk), narrow four-per-SM CTAs over float2 or raw
+    cint16 rings, and the segment correlator (raw cint16 ring, per-warp TMA
+    tensor copies, register captures); per-epoch replay parity for every
+    channel, and the host and device strided pushes give bit-identical
+    records."""
     import torch
     fs, ms, nrec = 65.472e6, 36, 4
     n = 65472
@@ -265,7 +267,8 @@ def test_batched_recordings_throughput_mode(ctx, oracle_mod, ring_raw):
     def make():
         return Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=nrec,
                        taps=taps, cfg=cfg, ring_samples=24 * n, max_records=ms,
-                       cta_mode=abi.CTA_THROUGHPUT, ring_raw=ring_raw)
+                       cta_mode=abi.CTA_SEGMENT if mode == "segment" else abi.CTA_THROUGHPUT,
+                       ring_raw=mode == "raw")
     a = make()
     for c0 in range(0, raw.shape[1], chunk):
         a.push_strided(raw[:, c0:c0 + chunk])
@@ -374,3 +377,50 @@ def test_odd_epoch_lengths(ctx, oracle_mod, fs, cta_mode):
     assert len(recs) >= 48
     x = oracle_mod.ingest(raw, abi.FMT_INT8_IQ, fs)
     replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=tsums)
+
+
+@pytest.mark.parametrize("fs,tapset,ms", [(65.472e6, "wideband", 12), (65.472e6, "epl", 12),
+                                          (16.368e6, "monitor", 8), (5.0e6, "epl", 12)])
+def test_segment_correlator_ties_and_slow_paths(ctx, oracle_mod, fs, tapset, ms):
+    """Segment correlator (cta_mode SEGMENT) per-epoch replay parity where
+    its fast path does not apply.  First epoch at exactly commensurate NCO
+    rates (Doppler 0, code rate 1.023 MHz: cps = 1/64 exactly at 65.472 MHz)
+    and a half-chip code phase, so chip boundaries sit on exact fp64 ties;
+    16 samples per chip with the 13-tap 0.1-chip monitor grid and 4.9
+    samples per chip at 5 MHz (n = 5000, a partial last run) drive most runs
+    through the exact per-sample slow path."""
+    n = int(round(fs / 1000))
+    if tapset == "wideband":
+        taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+    elif tapset == "monitor":
+        taps = abi.Taps.make([round(-0.5 + 0.1 * k, 10) for k in range(11)] + [0.25, -0.25],
+                             early=11, prompt=5, late=12, n_counted=11)
+    else:
+        taps = abi.Taps.epl(0.5)
+    svs = [ss.Sv(prn=9, cn0_dbhz=44.0, doppler_hz=0.0, delay_chips=12.5),
+           ss.Sv(prn=17, cn0_dbhz=46.0, doppler_hz=-2750.0, delay_chips=411.3)]
+    raw = _raw(ms + 2, fs, svs, "int16_iq", seed=23)
+    inits = [_init(sv, fs) for sv in svs]
+    assert inits[0].carrier_doppler_hz == 0.0 and inits[0].code_freq_hz == 1.023e6
+    cfg = abi.TrackingCfg.default()
+    trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, ring_samples=(ms + 4) * n, max_records=ms + 4,
+                  taps=taps, cfg=cfg, cta_mode=abi.CTA_SEGMENT)
+    trk.push(0, raw.view(np.int16))
+    trk.run()
+    x = oracle_mod.ingest(raw, abi.FMT_INT16_IQ, fs)
+    for c, init in enumerate(inits):
+        recs, tsums = trk.records(c, tap_sums=True)
+        assert len(recs) >= ms - 2
+        replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=tsums)
+
+
+def test_segment_mode_rejects_other_formats(ctx):
+    """The segment correlator takes complex int16 at fs >= 4.096 MHz only."""
+    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 2.048e6)
+    with pytest.raises(ValueError):
+        Tracker(ctx, abi.FMT_INT8_IQ, 2.048e6, 0.0, [init], ring_samples=8 * 2048,
+                cta_mode=abi.CTA_SEGMENT)
+    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 4.0e6)
+    with pytest.raises(ValueError):
+        Tracker(ctx, abi.FMT_INT16_IQ, 4.0e6, 0.0, [init], ring_samples=8 * 4000,
+                cta_mode=abi.CTA_SEGMENT)
