@@ -415,8 +415,15 @@ def run_batch(args, rank, world, local, dist, emit=True):
     stream = torch.cuda.ExternalStream(trk.cuda_stream(), device=dev)
     chunk = chunk_b * n * 4
 
+    attached = args.cta == "segment"
+    if attached:  # the resident recordings are the rings: no ingest pass, one launch per step
+        trk.attach_device(raw.data_ptr(), bytes_rec // 4, bytes_rec)
+
     def step_device():
         trk.reset(inits)
+        if attached:
+            trk.run()
+            return
         for o in range(0, bytes_rec, chunk):
             trk.push_device_strided(raw.data_ptr() + o, min(chunk, bytes_rec - o), bytes_rec)
             trk.run()
@@ -550,7 +557,10 @@ def run_batch(args, rank, world, local, dist, emit=True):
         "config": {"workload": BATCH["desc"], "recordings": n_rec_total, "channels": C_ch * world,
                    "taps_counted": T, "samples_per_block": n, "blocks_per_step": blocks,
                    "blocks_requested": want_blocks,
-                   "chunk_blocks": chunk_b, "cta_mode": args.cta,
+                   "chunk_blocks": None if attached else chunk_b, "cta_mode": args.cta,
+                   "ingest": ("recordings attached in place (l1rxg_tracker_attach_device): the segment "
+                              "correlator reads the resident cint16 by TMA, no ingest pass" if attached else
+                              "strided device pushes (decode or raw copy into the rings) per chunk"),
                    "parallelism": f"strong: {n_rec_total} recordings over {world} rank(s)",
                    "l2": "inputs larger than L2 (raw %.1f GB + baseband ring %.1f GB per rank)" % (
                        raw.numel() / 1e9, len(recs) * (chunk_b + 5) * n * 8 / 1e9),

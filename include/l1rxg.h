@@ -292,6 +292,16 @@ int l1rxg_tracker_push_strided(l1rxg_tracker* trk, const void* bytes,
 int l1rxg_tracker_push_device_strided(l1rxg_tracker* trk, const void* dev_bytes,
                                       int64_t nbytes_per_stream,
                                       int64_t stride_bytes);
+/* Segment correlator (cta_mode SEGMENT) only: the trackers' rings become
+ * complex-int16 recordings already resident in device memory (stream s at
+ * dev_bytes + s * stride_bytes, samples_per_stream samples each, a multiple
+ * of 32; 16-byte aligned base and stride): every sample is available at
+ * once and no ingest pass runs (the correlator reads the recordings in
+ * place by TMA).  The streams must be empty (fresh or reset); reset keeps
+ * the attachment.  Replaces SampleSource over a file already read
+ * (samples.hpp:136-211) for batch re-processing. */
+int l1rxg_tracker_attach_device(l1rxg_tracker* trk, const void* dev_bytes,
+                                int64_t samples_per_stream, int64_t stride_bytes);
 /* Runs every channel over every epoch whose 1-ms window is fully
  * ingested (at most max_epochs per channel; <0 = unbounded).  Async. */
 int l1rxg_tracker_run(l1rxg_tracker* trk, int max_epochs);

@@ -279,9 +279,10 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// The seg ring ([stream][R + apron] cint16) as a 3-D tensor of u32 samples:
-// {32 samples, rows of the stream, streams}, box 32 x 32 rows x 1, 128B swizzle.
-int encode_ring_map(CUtensorMap* map, void* ring, int64_t stride_samples, int n_streams) {
+// Complex-int16 streams as a 3-D tensor of u32 samples for the segment
+// correlator: {32 samples, rows per stream, streams} (stream s at
+// base + s * stride_bytes), box 32 x 32 rows x 1, 128-byte swizzle.
+int encode_ring_map(CUtensorMap* map, void* ring, int64_t rows, int64_t stride_bytes, int n_streams) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -291,8 +292,8 @@ int encode_ring_map(CUtensorMap* map, void* ring, int64_t stride_samples, int n_
             return set_err(L1RXG_ECUDA, "cuTensorMapEncodeTiled unavailable");
         fn = reinterpret_cast<EncodeTiledFn>(p);
     }
-    cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(stride_samples / 32), static_cast<cuuint64_t>(n_streams)};
-    cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(stride_samples) * 4};
+    cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(n_streams)};
+    cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(stride_bytes)};
     cuuint32_t box[3] = {32, 32, 1};
     cuuint32_t es[3] = {1, 1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, ring, dims, strides, box, es,
@@ -394,6 +395,7 @@ struct l1rxg_tracker {
     int thr = 0;     // throughput shape
     int seg = 0;     // segment correlator (track_seg_kernel) over a raw cint16 ring
     CUtensorMap tmap{};  // seg: the ring as [stream][row][32 samples] for TMA tensor copies
+    int64_t att_samples = 0;  // seg: > 0 while device recordings are attached in place of the ring
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
     int esz = 8;     // ring element bytes (ring_esz)
@@ -846,7 +848,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     for (size_t k = 0; k < t->streams.size(); ++k)
         t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride * t->esz;
     if (t->seg) {
-        if (int rc = encode_ring_map(&t->tmap, t->d_ring, stride, d->n_streams)) {
+        if (int rc = encode_ring_map(&t->tmap, t->d_ring, stride / 32, stride * 4, d->n_streams)) {
             const std::string msg = g_err;
             l1rxg_tracker_destroy(t);
             return set_err(rc, msg);
@@ -1040,6 +1042,35 @@ int l1rxg_tracker_push_strided(l1rxg_tracker* t, const void* bytes, int64_t nbyt
     return 0;
 }
 
+int l1rxg_tracker_attach_device(l1rxg_tracker* t, const void* dev_bytes, int64_t samples_per_stream,
+                                int64_t stride_bytes) {
+    if (!t || !dev_bytes)
+        return set_err(L1RXG_EINVAL, "null argument");
+    if (!t->seg)
+        return set_err(L1RXG_EINVAL, "attach needs the segment correlator (cta_mode SEGMENT)");
+    if (samples_per_stream <= 0 || samples_per_stream % 32 || stride_bytes < samples_per_stream * 4 ||
+        stride_bytes % 16 || (reinterpret_cast<uintptr_t>(dev_bytes) & 15))
+        return set_err(L1RXG_EINVAL, "attach: whole 32-sample rows, 16-byte aligned base and stride");
+    for (const auto& r : t->streams)
+        if (r.pushed != 0)
+            return set_err(L1RXG_EINVAL, "attach: the tracker's streams must be empty");
+    CK(cudaSetDevice(t->ctx->device));
+    CK(cudaStreamSynchronize(t->ctx->compute));
+    // the recordings become the rings: one tensor over them, no wrap (the
+    // capacity is the whole recording), every sample available
+    CUtensorMap m{};
+    if (int rc = encode_ring_map(&m, const_cast<void*>(dev_bytes), samples_per_stream / 32, stride_bytes,
+                                 static_cast<int>(t->streams.size())))
+        return rc;
+    t->tmap = m;
+    t->att_samples = samples_per_stream;
+    for (auto& r : t->streams)
+        r.pushed = samples_per_stream;
+    std::vector<int64_t> av(t->streams.size(), samples_per_stream);
+    CK(cudaMemcpy(t->d_avail, av.data(), 8 * av.size(), cudaMemcpyHostToDevice));
+    return 0;
+}
+
 int l1rxg_tracker_push(l1rxg_tracker* t, int s, const void* bytes, int64_t nbytes) {
     if (!t || s < 0 || s >= (int)t->streams.size())
         return set_err(L1RXG_EINVAL, "bad stream");
@@ -1076,7 +1107,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     TrackArgs a{};
     a.ring = t->d_ring;
     a.ring_stride = t->R + t->apron;
-    a.ring_cap = t->R;
+    a.ring_cap = t->att_samples > 0 ? t->att_samples : t->R;
     a.avail = t->d_avail;
     a.chans = t->d_chans;
     a.chan_stream = t->d_chan_stream;
@@ -1273,7 +1304,13 @@ int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
     CK(cudaStreamSynchronize(t->ctx->compute));
     const size_t C = static_cast<size_t>(std::max(1, t->d.n_channels));
     cudaStream_t st = t->ctx->compute;
-    CK(cudaMemsetAsync(t->d_avail, 0, 8 * t->streams.size(), st));
+    if (t->att_samples > 0) {  // attached recordings stay fully available
+        std::vector<int64_t> av(t->streams.size(), t->att_samples);
+        CK(cudaMemcpyAsync(t->d_avail, av.data(), 8 * av.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        CK(cudaMemsetAsync(t->d_avail, 0, 8 * t->streams.size(), st));
+    }
     CK(cudaMemsetAsync(t->d_ecount, 0, 8 * C, st));
     CK(cudaMemsetAsync(t->d_status, 0, 4 * C, st));
     for (auto& r : t->streams) {

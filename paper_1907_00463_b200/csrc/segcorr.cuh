@@ -72,6 +72,7 @@ struct SegSmem {
     int pending, stop;
     double nco_ph1, nco_cp1;
     int8_t chipx[CHIP_EXT];  // bit 0: chip[m] > 0, bit 1: chip[m+1] != chip[m]
+    uint32_t chipw[CHIP_EXT / 32 + 1];  // bit m % 32 of word m / 32: chip[m] > 0
     int16_t tm[TRANS_EXT];   // chip index of the g-th chip transition (as CodeTables)
     int16_t cum[1024];       // transitions at indices <= r within one period
     int L;                   // transitions per period
@@ -115,10 +116,11 @@ __device__ __forceinline__ int floor_idx(double v) {
     return __double2loint(__dadd_rd(v, 6755399441055744.0));
 }
 
-// cint16 word -> (re, im) * 65536 exactly (full-rate I2FP; the 2^-16 and
-// the format's 1/32768 are folded into the rotator table, exact powers of two)
-__device__ __forceinline__ float seg_re(uint32_t w) { return (float)(int)(w << 16); }
-__device__ __forceinline__ float seg_im(uint32_t w) { return (float)(int)(w & 0xffff0000u); }
+// cint16 word -> (re, im) exactly, one I2F.S16 per component (the halves
+// selected in the instruction; the format's 1/32768 is folded into the
+// rotator table, an exact power of two)
+__device__ __forceinline__ float seg_re(uint32_t w) { return (float)(short)(w & 0xffffu); }
+__device__ __forceinline__ float seg_im(uint32_t w) { return (float)(short)(w >> 16); }
 
 // Sample j of the run in row `row` of a 128B-swizzled unit buffer.
 __device__ __forceinline__ uint32_t seg_sample(const unsigned char* buf, int row, int j) {
@@ -153,46 +155,52 @@ template <bool MASK>
 __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, const float4* rot4, int q0,
                                         int q1, int jlo, int jhi, float2& p16, float2& c0, float2& c1,
                                         float2& tot) {
+    // the two halves as two independent chains A (samples 0..15) and B
+    // (16..31), interleaved for ILP: P(16 + j) = P(16) + B(j)
     const unsigned char* rowp = buf + lane * 128;
     const int sw = lane & 7;
-    float pr = 0.f, pi = 0.f;
-    float c0r = 0.f, c0i = 0.f, c1r = 0.f, c1i = 0.f, hr = 0.f, hi = 0.f;
+    float ar = 0.f, ai = 0.f, br = 0.f, bi = 0.f;
+    float c0r = 0.f, c0i = 0.f, c1r = 0.f, c1i = 0.f;
 #pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-        const uint4 w4 = *reinterpret_cast<const uint4*>(rowp + ((ch ^ sw) << 4));
+    for (int ch = 0; ch < 4; ++ch) {
+        const uint4 wa4 = *reinterpret_cast<const uint4*>(rowp + ((ch ^ sw) << 4));
+        const uint4 wb4 = *reinterpret_cast<const uint4*>(rowp + (((ch + 4) ^ sw) << 4));
         const float4 ra = rot4[2 * ch], rb = rot4[2 * ch + 1];
-        const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
-        const float rc[4] = {ra.x, ra.z, rb.x, rb.z};
-        const float rs[4] = {ra.y, ra.w, rb.y, rb.w};
+        const float4 rc_ = rot4[2 * ch + 8], rd = rot4[2 * ch + 9];
+        const uint32_t wa[4] = {wa4.x, wa4.y, wa4.z, wa4.w};
+        const uint32_t wb[4] = {wb4.x, wb4.y, wb4.z, wb4.w};
+        const float ac[4] = {ra.x, ra.z, rb.x, rb.z};
+        const float as[4] = {ra.y, ra.w, rb.y, rb.w};
+        const float bc[4] = {rc_.x, rc_.z, rd.x, rd.z};
+        const float bs[4] = {rc_.y, rc_.w, rd.y, rd.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const int j = 4 * ch + t;
-            uint32_t x = ws[t];
-            if (MASK)
-                x = (j >= jlo && j < jhi) ? x : 0u;
-            if (j == 16) {
-                hr = pr;
-                hi = pi;
-            } else if (j < 16) {
-                if (j == q0) {
-                    c0r = pr;
-                    c0i = pi;
-                }
-            } else {
-                if (j == q1) {
-                    c1r = pr;
-                    c1i = pi;
-                }
+            const int j = 4 * ch + t;  // A: sample j, B: sample 16 + j
+            uint32_t xa = wa[t], xb = wb[t];
+            if (MASK) {
+                xa = (j >= jlo && j < jhi) ? xa : 0u;
+                xb = (j + 16 >= jlo && j + 16 < jhi) ? xb : 0u;
             }
-            const float xr = seg_re(x), xi = seg_im(x);
-            pr = fmaf(xi, rs[t], fmaf(xr, rc[t], pr));
-            pi = fmaf(-xr, rs[t], fmaf(xi, rc[t], pi));
+            if (j > 0 && j == q0) {
+                c0r = ar;
+                c0i = ai;
+            }
+            if (j > 0 && j + 16 == q1) {
+                c1r = br;
+                c1i = bi;
+            }
+            const float xar = seg_re(xa), xai = seg_im(xa);
+            const float xbr = seg_re(xb), xbi = seg_im(xb);
+            ar = fmaf(xai, as[t], fmaf(xar, ac[t], ar));
+            ai = fmaf(-xar, as[t], fmaf(xai, ac[t], ai));
+            br = fmaf(xbi, bs[t], fmaf(xbr, bc[t], br));
+            bi = fmaf(-xbr, bs[t], fmaf(xbi, bc[t], bi));
         }
     }
-    p16 = make_float2(hr, hi);
+    p16 = make_float2(ar, ai);
     c0 = make_float2(c0r, c0i);
-    c1 = make_float2(c1r, c1i);
-    tot = make_float2(pr, pi);
+    c1 = make_float2(ar + c1r, ai + c1i);
+    tot = make_float2(ar + br, ai + bi);
 }
 
 // anchored value z * conj(anchor), anchor = (cos, sin) of theta(i0)
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     const int64_t avail = a.avail[strm];
     const int64_t R = a.ring_cap;  // multiple of 32
     const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
-    const float scale = 1.f / (32768.f * 65536.f);
+    const float scale = 1.f / 32768.f;
 
     if (tid == 0) {
         s->ch = a.chans[cidx];
@@ -314,6 +322,12 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
         for (int m = tid; m < CHIP_EXT; m += blockDim.x) {
             const int8_t c0 = cc[m % 1023], c1 = cc[(m + 1) % 1023];
             s->chipx[m] = (int8_t)((c0 > 0 ? 1 : 0) | (c0 != c1 ? 2 : 0));
+        }
+        for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
+            uint32_t wv = 0;
+            for (int b = 0; b < 32; ++b)
+                wv |= (cc[(32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
+            s->chipw[q] = wv;
         }
         if (warp == SEG_NW) {  // control warp: ballot-scan of the code's transitions
             int running = 0;
@@ -354,15 +368,18 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     // ---- per-work-warp unit stream (uniform across the warp's lanes) ----
     // unit = (epoch ie, warp-unit ik): rows [32 ik, 32 ik + 32) of epoch ie,
     // rows counted from the ring row holding the epoch's first sample
-    const bool ring_ok = !noop && off0 >= 0 && off0 >= avail - R;
+    // epochs whose windows are ingested and still in the ring
+    int e_adm = 0;
+    if (!noop && off0 >= 0 && off0 >= avail - R && off0 + n <= avail)
+        e_adm = (int)min((int64_t)a.max_epochs, (avail - off0 - n) / n + 1);
     int iss_e = 0, iss_k = warp;
-    int64_t iss_pos = ring_ok ? off0 % R : 0;  // ring position of epoch iss_e's first sample
+    int64_t iss_pos = e_adm > 0 ? off0 % R : 0;  // ring position of epoch iss_e's first sample
     int iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
-    int64_t issued = 0, consumed = 0;
+    int issued = 0, consumed = 0;
     auto issue_one = [&]() -> bool {
-        if (!ring_ok || iss_e >= a.max_epochs || off0 + (int64_t)iss_e * n + n > avail)
+        if (iss_e >= e_adm)
             return false;
-        const int b = (int)(issued % SEG_NBUF);
+        const int b = issued & (SEG_NBUF - 1);
         if (lane == 0) {
             uint64_t* bar = &s->fbar[warp][b];
             mbar_expect_tx(bar, SEG_UNIT_BYTES);
@@ -433,11 +450,17 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 // (the first run of an epoch starts before sample 0: its
                 // start chip is the one at the first sample it counts)
                 const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
+                // |d| <= 1 chip: every tap's index is in [m0, m0 + 4]; the
+                // 32 chip bits from m0 hold them all
+                const int m0 = floor_idx(phs) - 2;
+                const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
                 float cs[T];
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
-                    cs[t] = ((slow >> t) & 1u) ? 0.f : ((s->chipx[ms] & 1) ? 1.f : -1.f);
+                    // chip bit to bit 31, then +1.0f / -1.0f
+                    const uint32_t hb = win << (31 - (ms - m0));
+                    cs[t] = __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
                 }
                 // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
                 const double th = __fma_rn(c.w, (double)i0, c.phi);
@@ -456,7 +479,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                         }
                 }
                 // ---- the unit's samples
-                const int b = (int)(consumed % SEG_NBUF);
+                const int b = consumed & (SEG_NBUF - 1);
                 mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
                 const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
                 float2 p16, pc0, pc1, tot;
@@ -480,15 +503,17 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                     acc[2 * t] = fmaf(cs[t], v.x, acc[2 * t]);
                     acc[2 * t + 1] = fmaf(cs[t], v.y, acc[2 * t + 1]);
                 }
-                if (slow) {
+                if (slow) {  // exact per-sample sums replace the fast ones
 #pragma unroll
                     for (int t = 0; t < T; ++t)
                         if ((slow >> t) & 1u) {
+                            const int code = (int)(w >> (10 + 2 * t)) & 3;
+                            const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
                             const float2 z = seg_anchor(
                                 seg_slow_sum(buf, lane, s->rot, s->chipx, s->d[t], i0, jlo, jhi, c.cps, c.base),
                                 ca_, sa_);
-                            acc[2 * t] += z.x;
-                            acc[2 * t + 1] += z.y;
+                            acc[2 * t] += fmaf(-cs[t], v.x, z.x);
+                            acc[2 * t + 1] += fmaf(-cs[t], v.y, z.y);
                         }
                 }
                 if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
@@ -500,8 +525,8 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 }
                 __syncwarp();
                 ++consumed;
-                while (issued < consumed + SEG_NBUF && issue_one()) {
-                }
+                if (issued < consumed + SEG_NBUF)
+                    issue_one();
             }
             if (!snapped) {
 #pragma unroll
@@ -534,8 +559,8 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     if (warp == ctl && s->pending)
         finish_epoch<T>(s, a, lane, true);
     if (warp < SEG_NW) {  // never leave a bulk copy in flight into freed smem
-        for (int64_t u = consumed; u < issued; ++u)
-            mbar_wait(&s->fbar[warp][u % SEG_NBUF], (uint32_t)((u / SEG_NBUF) & 1));
+        for (int u = consumed; u < issued; ++u)
+            mbar_wait(&s->fbar[warp][u & (SEG_NBUF - 1)], (uint32_t)((u / SEG_NBUF) & 1));
     }
     __syncthreads();
     if (tid == 0) {

@@ -278,6 +278,13 @@ class Tracker:
                                                    data.shape[1] * data.itemsize, data.strides[0]))
         self._keep = data
 
+    def attach_device(self, dev_ptr: int, samples_per_stream: int, stride_bytes: int) -> None:
+        """Segment correlator only: complex-int16 recordings resident in device
+        memory (stream s at dev_ptr + s * stride_bytes) become the rings; no
+        ingest pass (l1rxg_tracker_attach_device)."""
+        check(self._lib.l1rxg_tracker_attach_device(self.handle, C.c_void_p(dev_ptr),
+                                                    C.c_int64(samples_per_stream), C.c_int64(stride_bytes)))
+
     def push_device_strided(self, dev_ptr: int, nbytes_per_stream: int, stride_bytes: int) -> None:
         """Same-length chunk for every stream in one launch (batched recordings)."""
         check(self._lib.l1rxg_tracker_push_device_strided(self.handle, C.c_void_p(dev_ptr),

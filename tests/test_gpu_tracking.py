@@ -282,10 +282,19 @@ def test_batched_recordings_throughput_mode(ctx, oracle_mod, mode):
     b.sync()
     ca, cb = a.epoch_counts(), b.epoch_counts()
     assert np.array_equal(ca, cb) and ca.min() >= ms - 2
+    att = None
+    if mode == "segment":  # recordings attached in place: one launch, no ingest pass
+        att = make()
+        att.attach_device(dev.data_ptr(), raw.shape[1] // 4, raw.shape[1])
+        att.run()
+        att.sync()
+        assert np.array_equal(att.epoch_counts(), ca)
     for c in range(len(inits)):
         ra, ta = a.records(c, tap_sums=True)
         rb = b.records(c)
         assert ra.tobytes() == rb.tobytes()
+        if att is not None:
+            assert ra.tobytes() == att.records(c).tobytes()
         x = oracle_mod.ingest(raw[cstream[c]], abi.FMT_INT16_IQ, fs)
         replay_check(oracle_mod, inits[c], ra, x, n, cfg, taps, fs, tap_sums=ta)
 
