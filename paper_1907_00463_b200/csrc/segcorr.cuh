@@ -54,9 +54,9 @@ struct __align__(64) SegArgs {
     CUtensorMap tmap;  // ring as [stream][row][32 x u32], SWIZZLE_128B, box 32 x 32 x 1
 };
 
-// chipx[m]: bit 0 = chip[m] > 0, bit 1 = chip[m+1] != chip[m]
 template <int T>
 struct SegSmem {
+    float2 vsel[4][32 * SEG_NW];  // per run: the four candidate tap sums, [slot][thread]
     l1rxg_channel ch;
     EpochConsts c;
     double d[T];
@@ -71,7 +71,6 @@ struct SegSmem {
     double rec_eenv;
     int pending, stop;
     double nco_ph1, nco_cp1;
-    int8_t chipx[CHIP_EXT];  // bit 0: chip[m] > 0, bit 1: chip[m+1] != chip[m]
     uint32_t chipw[CHIP_EXT / 32 + 1];  // bit m % 32 of word m / 32: chip[m] > 0
     int16_t tm[TRANS_EXT];   // chip index of the g-th chip transition (as CodeTables)
     int16_t cum[1024];       // transitions at indices <= r within one period
@@ -80,10 +79,12 @@ struct SegSmem {
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
 // counted from the ring row holding the epoch's first sample):
-//   bits [0,5)  q0: the first-half capture position (1..15; 0 = none)
-//   bits [5,10) q1: the second-half capture position (17..31; 0 = none)
+//   bits [0,4)  q0: the first-half capture position (1..15; 0 = none)
+//   bits [4,8)  q1 - 16: the second-half capture position (17..31; 0 = none)
+//   bits 8, 9:  half 0 / half 1 claimed by two different positions (ties):
+//               every tap stepping in that half takes the slow path
 //   bits 10+2k..: tap k's step in the run: 0 none, 1 at 16, 2 at q0, 3 at q1
-//   bit 10+2T+k: tap k takes the exact slow path in this run
+//   bit 10+2T+k: tap k takes the exact slow path in this run (two steps)
 template <int T>
 struct SegEntry {
     typedef typename std::conditional<(3 * T + 10 <= 32), uint32_t, unsigned long long>::type type;
@@ -131,7 +132,7 @@ __device__ __forceinline__ uint32_t seg_sample(const unsigned char* buf, int row
 // chip[idx(i0 + j, d)] * x_j * conj(rot_j) (un-anchored), the reference's
 // chip decision per sample.
 __device__ __noinline__ float2 seg_slow_sum(const unsigned char* buf, int row, const float2* rot,
-                                            const int8_t* chipx, double d, int i0, int jlo, int jhi,
+                                            const uint32_t* chipw, double d, int i0, int jlo, int jhi,
                                             double cps, double base) {
     float sr = 0.f, si = 0.f;
     for (int j = jlo; j < jhi; ++j) {
@@ -141,7 +142,7 @@ __device__ __noinline__ float2 seg_slow_sum(const unsigned char* buf, int row, c
         const float yr = fmaf(xi, q.y, xr * q.x);
         const float yi = fmaf(-xr, q.y, xi * q.x);
         const int m = floor_idx(__dadd_rn(__fma_rn((double)(i0 + j), cps, base), d));
-        const float ch = (chipx[m] & 1) ? 1.f : -1.f;
+        const float ch = ((chipw[m >> 5] >> (m & 31)) & 1u) ? 1.f : -1.f;
         sr = fmaf(ch, yr, sr);
         si = fmaf(ch, yi, si);
     }
@@ -243,34 +244,19 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
             const int r = pos >> 5, q = pos & 31;
             if (q == 0)
                 continue;
-            E code = 1;
-            if (q != 16) {
-                const int fsh = q < 16 ? 0 : 5;
-                code = q < 16 ? 2 : 3;
-                E old = tab[r];
-                for (;;) {
-                    const int f = (int)((old >> fsh) & 31);
-                    if (f == q)
-                        break;
-                    if (f != 0) {
-                        code = 0;  // this half already captures another position
-                        break;
-                    }
-                    const E prev = atomicCAS(&tab[r], old, old | ((E)q << fsh));
-                    if (prev == old)
-                        break;
-                    old = prev;
-                }
-            }
+            // one atomic OR enters the position and the tap's code; the
+            // previous word tells whether the half already held another
+            // position (tie -> conflict bit) or the tap already stepped here
             const int sh = 10 + 2 * k;
-            const E slowbit = (E)1 << (10 + 2 * T + k);
-            if (code) {
-                const E prev = atomicOr(&tab[r], code << sh);
-                if ((prev >> sh) & 3)
-                    atomicOr(&tab[r], slowbit);  // a second step of tap k in this run
-            } else {
-                atomicOr(&tab[r], slowbit);
-            }
+            const int h = q > 16;
+            const E code = q == 16 ? 1 : 2 + h;
+            const E qf = q == 16 ? 0 : (E)(q - 16 * h) << (4 * h);
+            const E prev = atomicOr(&tab[r], qf | (code << sh));
+            const int pf = (int)((prev >> (4 * h)) & 15);
+            if (q != 16 && pf != 0 && pf != q - 16 * h)
+                atomicOr(&tab[r], (E)1 << (8 + h));
+            if ((prev >> sh) & 3)
+                atomicOr(&tab[r], (E)1 << (10 + 2 * T + k));  // a second step of tap k in this run
         }
     }
 }
@@ -319,10 +305,6 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     __syncthreads();
     {
         const int8_t* cc = a.codes + s->ch.prn * 1023;
-        for (int m = tid; m < CHIP_EXT; m += blockDim.x) {
-            const int8_t c0 = cc[m % 1023], c1 = cc[(m + 1) % 1023];
-            s->chipx[m] = (int8_t)((c0 > 0 ? 1 : 0) | (c0 != c1 ? 2 : 0));
-        }
         for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
             uint32_t wv = 0;
             for (int b = 0; b < 32; ++b)
@@ -445,7 +427,15 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 const int jhi = max(jlo, min(32, n - i0));
                 const E w = tab[r];
                 tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
-                const uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
+                uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
+                if (w & 0x300u) {  // a half with two positions: its steppers take the slow path
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int code = (int)(w >> (10 + 2 * t)) & 3;
+                        if ((code == 2 && (w & 0x100u)) || (code == 3 && (w & 0x200u)))
+                            slow |= 1u << t;
+                    }
+                }
                 // start chips of the taps (the reference's chip index at i0)
                 // (the first run of an epoch starts before sample 0: its
                 // start chip is the one at the first sample it counts)
@@ -454,14 +444,12 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 // 32 chip bits from m0 hold them all
                 const int m0 = floor_idx(phs) - 2;
                 const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
-                float cs[T];
-#pragma unroll
-                for (int t = 0; t < T; ++t) {
+                // start chip of tap t: its chip bit moved to bit 31, then +1.0f / -1.0f
+                auto start_chip = [&](int t) -> float {
                     const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
-                    // chip bit to bit 31, then +1.0f / -1.0f
                     const uint32_t hb = win << (31 - (ms - m0));
-                    cs[t] = __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
-                }
+                    return __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
+                };
                 // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
                 const double th = __fma_rn(c.w, (double)i0, c.phi);
                 const double rr = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
@@ -483,7 +471,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
                 const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
                 float2 p16, pc0, pc1, tot;
-                const int q0 = (int)(w & 31), q1 = (int)((w >> 5) & 31);
+                const int q0 = (int)(w & 15), q1 = (w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0;
                 if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
                     seg_run<false>(buf, lane, rot4, q0, q1, 0, 32, p16, pc0, pc1, tot);
                 else
@@ -494,14 +482,19 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
                 const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
                 const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
+                // tap t picks V[code_t]: through this thread's scratch slots
+                // (one LDS.64 per tap instead of a three-level select)
+                s->vsel[0][tid] = v0;
+                s->vsel[1][tid] = v1;
+                s->vsel[2][tid] = v2;
+                s->vsel[3][tid] = v3;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     const int code = (int)(w >> (10 + 2 * t)) & 3;
-                    const float2 lo = (code & 1) ? v1 : v0;
-                    const float2 hi2 = (code & 1) ? v3 : v2;
-                    const float2 v = (code & 2) ? hi2 : lo;
-                    acc[2 * t] = fmaf(cs[t], v.x, acc[2 * t]);
-                    acc[2 * t + 1] = fmaf(cs[t], v.y, acc[2 * t + 1]);
+                    const float2 v = s->vsel[code][tid];
+                    const float cs = start_chip(t);
+                    acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
+                    acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
                 }
                 if (slow) {  // exact per-sample sums replace the fast ones
 #pragma unroll
@@ -510,14 +503,15 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                             const int code = (int)(w >> (10 + 2 * t)) & 3;
                             const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
                             const float2 z = seg_anchor(
-                                seg_slow_sum(buf, lane, s->rot, s->chipx, s->d[t], i0, jlo, jhi, c.cps, c.base),
+                                seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[t], i0, jlo, jhi, c.cps, c.base),
                                 ca_, sa_);
-                            acc[2 * t] += fmaf(-cs[t], v.x, z.x);
-                            acc[2 * t + 1] += fmaf(-cs[t], v.y, z.y);
+                            const float cs = start_chip(t);
+                            acc[2 * t] += fmaf(-cs, v.x, z.x);
+                            acc[2 * t + 1] += fmaf(-cs, v.y, z.y);
                         }
                 }
                 if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
-                    const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipx, s->d[a.kp], i0,
+                    const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[a.kp], i0,
                                                              jlo, max(jlo, min(jhi, nh - i0)), c.cps, c.base),
                                                 ca_, sa_);
                     hr += z.x;
