@@ -492,14 +492,19 @@ def run_batch(args, rank, world, local, dist, emit=True):
         pinned = ctx.host_alloc(len(recs) * eb).reshape(len(recs), eb)
         for j in range(len(recs)):  # row by row: a strided slice would stage a device copy
             pinned[j] = raw[j, :eb].cpu().numpy()
-        rec_bytes = trk.records_nbytes()
+        # the segment correlator's device leg reads attached recordings; the
+        # host leg streams into its own rings
+        te = trk if not attached else Tracker(
+            ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs), taps=taps,
+            cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks, cta_mode=abi.CTA_SEGMENT)
+        rec_bytes = te.records_nbytes()
 
         def step_e2e():
-            trk.reset(inits)
+            te.reset(inits)
             for o in range(0, eb, chunk):
-                trk.push_strided(pinned[:, o:o + chunk])
-                trk.run()
-            return trk.records_raw()
+                te.push_strided(pinned[:, o:o + chunk])
+                te.run()
+            return te.records_raw()
 
         step_e2e()
         barrier()
@@ -511,13 +516,16 @@ def run_batch(args, rank, world, local, dist, emit=True):
             tt = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
-        e2e_epochs = float(trk.epoch_counts().sum()) * (epochs_all / max(epochs_local, 1.0))
+        e2e_epochs = float(te.epoch_counts().sum()) * (epochs_all / max(epochs_local, 1.0))
         e2e = {"value": e2e_epochs * n * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(len(recs) * eb), "d2h_bytes_per_step": int(rec_bytes),
                "blocks_per_step": e2e_blocks,
                "path": "pinned host [recording][bytes] -> l1rxg_tracker_push_strided (one pitched "
-                       "H2D + one decode launch per %d-block chunk) -> run -> records_raw to host" % chunk_b}
+                       "H2D + one %s launch per %d-block chunk) -> run -> records_raw to host" % (
+                           "raw-ring copy" if attached else "decode", chunk_b)}
         del pinned
+        if te is not trk:
+            del te
     if rank != 0:
         if emit:
             dist.destroy_process_group()
@@ -531,8 +539,8 @@ def run_batch(args, rank, world, local, dist, emit=True):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic_config4.json")
-    launches_per_step = -(-blocks // chunk_b)
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic_config4.json" if attached else "ncu_traffic_config4_trackkernel.json")
+    launches_per_step = 1 if attached else -(-blocks // chunk_b)
     if os.path.exists(prof):  # measured DRAM bytes per channel-epoch x channel-epochs per launch
         per = json.load(open(prof)).get("dram_bytes_per_channel_epoch")
         traffic = per * epochs_local / launches_per_step if per else None
@@ -571,15 +579,20 @@ def run_batch(args, rank, world, local, dist, emit=True):
         "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_note": "DRAM bytes per track_kernel launch (one %d-block chunk of every "
-                                     "recording), profiles/ncu_traffic_config4.json" % chunk_b,
+                     "traffic_note": ("DRAM bytes per track_seg_kernel launch (all %d blocks of every "
+                                      "recording), profiles/ncu_traffic_config4.json" % blocks) if attached
+                                     else ("DRAM bytes per track_kernel launch (one %d-block chunk of every "
+                                           "recording), profiles/ncu_traffic_config4_trackkernel.json" % chunk_b),
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock under load "
                                     "(%.0f MHz); FP32 pipe roof per SURVEY 8d" % sm_mhz,
                      "alg_ops_per_sample_tap": ops_per_sample_tap(T, 12, False),
-                     "hbm": {"achieved_gbs": (len(recs) * blocks * n * 8) / (track_launch_ms * 1e-3) / 1e9,
+                     "hbm": {"achieved_gbs": (len(recs) * blocks * n * (4 if attached else 8))
+                                             / (track_launch_ms * 1e-3) / 1e9,
                              "peak_gbs": peaks.get("hbm_gbs", 6450.0),
-                             "note": "unique float2 baseband bytes per step (each recording's ring "
-                                     "read once; its 12 channels share it through L2)"}},
+                             "note": ("unique cint16 bytes per step (each recording read in place once; its "
+                                      "12 channels share it through L2)") if attached else
+                                     ("unique float2 baseband bytes per step (each recording's ring read "
+                                      "once; its 12 channels share it through L2)")}},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
     }
     if gathered is not None:
@@ -652,7 +665,7 @@ def companion_config4(args, rank, world, local, dist):
     import torch
     a = copy.copy(args)
     a.recordings, a.blocks, a.steps, a.warmup = 128, 100, 2, 1
-    a.no_cpu_baseline, a.no_e2e, a.cta, a.ring_raw = True, True, "throughput", False
+    a.no_cpu_baseline, a.no_e2e, a.cta, a.ring_raw = True, True, "segment", False
     try:
         ln = run_batch(a, rank, world, local, dist, emit=False)
         torch.cuda.empty_cache()
@@ -678,7 +691,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="config 4: skip the host-memory e2e leg")
     ap.add_argument("--e2e-chunk-ms", type=int, default=1000)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
-    ap.add_argument("--cta", default="throughput", choices=["segment", "throughput", "latency"],
+    ap.add_argument("--cta", default="segment", choices=["segment", "throughput", "latency"],
                     help="config 4 CTA shape: segment correlator (raw cint16 ring), throughput, latency")
     ap.add_argument("--ring-raw", action="store_true", help="config 4: keep cint16 raw in the rings")
     ap.add_argument("--no-companion", dest="companion", action="store_false",
