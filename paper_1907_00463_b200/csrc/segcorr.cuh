@@ -120,8 +120,15 @@ __device__ __forceinline__ int floor_idx(double v) {
 // cint16 word -> (re, im) exactly, one I2F.S16 per component (the halves
 // selected in the instruction; the format's 1/32768 is folded into the
 // rotator table, an exact power of two)
+#ifdef L1RXG_SEG_I2FP  // experiment switch: full-rate I2FP on the shifted halves (x 65536)
+__device__ __forceinline__ float seg_re(uint32_t w) { return (float)(int)(w << 16); }
+__device__ __forceinline__ float seg_im(uint32_t w) { return (float)(int)(w & 0xffff0000u); }
+constexpr float SEG_CVT_SCALE = 1.f / (32768.f * 65536.f);
+#else
 __device__ __forceinline__ float seg_re(uint32_t w) { return (float)(short)(w & 0xffffu); }
 __device__ __forceinline__ float seg_im(uint32_t w) { return (float)(short)(w >> 16); }
+constexpr float SEG_CVT_SCALE = 1.f / 32768.f;
+#endif
 
 // Sample j of the run in row `row` of a 128B-swizzled unit buffer.
 __device__ __forceinline__ uint32_t seg_sample(const unsigned char* buf, int row, int j) {
@@ -209,12 +216,30 @@ __device__ __forceinline__ float2 seg_anchor(float2 z, float ca, float sa) {
     return make_float2(fmaf(z.x, ca, z.y * sa), fmaf(z.y, ca, -(z.x * sa)));
 }
 
-// Step table fill for one epoch (the work threads, after the loop update):
-// every chip transition m of every tap with its step inside the epoch,
-// located exactly (tap_boundary), entered in the run holding it.  A step at
-// a run's first sample needs no entry (the run's start chip has it).  Two
-// positions competing for one half's capture, or two steps of one tap in
-// one run, send that tap to the slow path for that run.
+// Enters the step of tap k at epoch run position pos (= b + lead) with one
+// atomic OR of the position and the tap's code; the previous word tells
+// whether the half already held another position (tie -> conflict bit) or
+// the tap already stepped in this run (-> its slow bit).  A step at a run's
+// first sample needs no entry (the run's start chip has it).
+template <int T>
+__device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int pos, int k) {
+    typedef typename SegEntry<T>::type E;
+    const int r = pos >> 5, q = pos & 31;
+    if (q == 0)
+        return;
+    const int sh = 10 + 2 * k;
+    const int h = q > 16;
+    const E code = q == 16 ? 1 : 2 + h;
+    const E qf = q == 16 ? 0 : (E)(q - 16 * h) << (4 * h);
+    const E prev = atomicOr(&tab[r], qf | (code << sh));
+    const int pf = (int)((prev >> (4 * h)) & 15);
+    if (q != 16 && pf != 0 && pf != q - 16 * h)
+        atomicOr(&tab[r], (E)1 << (8 + h));
+    if ((prev >> sh) & 3)
+        atomicOr(&tab[r], (E)1 << (10 + 2 * T + k));
+}
+
+// transitions of the PRN's code at chip indices <= m (CodeTables' trans_count)
 template <int T>
 __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
     const int p = m / 1023;
@@ -230,7 +255,6 @@ __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
 template <int T>
 __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const SegSmem<T>* s,
                                         const EpochConsts& c, int lead, int tid, int nthr) {
-    typedef typename SegEntry<T>::type E;
     const int n = c.n;
 #pragma unroll 1
     for (int k = 0; k < T; ++k) {
@@ -238,25 +262,15 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         // transitions at chip indices in (idx(0), idx(n-1)]
         const int g0 = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));
         const int g1 = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk));
-        for (int g = g0 + tid; g < g1; g += nthr) {
-            const int b = tap_boundary(s->tm[g], dk, c, 1, n - 1);
-            const int pos = b + lead;
-            const int r = pos >> 5, q = pos & 31;
-            if (q == 0)
-                continue;
-            // one atomic OR enters the position and the tap's code; the
-            // previous word tells whether the half already held another
-            // position (tie -> conflict bit) or the tap already stepped here
-            const int sh = 10 + 2 * k;
-            const int h = q > 16;
-            const E code = q == 16 ? 1 : 2 + h;
-            const E qf = q == 16 ? 0 : (E)(q - 16 * h) << (4 * h);
-            const E prev = atomicOr(&tab[r], qf | (code << sh));
-            const int pf = (int)((prev >> (4 * h)) & 15);
-            if (q != 16 && pf != 0 && pf != q - 16 * h)
-                atomicOr(&tab[r], (E)1 << (8 + h));
-            if ((prev >> sh) & 3)
-                atomicOr(&tab[r], (E)1 << (10 + 2 * T + k));  // a second step of tap k in this run
+        // two transitions per iteration: the fp64 searches and the atomics
+        // of the pair overlap
+        for (int g = g0 + tid; g < g1; g += 2 * nthr) {
+            const bool two = g + nthr < g1;
+            const int ba = tap_boundary(s->tm[g], dk, c, 1, n - 1);
+            const int bb = two ? tap_boundary(s->tm[g + nthr], dk, c, 1, n - 1) : 0;
+            seg_enter<T>(tab, ba + lead, k);
+            if (two)
+                seg_enter<T>(tab, bb + lead, k);
         }
     }
 }
@@ -287,7 +301,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     const int64_t avail = a.avail[strm];
     const int64_t R = a.ring_cap;  // multiple of 32
     const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
-    const float scale = 1.f / 32768.f;
+    const float scale = SEG_CVT_SCALE;
 
     if (tid == 0) {
         s->ch = a.chans[cidx];
@@ -398,6 +412,12 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
             break;
         }
         EpochConsts c = s->c;
+        // the step table of this epoch: every thread (the control warp too)
+        if (!noop) {
+            c.inv_cps = fast_rcp(c.cps);
+            seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT);
+            __syncthreads();
+        }
         if (warp == ctl) {
             nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
             if (s->pending) {
@@ -414,10 +434,6 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
             c.inv_cps = fast_rcp(c.cps);
             const int lead = (int)(off & 31);
             const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
-            if (!noop) {
-                seg_fill<T>(tab, s, c, lead, tid, NWT);
-                named_bar_sync(1, NWT);
-            }
             bool snapped = false;
             float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
             for (int k = warp; k < nwu && !noop; k += SEG_NW) {
