@@ -43,11 +43,12 @@
 
 namespace l1rxg {
 
-constexpr int SEG_NW = 4;                    // work warps per CTA
-constexpr int SEG_NT = 32 * (SEG_NW + 1);    // + the control warp
+constexpr int SEG_NW = 5;                    // warps per CTA, all correlate
+constexpr int SEG_NT = 32 * SEG_NW;
 constexpr int SEG_NBUF = 2;                  // TMA buffers per work warp
 constexpr int SEG_UNIT_BYTES = 32 * 128;     // 32 rows x 32 cint16 samples
-constexpr int SEG_MIN_N = 32 * 32 * SEG_NW;  // every work warp has >= 1 unit per epoch
+constexpr int SEG_MIN_N = 32 * 32 * (SEG_NW - 1) + 1;  // every warp has >= 1 unit per epoch
+constexpr int SEG_TRANS_P = 576;             // transitions per code period (<= 544 for C/A codes)
 
 struct __align__(64) SegArgs {
     TrackArgs t;
@@ -56,7 +57,6 @@ struct __align__(64) SegArgs {
 
 template <int T>
 struct SegSmem {
-    float2 vsel[4][32 * SEG_NW];  // per run: the four candidate tap sums, [slot][thread]
     l1rxg_channel ch;
     EpochConsts c;
     double d[T];
@@ -72,9 +72,10 @@ struct SegSmem {
     int pending, stop;
     double nco_ph1, nco_cp1;
     uint32_t chipw[CHIP_EXT / 32 + 1];  // bit m % 32 of word m / 32: chip[m] > 0
-    int16_t tm[TRANS_EXT];   // chip index of the g-th chip transition (as CodeTables)
+    int16_t tm[SEG_TRANS_P];  // chip index of the g-th chip transition of one period
     int16_t cum[1024];       // transitions at indices <= r within one period
     int L;                   // transitions per period
+    float inv_L;             // 1 / L (period of a transition index, exact for g < 2^13)
 };
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
@@ -245,6 +246,12 @@ __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
     const int p = m / 1023;
     return p * s->L + s->cum[m - p * 1023];
 }
+// chip index of the g-th transition (any period): p * 1023 + tm[g - p * L]
+template <int T>
+__device__ __forceinline__ int seg_trans_at(const SegSmem<T>* s, int g) {
+    const int p = (int)(((float)g + 0.5f) * s->inv_L);
+    return p * 1023 + s->tm[g - p * s->L];
+}
 
 // Step table fill for one epoch (the work threads, after the loop update):
 // every chip transition m of every tap with its step inside the epoch,
@@ -266,8 +273,8 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         // of the pair overlap
         for (int g = g0 + tid; g < g1; g += 2 * nthr) {
             const bool two = g + nthr < g1;
-            const int ba = tap_boundary(s->tm[g], dk, c, 1, n - 1);
-            const int bb = two ? tap_boundary(s->tm[g + nthr], dk, c, 1, n - 1) : 0;
+            const int ba = tap_boundary(seg_trans_at(s, g), dk, c, 1, n - 1);
+            const int bb = two ? tap_boundary(seg_trans_at(s, g + nthr), dk, c, 1, n - 1) : 0;
             seg_enter<T>(tab, ba + lead, k);
             if (two)
                 seg_enter<T>(tab, bb + lead, k);
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     const int cidx = blockIdx.x;
     const int strm = a.chan_stream[cidx];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int ctl = SEG_NW;  // control warp
+    const int ctl = SEG_NW - 1;  // also finishes each epoch (metrics, record) before its runs
     constexpr int NWT = 32 * SEG_NW;
     constexpr int V = 2 * T + 2;
     const int nh = n / 2;
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 wv |= (cc[(32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
             s->chipw[q] = wv;
         }
-        if (warp == SEG_NW) {  // control warp: ballot-scan of the code's transitions
+        if (warp == ctl) {  // ballot-scan of the code's transitions
             int running = 0;
             for (int base = 0; base < 1023; base += 32) {
                 const int r = base + lane;
@@ -339,13 +346,9 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 }
                 running += __popc(mask);
             }
-            if (lane == 0)
+            if (lane == 0) {
                 s->L = running;
-            __syncwarp();
-            for (int g = running + lane; g < TRANS_EXT; g += 32) {  // later periods
-                const int p = g / running, q = g - p * running;
-                const int m = p * 1023 + s->tm[q];
-                s->tm[g] = (int16_t)(m < 32767 ? m : 32767);
+                s->inv_L = 1.f / (float)running;
             }
         }
     }
@@ -353,6 +356,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
         const l1rxg_channel& ch = s->ch;
         make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
                     ch.carrier_phase_rad, a.lc.fs, n);
+        s->c.inv_cps = fast_rcp(s->c.cps);  // tap_boundary's estimate
     }
     __syncthreads();
     if (tid < 32) {
@@ -411,15 +415,17 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 a.status[cidx] = 1;
             break;
         }
-        EpochConsts c = s->c;
+        // the epoch's NCO constants stay in shared memory (s->c, unchanged
+        // until the loop update) rather than in registers across the runs
+        const EpochConsts& c = s->c;
         // the step table of this epoch: every thread (the control warp too)
         if (!noop) {
-            c.inv_cps = fast_rcp(c.cps);
             seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT);
             __syncthreads();
         }
         if (warp == ctl) {
-            nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
+            const EpochConsts cc = s->c;
+            nco_advance_lanes(s->nco_ph1, s->nco_cp1, cc, s->ch, lane);
             if (s->pending) {
                 finish_epoch<T>(s, a, lane, true);
                 if (lane == 0)
@@ -431,7 +437,6 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
         for (int v = 0; v < V; ++v)
             acc[v] = 0.f;
         if (warp < SEG_NW) {
-            c.inv_cps = fast_rcp(c.cps);
             const int lead = (int)(off & 31);
             const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
             bool snapped = false;
@@ -498,16 +503,12 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
                 const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
                 const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
-                // tap t picks V[code_t]: through this thread's scratch slots
-                // (one LDS.64 per tap instead of a three-level select)
-                s->vsel[0][tid] = v0;
-                s->vsel[1][tid] = v1;
-                s->vsel[2][tid] = v2;
-                s->vsel[3][tid] = v3;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     const int code = (int)(w >> (10 + 2 * t)) & 3;
-                    const float2 v = s->vsel[code][tid];
+                    const float2 lo = (code & 1) ? v1 : v0;
+                    const float2 hi2 = (code & 1) ? v3 : v2;
+                    const float2 v = (code & 2) ? hi2 : lo;
                     const float cs = start_chip(t);
                     acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
                     acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
@@ -552,7 +553,10 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
         }
         __syncthreads();
         if (warp == 0) {
-            warp0_update<T>(s, a, c, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
+            const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
+            warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
+            if (lane == 0)
+                s->c.inv_cps = fast_rcp(s->c.cps);
             float sn, co;
             sincosf((float)(s->c.w * (double)lane), &sn, &co);
             s->rot[lane] = make_float2(co * scale, sn * scale);

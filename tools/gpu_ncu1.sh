@@ -1,0 +1,4 @@
+# one ncu --set full capture of the segment kernel (config 4 scaled): gpurun -- "bash tools/gpu_ncu1.sh tag"
+T=$1
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/$T
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:track_seg -c 1 -o gpurun_out/$T/seg python bench.py --config 4 --recordings 64 --blocks 50 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --cta segment > gpurun_out/$T/ncu.log 2>&1
