@@ -63,6 +63,7 @@ struct SegSmem {
     double sums[2 * T + 2];
     float red[SEG_NW * (2 * T + 2)];
     __align__(16) float2 rot[32];
+    __align__(16) float2 rotq[32];  // rot transposed by quarter: rotq[4 t + Q] = rot[8 Q + t]
     uint64_t fbar[SEG_NW][SEG_NBUF];  // per work warp: its unit buffers' TMA completion
     uint64_t pbar[2];                 // (cluster exchange: unused, csize == 1)
     l1rxg_epoch_record rec;
@@ -211,6 +212,60 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
     c1 = make_float2(ar + c1r, ai + c1i);
     tot = make_float2(ar + br, ai + bi);
 }
+
+#ifdef L1RXG_SEG_CHAINS4
+// Four independent chains (quarters of the run: samples 8Q + t, t < 8), for
+// more ILP; P(q0) = q0 < 8 ? A(q0) : A(8) + B(q0 - 8), likewise in the
+// second half.  rotq holds the rotators transposed by quarter so one
+// broadcast LDS.128 gives two quarters' rotators for step t.
+template <bool MASK>
+__device__ __forceinline__ void seg_run4(const unsigned char* buf, int lane, const float4* rq4, int q0,
+                                         int q1, int jlo, int jhi, float2& p16, float2& c0, float2& c1,
+                                         float2& tot) {
+    const unsigned char* rowp = buf + lane * 128;
+    const int sw = lane & 7;
+    float pr[4] = {0.f, 0.f, 0.f, 0.f}, pi[4] = {0.f, 0.f, 0.f, 0.f};
+    float car = 0.f, cai = 0.f, cbr = 0.f, cbi = 0.f, ccr = 0.f, cci = 0.f, cdr = 0.f, cdi = 0.f;
+    const int q1r = q1 - 16;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // chunk h of each quarter: samples 8Q + 4h + u
+        uint4 wq[4];
+#pragma unroll
+        for (int Q = 0; Q < 4; ++Q)
+            wq[Q] = *reinterpret_cast<const uint4*>(rowp + (((2 * Q + h) ^ sw) << 4));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = 4 * h + u;
+            const float4 r01 = rq4[2 * t], r23 = rq4[2 * t + 1];
+            const float rc[4] = {r01.x, r01.z, r23.x, r23.z};
+            const float rs[4] = {r01.y, r01.w, r23.y, r23.w};
+            // captures before adding step t: A at q0, B at q0 - 8, C at q1 - 16, D at q1 - 24
+            if (t > 0 && t == q0) { car = pr[0]; cai = pi[0]; }
+            if (t == q0 - 8) { cbr = pr[1]; cbi = pi[1]; }
+            if (t > 0 && t == q1r) { ccr = pr[2]; cci = pi[2]; }
+            if (t == q1r - 8) { cdr = pr[3]; cdi = pi[3]; }
+#pragma unroll
+            for (int Q = 0; Q < 4; ++Q) {
+                const uint32_t wv[4] = {wq[Q].x, wq[Q].y, wq[Q].z, wq[Q].w};
+                uint32_t x = wv[u];
+                const int j = 8 * Q + t;
+                if (MASK)
+                    x = (j >= jlo && j < jhi) ? x : 0u;
+                const float xr = seg_re(x), xi = seg_im(x);
+                pr[Q] = fmaf(xi, rs[Q], fmaf(xr, rc[Q], pr[Q]));
+                pi[Q] = fmaf(-xr, rs[Q], fmaf(xi, rc[Q], pi[Q]));
+            }
+        }
+    }
+    const float a8r = pr[0], a8i = pi[0];
+    const float h16r = a8r + pr[1], h16i = a8i + pi[1];
+    const float c24r = h16r + pr[2], c24i = h16i + pi[2];
+    p16 = make_float2(h16r, h16i);
+    c0 = q0 < 8 ? make_float2(car, cai) : make_float2(a8r + cbr, a8i + cbi);
+    c1 = q1r < 8 ? make_float2(h16r + ccr, h16i + cci) : make_float2(c24r + cdr, c24i + cdi);
+    tot = make_float2(c24r + pr[3], c24i + pi[3]);
+}
+#endif
 
 // anchored value z * conj(anchor), anchor = (cos, sin) of theta(i0)
 __device__ __forceinline__ float2 seg_anchor(float2 z, float ca, float sa) {
@@ -363,6 +418,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
         float sn, co;
         sincosf((float)(s->c.w * (double)tid), &sn, &co);
         s->rot[tid] = make_float2(co * scale, sn * scale);
+        s->rotq[(tid & 7) * 4 + (tid >> 3)] = make_float2(co * scale, sn * scale);
     }
 
     // ---- per-work-warp unit stream (uniform across the warp's lanes) ----
@@ -493,10 +549,18 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
                 float2 p16, pc0, pc1, tot;
                 const int q0 = (int)(w & 15), q1 = (w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0;
+#ifdef L1RXG_SEG_CHAINS4
+                const float4* rq4 = reinterpret_cast<const float4*>(s->rotq);
+                if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
+                    seg_run4<false>(buf, lane, rq4, q0, q1, 0, 32, p16, pc0, pc1, tot);
+                else
+                    seg_run4<true>(buf, lane, rq4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
+#else
                 if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
                     seg_run<false>(buf, lane, rot4, q0, q1, 0, 32, p16, pc0, pc1, tot);
                 else
                     seg_run<true>(buf, lane, rot4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
+#endif
                 // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
                 // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
                 const float2 v0 = seg_anchor(tot, ca_, sa_);
@@ -560,6 +624,7 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
             float sn, co;
             sincosf((float)(s->c.w * (double)lane), &sn, &co);
             s->rot[lane] = make_float2(co * scale, sn * scale);
+            s->rotq[(lane & 7) * 4 + (lane >> 3)] = make_float2(co * scale, sn * scale);
         }
         __syncthreads();
         if (s->stop)
