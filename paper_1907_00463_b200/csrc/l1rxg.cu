@@ -218,11 +218,20 @@ int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
 // Segment correlator: one CTA per channel, four per SM.
 template <int T>
 int launch_seg(const SegArgs& sa, int n_ch, cudaStream_t s) {
+    (void)n_ch;
     const size_t sm = seg_smem_bytes<T>(sa.t.n);
     CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
-    track_seg_kernel<T><<<n_ch, SEG_NT, sm, s>>>(sa);
+    // persistent: as many CTAs as fit, each looping over work items
+    int per_sm = 0, nsm = 148, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_seg_kernel<T>, SEG_NT, sm));
+    int grid = std::max(1, std::min(sa.n_items, std::max(1, per_sm) * nsm));
+    if (const char* ev = std::getenv("L1RXG_SEG_GRID"))  // tests: many work items per CTA
+        grid = std::max(1, std::min(grid, std::atoi(ev)));
+    track_seg_kernel<T><<<grid, SEG_NT, sm, s>>>(sa);
     CK(cudaGetLastError());
     return 0;
 }
@@ -396,6 +405,7 @@ struct l1rxg_tracker {
     int seg = 0;     // segment correlator (track_seg_kernel) over a raw cint16 ring
     CUtensorMap tmap{};  // seg: the ring as [stream][row][32 samples] for TMA tensor copies
     int64_t att_samples = 0;  // seg: > 0 while device recordings are attached in place of the ring
+    int* d_segq = nullptr;    // seg: work-item counter + per-channel chunks done
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
     int esz = 8;     // ring element bytes (ring_esz)
@@ -847,6 +857,8 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         return fail(e);
     for (size_t k = 0; k < t->streams.size(); ++k)
         t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride * t->esz;
+    if (t->seg && (e = cudaMalloc(&t->d_segq, 4 * (1 + std::max(1, d->n_channels)))) != cudaSuccess)
+        return fail(e);
     if (t->seg) {
         if (int rc = encode_ring_map(&t->tmap, t->d_ring, stride / 32, stride * 4, d->n_streams)) {
             const std::string msg = g_err;
@@ -896,6 +908,7 @@ int l1rxg_tracker_destroy(l1rxg_tracker* t) {
     cudaSetDevice(t->ctx->device);
     cudaDeviceSynchronize();
     cudaFree(t->d_ring);
+    cudaFree(t->d_segq);
     for (auto& r : t->streams) {
         for (int k = 0; k < 2; ++k) {
             cudaFree(r.hist8[k]);
@@ -1145,6 +1158,23 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
         if (t->seg) {
             sa.t = a;
             sa.tmap = t->tmap;
+            // work items: chunks of the launch's epochs per channel, so the
+            // persistent CTAs end together (no wave-quantisation tail)
+            int64_t most = t->att_samples;
+            for (const auto& r : t->streams)
+                most = std::max(most, r.pushed);
+            const int64_t max_e = std::min<int64_t>(a.max_epochs, most / a.n + 1);
+            const int chunk = static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
+            const int64_t nchunk = std::max<int64_t>(1, (max_e + chunk - 1) / chunk);
+            const int64_t items = nchunk * t->d.n_channels;
+            if (items > 0x7fffffff)
+                return set_err(L1RXG_EINVAL, "too many work items in one run");
+            sa.next = t->d_segq;
+            sa.ready = t->d_segq + 1;
+            sa.n_items = static_cast<int>(items);
+            sa.n_channels = t->d.n_channels;
+            sa.chunk_epochs = chunk;
+            CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels)), st));
             DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
         }
         DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st, sk);

@@ -53,6 +53,12 @@ constexpr int SEG_TRANS_P = 576;             // transitions per code period (<= 
 struct __align__(64) SegArgs {
     TrackArgs t;
     CUtensorMap tmap;  // ring as [stream][row][32 x u32], SWIZZLE_128B, box 32 x 32 x 1
+    // persistent CTAs over work items (chunk j, channel c), chunk-major: item
+    // (j, c) runs channel c for up to chunk_epochs epochs once item (j-1, c)
+    // has finished (ready[c] == j), so a launch has no wave-quantisation tail
+    int* next;          // work-item counter (zeroed before the launch)
+    int* ready;         // [n_channels] chunks finished (zeroed before the launch)
+    int n_items, n_channels, chunk_epochs;
 };
 
 template <int T>
@@ -71,6 +77,7 @@ struct SegSmem {
     int64_t rec_esh;
     double rec_eenv;
     int pending, stop;
+    int item, prn_cached;
     double nco_ph1, nco_cp1;
     uint32_t chipw[CHIP_EXT / 32 + 1];  // bit m % 32 of word m / 32: chip[m] > 0
     int16_t tm[SEG_TRANS_P];  // chip index of the g-th chip transition of one period
@@ -352,299 +359,336 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
     const uint32_t boff = ((sbase + tend + 1023u) & ~1023u) - sbase;  // unit buffers, 1024-B aligned
     const float4* rot4 = reinterpret_cast<const float4*>(s->rot);
 
-    const int cidx = blockIdx.x;
-    const int strm = a.chan_stream[cidx];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ctl = SEG_NW - 1;  // also finishes each epoch (metrics, record) before its runs
-    constexpr int NWT = 32 * SEG_NW;
     constexpr int V = 2 * T + 2;
     const int nh = n / 2;
     const bool noop = a.lc.kernel == L1RXG_KERNEL_NOOP;
-    const int64_t avail = a.avail[strm];
     const int64_t R = a.ring_cap;  // multiple of 32
-    const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
     const float scale = SEG_CVT_SCALE;
 
     if (tid == 0) {
-        s->ch = a.chans[cidx];
         for (int w = 0; w < SEG_NW; ++w)
             for (int b = 0; b < SEG_NBUF; ++b)
                 mbar_init(&s->fbar[w][b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s->pending = 0;
-        s->stop = 0;
+        s->prn_cached = -1;
     }
     for (int k = tid; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
     for (int r = tid; r < truns; r += blockDim.x)
-        tab[r] = 0;
-    __syncthreads();
-    {
-        const int8_t* cc = a.codes + s->ch.prn * 1023;
-        for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
-            uint32_t wv = 0;
-            for (int b = 0; b < 32; ++b)
-                wv |= (cc[(32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
-            s->chipw[q] = wv;
-        }
-        if (warp == ctl) {  // ballot-scan of the code's transitions
-            int running = 0;
-            for (int base = 0; base < 1023; base += 32) {
-                const int r = base + lane;
-                const bool t = r < 1023 && cc[r] != cc[(r + 1022) % 1023];
-                const unsigned mask = __ballot_sync(0xffffffffu, t);
-                const int before = __popc(mask & ((1u << lane) - 1u));
-                if (r < 1023) {
-                    if (t)
-                        s->tm[running + before] = (int16_t)r;
-                    s->cum[r] = (int16_t)(running + before + (t ? 1 : 0));
-                }
-                running += __popc(mask);
-            }
-            if (lane == 0) {
-                s->L = running;
-                s->inv_L = 1.f / (float)running;
-            }
-        }
-    }
-    if (tid == 0) {
-        const l1rxg_channel& ch = s->ch;
-        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
-                    ch.carrier_phase_rad, a.lc.fs, n);
-        s->c.inv_cps = fast_rcp(s->c.cps);  // tap_boundary's estimate
-    }
-    __syncthreads();
-    if (tid < 32) {
-        float sn, co;
-        sincosf((float)(s->c.w * (double)tid), &sn, &co);
-        s->rot[tid] = make_float2(co * scale, sn * scale);
-        s->rotq[(tid & 7) * 4 + (tid >> 3)] = make_float2(co * scale, sn * scale);
-    }
-
-    // ---- per-work-warp unit stream (uniform across the warp's lanes) ----
-    // unit = (epoch ie, warp-unit ik): rows [32 ik, 32 ik + 32) of epoch ie,
-    // rows counted from the ring row holding the epoch's first sample
-    // epochs whose windows are ingested and still in the ring
-    int e_adm = 0;
-    if (!noop && off0 >= 0 && off0 >= avail - R && off0 + n <= avail)
-        e_adm = (int)min((int64_t)a.max_epochs, (avail - off0 - n) / n + 1);
-    int iss_e = 0, iss_k = warp;
-    int64_t iss_pos = e_adm > 0 ? off0 % R : 0;  // ring position of epoch iss_e's first sample
-    int iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+        tab[r] = 0;  // every later epoch leaves the table clean (owners clear their entries)
+    // per-warp TMA unit counters: persistent across work items (every item
+    // waits for its last copies, so the mbarrier parities continue)
     int issued = 0, consumed = 0;
-    auto issue_one = [&]() -> bool {
-        if (iss_e >= e_adm)
-            return false;
-        const int b = issued & (SEG_NBUF - 1);
-        if (lane == 0) {
-            uint64_t* bar = &s->fbar[warp][b];
-            mbar_expect_tx(bar, SEG_UNIT_BYTES);
-            tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
-                          (int)(iss_pos >> 5) + 32 * iss_k, strm, bar);
-        }
-        ++issued;
-        iss_k += SEG_NW;
-        if (iss_k >= iss_nwu) {
-            ++iss_e;
-            iss_k = warp;
-            iss_pos += n;
-            if (iss_pos >= R)
-                iss_pos -= R;
-            iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
-        }
-        return true;
-    };
-    if (warp < SEG_NW)
-        while (issued < SEG_NBUF && issue_one()) {
-        }
-    __syncthreads();
 
-    int e = 0;
-    int64_t done = a.ecount[cidx];
-    int rec_i = (int)(done % a.max_records);
     for (;;) {
-        const int64_t off = s->ch.sample_offset_next_epoch;
-        if (s->ch.state == L1RXG_IDLE || e >= a.max_epochs || off + n > avail)
+        // ---- next work item
+        if (tid == 0)
+            s->item = atomicAdd(sa.next, 1);
+        __syncthreads();
+        const int item = s->item;
+        if (item >= sa.n_items)
             break;
-        if (off < avail - R || off < 0) {  // window already overwritten
-            if (tid == 0)
-                a.status[cidx] = 1;
-            break;
+        const int cidx = item % sa.n_channels;
+        const int chunk = item / sa.n_channels;
+        const int max_e = min(sa.chunk_epochs, a.max_epochs - chunk * sa.chunk_epochs);
+        if (tid == 0) {
+            if (chunk > 0) {  // the channel's previous chunk (dequeued earlier, so resident) must be done
+                while (*(volatile int*)&sa.ready[cidx] < chunk)
+                    __nanosleep(2000);
+                __threadfence();
+            }
+            // state written by another SM: read around L1
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.chans + cidx);
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s->ch);
+            for (int q = 0; q < (int)(sizeof(l1rxg_channel) / 8); ++q)
+                dst[q] = __ldcg(src + q);
+            s->pending = 0;
+            s->stop = 0;
         }
-        // the epoch's NCO constants stay in shared memory (s->c, unchanged
-        // until the loop update) rather than in registers across the runs
-        const EpochConsts& c = s->c;
-        // the step table of this epoch: every thread (the control warp too)
-        if (!noop) {
-            seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT);
+        __syncthreads();
+        if (max_e <= 0) {  // past the launch's epoch budget
             __syncthreads();
+            if (tid == 0)
+                atomicExch(&sa.ready[cidx], chunk + 1);
+            continue;
         }
-        if (warp == ctl) {
-            const EpochConsts cc = s->c;
-            nco_advance_lanes(s->nco_ph1, s->nco_cp1, cc, s->ch, lane);
-            if (s->pending) {
-                finish_epoch<T>(s, a, lane, true);
-                if (lane == 0)
-                    s->pending = 0;
+        const int strm = a.chan_stream[cidx];
+        const int64_t avail = a.avail[strm];
+        const int64_t off0 = s->ch.sample_offset_next_epoch;
+        if (s->prn_cached != s->ch.prn) {  // the PRN's chip bits and transition list
+            __syncthreads();
+            const int8_t* cc = a.codes + s->ch.prn * 1023;
+            for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
+                uint32_t wv = 0;
+                for (int b = 0; b < 32; ++b)
+                    wv |= (cc[(32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
+                s->chipw[q] = wv;
+            }
+            if (warp == ctl) {  // ballot-scan of the code's transitions
+                int running = 0;
+                for (int base = 0; base < 1023; base += 32) {
+                    const int r = base + lane;
+                    const bool t = r < 1023 && cc[r] != cc[(r + 1022) % 1023];
+                    const unsigned mask = __ballot_sync(0xffffffffu, t);
+                    const int before = __popc(mask & ((1u << lane) - 1u));
+                    if (r < 1023) {
+                        if (t)
+                            s->tm[running + before] = (int16_t)r;
+                        s->cum[r] = (int16_t)(running + before + (t ? 1 : 0));
+                    }
+                    running += __popc(mask);
+                }
+                if (lane == 0) {
+                    s->L = running;
+                    s->inv_L = 1.f / (float)running;
+                    s->prn_cached = s->ch.prn;
+                }
             }
         }
-        float acc[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            acc[v] = 0.f;
-        if (warp < SEG_NW) {
-            const int lead = (int)(off & 31);
-            const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
-            bool snapped = false;
-            float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
-            for (int k = warp; k < nwu && !noop; k += SEG_NW) {
-                const int r = 32 * k + lane;  // the lane's run: epoch run index
-                const int i0 = 32 * r - lead;  // epoch index of its first sample
-                const int jlo = max(0, -i0);
-                const int jhi = max(jlo, min(32, n - i0));
-                const E w = tab[r];
-                tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
-                uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
-                if (w & 0x300u) {  // a half with two positions: its steppers take the slow path
-#pragma unroll
+        if (tid == 0) {
+            const l1rxg_channel& ch = s->ch;
+            make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
+                        ch.carrier_phase_rad, a.lc.fs, n);
+            s->c.inv_cps = fast_rcp(s->c.cps);  // tap_boundary's estimate
+        }
+        __syncthreads();
+        if (tid < 32) {
+            float sn, co;
+            sincosf((float)(s->c.w * (double)tid), &sn, &co);
+            s->rot[tid] = make_float2(co * scale, sn * scale);
+            s->rotq[(tid & 7) * 4 + (tid >> 3)] = make_float2(co * scale, sn * scale);
+        }
+        // ---- per-work-warp unit stream (uniform across the warp's lanes) ----
+        // unit = (epoch ie, warp-unit ik): rows [32 ik, 32 ik + 32) of epoch ie,
+        // rows counted from the ring row holding the epoch's first sample
+        // epochs whose windows are ingested and still in the ring
+        int e_adm = 0;
+        if (!noop && off0 >= 0 && off0 >= avail - R && off0 + n <= avail)
+            e_adm = (int)min((int64_t)max_e, (avail - off0 - n) / n + 1);
+        int iss_e = 0, iss_k = warp;
+        int64_t iss_pos = e_adm > 0 ? off0 % R : 0;  // ring position of epoch iss_e's first sample
+        int iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+        auto issue_one = [&]() -> bool {
+            if (iss_e >= e_adm)
+                return false;
+            const int b = issued & (SEG_NBUF - 1);
+            if (lane == 0) {
+                uint64_t* bar = &s->fbar[warp][b];
+                mbar_expect_tx(bar, SEG_UNIT_BYTES);
+                tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
+                              (int)(iss_pos >> 5) + 32 * iss_k, strm, bar);
+            }
+            ++issued;
+            iss_k += SEG_NW;
+            if (iss_k >= iss_nwu) {
+                ++iss_e;
+                iss_k = warp;
+                iss_pos += n;
+                if (iss_pos >= R)
+                    iss_pos -= R;
+                iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+            }
+            return true;
+        };
+        if (warp < SEG_NW)
+            while (issued < consumed + SEG_NBUF && issue_one()) {
+            }
+        __syncthreads();
+
+        int e = 0;
+        int64_t done = (int64_t)__ldcg(reinterpret_cast<const unsigned long long*>(a.ecount + cidx));
+        int rec_i = (int)(done % a.max_records);
+        for (;;) {
+            const int64_t off = s->ch.sample_offset_next_epoch;
+            if (s->ch.state == L1RXG_IDLE || e >= max_e || off + n > avail)
+                break;
+            if (off < avail - R || off < 0) {  // window already overwritten
+                if (tid == 0)
+                    a.status[cidx] = 1;
+                break;
+            }
+            // the epoch's NCO constants stay in shared memory (s->c, unchanged
+            // until the loop update) rather than in registers across the runs
+            const EpochConsts& c = s->c;
+            // the step table of this epoch: every thread (the control warp too)
+            if (!noop) {
+                seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT);
+                __syncthreads();
+            }
+            if (warp == ctl) {
+                const EpochConsts cc = s->c;
+                nco_advance_lanes(s->nco_ph1, s->nco_cp1, cc, s->ch, lane);
+                if (s->pending) {
+                    finish_epoch<T>(s, a, lane, true);
+                    if (lane == 0)
+                        s->pending = 0;
+                }
+            }
+            float acc[V];
+    #pragma unroll
+            for (int v = 0; v < V; ++v)
+                acc[v] = 0.f;
+            if (warp < SEG_NW) {
+                const int lead = (int)(off & 31);
+                const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
+                bool snapped = false;
+                float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
+                for (int k = warp; k < nwu && !noop; k += SEG_NW) {
+                    const int r = 32 * k + lane;  // the lane's run: epoch run index
+                    const int i0 = 32 * r - lead;  // epoch index of its first sample
+                    const int jlo = max(0, -i0);
+                    const int jhi = max(jlo, min(32, n - i0));
+                    const E w = tab[r];
+                    tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
+                    uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
+                    if (w & 0x300u) {  // a half with two positions: its steppers take the slow path
+    #pragma unroll
+                        for (int t = 0; t < T; ++t) {
+                            const int code = (int)(w >> (10 + 2 * t)) & 3;
+                            if ((code == 2 && (w & 0x100u)) || (code == 3 && (w & 0x200u)))
+                                slow |= 1u << t;
+                        }
+                    }
+                    // start chips of the taps (the reference's chip index at i0)
+                    // (the first run of an epoch starts before sample 0: its
+                    // start chip is the one at the first sample it counts)
+                    const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
+                    // |d| <= 1 chip: every tap's index is in [m0, m0 + 4]; the
+                    // 32 chip bits from m0 hold them all
+                    const int m0 = floor_idx(phs) - 2;
+                    const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
+                    // start chip of tap t: its chip bit moved to bit 31, then +1.0f / -1.0f
+                    auto start_chip = [&](int t) -> float {
+                        const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
+                        const uint32_t hb = win << (31 - (ms - m0));
+                        return __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
+                    };
+                    // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
+                    const double th = __fma_rn(c.w, (double)i0, c.phi);
+                    const double rr = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
+                    float sa_, ca_;
+                    __sincosf((float)rr, &sa_, &ca_);
+                    // half-epoch prompt: snapshot of the prompt tap before the
+                    // first run that reaches past n/2 (a thread's runs ascend)
+                    if (!snapped && i0 + 32 > nh) {
+                        snapped = true;
+    #pragma unroll
+                        for (int t = 0; t < T; ++t)
+                            if (t == a.kp) {
+                                hr = acc[2 * t];
+                                hi = acc[2 * t + 1];
+                            }
+                    }
+                    // ---- the unit's samples
+                    const int b = consumed & (SEG_NBUF - 1);
+                    mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
+                    const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
+                    float2 p16, pc0, pc1, tot;
+                    const int q0 = (int)(w & 15), q1 = (w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0;
+    #ifdef L1RXG_SEG_CHAINS4
+                    const float4* rq4 = reinterpret_cast<const float4*>(s->rotq);
+                    if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
+                        seg_run4<false>(buf, lane, rq4, q0, q1, 0, 32, p16, pc0, pc1, tot);
+                    else
+                        seg_run4<true>(buf, lane, rq4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
+    #else
+                    if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
+                        seg_run<false>(buf, lane, rot4, q0, q1, 0, 32, p16, pc0, pc1, tot);
+                    else
+                        seg_run<true>(buf, lane, rot4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
+    #endif
+                    // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
+                    // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
+                    const float2 v0 = seg_anchor(tot, ca_, sa_);
+                    const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
+                    const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
+                    const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
+    #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int code = (int)(w >> (10 + 2 * t)) & 3;
-                        if ((code == 2 && (w & 0x100u)) || (code == 3 && (w & 0x200u)))
-                            slow |= 1u << t;
+                        const float2 lo = (code & 1) ? v1 : v0;
+                        const float2 hi2 = (code & 1) ? v3 : v2;
+                        const float2 v = (code & 2) ? hi2 : lo;
+                        const float cs = start_chip(t);
+                        acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
+                        acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
                     }
+                    if (slow) {  // exact per-sample sums replace the fast ones
+    #pragma unroll
+                        for (int t = 0; t < T; ++t)
+                            if ((slow >> t) & 1u) {
+                                const int code = (int)(w >> (10 + 2 * t)) & 3;
+                                const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
+                                const float2 z = seg_anchor(
+                                    seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[t], i0, jlo, jhi, c.cps, c.base),
+                                    ca_, sa_);
+                                const float cs = start_chip(t);
+                                acc[2 * t] += fmaf(-cs, v.x, z.x);
+                                acc[2 * t + 1] += fmaf(-cs, v.y, z.y);
+                            }
+                    }
+                    if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
+                        const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[a.kp], i0,
+                                                                 jlo, max(jlo, min(jhi, nh - i0)), c.cps, c.base),
+                                                    ca_, sa_);
+                        hr += z.x;
+                        hi += z.y;
+                    }
+                    __syncwarp();
+                    ++consumed;
+                    if (issued < consumed + SEG_NBUF)
+                        issue_one();
                 }
-                // start chips of the taps (the reference's chip index at i0)
-                // (the first run of an epoch starts before sample 0: its
-                // start chip is the one at the first sample it counts)
-                const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
-                // |d| <= 1 chip: every tap's index is in [m0, m0 + 4]; the
-                // 32 chip bits from m0 hold them all
-                const int m0 = floor_idx(phs) - 2;
-                const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
-                // start chip of tap t: its chip bit moved to bit 31, then +1.0f / -1.0f
-                auto start_chip = [&](int t) -> float {
-                    const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
-                    const uint32_t hb = win << (31 - (ms - m0));
-                    return __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
-                };
-                // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
-                const double th = __fma_rn(c.w, (double)i0, c.phi);
-                const double rr = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
-                float sa_, ca_;
-                __sincosf((float)rr, &sa_, &ca_);
-                // half-epoch prompt: snapshot of the prompt tap before the
-                // first run that reaches past n/2 (a thread's runs ascend)
-                if (!snapped && i0 + 32 > nh) {
-                    snapped = true;
-#pragma unroll
+                if (!snapped) {
+    #pragma unroll
                     for (int t = 0; t < T; ++t)
                         if (t == a.kp) {
                             hr = acc[2 * t];
                             hi = acc[2 * t + 1];
                         }
                 }
-                // ---- the unit's samples
-                const int b = consumed & (SEG_NBUF - 1);
-                mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
-                const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
-                float2 p16, pc0, pc1, tot;
-                const int q0 = (int)(w & 15), q1 = (w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0;
-#ifdef L1RXG_SEG_CHAINS4
-                const float4* rq4 = reinterpret_cast<const float4*>(s->rotq);
-                if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
-                    seg_run4<false>(buf, lane, rq4, q0, q1, 0, 32, p16, pc0, pc1, tot);
-                else
-                    seg_run4<true>(buf, lane, rq4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
-#else
-                if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
-                    seg_run<false>(buf, lane, rot4, q0, q1, 0, 32, p16, pc0, pc1, tot);
-                else
-                    seg_run<true>(buf, lane, rot4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
-#endif
-                // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
-                // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
-                const float2 v0 = seg_anchor(tot, ca_, sa_);
-                const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
-                const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
-                const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
-#pragma unroll
-                for (int t = 0; t < T; ++t) {
-                    const int code = (int)(w >> (10 + 2 * t)) & 3;
-                    const float2 lo = (code & 1) ? v1 : v0;
-                    const float2 hi2 = (code & 1) ? v3 : v2;
-                    const float2 v = (code & 2) ? hi2 : lo;
-                    const float cs = start_chip(t);
-                    acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
-                    acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
-                }
-                if (slow) {  // exact per-sample sums replace the fast ones
-#pragma unroll
-                    for (int t = 0; t < T; ++t)
-                        if ((slow >> t) & 1u) {
-                            const int code = (int)(w >> (10 + 2 * t)) & 3;
-                            const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
-                            const float2 z = seg_anchor(
-                                seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[t], i0, jlo, jhi, c.cps, c.base),
-                                ca_, sa_);
-                            const float cs = start_chip(t);
-                            acc[2 * t] += fmaf(-cs, v.x, z.x);
-                            acc[2 * t + 1] += fmaf(-cs, v.y, z.y);
-                        }
-                }
-                if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
-                    const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[a.kp], i0,
-                                                             jlo, max(jlo, min(jhi, nh - i0)), c.cps, c.base),
-                                                ca_, sa_);
-                    hr += z.x;
-                    hi += z.y;
-                }
-                __syncwarp();
-                ++consumed;
-                if (issued < consumed + SEG_NBUF)
-                    issue_one();
+                acc[2 * T] = hr;
+                acc[2 * T + 1] = hi;
+                warp_partials<V>(acc, s->red, lane, warp);
             }
-            if (!snapped) {
-#pragma unroll
-                for (int t = 0; t < T; ++t)
-                    if (t == a.kp) {
-                        hr = acc[2 * t];
-                        hi = acc[2 * t + 1];
-                    }
+            __syncthreads();
+            if (warp == 0) {
+                const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
+                warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
+                if (lane == 0)
+                    s->c.inv_cps = fast_rcp(s->c.cps);
+                float sn, co;
+                sincosf((float)(s->c.w * (double)lane), &sn, &co);
+                s->rot[lane] = make_float2(co * scale, sn * scale);
+                s->rotq[(lane & 7) * 4 + (lane >> 3)] = make_float2(co * scale, sn * scale);
             }
-            acc[2 * T] = hr;
-            acc[2 * T + 1] = hi;
-            warp_partials<V>(acc, s->red, lane, warp);
+            __syncthreads();
+            if (s->stop)
+                break;
+            ++e;
+            ++done;
+            if (++rec_i == a.max_records)
+                rec_i = 0;
         }
         __syncthreads();
-        if (warp == 0) {
-            const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
-            warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
-            if (lane == 0)
-                s->c.inv_cps = fast_rcp(s->c.cps);
-            float sn, co;
-            sincosf((float)(s->c.w * (double)lane), &sn, &co);
-            s->rot[lane] = make_float2(co * scale, sn * scale);
-            s->rotq[(lane & 7) * 4 + (lane >> 3)] = make_float2(co * scale, sn * scale);
+        if (warp == ctl && s->pending)
+            finish_epoch<T>(s, a, lane, true);
+        if (warp < SEG_NW) {  // drain this item's prefetched copies (the parities continue)
+            for (int u = consumed; u < issued; ++u)
+                mbar_wait(&s->fbar[warp][u & (SEG_NBUF - 1)], (uint32_t)((u / SEG_NBUF) & 1));
+            consumed = issued;
         }
         __syncthreads();
-        if (s->stop)
-            break;
-        ++e;
-        ++done;
-        if (++rec_i == a.max_records)
-            rec_i = 0;
-    }
-    __syncthreads();
-    if (warp == ctl && s->pending)
-        finish_epoch<T>(s, a, lane, true);
-    if (warp < SEG_NW) {  // never leave a bulk copy in flight into freed smem
-        for (int u = consumed; u < issued; ++u)
-            mbar_wait(&s->fbar[warp][u & (SEG_NBUF - 1)], (uint32_t)((u / SEG_NBUF) & 1));
-    }
-    __syncthreads();
-    if (tid == 0) {
-        a.chans[cidx] = s->ch;
-        a.ecount[cidx] = done;
+        if (tid == 0) {
+            a.chans[cidx] = s->ch;
+            a.ecount[cidx] = done;
+        }
+        __threadfence();  // records, tap sums and state visible before the chunk is marked done
+        __syncthreads();
+        if (tid == 0)
+            atomicExch(&sa.ready[cidx], chunk + 1);
     }
 }
 

@@ -433,3 +433,33 @@ def test_segment_mode_rejects_other_formats(ctx):
     with pytest.raises(ValueError):
         Tracker(ctx, abi.FMT_INT16_IQ, 4.0e6, 0.0, [init], ring_samples=8 * 4000,
                 cta_mode=abi.CTA_SEGMENT)
+
+
+def test_segment_persistent_work_items(ctx, oracle_mod, monkeypatch):
+    """The segment correlator's persistent CTAs take (chunk, channel) work
+    items in order; a CTA that runs many items (grid capped to 3 CTAs) and
+    chunks that wait for their predecessors give bit-identical records to the
+    full grid; per-epoch replay parity on top."""
+    import torch
+    fs, ms, nrec = 65.472e6, 40, 3
+    n = 65472
+    raw, inits, cstream = _batch_scenario(nrec, fs, ms, seed=57)
+    taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+    cfg = abi.TrackingCfg.default()
+    dev = torch.from_numpy(raw).cuda()
+    outs = []
+    for grid in (None, "3"):
+        if grid:
+            monkeypatch.setenv("L1RXG_SEG_GRID", grid)
+        trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=nrec,
+                      taps=taps, cfg=cfg, ring_samples=8 * n, max_records=ms, cta_mode=abi.CTA_SEGMENT)
+        trk.attach_device(dev.data_ptr(), raw.shape[1] // 4, raw.shape[1])
+        trk.run()
+        trk.sync()
+        outs.append([trk.records(c, tap_sums=True) for c in range(len(inits))])
+        assert trk.epoch_counts().min() >= ms - 2
+    monkeypatch.delenv("L1RXG_SEG_GRID", raising=False)
+    for c in range(len(inits)):
+        assert outs[0][c][0].tobytes() == outs[1][c][0].tobytes()
+    x = oracle_mod.ingest(raw[cstream[0]], abi.FMT_INT16_IQ, fs)
+    replay_check(oracle_mod, inits[0], outs[1][0][0], x, n, cfg, taps, fs, tap_sums=outs[1][0][1])
