@@ -291,15 +291,16 @@ __device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int p
     if (q == 0)
         return;
     const int sh = 10 + 2 * k;
-    const int h = q > 16;
-    const E code = q == 16 ? 1 : 2 + h;
-    const E qf = q == 16 ? 0 : (E)(q - 16 * h) << (4 * h);
+    const int h = q >> 4 & (q != 16);  // half 1 for q in 17..31
+    const bool mid = q == 16;
+    const E qf = mid ? 0 : (E)(q & 15) << (4 * h);
+    const E code = mid ? 1 : 2 + h;
     const E prev = atomicOr(&tab[r], qf | (code << sh));
     const int pf = (int)((prev >> (4 * h)) & 15);
-    if (q != 16 && pf != 0 && pf != q - 16 * h)
-        atomicOr(&tab[r], (E)1 << (8 + h));
-    if ((prev >> sh) & 3)
-        atomicOr(&tab[r], (E)1 << (10 + 2 * T + k));
+    const bool conflict = !mid && pf != 0 && pf != (q & 15);
+    const bool twice = ((prev >> sh) & 3) != 0;
+    if (conflict || twice)  // rare: ties, or two steps of one tap at low sample rates
+        atomicOr(&tab[r], (conflict ? (E)1 << (8 + h) : (E)0) | (twice ? (E)1 << (10 + 2 * T + k) : (E)0));
 }
 
 // transitions of the PRN's code at chip indices <= m (CodeTables' trans_count)
@@ -308,38 +309,56 @@ __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
     const int p = m / 1023;
     return p * s->L + s->cum[m - p * 1023];
 }
-// chip index of the g-th transition (any period): p * 1023 + tm[g - p * L]
-template <int T>
-__device__ __forceinline__ int seg_trans_at(const SegSmem<T>* s, int g) {
-    const int p = (int)(((float)g + 0.5f) * s->inv_L);
-    return p * 1023 + s->tm[g - p * s->L];
+
+// Exact first sample b >= 1 whose replica index of tap offset d reaches m
+// (tap_boundary's contract, lo = 1, hi = n - 1): the estimate e = (m + kb) /
+// cps, kb = -d - base, is within ~1e-10 samples of the reference's crossing;
+// away from ties ceil(e) is the answer (one round-up add of 1.5 * 2^52),
+// near one the reference expression decides (tap_boundary).
+__device__ __forceinline__ int seg_boundary(int m, double kb, double d, const EpochConsts& c) {
+    const double e = ((double)m + kb) * c.inv_cps;
+    if (fabs(e - rint(e)) > 1e-9)
+        return __double2loint(__dadd_ru(e, 6755399441055744.0));
+    return tap_boundary(m, d, c, 1, c.n - 1);
 }
 
-// Step table fill for one epoch (the work threads, after the loop update):
-// every chip transition m of every tap with its step inside the epoch,
-// located exactly (tap_boundary), entered in the run holding it.  A step at
-// a run's first sample needs no entry (the run's start chip has it).  Two
-// positions competing for one half's capture, or two steps of one tap in
-// one run, send that tap to the slow path for that run.
+// Step table fill for one epoch (every thread, after the loop update): every
+// chip transition m of every tap with its step inside the epoch, located
+// exactly, entered in the run holding it (seg_enter).  Transition g of the
+// code is chip index p * 1023 + tm[q], g = p * L + q; each thread walks its
+// g's with stride nthr (< L) and carries (p, q) along, two at a time so the
+// fp64 estimates and the atomics of the pair overlap.
 template <int T>
 __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const SegSmem<T>* s,
                                         const EpochConsts& c, int lead, int tid, int nthr) {
-    const int n = c.n;
+    const int n = c.n, L = s->L;
 #pragma unroll 1
     for (int k = 0; k < T; ++k) {
         const double dk = s->d[k];
+        const double kb = -dk - c.base;
         // transitions at chip indices in (idx(0), idx(n-1)]
         const int g0 = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));
         const int g1 = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk));
-        // two transitions per iteration: the fp64 searches and the atomics
-        // of the pair overlap
-        for (int g = g0 + tid; g < g1; g += 2 * nthr) {
+        int g = g0 + tid;
+        int p = g / L, q = g - p * L;
+        for (; g < g1; g += 2 * nthr) {
+            int q2 = q + nthr, p2 = p;
+            if (q2 >= L) {
+                q2 -= L;
+                ++p2;
+            }
             const bool two = g + nthr < g1;
-            const int ba = tap_boundary(seg_trans_at(s, g), dk, c, 1, n - 1);
-            const int bb = two ? tap_boundary(seg_trans_at(s, g + nthr), dk, c, 1, n - 1) : 0;
+            const int ba = seg_boundary(p * 1023 + s->tm[q], kb, dk, c);
+            const int bb = two ? seg_boundary(p2 * 1023 + s->tm[q2], kb, dk, c) : 0;
             seg_enter<T>(tab, ba + lead, k);
             if (two)
                 seg_enter<T>(tab, bb + lead, k);
+            q = q2 + nthr;
+            p = p2;
+            if (q >= L) {
+                q -= L;
+                ++p;
+            }
         }
     }
 }
