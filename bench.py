@@ -113,6 +113,19 @@ def stream_manifest(raw_row, seed, svs, fmt):
                      "delay_chips": round(sv.delay_chips, 4)} for sv in svs]}
 
 
+def synth_config4(ctx, seed0, n_rec, blocks, fs, out=None):
+    """Config-4 recordings seed0 .. seed0 + n_rec - 1 on the GPU in one call
+    (l1rxg_simulate, the CUDA SimStream restatement): recording j's visible
+    SVs (scenario(4, seed0 + j)) padded to 12 with silent entries; noise keyed
+    by (seed0, j)."""
+    from paper_1907_00463_b200 import simsource as ss
+    rows = []
+    for j in range(n_rec):
+        _, svs, _ = scenario(4, seed0 + j)
+        rows.append(svs + [ss.Sv(prn=1, cn0_dbhz=-200.0)] * (12 - len(svs)))
+    return ss.synth_gpu(ctx, blocks, fs, rows, fmt="int16_iq", seed=seed0, out=out)
+
+
 def channel_inits(chans, fs, lock_fail_limit_inf=True):
     from paper_1907_00463_b200 import simsource as ss
     from paper_1907_00463_b200.tracking import init_channel_from_acquisition
@@ -394,10 +407,12 @@ def run_batch(args, rank, world, local, dist, emit=True):
     inits, cstream = [], []
     bytes_rec = blocks * n * 4
     raw = torch.empty((len(recs), bytes_rec), dtype=torch.uint8, device=dev)
+    ctx = Context(local)
     t_syn = time.perf_counter()
+    if len(recs):  # recs are consecutive: one simulator call for this rank's recordings
+        synth_config4(ctx, c["seed"] + recs[0], len(recs), blocks, fs, out=raw)
     for j, r in enumerate(recs):
         _, svs, chans = scenario(4, c["seed"] + r)
-        raw[j] = ss.synth(blocks, fs, svs, fmt="int16_iq", seed=c["seed"] + r, device=str(dev))
         ci = channel_inits(chans, fs)
         inits += ci
         cstream += [j] * len(ci)
@@ -406,7 +421,9 @@ def run_batch(args, rank, world, local, dist, emit=True):
     C_ch = len(inits)
     manifest0 = stream_manifest(raw[0], c["seed"] + recs[0], scenario(4, c["seed"] + recs[0])[1],
                                 "int16_iq") if len(recs) else None
-    ctx = Context(local)
+    if manifest0:
+        manifest0["generator"] = ("l1rxg_simulate (CUDA SimStream raw mode), Philox noise keyed by "
+                                  "(seed %d, recording index)" % (c["seed"] + recs[0]))
     trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs),
                   taps=taps, cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks,
                   cta_mode={"segment": abi.CTA_SEGMENT, "throughput": abi.CTA_THROUGHPUT,
@@ -626,10 +643,11 @@ def run_batch_reference(args, rank):
     T = taps.n_counted
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     xs, inits, cstream = [], [], []
+    from paper_1907_00463_b200.tracking import Context
+    raws = synth_config4(Context(0), c["seed"], R, per_step, fs).cpu().numpy()  # the device arm's rank-0 bytes
     for r in range(R):
         _, svs, chans = scenario(4, c["seed"] + r)
-        raw = ss.synth(per_step, fs, svs, fmt="int16_iq", seed=c["seed"] + r, device=dev)
-        xs.append(oracle.ingest(raw.cpu().numpy(), abi.FMT_INT16_IQ, fs))
+        xs.append(oracle.ingest(raws[r], abi.FMT_INT16_IQ, fs))
         ci = channel_inits(chans, fs)
         inits += ci
         cstream += [r] * len(ci)

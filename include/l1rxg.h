@@ -350,6 +350,30 @@ int l1rxg_search_grid(l1rxg_ctx* ctx, int format, const void* bytes,
 int l1rxg_search_grid_timing(l1rxg_ctx* ctx, double* ingest_fold_ms,
                              double* corr_ms);
 
+/* ---- scenario synthesizer (test and benchmark corpora) ----------------- */
+/* SimSatellite in raw mode (simsource.hpp:24-40). */
+typedef struct {
+    double code_delay_chips;
+    double doppler_hz;
+    double doppler_rate_hz_per_s;
+    double initial_carrier_phase_rad;
+    double cn0_dbhz;
+    int32_t prn;
+    int32_t pad_;
+} l1rxg_sim_sv;
+
+/* SimStream::next_block + generate_recording (simsource.hpp:194-413) on the
+ * GPU for n_rec recordings at once: recording r has the n_sv satellites
+ * svs[r * n_sv ...], milliseconds [ms0, ms0 + n_ms) are written as raw bytes
+ * of `format` (int8/int16 IQ; int8 real IF at if_hz is a builder extension)
+ * to dev_out + r * rec_stride_bytes (device memory).  Noise (noise != 0) is
+ * Philox4x32-10 keyed by (seed, r) and counted by sample index, so any
+ * chunking of a recording gives the same bytes.  Synchronous. */
+int l1rxg_simulate(l1rxg_ctx* ctx, const l1rxg_sim_sv* svs, int n_sv, int n_rec,
+                   double sample_rate_hz, double if_frequency_hz, int format,
+                   int64_t ms0, int n_ms, uint64_t seed, int noise,
+                   void* dev_out, int64_t rec_stride_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ EXPORTS = [
     "l1rxg_tracker_sync", "l1rxg_tracker_channels", "l1rxg_tracker_epoch_counts",
     "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_reset",
     "l1rxg_tracker_stream", "l1rxg_tracker_read_samples",
-    "l1rxg_tracker_timing", "l1rxg_search_grid", "l1rxg_search_grid_timing",
+    "l1rxg_tracker_timing", "l1rxg_search_grid", "l1rxg_search_grid_timing", "l1rxg_simulate",
 ]
 
 
@@ -82,6 +82,8 @@ def lib():
     _sig(L, "l1rxg_search_grid", C.c_int, vp, C.c_int, vp, C.c_int, i64, C.c_double, C.c_double,
          C.c_int, P(C.c_int32), C.c_int, dp, C.c_int, C.c_int, C.c_int, dp)
     _sig(L, "l1rxg_search_grid_timing", C.c_int, vp, dp, dp)
+    _sig(L, "l1rxg_simulate", C.c_int, vp, vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, i64,
+         C.c_int, C.c_uint64, C.c_int, vp, i64)
     if L.l1rxg_abi_version() != abi.ABI_VERSION:
         raise L1rxgError("libl1rxg ABI version mismatch")
     return L

@@ -161,6 +161,13 @@ class TrackerDesc(C.Structure):
                 ("taps", Taps), ("cfg", TrackingCfg)]
 
 
+class SimSv(C.Structure):
+    """l1rxg_sim_sv: SimSatellite in raw mode (simsource.hpp:24-40)."""
+    _fields_ = [("code_delay_chips", C.c_double), ("doppler_hz", C.c_double),
+                ("doppler_rate_hz_per_s", C.c_double), ("initial_carrier_phase_rad", C.c_double),
+                ("cn0_dbhz", C.c_double), ("prn", C.c_int32), ("pad_", C.c_int32)]
+
+
 RECORD_DTYPE_FIELDS = [f[0] for f in EpochRecord._fields_]
 
 

@@ -22,6 +22,7 @@
 #include "ingest.cuh"
 #include "search.cuh"
 #include "segcorr.cuh"
+#include "simgen.cuh"
 #include "l1rxg.h"
 
 using namespace l1rxg;
@@ -377,6 +378,7 @@ struct l1rxg_ctx {
     int8_t* d_codes = nullptr;
     DevBuf iq64, iq32, states, prns, sums, corr;
     DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
+    DevBuf gsim;  // simulator scenario
     DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
     std::vector<int32_t> gMt_prns;                        // PRNs whose circulants gMt holds
     cublasHandle_t blas = nullptr;
@@ -593,7 +595,7 @@ int l1rxg_destroy(l1rxg_ctx* c) {
     for (auto e : c->gev)
         if (e)
             cudaEventDestroy(e);
-    for (DevBuf* b : {&c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
+    for (DevBuf* b : {&c->gsim, &c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
                       &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist, &c->gA,
                       &c->gMt, &c->gC})
         b->release();
@@ -1577,6 +1579,51 @@ int l1rxg_search_grid_timing(l1rxg_ctx* c, double* ingest_fold_ms, double* corr_
         return set_err(L1RXG_EINVAL, "null context");
     if (ingest_fold_ms) *ingest_fold_ms = c->grid_ms[0];
     if (corr_ms) *corr_ms = c->grid_ms[1];
+    return 0;
+}
+
+// ---- scenario synthesizer (SimStream raw mode, simsource.hpp:194-413) ----
+int l1rxg_simulate(l1rxg_ctx* c, const l1rxg_sim_sv* svs, int n_sv, int n_rec, double fs, double if_hz,
+                   int format, int64_t ms0, int n_ms, uint64_t seed, int noise, void* dev_out,
+                   int64_t rec_stride_bytes) {
+    if (!c || (!svs && n_sv > 0) || !dev_out)
+        return set_err(L1RXG_EINVAL, "null argument");
+    if (n_sv < 0 || n_sv > SIM_MAX_SV || n_rec < 1 || n_ms < 1 || ms0 < 0)
+        return set_err(L1RXG_EINVAL, "n_sv must be in 0..32, n_rec and n_ms >= 1, ms0 >= 0");
+    const int n = static_cast<int>(std::llround(fs / 1000.0));
+    if (!(fs > 0) || std::fabs(fs / 1000.0 - n) > 1e-9)  // simsource.hpp:203-206
+        return set_err(L1RXG_EINVAL, "simulator requires an integer number of samples per ms");
+    if (format != L1RXG_FMT_INT8_IQ && format != L1RXG_FMT_INT16_IQ && format != L1RXG_FMT_INT8_REAL_IF)
+        return set_err(L1RXG_EINVAL, "format must be int8_iq, int16_iq or int8_real_if");
+    const int bps = bytes_per_sample(format);
+    if (rec_stride_bytes < static_cast<int64_t>(n_ms) * n * bps)
+        return set_err(L1RXG_EINVAL, "rec_stride_bytes shorter than one recording");
+    std::vector<SimSvDev> h(static_cast<size_t>(n_rec) * std::max(1, n_sv));
+    for (int r = 0; r < n_rec; ++r)
+        for (int k = 0; k < n_sv; ++k) {
+            const l1rxg_sim_sv& v = svs[static_cast<size_t>(r) * n_sv + k];
+            if (v.prn < 1 || v.prn > 32)
+                return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
+            SimSvDev& d = h[static_cast<size_t>(r) * n_sv + k];
+            d.delay_s = v.code_delay_chips / CHIP_RATE_HZ;
+            d.fd_over_l1 = v.doppler_hz / F_L1_HZ;
+            d.rate_over_l1 = v.doppler_rate_hz_per_s / F_L1_HZ;
+            d.phase0 = v.initial_carrier_phase_rad;
+            d.amp = (noise ? 0.25 : 1.0) * std::sqrt(std::pow(10.0, v.cn0_dbhz / 10.0) / fs);  // :237-239
+            d.prn = v.prn;
+            d.pad = 0;
+        }
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->compute;
+    if (c->gsim.ensure(h.size() * sizeof(SimSvDev)))
+        return L1RXG_ENOMEM;
+    CK(cudaMemcpyAsync(c->gsim.p, h.data(), h.size() * sizeof(SimSvDev), cudaMemcpyHostToDevice, st));
+    const dim3 grid(static_cast<unsigned>(n_ms), static_cast<unsigned>(n_rec));
+    simgen_kernel<<<grid, 256, 0, st>>>(static_cast<const SimSvDev*>(c->gsim.p), n_sv, c->d_codes, n, fs, if_hz,
+                                        ms0, format, static_cast<unsigned long long>(seed), noise ? 1 : 0,
+                                        static_cast<unsigned char*>(dev_out), rec_stride_bytes);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
     return 0;
 }
 

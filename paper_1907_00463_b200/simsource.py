@@ -157,3 +157,39 @@ def truth_channel_start(sv: Sv, fs: float):
     the acquisition hit run_closed_loop derives (test_tracking.cpp:378-384)."""
     boundary = int(round(sv.delay_chips / CHIP_RATE * fs))
     return boundary, sv.doppler_hz
+
+
+def synth_gpu(ctx, n_ms: int, fs: float, recordings, *, fmt: str = "int16_iq", if_hz: float = 0.0,
+              seed: int = 1, noise: bool = True, ms0: int = 0, out=None):
+    """Many recordings at once on the GPU (l1rxg_simulate, the CUDA
+    restatement of SimStream's raw mode, simsource.hpp:194-413):
+    `recordings` is a list of Sv lists (one per recording, the same length);
+    returns (or fills) a torch uint8 tensor [n_rec, n_ms * n * bytes_per_sample]
+    on the context's device.  Noise is Philox-counted by sample index, so
+    chunked calls (ms0) give the same bytes as one call."""
+    import ctypes as C
+
+    import torch
+
+    from . import abi
+    from ._native import check
+    fmts = {"int8_iq": (abi.FMT_INT8_IQ, 2), "int16_iq": (abi.FMT_INT16_IQ, 4),
+            "int8_real_if": (abi.FMT_INT8_REAL_IF, 1)}
+    f, bps = fmts[fmt]
+    n = int(round(fs / 1000.0))
+    n_rec = len(recordings)
+    n_sv = len(recordings[0]) if n_rec else 0
+    arr = (abi.SimSv * max(1, n_rec * n_sv))()
+    for r, svs in enumerate(recordings):
+        if len(svs) != n_sv:
+            raise ValueError("every recording needs the same number of satellites")
+        for k, sv in enumerate(svs):
+            arr[r * n_sv + k] = abi.SimSv(sv.delay_chips, sv.doppler_hz, sv.doppler_rate, sv.phase0,
+                                          sv.cn0_dbhz, sv.prn, 0)
+    nbytes = n_ms * n * bps
+    if out is None:
+        out = torch.empty((n_rec, nbytes), dtype=torch.uint8, device=f"cuda:{ctx.device}")
+    check(ctx._lib.l1rxg_simulate(ctx.handle, C.cast(arr, C.c_void_p), n_sv, n_rec, C.c_double(fs),
+                                 C.c_double(if_hz), f, C.c_int64(ms0), n_ms, C.c_uint64(seed & (2**64 - 1)),
+                                 1 if noise else 0, C.c_void_p(out.data_ptr()), C.c_int64(out.stride(0))))
+    return out

@@ -463,3 +463,65 @@ def test_segment_persistent_work_items(ctx, oracle_mod, monkeypatch):
         assert outs[0][c][0].tobytes() == outs[1][c][0].tobytes()
     x = oracle_mod.ingest(raw[cstream[0]], abi.FMT_INT16_IQ, fs)
     replay_check(oracle_mod, inits[0], outs[1][0][0], x, n, cfg, taps, fs, tap_sums=outs[1][0][1])
+
+
+# ---- the CUDA scenario synthesizer (SimStream raw mode, l1rxg_simulate) ----
+
+def _sim_svs():
+    return [ss.Sv(prn=7, cn0_dbhz=48.0, doppler_hz=1200.0, delay_chips=61.38, phase0=0.3),
+            ss.Sv(prn=12, cn0_dbhz=44.0, doppler_hz=-2600.0, delay_chips=500.25, phase0=1.1)]
+
+
+@pytest.mark.parametrize("fmt", ["int16_iq", "int8_iq", "int8_real_if"])
+def test_simulator_matches_torch_restatement_noise_free(ctx, fmt):
+    """Noise-free bytes agree with the vectorised restatement (simsource.py)
+    to one LSB (fp32 vs fp64 cos/sin at rounding ties only)."""
+    fs, ms = 16.368e6, 6
+    if_hz = 4.092e6 if fmt == "int8_real_if" else 0.0
+    svs = _sim_svs()
+    g = ss.synth_gpu(ctx, ms, fs, [svs], fmt=fmt, if_hz=if_hz, noise=False).cpu().numpy()[0]
+    t = ss.synth(ms, fs, svs, fmt=fmt, if_hz=if_hz, noise=False, device="cuda").cpu().numpy()
+    dt = np.int16 if fmt == "int16_iq" else np.int8
+    a, b = g.view(dt).astype(np.int64), t.view(dt).astype(np.int64)
+    d = np.abs(a - b)
+    assert d.max() <= 1 and (d == 0).mean() > 0.999, (d.max(), (d == 0).mean())
+
+
+def test_simulator_superposition_chunking_and_reproducibility(ctx):
+    """test_simsource.cpp:80-119 properties: a two-SV stream is the sum of the
+    single-SV streams (noise-free, within quantisation); fixed-seed bytes are
+    reproducible and independent of chunking (ms0); recordings differ."""
+    fs, ms = 16.368e6, 4
+    svs = _sim_svs()
+    both = ss.synth_gpu(ctx, ms, fs, [svs], noise=False).cpu().numpy()[0].view(np.int16).astype(np.int64)
+    one = ss.synth_gpu(ctx, ms, fs, [svs[:1]], noise=False).cpu().numpy()[0].view(np.int16).astype(np.int64)
+    two = ss.synth_gpu(ctx, ms, fs, [svs[1:]], noise=False).cpu().numpy()[0].view(np.int16).astype(np.int64)
+    assert np.abs(both - (one + two)).max() <= 1
+    a = ss.synth_gpu(ctx, ms, fs, [svs, svs], seed=77).cpu().numpy()
+    b = ss.synth_gpu(ctx, ms, fs, [svs, svs], seed=77).cpu().numpy()
+    assert a.tobytes() == b.tobytes()
+    assert a[0].tobytes() != a[1].tobytes()  # noise keyed by recording
+    c0 = ss.synth_gpu(ctx, 1, fs, [svs, svs], seed=77, ms0=0).cpu().numpy()
+    c1 = ss.synth_gpu(ctx, ms - 1, fs, [svs, svs], seed=77, ms0=1).cpu().numpy()
+    assert np.concatenate([c0, c1], axis=1).tobytes() == a.tobytes()
+
+
+def test_simulator_noise_and_post_correlation_snr(ctx):
+    """Noise of sigma/sqrt(2) per component (simsource.hpp:325-327) and the
+    post-correlation SNR over 1 ms = C/N0 - 30 dB (test_simsource.cpp:149-179),
+    measured with the GPU correlator (open-loop batch at the true code phase)."""
+    fs, ms, cn0 = 5e6, 400, 45.0
+    n = 5000
+    noise_only = ss.synth_gpu(ctx, 50, fs, [[ss.Sv(prn=7, cn0_dbhz=-200.0)]], seed=3).cpu().numpy()[0]
+    v = noise_only.view(np.int16).astype(np.float64) / 32768.0
+    assert abs(v.std() - 0.25 / math.sqrt(2.0)) < 0.002 and abs(v.mean()) < 1e-3
+    raw = ss.synth_gpu(ctx, ms, fs, [[ss.Sv(prn=7, cn0_dbhz=cn0)]], seed=2024).cpu().numpy()[0]
+    iq = raw.view(np.int16).astype(np.float64) / 32768.0
+    x = (iq[0::2] + 1j * iq[1::2]).reshape(ms, n)
+    taps = abi.Taps.epl(0.5)
+    st = [abi.Nco(0.0, 1.023e6, 0.0, 0.0, 0.0) for _ in range(ms)]
+    sums, _ = ctx.correlate_batch(x, st, [7] * ms, taps, fs)
+    p = sums[:, 2 * taps.prompt] + 1j * sums[:, 2 * taps.prompt + 1]
+    m = p.mean()
+    snr = 10 * math.log10(abs(m) ** 2 / (np.abs(p - m) ** 2).sum() * (len(p) - 1))
+    assert abs(snr - (cn0 - 30.0)) < 1.0, snr
