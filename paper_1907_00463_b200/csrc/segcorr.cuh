@@ -83,7 +83,6 @@ struct SegSmem {
     int16_t tm[SEG_TRANS_P];  // chip index of the g-th chip transition of one period
     int16_t cum[1024];       // transitions at indices <= r within one period
     int L;                   // transitions per period
-    float inv_L;             // 1 / L (period of a transition index, exact for g < 2^13)
 };
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
@@ -364,7 +363,10 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
 }
 
 template <int T>
-__global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_constant__ SegArgs sa) {
+#ifndef L1RXG_SEG_MINB
+#define L1RXG_SEG_MINB 4
+#endif
+__global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const __grid_constant__ SegArgs sa) {
     typedef typename SegEntry<T>::type E;
     const TrackArgs& a = sa.t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -461,7 +463,6 @@ __global__ void __launch_bounds__(SEG_NT, 4) track_seg_kernel(const __grid_const
                 }
                 if (lane == 0) {
                     s->L = running;
-                    s->inv_L = 1.f / (float)running;
                     s->prn_cached = s->ch.prn;
                 }
             }
