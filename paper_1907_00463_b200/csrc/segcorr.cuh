@@ -71,6 +71,10 @@ struct SegSmem {
     __align__(16) float2 rot[32];
     __align__(16) float2 rotq[32];  // rot transposed by quarter: rotq[4 t + Q] = rot[8 Q + t]
     uint64_t fbar[SEG_NW][SEG_NBUF];  // per work warp: its unit buffers' TMA completion
+    struct {                          // per warp: lane 0's unit stream (kept out of registers)
+        long long pos;                // ring position of epoch e's first sample
+        int e, k, nwu, e_adm;         // next unit: epoch, warp-unit, units of that epoch; admitted epochs
+    } q[SEG_NW];
     uint64_t pbar[2];                 // (cluster exchange: unused, csize == 1)
     l1rxg_epoch_record rec;
     int64_t rec_slot;
@@ -484,33 +488,44 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
         // unit = (epoch ie, warp-unit ik): rows [32 ik, 32 ik + 32) of epoch ie,
         // rows counted from the ring row holding the epoch's first sample
         // epochs whose windows are ingested and still in the ring
-        int e_adm = 0;
-        if (!noop && off0 >= 0 && off0 >= avail - R && off0 + n <= avail)
-            e_adm = (int)min((int64_t)max_e, (avail - off0 - n) / n + 1);
-        int iss_e = 0, iss_k = warp;
-        int64_t iss_pos = e_adm > 0 ? off0 % R : 0;  // ring position of epoch iss_e's first sample
-        int iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
+        if (lane == 0 && warp < SEG_NW) {
+            int e_adm = 0;
+            if (!noop && off0 >= 0 && off0 >= avail - R && off0 + n <= avail)
+                e_adm = (int)min((int64_t)max_e, (avail - off0 - n) / n + 1);
+            const long long pos = e_adm > 0 ? off0 % R : 0;
+            s->q[warp].pos = pos;
+            s->q[warp].e = 0;
+            s->q[warp].k = warp;
+            s->q[warp].nwu = (((((int)(pos & 31)) + n + 31) >> 5) + 31) >> 5;
+            s->q[warp].e_adm = e_adm;
+        }
+        // lane 0 issues the warp's next unit (if admitted) and advances its
+        // stream; the warp learns whether a copy was issued
         auto issue_one = [&]() -> bool {
-            if (iss_e >= e_adm)
-                return false;
-            const int b = issued & (SEG_NBUF - 1);
+            int ok = 0;
             if (lane == 0) {
-                uint64_t* bar = &s->fbar[warp][b];
-                mbar_expect_tx(bar, SEG_UNIT_BYTES);
-                tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
-                              (int)(iss_pos >> 5) + 32 * iss_k, strm, bar);
+                auto& Q = s->q[warp];
+                if (Q.e < Q.e_adm) {
+                    const int b = issued & (SEG_NBUF - 1);
+                    uint64_t* bar = &s->fbar[warp][b];
+                    mbar_expect_tx(bar, SEG_UNIT_BYTES);
+                    tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
+                                  (int)(Q.pos >> 5) + 32 * Q.k, strm, bar);
+                    Q.k += SEG_NW;
+                    if (Q.k >= Q.nwu) {
+                        ++Q.e;
+                        Q.k = warp;
+                        Q.pos += n;
+                        if (Q.pos >= R)
+                            Q.pos -= R;
+                        Q.nwu = (((((int)(Q.pos & 31)) + n + 31) >> 5) + 31) >> 5;
+                    }
+                    ok = 1;
+                }
             }
-            ++issued;
-            iss_k += SEG_NW;
-            if (iss_k >= iss_nwu) {
-                ++iss_e;
-                iss_k = warp;
-                iss_pos += n;
-                if (iss_pos >= R)
-                    iss_pos -= R;
-                iss_nwu = (((((int)(iss_pos & 31)) + n + 31) >> 5) + 31) >> 5;
-            }
-            return true;
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            issued += ok;
+            return ok != 0;
         };
         if (warp < SEG_NW)
             while (issued < consumed + SEG_NBUF && issue_one()) {
