@@ -609,12 +609,15 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     // first run that reaches past n/2 (a thread's runs ascend)
                     if (!snapped && i0 + 32 > nh) {
                         snapped = true;
+                        // the prompt tap's sums by a weighted sum, not an
+                        // index (a dynamic index would put acc in local memory)
+                        hr = hi = 0.f;
     #pragma unroll
-                        for (int t = 0; t < T; ++t)
-                            if (t == a.kp) {
-                                hr = acc[2 * t];
-                                hi = acc[2 * t + 1];
-                            }
+                        for (int t = 0; t < T; ++t) {
+                            const float m = t == a.kp ? 1.f : 0.f;
+                            hr = fmaf(m, acc[2 * t], hr);
+                            hi = fmaf(m, acc[2 * t + 1], hi);
+                        }
                     }
                     // ---- the unit's samples
                     const int b = consumed & (SEG_NBUF - 1);
@@ -677,12 +680,13 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         issue_one();
                 }
                 if (!snapped) {
+                    hr = hi = 0.f;
     #pragma unroll
-                    for (int t = 0; t < T; ++t)
-                        if (t == a.kp) {
-                            hr = acc[2 * t];
-                            hi = acc[2 * t + 1];
-                        }
+                    for (int t = 0; t < T; ++t) {
+                        const float m = t == a.kp ? 1.f : 0.f;
+                        hr = fmaf(m, acc[2 * t], hr);
+                        hi = fmaf(m, acc[2 * t + 1], hi);
+                    }
                 }
                 acc[2 * T] = hr;
                 acc[2 * T + 1] = hi;
