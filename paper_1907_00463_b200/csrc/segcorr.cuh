@@ -443,8 +443,11 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
         const int64_t avail = a.avail[strm];
         const int64_t off0 = s->ch.sample_offset_next_epoch;
         if (s->prn_cached != s->ch.prn) {  // the PRN's chip bits and transition list
+            // stage the code in the (drained) unit buffers, then build from shared memory
+            int8_t* cc = reinterpret_cast<int8_t*>(smem_raw + boff);
+            for (int j = tid; j < 1023; j += blockDim.x)
+                cc[j] = a.codes[s->ch.prn * 1023 + j];
             __syncthreads();
-            const int8_t* cc = a.codes + s->ch.prn * 1023;
             for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
                 uint32_t wv = 0;
                 for (int b = 0; b < 32; ++b)
@@ -470,6 +473,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     s->prn_cached = s->ch.prn;
                 }
             }
+            __syncthreads();  // the staging area is a unit buffer again
         }
         if (tid == 0) {
             const l1rxg_channel& ch = s->ch;
