@@ -579,6 +579,28 @@ __device__ __forceinline__ double atan2_bf(double y, double x) {
     return copysign(r, y);
 }
 
+// atan2(y, x) in fp32 with the same branch-free octant reduction: angle
+// error < 2e-7 rad (fp32 quotient + the atan(t)/t series to u^7 on
+// |t| <= tan(pi/8)); the loop-filter outputs it feeds carry a 1e-5 bar and
+// the NCO advance does not depend on it.  Shorter dependency chain than the
+// fp64 polynomial on the per-epoch critical path.
+__device__ __forceinline__ double atan2_f32(double y, double x) {
+    const float ax = fabsf((float)x), ay = fabsf((float)y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const bool big = mn > 0.41421356237f * mx;
+    const float num = big ? mn - mx : mn;
+    const float den = big ? mn + mx : mx;
+    const float t = den > 0.f ? __fdividef(num, den) : 0.f;
+    const float u = t * t, u2 = u * u;
+    const float a0 = fmaf(-1.f / 3.f, u, 1.f), a1 = fmaf(-1.f / 7.f, u, 0.2f);
+    const float a2 = fmaf(-1.f / 11.f, u, 1.f / 9.f), a3 = fmaf(-1.f / 15.f, u, 1.f / 13.f);
+    const float p = fmaf(fmaf(a3, u2, a2), u2 * u2, fmaf(a1, u2, a0));
+    double r = (double)(t * p) + (big ? PI_D / 4.0 : 0.0);
+    r = ay > ax ? PI_D / 2.0 - r : r;
+    r = x < 0.0 ? PI_D - r : r;
+    return copysign(r, y);
+}
+
 // C fmod(x, y) for y > 0 and |x| < 2^40 y, exactly: the remainder
 // x - k*y (k = trunc(x/y)) is representable, so one fma computes it
 // without rounding; the quotient estimate is corrected by +-1 so the result
@@ -1108,7 +1130,11 @@ __device__ __forceinline__ void warp0_update(S* s, const TrackArgs& a, const Epo
         x = dot;
         zero = cross == 0.0 && dot == 0.0;
     }
+#ifdef L1RXG_ATAN_F32  // experiment switch: measured 0.4 % on config 2, not worth the precision
+    const double ang = atan2_f32(y, x);
+#else
     const double ang = atan2_bf(y, x);
+#endif
     // sqrt lanes
     const double sq = fast_sqrt(lane == 3 ? __dadd_rn(__dmul_rn(ie, ie), __dmul_rn(qe, qe))
                                           : __dadd_rn(__dmul_rn(il, il), __dmul_rn(ql, ql)));
