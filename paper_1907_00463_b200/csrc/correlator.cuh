@@ -28,7 +28,10 @@
 
 namespace l1rxg {
 
-constexpr int RUN = 31;     // samples per thread run; odd -> LDS.64 conflict-free
+#ifndef L1RXG_RUN
+#define L1RXG_RUN 31
+#endif
+constexpr int RUN = L1RXG_RUN;  // samples per thread run; odd -> LDS.64 conflict-free
 constexpr int MAX_NT = 640; // correlator CTA size cap (<= 102 registers)
 constexpr double PI_D = 3.14159265358979323846;  // constants.hpp:20
 constexpr double TWO_PI_D = 2.0 * PI_D;
