@@ -1176,6 +1176,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             sa.n_items = static_cast<int>(items);
             sa.n_channels = t->d.n_channels;
             sa.chunk_epochs = chunk;
+            sa.fast_geom = seg_geometry_ok(&t->d) ? 1 : 0;
             CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels)), st));
             DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
         }

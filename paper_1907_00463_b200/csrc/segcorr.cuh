@@ -59,6 +59,7 @@ struct __align__(64) SegArgs {
     int* next;          // work-item counter (zeroed before the launch)
     int* ready;         // [n_channels] chunks finished (zeroed before the launch)
     int n_items, n_channels, chunk_epochs;
+    int fast_geom;      // seg_geometry_ok: unchecked step-table entries away from ties
 };
 
 template <int T>
@@ -282,13 +283,17 @@ __device__ __forceinline__ float2 seg_anchor(float2 z, float ca, float sa) {
     return make_float2(fmaf(z.x, ca, z.y * sa), fmaf(z.y, ca, -(z.x * sa)));
 }
 
-// Enters the step of tap k at epoch run position pos (= b + lead) with one
-// atomic OR of the position and the tap's code; the previous word tells
-// whether the half already held another position (tie -> conflict bit) or
-// the tap already stepped in this run (-> its slow bit).  A step at a run's
-// first sample needs no entry (the run's start chip has it).
+// Enters the step of tap k at epoch run position pos (= b + lead).  A step
+// at a run's first sample needs no entry (the run's start chip has it).
+// checked: one atomic OR of the position and the tap's code whose previous
+// word tells whether the half already held another position (-> conflict
+// bit) or the tap already stepped in this run (-> its slow bit).  Unchecked
+// (a fire-and-forget RED): for steps located away from fp64 ties when the
+// geometry rules both out (taps' residues > 15.5 samples apart, > 33 samples
+// per chip: steps of different residues are >= 15 samples apart, steps of
+// one residue coincide exactly, one tap steps at most once per run).
 template <int T>
-__device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int pos, int k) {
+__device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int pos, int k, bool checked) {
     typedef typename SegEntry<T>::type E;
     const int r = pos >> 5, q = pos & 31;
     if (q == 0)
@@ -298,6 +303,10 @@ __device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int p
     const bool mid = q == 16;
     const E qf = mid ? 0 : (E)(q & 15) << (4 * h);
     const E code = mid ? 1 : 2 + h;
+    if (!checked) {
+        atomicOr(&tab[r], qf | (code << sh));  // result unused: RED
+        return;
+    }
     const E prev = atomicOr(&tab[r], qf | (code << sh));
     const int pf = (int)((prev >> (4 * h)) & 15);
     const bool conflict = !mid && pf != 0 && pf != (q & 15);
@@ -313,56 +322,53 @@ __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
     return p * s->L + s->cum[m - p * 1023];
 }
 
-// Exact first sample b >= 1 whose replica index of tap offset d reaches m
-// (tap_boundary's contract, lo = 1, hi = n - 1): the estimate e = (m + kb) /
-// cps, kb = -d - base, is within ~1e-10 samples of the reference's crossing;
-// away from ties ceil(e) is the answer (one round-up add of 1.5 * 2^52),
-// near one the reference expression decides (tap_boundary).
-__device__ __forceinline__ int seg_boundary(int m, double kb, double d, const EpochConsts& c) {
-    const double e = ((double)m + kb) * c.inv_cps;
-    if (fabs(e - rint(e)) > 1e-9)
-        return __double2loint(__dadd_ru(e, 6755399441055744.0));
-    return tap_boundary(m, d, c, 1, c.n - 1);
-}
-
 // Step table fill for one epoch (every thread, after the loop update): every
-// chip transition m of every tap with its step inside the epoch, located
-// exactly, entered in the run holding it (seg_enter).  Transition g of the
-// code is chip index p * 1023 + tm[q], g = p * L + q; each thread walks its
-// g's with stride nthr (< L) and carries (p, q) along, two at a time so the
-// fp64 estimates and the atomics of the pair overlap.
+// chip transition of every tap with its step inside the epoch, located
+// exactly, entered in the run holding it (seg_enter).  The (tap, transition)
+// pairs are flattened so every thread gets the same share; transition g of
+// the code is chip index p * 1023 + tm[g - p * L].  Each step's estimate
+// e = (m - d - base) / cps is within ~1e-10 samples of the reference's
+// crossing, so away from ties ceil(e) is the answer (a round-up add of
+// 1.5 * 2^52); near one the reference expression decides (tap_boundary);
+// entries within 1e-7 samples of a tie are checked.
 template <int T>
 __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const SegSmem<T>* s,
-                                        const EpochConsts& c, int lead, int tid, int nthr) {
+                                        const EpochConsts& c, int lead, int tid, int nthr, bool fast_geom) {
     const int n = c.n, L = s->L;
-#pragma unroll 1
+    const int lane = tid & 31;
+    // each warp: lane k < T computes tap k's transition range, all lanes get them
+    int g0k = 0, cntk = 0;
+    if (lane < T) {
+        const double dk = s->d[lane];
+        g0k = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));  // transitions in (idx(0), idx(n-1)]
+        cntk = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk)) - g0k;
+    }
+    int g0[T], pre[T + 1];
+    pre[0] = 0;
+#pragma unroll
     for (int k = 0; k < T; ++k) {
+        g0[k] = __shfl_sync(0xffffffffu, g0k, k);
+        pre[k + 1] = pre[k] + __shfl_sync(0xffffffffu, cntk, k);
+    }
+    const float inv_L = 1.f / (float)L;  // p = g / L exactly for g < 2^13 (the +0.5 keeps off integers)
+    for (int f = tid; f < pre[T]; f += nthr) {
+        int k = 0, g = 0;
+#pragma unroll
+        for (int j = 0; j < T; ++j)
+            if (f >= pre[j]) {
+                k = j;
+                g = g0[j] + (f - pre[j]);
+            }
+        const int p = (int)(((float)g + 0.5f) * inv_L);
+        const int m = p * 1023 + s->tm[g - p * L];
         const double dk = s->d[k];
-        const double kb = -dk - c.base;
-        // transitions at chip indices in (idx(0), idx(n-1)]
-        const int g0 = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));
-        const int g1 = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk));
-        int g = g0 + tid;
-        int p = g / L, q = g - p * L;
-        for (; g < g1; g += 2 * nthr) {
-            int q2 = q + nthr, p2 = p;
-            if (q2 >= L) {
-                q2 -= L;
-                ++p2;
-            }
-            const bool two = g + nthr < g1;
-            const int ba = seg_boundary(p * 1023 + s->tm[q], kb, dk, c);
-            const int bb = two ? seg_boundary(p2 * 1023 + s->tm[q2], kb, dk, c) : 0;
-            seg_enter<T>(tab, ba + lead, k);
-            if (two)
-                seg_enter<T>(tab, bb + lead, k);
-            q = q2 + nthr;
-            p = p2;
-            if (q >= L) {
-                q -= L;
-                ++p;
-            }
-        }
+        const double e = ((double)m + (-dk - c.base)) * c.inv_cps;
+        const double dist = fabs(e - rint(e));
+        const bool tie = !(dist > 1e-9);
+        const int b = tie ? tap_boundary(m, dk, c, 1, n - 1) : __double2loint(__dadd_ru(e, 6755399441055744.0));
+        // checked within 1e-7 of a tie: steps of one residue differ in e by
+        // ~1e-11, so a step near a tie and its partner are both checked
+        seg_enter<T>(tab, b + lead, k, !(dist > 1e-7) || !fast_geom);
     }
 }
 
@@ -553,7 +559,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             const EpochConsts& c = s->c;
             // the step table of this epoch: every thread (the control warp too)
             if (!noop) {
-                seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT);
+                seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT, sa.fast_geom != 0);
                 __syncthreads();
             }
             if (warp == ctl) {
