@@ -705,7 +705,17 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             __syncthreads();
             if (warp == 0) {
                 const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
+#ifdef L1RXG_SEG_XSKIP_UPDATE  // experiment: bound on hiding the loop update (wrong results)
+                if (lane == 0) {
+                    s->c.phi = cc.phi;
+                    s->c.base = cc.base;
+                    s->ch.sample_offset_next_epoch += cc.n;
+                    s->ch.epoch_ms_count += 1;
+                }
+                __syncwarp();
+#else
                 warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
+#endif
                 if (lane == 0)
                     s->c.inv_cps = fast_rcp(s->c.cps);
                 float sn, co;
