@@ -525,3 +525,33 @@ def test_simulator_noise_and_post_correlation_snr(ctx):
     m = p.mean()
     snr = 10 * math.log10(abs(m) ** 2 / (np.abs(p - m) ** 2).sum() * (len(p) - 1))
     assert abs(snr - (cn0 - 30.0)) < 1.0, snr
+
+
+def test_auto_picks_segment_correlator_for_many_channels(ctx):
+    """cta_mode AUTO with >= 2 x SMs channels of complex int16 at 64 samples
+    per chip on the 0.25-chip grid selects the segment correlator: records
+    bit-identical to an explicit CTA_SEGMENT tracker."""
+    import torch
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    fs, ms = 65.472e6, 5
+    nrec = (2 * nsm + 11) // 12
+    rng = np.random.default_rng(5)
+    raws, inits, cstream = [], [], []
+    for r in range(nrec):
+        prns = rng.choice(np.arange(1, 33), 12, replace=False)
+        svs = [ss.Sv(prn=int(p), cn0_dbhz=45.0, doppler_hz=rng.uniform(-4000, 4000),
+                     delay_chips=rng.uniform(0, 1023)) for p in prns]
+        inits += [_init(sv, fs) for sv in svs]
+        cstream += [r] * 12
+        raws.append(svs)
+    dev = ss.synth_gpu(ctx, ms, fs, raws, seed=9)
+    taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+    outs = []
+    for mode in (abi.CTA_AUTO, abi.CTA_SEGMENT):
+        trk = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=nrec, taps=taps,
+                      ring_samples=(ms + 4) * 65472, max_records=ms, cta_mode=mode)
+        trk.attach_device(dev.data_ptr(), dev.shape[1] // 4, dev.shape[1])
+        trk.run()
+        trk.sync()
+        outs.append(trk.records_raw())
+    assert outs[0].tobytes() == outs[1].tobytes()
