@@ -553,5 +553,6 @@ def test_auto_picks_segment_correlator_for_many_channels(ctx):
         trk.attach_device(dev.data_ptr(), dev.shape[1] // 4, dev.shape[1])
         trk.run()
         trk.sync()
-        outs.append(trk.records_raw())
-    assert outs[0].tobytes() == outs[1].tobytes()
+        outs.append([trk.records(c) for c in range(len(inits))])  # the valid records only
+    for a_, b_ in zip(*outs):
+        assert len(a_) >= ms - 1 and a_.tobytes() == b_.tobytes()
