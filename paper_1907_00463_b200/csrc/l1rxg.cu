@@ -892,6 +892,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         (e = cudaMalloc(&t->d_status, 4 * C)) != cudaSuccess)
         return fail(e);
     cudaMemset(t->d_avail, 0, 8 * t->streams.size());
+    cudaMemset(t->d_recs, 0, sizeof(l1rxg_epoch_record) * nrec);  // unused record slots read as zeros
     cudaMemset(t->d_ecount, 0, 8 * C);
     cudaMemset(t->d_status, 0, 4 * C);
     if (d->n_channels > 0) {
