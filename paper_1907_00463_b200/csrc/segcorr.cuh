@@ -30,9 +30,15 @@
 //     same shared-memory row -- correct for every geometry, fast for the
 //     one it is chosen for.
 //
-// Per-epoch critical path, control warp and records: identical to the
-// throughput shape of track_kernel (warp0_update, finish_epoch, loop_fast,
-// loop_metrics are shared).
+//   * per epoch: the step table (every transition of every tap located and
+//     entered by all threads), the runs, the warps' partial sums, the loop
+//     update on warp 0 (warp0_update / loop_fast, shared with track_kernel);
+//     the last warp finishes the previous epoch (loop_metrics, record) before
+//     its runs and takes one unit fewer -- all five warps correlate;
+//   * persistent CTAs (4 per SM) take work items (chunk of epochs, channel)
+//     in chunk-major order; a chunk waits for its channel's previous chunk,
+//     so a launch has no wave-quantisation tail.
+// DESIGN.md section 3 has the measurements behind each choice.
 #pragma once
 
 #include <cuda.h>  // CUtensorMap (the map itself is encoded on the host)
