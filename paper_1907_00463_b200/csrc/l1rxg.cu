@@ -1260,10 +1260,14 @@ int l1rxg_tracker_sync(l1rxg_tracker* t) {
     std::vector<int32_t> status(static_cast<size_t>(std::max(1, t->d.n_channels)));
     if (t->d.n_channels > 0) {
         CK(cudaMemcpy(status.data(), t->d_status, 4 * status.size(), cudaMemcpyDeviceToHost));
-        for (int k = 0; k < t->d.n_channels; ++k)
+        for (int k = 0; k < t->d.n_channels; ++k) {
+            if (status[static_cast<size_t>(k)] == 2)
+                return set_err(L1RXG_ECUDA, "segment correlator: a work item timed out waiting for its "
+                                            "channel's previous chunk");
             if (status[static_cast<size_t>(k)])
                 return set_err(L1RXG_EINVAL, "ring overrun: a channel's window was overwritten "
                                              "before it was tracked (ring_samples too small)");
+        }
     }
     return 0;
 }

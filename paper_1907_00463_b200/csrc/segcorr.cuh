@@ -431,9 +431,16 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
         const int chunk = item / sa.n_channels;
         const int max_e = min(sa.chunk_epochs, a.max_epochs - chunk * sa.chunk_epochs);
         if (tid == 0) {
+            s->stop = 0;
             if (chunk > 0) {  // the channel's previous chunk (dequeued earlier, so resident) must be done
-                while (*(volatile int*)&sa.ready[cidx] < chunk)
+                // bounded (~20 s): a broken invariant reports an error instead of hanging the GPU
+                long long spins = 0;
+                while (*(volatile int*)&sa.ready[cidx] < chunk && ++spins < (1LL << 23))
                     __nanosleep(2000);
+                if (spins >= (1LL << 23)) {
+                    a.status[cidx] = 2;
+                    s->stop = 1;
+                }
                 __threadfence();
             }
             // state written by another SM: read around L1
@@ -442,10 +449,9 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             for (int q = 0; q < (int)(sizeof(l1rxg_channel) / 8); ++q)
                 dst[q] = __ldcg(src + q);
             s->pending = 0;
-            s->stop = 0;
         }
         __syncthreads();
-        if (max_e <= 0) {  // past the launch's epoch budget
+        if (max_e <= 0 || s->stop) {  // past the launch's epoch budget (or the wait gave up)
             __syncthreads();
             if (tid == 0)
                 atomicExch(&sa.ready[cidx], chunk + 1);
