@@ -556,3 +556,35 @@ def test_auto_picks_segment_correlator_for_many_channels(ctx):
         outs.append([trk.records(c) for c in range(len(inits))])  # the valid records only
     for a_, b_ in zip(*outs):
         assert len(a_) >= ms - 1 and a_.tobytes() == b_.tobytes()
+
+
+def test_segment_max_epochs_and_noop(ctx, oracle_mod):
+    """Segment correlator: run(max_epochs) in pieces gives the same records
+    as one run (the persistent work items honour the epoch budget), and the
+    Noop kernel advances the NCO only (test_tracking.cpp:481-493)."""
+    fs, ms, n = 65.472e6, 12, 65472
+    svs = [[ss.Sv(prn=5, cn0_dbhz=46.0, doppler_hz=900.0, delay_chips=40.5),
+            ss.Sv(prn=23, cn0_dbhz=44.0, doppler_hz=-1700.0, delay_chips=800.0)]]
+    dev = ss.synth_gpu(ctx, ms, fs, svs, seed=31)
+    inits = [_init(sv, fs) for sv in svs[0]]
+    taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+
+    def make(kernel=abi.KERNEL_BATCHED):
+        t = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, taps=taps, ring_samples=(ms + 4) * n,
+                    max_records=ms, cta_mode=abi.CTA_SEGMENT, kernel=kernel)
+        t.attach_device(dev.data_ptr(), dev.shape[1] // 4, dev.shape[1])
+        return t
+    one = make()
+    one.run()
+    pieces = make()
+    for _ in range(6):
+        pieces.run(max_epochs=3)
+    assert np.array_equal(one.epoch_counts(), pieces.epoch_counts())
+    for c in range(2):
+        assert one.records(c).tobytes() == pieces.records(c).tobytes()
+    noop = make(abi.KERNEL_NOOP)
+    noop.run(max_epochs=4)
+    r = noop.records(0)
+    assert len(r) == 4 and np.all(r["ip"] == 0.0)
+    for k in range(1, 4):
+        assert abs((r[k]["chi_chips"] - r[k - 1]["chi_chips"]) - r[k - 1]["code_freq_hz"] / 1000.0) < 1e-9
