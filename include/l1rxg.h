@@ -246,7 +246,7 @@ typedef struct {
      * L1RXG_CTA_SEGMENT: the throughput shape's segment correlator over a
      * raw complex-int16 ring (no decode pass; per-warp TMA tensor copies;
      * the run sums captured in registers instead of a shared-memory prefix
-     * tile); complex int16 only, fs >= 4.096 MHz.  Auto picks it for the
+     * tile); complex int16 only, fs >= 3.073 MHz.  Auto picks it for the
      * throughput shape on complex int16 recordings whose chips span > 33
      * samples with tap residues > 15.5 samples apart (BASELINE config 4). */
     int32_t cta_mode;

@@ -751,7 +751,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     if (n > MAXSUB * (MAX_NT - 32) * RUN)
         return set_err(L1RXG_EINVAL, "epoch longer than the correlator supports (fs <= 150 MHz)");
     if (d->cta_mode == L1RXG_CTA_SEGMENT && (d->format != L1RXG_FMT_INT16_IQ || n < SEG_MIN_N))
-        return set_err(L1RXG_EINVAL, "the segment correlator takes complex int16 at fs >= 4.096 MHz");
+        return set_err(L1RXG_EINVAL, "the segment correlator takes complex int16 at fs >= 3.073 MHz");
     for (int k = 0; k < d->n_channels; ++k) {
         if (chan_stream[k] < 0 || chan_stream[k] >= d->n_streams)
             return set_err(L1RXG_EINVAL, "channel bound to a missing stream");

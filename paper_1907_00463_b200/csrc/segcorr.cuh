@@ -49,7 +49,18 @@
 
 namespace l1rxg {
 
-constexpr int SEG_NW = 5;                    // warps per CTA, all correlate
+// Defaults (measured, config 4): four correlating warps per CTA and five
+// CTAs per SM (44 KB of shared memory each: the unit buffers first at the
+// 1024-B aligned dynamic base, no transition-count table) beat five warps x
+// four CTAs by 2 %.
+#ifndef L1RXG_SEG_NW
+#define L1RXG_SEG_NW 4
+#endif
+#ifndef L1RXG_SEG_PAD
+#define L1RXG_SEG_NOPAD
+#define L1RXG_SEG_NOCUM
+#endif
+constexpr int SEG_NW = L1RXG_SEG_NW;         // warps per CTA, all correlate
 constexpr int SEG_NT = 32 * SEG_NW;
 constexpr int SEG_NBUF = 2;                  // TMA buffers per work warp
 constexpr int SEG_UNIT_BYTES = 32 * 128;     // 32 rows x 32 cint16 samples
@@ -92,7 +103,9 @@ struct SegSmem {
     double nco_ph1, nco_cp1;
     uint32_t chipw[CHIP_EXT / 32 + 1];  // bit m % 32 of word m / 32: chip[m] > 0
     int16_t tm[SEG_TRANS_P];  // chip index of the g-th chip transition of one period
+#ifndef L1RXG_SEG_NOCUM
     int16_t cum[1024];       // transitions at indices <= r within one period
+#endif
     int L;                   // transitions per period
 };
 
@@ -114,9 +127,13 @@ __host__ __device__ constexpr int seg_table_runs(int n) { return (((n + 62) >> 5
 template <int T>
 __host__ __device__ constexpr size_t seg_smem_bytes(int n) {
     // header, step table, then up to 1 KB of padding to the 1024-B aligned unit buffers
+    // (L1RXG_SEG_NOPAD: the buffers first, at the 1024-B aligned dynamic base)
     return ((sizeof(SegSmem<T>) + 15) & ~size_t(15)) +
            ((static_cast<size_t>(seg_table_runs(n)) * sizeof(typename SegEntry<T>::type) + 15) & ~size_t(15)) +
-           1024 + static_cast<size_t>(SEG_NW) * SEG_NBUF * SEG_UNIT_BYTES;
+#ifndef L1RXG_SEG_NOPAD
+           1024 +
+#endif
+           static_cast<size_t>(SEG_NW) * SEG_NBUF * SEG_UNIT_BYTES;
 }
 
 // 3-D tensor TMA: box {32 u32, 32 rows, 1 stream} at (0, row, stream).
@@ -325,7 +342,20 @@ __device__ __forceinline__ void seg_enter(typename SegEntry<T>::type* tab, int p
 template <int T>
 __device__ __forceinline__ int seg_trans_count(const SegSmem<T>* s, int m) {
     const int p = m / 1023;
+#ifdef L1RXG_SEG_NOCUM  // upper bound of r in tm[0, L) by binary search
+    const int r = m - p * 1023;
+    int lo = 0, hi = s->L;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s->tm[mid] <= r)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return p * s->L + lo;
+#else
     return p * s->L + s->cum[m - p * 1023];
+#endif
 }
 
 // Step table fill for one epoch (every thread, after the loop update): every
@@ -380,20 +410,30 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
 
 template <int T>
 #ifndef L1RXG_SEG_MINB
-#define L1RXG_SEG_MINB 4
-#endif
+#define L1RXG_SEG_MINB (SEG_NW == 4 ? 5 : 4)
+#endif  // (CTAs per SM the registers are budgeted for)
 __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const __grid_constant__ SegArgs sa) {
     typedef typename SegEntry<T>::type E;
     const TrackArgs& a = sa.t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SegSmem<T>* s = reinterpret_cast<SegSmem<T>*>(smem_raw);
     const int n = a.n;
     const uint32_t sbase = smem_u32(smem_raw);
-    const uint32_t hdr = (uint32_t)((sizeof(SegSmem<T>) + 15) & ~size_t(15));
-    E* tab = reinterpret_cast<E*>(smem_raw + hdr);
     const int truns = seg_table_runs(n);
+#ifdef L1RXG_SEG_NOPAD
+    if (sbase & 1023u)
+        __trap();  // the unit buffers need the 1024-B alignment of the 128-B swizzle
+    const uint32_t boff = 0;
+    const uint32_t hoff = (uint32_t)(SEG_NW * SEG_NBUF * SEG_UNIT_BYTES);
+#else
+    const uint32_t hoff = 0;
+#endif
+    SegSmem<T>* s = reinterpret_cast<SegSmem<T>*>(smem_raw + hoff);
+    const uint32_t hdr = hoff + (uint32_t)((sizeof(SegSmem<T>) + 15) & ~size_t(15));
+    E* tab = reinterpret_cast<E*>(smem_raw + hdr);
+#ifndef L1RXG_SEG_NOPAD
     const uint32_t tend = hdr + (uint32_t)((truns * sizeof(E) + 15) & ~size_t(15));
     const uint32_t boff = ((sbase + tend + 1023u) & ~1023u) - sbase;  // unit buffers, 1024-B aligned
+#endif
     const float4* rot4 = reinterpret_cast<const float4*>(s->rot);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -482,7 +522,9 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     if (r < 1023) {
                         if (t)
                             s->tm[running + before] = (int16_t)r;
+#ifndef L1RXG_SEG_NOCUM
                         s->cum[r] = (int16_t)(running + before + (t ? 1 : 0));
+#endif
                     }
                     running += __popc(mask);
                 }

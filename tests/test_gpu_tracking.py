@@ -424,14 +424,15 @@ def test_segment_correlator_ties_and_slow_paths(ctx, oracle_mod, fs, tapset, ms)
 
 
 def test_segment_mode_rejects_other_formats(ctx):
-    """The segment correlator takes complex int16 at fs >= 4.096 MHz only."""
+    """The segment correlator takes complex int16 with enough samples per
+    epoch for every warp of a CTA to own a unit (fs >= 3.073 MHz)."""
     init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 2.048e6)
     with pytest.raises(ValueError):
         Tracker(ctx, abi.FMT_INT8_IQ, 2.048e6, 0.0, [init], ring_samples=8 * 2048,
                 cta_mode=abi.CTA_SEGMENT)
-    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 4.0e6)
+    init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 3.0e6)
     with pytest.raises(ValueError):
-        Tracker(ctx, abi.FMT_INT16_IQ, 4.0e6, 0.0, [init], ring_samples=8 * 4000,
+        Tracker(ctx, abi.FMT_INT16_IQ, 3.0e6, 0.0, [init], ring_samples=8 * 3000,
                 cta_mode=abi.CTA_SEGMENT)
 
 
