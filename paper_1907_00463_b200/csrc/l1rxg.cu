@@ -21,6 +21,7 @@
 #include "correlator.cuh"
 #include "ingest.cuh"
 #include "search.cuh"
+#include "ovlcorr.cuh"
 #include "segcorr.cuh"
 #include "simgen.cuh"
 #include "l1rxg.h"
@@ -210,8 +211,55 @@ int launch_track_thr(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int s
     default: return launch_track_sk<T, SK_F32, THR>(a, n_ch, nt, s);
     }
 }
+// Overlapped latency kernel (ovlcorr.cuh): float2 rings, two tiles, one unit
+// per epoch, and its P'/M' tiles within the shared-memory budget.  Returns
+// -1 when not applicable (the caller then runs track_kernel).
+template <int T>
+int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
+    static const char* ev = std::getenv("L1RXG_OVL");
+    if ((ev && ev[0] == '0') || a.thr || sk != SK_F32 || a.nbuf != 2 ||
+        a.lc.kernel == L1RXG_KERNEL_NOOP)
+        return -1;
+    const int nwork = nt - 32;
+    if ((a.csize > 1 ? a.share : a.n) > nwork * RUN)
+        return -1;
+    const size_t xsl = (2u * a.csize * (2 * T + 2) * sizeof(double) + 15) & ~size_t(15);
+    const size_t sm = smem_bytes<T>(nwork, 2, 8) + xsl + ovl_extra_bytes(nwork);
+    if (sm > 227u * 1024u)
+        return -1;
+    CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    if (a.csize <= 1) {
+        track_ovl_kernel<T><<<n_ch, nt, sm, s>>>(a);
+    } else {
+        if (a.csize > 8)
+            CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(n_ch * a.csize));
+        cfg.blockDim = dim3(static_cast<unsigned>(nt));
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(a.csize);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, track_ovl_kernel<T>, a));
+    }
+    CK(cudaGetLastError());
+    return 0;
+}
+
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
+    if (!a.thr) {
+        const int rc = launch_ovl<T>(a, n_ch, nt, s, sk);
+        if (rc != -1)
+            return rc;
+    }
     return a.thr ? launch_track_thr<T, true>(a, n_ch, nt, s, sk)
                  : launch_track_thr<T, false>(a, n_ch, nt, s, sk);
 }

@@ -1,0 +1,387 @@
+// ovlcorr.cuh -- latency-shape tracking kernel with the next epoch's phase A
+// overlapped with this epoch's loop update (configs 1-3; sm_100a).
+//
+// Same contract, phases and results as track_kernel's latency shape
+// (correlator.cuh; reference tracking.hpp:226-282 + :520-618), scheduled so
+// that the per-sample work of epoch e+1 is off the per-epoch critical path:
+//
+//   * the loop update of epoch e runs on the control warp (warp0_update is a
+//     warp-level function); meanwhile the work warps already compute phase A'
+//     of epoch e+1 -- the wiped run-local prefix P'(j) = sum_{t<j} y'_t and
+//     its first moment M'(j) = sum_{t<j} t y'_t, y'_t = x_t e^{-j w_e t} --
+//     with the rotator table of the CURRENT carrier rate w_e;
+//   * when the update has produced w_{e+1}, each run's sums are corrected to
+//     the true rate: sum_t x_t e^{-j w t} = P' - j dw M' + O((dw t)^2 / 2),
+//     dw = w_{e+1} - w_e, t < RUN = 31 -- below 1e-9 relative for the
+//     per-epoch rate changes of a tracking loop (|dw| 30 < 1e-4); larger
+//     changes (FLL pull-in) recompute phase A exactly with the new table.
+//     The run anchors e^{-j theta(i0)} use the new rate exactly (fp64), so
+//     the approximation never spans more than one run;
+//   * phase B reads P' - j dw M' at each step (one more LDS.64 and two FFMA
+//     per transition).
+// The per-epoch chain becomes: update -> per-run anchors and run totals ->
+// phase B -> partial sums -> next update.
+#pragma once
+
+#include "correlator.cuh"
+
+namespace l1rxg {
+
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// |dw| * RUN above this recomputes phase A exactly (second-order term below
+// 5e-7 of the run's magnitude; the parity bar is 1e-5)
+#ifndef L1RXG_OVL_DWMAX
+#define L1RXG_OVL_DWMAX 1e-3f
+#endif
+constexpr float OVL_DW_RUN_MAX = L1RXG_OVL_DWMAX;
+
+// Extra shared memory of the overlapped kernel, after track_kernel's layout
+// (header, anchors, 2 sample tiles, cluster exchange slots): P' and M' tiles
+// for both buffers, per-run totals, double-buffered rotator tables.
+__host__ __device__ inline size_t ovl_extra_bytes(int nwork) {
+    const size_t cap = (size_t)nwork * RUN;
+    return 4 * cap * sizeof(float2) + 2 * (size_t)nwork * sizeof(float2) + 2 * 32 * sizeof(float2) +
+           4 * sizeof(double) + 64;
+}
+
+// Phase A' of one run: exclusive prefixes P'(j), M'(j) into pp/mp, totals out.
+template <bool FULL>
+__device__ __forceinline__ void ovl_phase_a(const float2* raw, float2* pp, float2* mp, const float2* rot,
+                                            int cnt, float2& ptot, float2& mtot) {
+    float pr = 0.f, pi = 0.f, mr = 0.f, mi = 0.f;
+#pragma unroll
+    for (int j = 0; j < RUN; ++j) {
+        pp[j] = make_float2(pr, pi);
+        mp[j] = make_float2(mr, mi);
+        const float2 x = (FULL || j < cnt) ? raw[j] : make_float2(0.f, 0.f);
+        const float2 q = rot[j];
+        const float yr = fmaf(x.y, q.y, x.x * q.x);   // x conj(rot): (xr c + xi s,
+        const float yi = fmaf(-x.x, q.y, x.y * q.x);  //   xi c - xr s), tracking.hpp:248-249
+        pr += yr;
+        pi += yi;
+        mr = fmaf((float)j, yr, mr);
+        mi = fmaf((float)j, yi, mi);
+    }
+    ptot = make_float2(pr, pi);
+    mtot = make_float2(mr, mi);
+}
+
+// P - j dw M
+__device__ __forceinline__ float2 ovl_corr(float2 p, float2 m, float dw) {
+    return make_float2(fmaf(dw, m.y, p.x), fmaf(-dw, m.x, p.y));
+}
+
+// One step: acc -= delta * anchor(run(b)) * (P'(b) - j dw M'(b)).
+__device__ __forceinline__ void ovl_b_one(PhaseB& pb, const float2* pt, const float2* mt, const float2* anchors,
+                                          int u0, int nh, int b, float dlt, float dw) {
+    const int off = b - u0;
+    const float2 p = ovl_corr(pt[off], mt[off], dw);
+    const float2 an = anchors[off / RUN];
+    const float ar = fmaf(p.x, an.x, p.y * an.y);
+    const float ai = fmaf(p.y, an.x, -(p.x * an.y));
+    pb.re = fmaf(-dlt, ar, pb.re);
+    pb.im = fmaf(-dlt, ai, pb.im);
+    if (pb.prompt && b < nh) {
+        pb.hre = fmaf(-dlt, ar, pb.hre);
+        pb.him = fmaf(-dlt, ai, pb.him);
+    }
+}
+
+// Phase B over the tap's transitions (the latency walk of phase_b<T, false>).
+template <int T>
+__device__ __forceinline__ void ovl_phase_b(PhaseB& pb, const EpochConsts& c, const float2* pt, const float2* mt,
+                                            const float2* anchors, const CodeTables& ct, int u0, int len, float dw) {
+    if (pb.kt >= T)
+        return;
+    const int hi = u0 + len - 1;
+    const int g0 = pb.g0, cnt = pb.cnt;
+    for (int j = pb.jt; j < cnt; j += 2 * pb.gsz) {
+        const int j2 = j + pb.gsz;
+        const bool two = j2 < cnt;
+        const int ga = g0 + j, gb = g0 + (two ? j2 : j);
+        const int ma = ct.tm[ga], mb = ct.tm[gb];
+        const float da = (float)ct.td[ga], db = (float)ct.td[gb];
+        const int ba = tap_boundary(ma, pb.dk, c, u0, hi);
+        const int bb = tap_boundary(mb, pb.dk, c, u0, hi);
+        ovl_b_one(pb, pt, mt, anchors, u0, c.nh, ba, da, dw);
+        if (two)
+            ovl_b_one(pb, pt, mt, anchors, u0, c.nh, bb, db, dw);
+    }
+}
+
+// Run totals after the update (what phase_a adds per run): the run's anchor
+// with the true rate, chip_k(last) * anchor * (P'tot - j dw M'tot) per tap,
+// and the first-half prompt (tracking.hpp:259-271).
+template <int T>
+__device__ __forceinline__ void ovl_run_totals(const EpochConsts& c, const CodeTables& ct, const double* d, int kp,
+                                               int i0, int cnt, float2 ptot, float2 mtot, const float2* pt,
+                                               const float2* mt, float dw, float* acc, float2* anchor_slot) {
+    const double th = __fma_rn(c.w, (double)i0, c.phi);
+    const double r = fma(-rint(th * (1.0 / TWO_PI_D)), TWO_PI_D, th);
+    float sa, ca;
+    __sincosf((float)r, &sa, &ca);
+    *anchor_slot = make_float2(ca, sa);
+    const float2 z0 = ovl_corr(ptot, mtot, dw);
+    const float zr = fmaf(z0.x, ca, z0.y * sa);
+    const float zi = fmaf(z0.y, ca, -(z0.x * sa));
+    const int i_last = i0 + cnt - 1;
+    const double dl = (double)i_last;
+    float chip_p = 0.f;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const float ch = (float)ct.chip[__double2int_rz(tap_value(dl, c.cps, c.base, d[k]))];
+        acc[2 * k] = fmaf(ch, zr, acc[2 * k]);
+        acc[2 * k + 1] = fmaf(ch, zi, acc[2 * k + 1]);
+        if (k == kp)
+            chip_p = ch;
+    }
+    if (i_last < c.nh) {
+        acc[2 * T] = fmaf(chip_p, zr, acc[2 * T]);
+        acc[2 * T + 1] = fmaf(chip_p, zi, acc[2 * T + 1]);
+    } else if (i0 < c.nh) {  // the run straddling n/2: chip(nh-1) * P(nh)
+        const float ch = (float)ct.chip[tap_index(c.nh - 1, c.cps, c.base, d[kp])];
+        const float2 pn = ovl_corr(pt[c.nh - i0], mt[c.nh - i0], dw);
+        acc[2 * T] = fmaf(ch, fmaf(pn.x, ca, pn.y * sa), acc[2 * T]);
+        acc[2 * T + 1] = fmaf(ch, fmaf(pn.y, ca, -(pn.x * sa)), acc[2 * T + 1]);
+    }
+}
+
+__device__ __forceinline__ void ovl_fill_rot(float2* rot, double w, int lane) {
+    float sn, co;
+    sincosf((float)(w * (double)lane), &sn, &co);
+    rot[lane] = make_float2(co, sn);
+}
+
+// Latency shape only: float2 rings, two sample tiles, one unit per epoch
+// (the host selects it), Scalar/Batched kernels (Noop stays on track_kernel).
+template <int T>
+__global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
+    constexpr int esz = 8;
+    constexpr int A = 2;  // samples per 16-byte bulk-copy granule
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
+    const int csize = a.csize;
+    const int crank = csize > 1 ? (int)(blockIdx.x % csize) : 0;
+    const int cidx = blockIdx.x / csize;
+    const bool writer = crank == 0;
+    const int strm = a.chan_stream[cidx];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    const int ctl = nwarps - 1;
+    const int nwork = blockDim.x - 32;
+    const int nthr = blockDim.x;
+    const int nwork_warps = nwarps - 1;
+    constexpr int V = 2 * T + 2;
+    const int cap = nwork * RUN;
+    const int n = a.n;
+    const int r0 = csize > 1 ? crank * a.share : 0;
+    const int rend = csize > 1 ? min(n, r0 + a.share) : n;
+    const int len = rend - r0;  // one unit per epoch
+    const int skip = n - len;
+    const int64_t avail = a.avail[strm];
+    const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * esz;
+    float2* anchors = anchors_of(s);
+    double* xs = xslots_of(s, nwork, 2, esz);
+    unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ((2 * csize * V * sizeof(double) + 15) & ~size_t(15));
+    float2* const pm0 = reinterpret_cast<float2*>(xb);  // P' tiles [2][cap], then M' tiles [2][cap]
+    auto pm = [&](int b) { return pm0 + b * cap; };
+    auto mm = [&](int b) { return pm0 + (2 + b) * cap; };
+    float2* ptot = reinterpret_cast<float2*>(xb) + 4 * cap;
+    float2* mtot = ptot + nwork;
+    float2* rot2 = mtot + nwork;  // [2][32]
+    double* wp = reinterpret_cast<double*>(rot2 + 64);  // [2]: the rate each buffer's P'/M' were made with
+    int* ie = reinterpret_cast<int*>(wp + 2);            // [2]: epoch whose copy was issued into each tile
+    long long* dn = reinterpret_cast<long long*>(ie + 2); // epochs done (control warp -> writeback)
+    const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
+    const bool ring_ok = off0 >= 0 && off0 >= avail - a.ring_cap;
+    // epoch v's unit into tile v & 1 (range admission only; an Idle channel's
+    // speculative copies are drained at exit)
+    auto try_issue = [&](int v) {
+        const int64_t offv = off0 + (int64_t)v * n;
+        if (!ring_ok || v >= a.max_epochs || offv + n > avail)
+            return;
+        const int b = v & 1;
+        const int64_t pos = s->issue_pos;
+        issue_unit(s, b, tile_of(s, nwork, b, esz), ring, pos, len, esz);
+        ie[b] = v;
+        int64_t nxt = pos + len + skip;
+        while (nxt >= a.ring_cap)
+            nxt -= a.ring_cap;
+        s->issue_pos = nxt;
+    };
+    // ring position of epoch v's unit (the copy's 16-byte alignment slack)
+    auto unit_pos = [&](int v) -> int64_t { return (off0 + r0 + (int64_t)v * n) % a.ring_cap; };
+
+    if (tid == 0) {
+        s->ch = a.chans[cidx];
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s->bars[b][0], 1);
+            mbar_init(&s->bars[b][1], 1);
+            mbar_init(&s->pbar[b], 1);
+            s->inflight[b] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s->pending = 0;
+        s->stop = 0;
+    }
+    for (int k = tid; k < T; k += blockDim.x)
+        s->d[k] = a.taps.offsets_chips[k];
+    if (csize > 1)
+        cluster_sync_all();
+    __syncthreads();
+    PhaseB pb;
+    phase_b_init<T>(pb, s->d, a.kp, tid, nwork);
+    build_code_tables(s->ct, a.codes, s->ch.prn);
+    if (tid == 0) {
+        s->issue_pos = ring_ok ? (off0 + r0) % a.ring_cap : 0;
+        const l1rxg_channel& ch = s->ch;
+        make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz, ch.carrier_phase_rad,
+                    a.lc.fs, n);
+        try_issue(0);
+        try_issue(1);
+        wp[0] = s->c.w;
+    }
+    __syncthreads();
+    if (tid < 32)
+        ovl_fill_rot(rot2, s->c.w, tid);
+    __syncthreads();
+
+    // prologue: phase A' of epoch 0 with its own rate (dw = 0)
+    auto phase_a_epoch = [&](int v, const float2* rot) {
+        const int b = v & 1;
+        const int delta = (int)(unit_pos(v) & (A - 1));
+        const int h = A * ((len + delta) / (2 * A));
+        const float2* rawt = reinterpret_cast<const float2*>(tile_of(s, nwork, b, esz)) + delta;
+        const int i0 = r0 + tid * RUN;
+        const int cnt = min(RUN, rend - i0);
+        const int r0t = delta + tid * RUN;
+        const uint32_t par = (uint32_t)(v >> 1) & 1u;
+        if (cnt > 0) {
+            if (r0t < h)
+                mbar_wait(&s->bars[b][0], par);
+            if (r0t + RUN > h)
+                mbar_wait(&s->bars[b][1], par);
+            if (cnt == RUN)
+                ovl_phase_a<true>(rawt + tid * RUN, pm(b) + tid * RUN, mm(b) + tid * RUN, rot, cnt, ptot[tid],
+                                  mtot[tid]);
+            else
+                ovl_phase_a<false>(rawt + tid * RUN, pm(b) + tid * RUN, mm(b) + tid * RUN, rot, cnt, ptot[tid],
+                                   mtot[tid]);
+        }
+    };
+    if (tid == 0)
+        *dn = a.ecount[cidx];
+    const bool first_ok = ring_ok && a.max_epochs > 0 && off0 + n <= avail && s->ch.state != L1RXG_IDLE;
+    if (tid < nwork && first_ok)
+        phase_a_epoch(0, rot2);
+
+    int e = 0;
+    int64_t done = a.ecount[cidx];
+    int rec_i = (int)(done % a.max_records);
+    if (!first_ok) {  // nothing admitted (also: overwritten window)
+        if (tid == 0 && s->ch.state != L1RXG_IDLE && a.max_epochs > 0 && off0 + n <= avail && !ring_ok)
+            a.status[cidx] = 1;
+    } else if (warp == ctl) {
+        // ---- control warp: the loop update of every epoch
+        for (;;) {
+            const EpochConsts c = s->c;  // epoch e's constants (written by the previous update)
+            const int64_t off = s->ch.sample_offset_next_epoch;
+            nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
+            named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
+            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
+            const bool stop = s->stop != 0;
+            if (!stop)
+                ovl_fill_rot(rot2 + 32 * ((e + 1) & 1), s->c.w, lane);
+            __syncwarp();
+            named_bar_arrive(3, nthr);  // Y: epoch e+1's constants and rotators (or stop)
+            if (s->pending) {           // epoch e's metrics and record, while e+1 correlates
+                finish_epoch<T>(s, a, lane, writer);
+                __syncwarp();
+                if (lane == 0)
+                    s->pending = 0;
+                __syncwarp();
+            }
+            if (stop)
+                break;
+            ++e;
+            ++done;
+            if (++rec_i == a.max_records)
+                rec_i = 0;
+            const int64_t offn = off0 + (int64_t)e * n;
+            if (e >= a.max_epochs || offn + n > avail)
+                break;
+        }
+        if (lane == 0)
+            *dn = done;
+    } else {
+        // ---- work warps: correlation of epoch e, then phase A' of epoch e+1
+        for (;;) {
+            const int b = e & 1;
+            const EpochConsts cc = s->c;
+            EpochConsts c = cc;
+            c.inv_cps = fast_rcp(c.cps);
+            const int u0 = r0;
+            float dw = (float)(c.w - wp[b]);
+            if (fabsf(dw) * (float)RUN > OVL_DW_RUN_MAX) {  // rate moved too far: exact phase A
+                if (tid < nwork)
+                    phase_a_epoch(e, rot2 + 32 * b);
+                dw = 0.f;
+                named_bar_sync(1, nwork);
+            }
+            float acc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                acc[v] = 0.f;
+            phase_b_range<T>(pb, c, s->ct, u0, len);
+            {
+                const int i0 = u0 + tid * RUN;
+                const int cnt = min(RUN, rend - i0);
+                if (cnt > 0)
+                    ovl_run_totals<T>(c, s->ct, s->d, a.kp, i0, cnt, ptot[tid], mtot[tid], pm(b) + tid * RUN,
+                                      mm(b) + tid * RUN, dw, acc, &anchors[tid]);
+            }
+            named_bar_sync(1, nwork);  // anchors visible
+            ovl_phase_b<T>(pb, c, pm(b), mm(b), anchors, s->ct, u0, len, dw);
+            phase_b_fold<T>(pb, acc);
+            warp_partials<V>(acc, s->red, lane, warp);
+            named_bar_sync(1, nwork);  // tile b consumed; partials written
+            if (tid == 0) {
+                s->inflight[b] = 0;
+                try_issue(e + 2);
+            }
+            named_bar_arrive(2, nthr);  // X
+            // speculative phase A' of epoch e+1 with this epoch's rate
+            const int64_t offn = off0 + (int64_t)(e + 1) * n;
+            const bool next_ok = e + 1 < a.max_epochs && offn + n <= avail;
+            if (next_ok) {
+                phase_a_epoch(e + 1, rot2 + 32 * b);
+                if (tid == 0)
+                    wp[b ^ 1] = cc.w;
+            }
+            named_bar_sync(3, nthr);  // Y
+            if (s->stop || !next_ok)
+                break;
+            ++e;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b)
+            if (s->inflight[b]) {  // never leave a bulk copy in flight into freed smem
+                const uint32_t par = (uint32_t)(ie[b] >> 1) & 1u;
+                mbar_wait(&s->bars[b][0], par);
+                mbar_wait(&s->bars[b][1], par);
+            }
+        if (writer) {
+            a.chans[cidx] = s->ch;
+            a.ecount[cidx] = *dn;
+        }
+    }
+    if (csize > 1)
+        cluster_sync_all();
+}
+
+}  // namespace l1rxg
