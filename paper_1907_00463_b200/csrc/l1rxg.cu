@@ -230,6 +230,15 @@ int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
     CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
+    // the P'/M' tiles must not cost co-residency: every CTA of the launch
+    // resident at once, as with track_kernel (measured: config 3's paired
+    // CTAs at one per SM run 2.3x slower)
+    int per_sm = 0, nsm = 148, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_ovl_kernel<T>, nt, sm));
+    if (static_cast<long long>(n_ch) * a.csize > static_cast<long long>(per_sm) * nsm)
+        return -1;
     if (a.csize <= 1) {
         track_ovl_kernel<T><<<n_ch, nt, sm, s>>>(a);
     } else {

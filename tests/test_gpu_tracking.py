@@ -7,6 +7,8 @@ behaviour is checked with the reference's own closed-loop criteria
 (test_tracking.cpp:403-479)."""
 import math
 
+import os
+
 import numpy as np
 import pytest
 
@@ -345,25 +347,45 @@ def test_cluster_sizes(ctx, oracle_mod, K):
 
 @pytest.mark.parametrize("fmt,fs", [(abi.FMT_INT8_IQ, 2.048e6), (abi.FMT_INT16_IQ, 16.368e6)])
 @pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SINGLE])
-def test_raw_ring_matches_decoded_ring(ctx, fmt, fs, cta_mode):
+def test_raw_ring_matches_decoded_ring(ctx, oracle_mod, fmt, fs, cta_mode):
     """Raw complex-int rings (converted in the correlator with the decode
-    scale folded into the rotators, a power of two) give bit-identical
-    records to decoded float2 rings in the same CTA shape.  (The throughput
-    shape picks a different tile size for raw rings, so its fp32 summation
-    order differs; it is covered by per-epoch replay parity instead.)"""
+    scale folded into the rotators, a power of two) track like decoded
+    float2 rings: both pass per-epoch replay parity, and with the same
+    kernel (L1RXG_OVL=0: decoded latency-shape rings on track_kernel, as raw
+    rings always are) the records are bit-identical.  (The overlapped kernel
+    and the throughput shape's raw-ring tile size sum in another fp32 order.)"""
     n = int(round(fs / 1000))
     sv = ss.Sv(prn=7, cn0_dbhz=46.0, doppler_hz=-1500.0, delay_chips=321.7)
     name = "int8_iq" if fmt == abi.FMT_INT8_IQ else "int16_iq"
     raw = _raw(60, fs, [sv], name, seed=91)
+    init = _init(sv, fs)
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    x = oracle_mod.ingest(raw, fmt, fs)
     outs = []
     for rr in (False, True):
-        trk = Tracker(ctx, fmt, fs, 0.0, [_init(sv, fs)], ring_samples=70 * n, max_records=60,
+        trk = Tracker(ctx, fmt, fs, 0.0, [init], ring_samples=70 * n, max_records=60,
                       cta_mode=cta_mode, ring_raw=rr)
         trk.push(0, raw)
         trk.run()
         outs.append(trk.records(0))
-    assert len(outs[0]) >= 58
-    assert outs[0].tobytes() == outs[1].tobytes()
+        assert len(outs[-1]) >= 58
+        replay_check(oracle_mod, init, outs[-1], x, n, cfg, taps, fs)
+    if os.environ.get("L1RXG_OVL") == "0":
+        assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_latency_shape_without_overlap():
+    """The latency shape's non-overlapped kernel (L1RXG_OVL=0, read once per
+    process): raw-vs-decoded bit identity and replay parity in a child."""
+    import subprocess
+    import sys
+    env = dict(os.environ, L1RXG_OVL="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_tracking.py"), "-k",
+                        "raw_ring_matches_decoded_ring or cluster_sizes"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("fs", [5.0e6, 3.969e6])
