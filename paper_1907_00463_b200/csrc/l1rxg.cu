@@ -220,11 +220,12 @@ int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
     if ((ev && ev[0] == '0') || a.thr || sk != SK_F32 || a.nbuf != 2 ||
         a.lc.kernel == L1RXG_KERNEL_NOOP)
         return -1;
-    const int nwork = nt - 32;
-    if ((a.csize > 1 ? a.share : a.n) > nwork * RUN)
+    const int len = a.csize > 1 ? std::min(a.n, a.share) : a.n;  // rank 0's unit: the largest
+    if (len > (nt - 32) * RUN)
         return -1;
+    const int nrun = (len + RUN - 1) / RUN;  // the kernel's layout unit
     const size_t xsl = (2u * a.csize * (2 * T + 2) * sizeof(double) + 15) & ~size_t(15);
-    const size_t sm = smem_bytes<T>(nwork, 2, 8) + xsl + ovl_extra_bytes(nwork);
+    const size_t sm = smem_bytes<T>(nrun, 2, 8) + xsl + ovl_extra_bytes(nrun);
     if (sm > 227u * 1024u)
         return -1;
     CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

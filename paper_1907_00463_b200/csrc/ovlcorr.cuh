@@ -38,12 +38,14 @@ __device__ __forceinline__ void named_bar_arrive(int id, int count) {
 #endif
 constexpr float OVL_DW_RUN_MAX = L1RXG_OVL_DWMAX;
 
-// Extra shared memory of the overlapped kernel, after track_kernel's layout
-// (header, anchors, 2 sample tiles, cluster exchange slots): P' and M' tiles
-// for both buffers, per-run totals, double-buffered rotator tables.
-__host__ __device__ inline size_t ovl_extra_bytes(int nwork) {
-    const size_t cap = (size_t)nwork * RUN;
-    return 4 * cap * sizeof(float2) + 2 * (size_t)nwork * sizeof(float2) + 2 * 32 * sizeof(float2) +
+// Shared memory of the overlapped kernel: track_kernel's layout (header,
+// anchors, 2 sample tiles, cluster exchange slots) sized by the runs of one
+// unit (nrun = ceil(len / RUN), not the CTA's work threads), then one P' and
+// one M' tile (epoch e's are dead once its phase B is done, before phase A'
+// of e+1 starts), per-run totals, double-buffered rotator tables.
+__host__ __device__ inline size_t ovl_extra_bytes(int nrun) {
+    const size_t cap = (size_t)nrun * RUN;
+    return 2 * cap * sizeof(float2) + 2 * (size_t)nrun * sizeof(float2) + 2 * 32 * sizeof(float2) +
            4 * sizeof(double) + 64;
 }
 
@@ -175,23 +177,25 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     const int nthr = blockDim.x;
     const int nwork_warps = nwarps - 1;
     constexpr int V = 2 * T + 2;
-    const int cap = nwork * RUN;
     const int n = a.n;
     const int r0 = csize > 1 ? crank * a.share : 0;
     const int rend = csize > 1 ? min(n, r0 + a.share) : n;
     const int len = rend - r0;  // one unit per epoch
     const int skip = n - len;
+    // shared-memory layout unit: rank 0's (largest) unit in every CTA, so the
+    // cluster exchange slots sit at the same offset in all of them
+    const int nrun = ((csize > 1 ? min(n, a.share) : n) + RUN - 1) / RUN;
+    const int cap = nrun * RUN;
     const int64_t avail = a.avail[strm];
     const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * esz;
     float2* anchors = anchors_of(s);
-    double* xs = xslots_of(s, nwork, 2, esz);
+    double* xs = xslots_of(s, nrun, 2, esz);
     unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ((2 * csize * V * sizeof(double) + 15) & ~size_t(15));
-    float2* const pm0 = reinterpret_cast<float2*>(xb);  // P' tiles [2][cap], then M' tiles [2][cap]
-    auto pm = [&](int b) { return pm0 + b * cap; };
-    auto mm = [&](int b) { return pm0 + (2 + b) * cap; };
-    float2* ptot = reinterpret_cast<float2*>(xb) + 4 * cap;
-    float2* mtot = ptot + nwork;
-    float2* rot2 = mtot + nwork;  // [2][32]
+    float2* const pm0 = reinterpret_cast<float2*>(xb);  // P' tile [cap]
+    float2* const mm0 = pm0 + cap;                       // M' tile [cap]
+    float2* ptot = mm0 + cap;
+    float2* mtot = ptot + nrun;
+    float2* rot2 = mtot + nrun;  // [2][32]
     double* wp = reinterpret_cast<double*>(rot2 + 64);  // [2]: the rate each buffer's P'/M' were made with
     int* ie = reinterpret_cast<int*>(wp + 2);            // [2]: epoch whose copy was issued into each tile
     long long* dn = reinterpret_cast<long long*>(ie + 2); // epochs done (control warp -> writeback)
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             return;
         const int b = v & 1;
         const int64_t pos = s->issue_pos;
-        issue_unit(s, b, tile_of(s, nwork, b, esz), ring, pos, len, esz);
+        issue_unit(s, b, tile_of(s, nrun, b, esz), ring, pos, len, esz);
         ie[b] = v;
         int64_t nxt = pos + len + skip;
         while (nxt >= a.ring_cap)
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
         const int b = v & 1;
         const int delta = (int)(unit_pos(v) & (A - 1));
         const int h = A * ((len + delta) / (2 * A));
-        const float2* rawt = reinterpret_cast<const float2*>(tile_of(s, nwork, b, esz)) + delta;
+        const float2* rawt = reinterpret_cast<const float2*>(tile_of(s, nrun, b, esz)) + delta;
         const int i0 = r0 + tid * RUN;
         const int cnt = min(RUN, rend - i0);
         const int r0t = delta + tid * RUN;
@@ -265,10 +269,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             if (r0t + RUN > h)
                 mbar_wait(&s->bars[b][1], par);
             if (cnt == RUN)
-                ovl_phase_a<true>(rawt + tid * RUN, pm(b) + tid * RUN, mm(b) + tid * RUN, rot, cnt, ptot[tid],
+                ovl_phase_a<true>(rawt + tid * RUN, pm0 + tid * RUN, mm0 + tid * RUN, rot, cnt, ptot[tid],
                                   mtot[tid]);
             else
-                ovl_phase_a<false>(rawt + tid * RUN, pm(b) + tid * RUN, mm(b) + tid * RUN, rot, cnt, ptot[tid],
+                ovl_phase_a<false>(rawt + tid * RUN, pm0 + tid * RUN, mm0 + tid * RUN, rot, cnt, ptot[tid],
                                    mtot[tid]);
         }
     };
@@ -340,11 +344,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
                 const int i0 = u0 + tid * RUN;
                 const int cnt = min(RUN, rend - i0);
                 if (cnt > 0)
-                    ovl_run_totals<T>(c, s->ct, s->d, a.kp, i0, cnt, ptot[tid], mtot[tid], pm(b) + tid * RUN,
-                                      mm(b) + tid * RUN, dw, acc, &anchors[tid]);
+                    ovl_run_totals<T>(c, s->ct, s->d, a.kp, i0, cnt, ptot[tid], mtot[tid], pm0 + tid * RUN,
+                                      mm0 + tid * RUN, dw, acc, &anchors[tid]);
             }
             named_bar_sync(1, nwork);  // anchors visible
-            ovl_phase_b<T>(pb, c, pm(b), mm(b), anchors, s->ct, u0, len, dw);
+            ovl_phase_b<T>(pb, c, pm0, mm0, anchors, s->ct, u0, len, dw);
             phase_b_fold<T>(pb, acc);
             warp_partials<V>(acc, s->red, lane, warp);
             named_bar_sync(1, nwork);  // tile b consumed; partials written
