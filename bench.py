@@ -903,10 +903,13 @@ def main():
     achieved = alg_flops / (track_launch_ms * 1e-3) / 1e12
     peak = fp32_peak_tflops(sm_mhz)
     traffic = None
+    traffic_kernel = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("track_kernel_dram_bytes_per_launch")
+            tj = json.load(open(prof))
+            traffic = tj.get("track_kernel_dram_bytes_per_launch")
+            traffic_kernel = tj.get("kernel")
         except Exception:
             traffic = None
     peaks = {}
@@ -958,7 +961,9 @@ def main():
         "epoch_latency_us": track_launch_ms * 1e3 / max(1.0, float(counts.max())),
         "kernel_ms_per_step": {"ingest": ingest_ms / args.steps, "track": track_launch_ms},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_kernel": traffic_kernel,
+                     "kernel": "track_ovl_kernel (latency shape, L1RXG_OVL=0 -> track_kernel) "
+                               "or track_kernel where the overlap tiles do not fit",
                      "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock under load "
                                     "(%.0f MHz); FP32 pipe roof per SURVEY 8d" % sm_mhz,
                      "alg_ops_per_sample_tap": ops_per_sample_tap(T, C_ch, False),
