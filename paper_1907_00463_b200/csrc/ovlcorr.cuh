@@ -297,10 +297,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
             warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
             const bool stop = s->stop != 0;
-            if (!stop)
-                ovl_fill_rot(rot2 + 32 * ((e + 1) & 1), s->c.w, lane);
-            __syncwarp();
-            named_bar_arrive(3, nthr);  // Y: epoch e+1's constants and rotators (or stop)
+            named_bar_arrive(3, nthr);  // Y: epoch e+1's constants (or stop)
             if (s->pending) {           // epoch e's metrics and record, while e+1 correlates
                 finish_epoch<T>(s, a, lane, writer);
                 __syncwarp();
@@ -329,9 +326,14 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             c.inv_cps = fast_rcp(c.cps);
             const int u0 = r0;
             float dw = (float)(c.w - wp[b]);
+            // work warp 0: this epoch's rotator table (rate w_e), for phase A'
+            // of e+1 (published by the barrier after the run totals) and the
+            // exact fallback -- off the control warp's update path
+            if (tid < 32)
+                ovl_fill_rot(rot2 + 32 * b, c.w, tid);
             if (fabsf(dw) * (float)RUN > OVL_DW_RUN_MAX) {  // rate moved too far: exact phase A
-                if (tid < nwork)
-                    phase_a_epoch(e, rot2 + 32 * b);
+                named_bar_sync(1, nwork);
+                phase_a_epoch(e, rot2 + 32 * b);
                 dw = 0.f;
                 named_bar_sync(1, nwork);
             }
@@ -352,11 +354,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             phase_b_fold<T>(pb, acc);
             warp_partials<V>(acc, s->red, lane, warp);
             named_bar_sync(1, nwork);  // tile b consumed; partials written
-            if (tid == 0) {
+            named_bar_arrive(2, nthr);  // X
+            if (tid == 0) {  // the copy of epoch e+2 into tile b, after X (off the update's path)
                 s->inflight[b] = 0;
                 try_issue(e + 2);
             }
-            named_bar_arrive(2, nthr);  // X
             // speculative phase A' of epoch e+1 with this epoch's rate
             const int64_t offn = off0 + (int64_t)(e + 1) * n;
             const bool next_ok = e + 1 < a.max_epochs && offn + n <= avail;
