@@ -935,6 +935,7 @@ struct TrackArgs {
     int csize;        // CTAs per channel (a thread-block cluster when > 1)
     int share;        // samples of each epoch per cluster CTA (multiple of RUN)
     int thr;          // throughput-shape instantiation (track_kernel<..., true>)
+    float ovl_dwmax;  // overlapped kernel: |dw| * RUN above this recomputes phase A exactly
 };
 
 // Stage clocks (profiling builds only: -DL1RXG_PROFILE, run with

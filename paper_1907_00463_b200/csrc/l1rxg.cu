@@ -1206,6 +1206,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.csize = t->csize;
     a.share = t->share;
     a.thr = t->thr;
+    static const char* ev_dw = std::getenv("L1RXG_OVL_DWMAX");
+    a.ovl_dwmax = ev_dw ? static_cast<float>(std::atof(ev_dw)) : 1e-3f;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);

@@ -31,12 +31,10 @@ __device__ __forceinline__ void named_bar_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// |dw| * RUN above this recomputes phase A exactly (second-order term below
-// 5e-7 of the run's magnitude; the parity bar is 1e-5)
-#ifndef L1RXG_OVL_DWMAX
-#define L1RXG_OVL_DWMAX 1e-3f
-#endif
-constexpr float OVL_DW_RUN_MAX = L1RXG_OVL_DWMAX;
+// |dw| * RUN above TrackArgs::ovl_dwmax recomputes phase A exactly; the
+// host default 1e-3 keeps the second-order term below 5e-7 of the run's
+// magnitude (the parity bar is 1e-5).  Env L1RXG_OVL_DWMAX (tests: -1 runs
+// the exact recompute every epoch).
 
 // Shared memory of the overlapped kernel: track_kernel's layout (header,
 // anchors, 2 sample tiles, cluster exchange slots) sized by the runs of one
@@ -331,7 +329,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             // exact fallback -- off the control warp's update path
             if (tid < 32)
                 ovl_fill_rot(rot2 + 32 * b, c.w, tid);
-            if (fabsf(dw) * (float)RUN > OVL_DW_RUN_MAX) {  // rate moved too far: exact phase A
+            if (fabsf(dw) * (float)RUN > a.ovl_dwmax) {  // rate moved too far: exact phase A
                 named_bar_sync(1, nwork);
                 phase_a_epoch(e, rot2 + 32 * b);
                 dw = 0.f;

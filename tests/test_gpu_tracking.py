@@ -374,17 +374,21 @@ def test_raw_ring_matches_decoded_ring(ctx, oracle_mod, fmt, fs, cta_mode):
         assert outs[0].tobytes() == outs[1].tobytes()
 
 
-def test_latency_shape_without_overlap():
-    """The latency shape's non-overlapped kernel (L1RXG_OVL=0, read once per
-    process): raw-vs-decoded bit identity and replay parity in a child."""
+@pytest.mark.parametrize("env,sel", [
+    ({"L1RXG_OVL": "0"}, "raw_ring_matches_decoded_ring or cluster_sizes"),
+    ({"L1RXG_OVL_DWMAX": "-1"}, "cluster_sizes or odd_epoch_lengths or config1_shape or twelve_channel or multitap"),
+], ids=["no_overlap", "overlap_exact_every_epoch"])
+def test_latency_shape_variants(env, sel):
+    """In a child process (the switches are read once per process): the
+    non-overlapped kernel (L1RXG_OVL=0: raw-vs-decoded bit identity, replay
+    parity), and the overlapped kernel's exact phase-A recompute forced on
+    every epoch (L1RXG_OVL_DWMAX=-1: replay parity through that path)."""
     import subprocess
     import sys
-    env = dict(os.environ, L1RXG_OVL="0")
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_tracking.py"), "-k",
-                        "raw_ring_matches_decoded_ring or cluster_sizes"],
-                       env=env, capture_output=True, text=True, timeout=600)
+                        os.path.join(here, "test_gpu_tracking.py"), "-k", sel],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
