@@ -875,10 +875,17 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             } else {
                 // CTAs with <= 4096 samples are small enough to pair up on an
                 // SM (measured: config 3's 32 channels run 6 % faster as
-                // 8-CTA clusters, two CTAs per SM, than as 4-CTA clusters)
-                while (K < 16 && n / (K * 2) >= 1024 &&
-                       d->n_channels * K * 2 <= (n / (K * 2) <= 4096 ? 2 * nsm : nsm))
+                // 8-CTA clusters, two CTAs per SM, than as 4-CTA clusters);
+                // at one CTA per SM a share down to 32 runs still pays
+                // (config 1, overlapped kernel: 16-CTA cluster +3 % over 8)
+                while (K < 16) {
+                    const int per = n / (K * 2);
+                    const int ctas = d->n_channels * K * 2;
+                    if (!(ctas <= nsm ? per >= 32 * RUN
+                                      : per >= 1024 && per <= 4096 && ctas <= 2 * nsm))
+                        break;
                     K *= 2;
+                }
             }
             const int share = ((n + K * RUN - 1) / (K * RUN)) * RUN;
             while (K > 1 && (K - 1) * share >= n)
