@@ -371,6 +371,141 @@ BATCH = dict(recordings=512, chunk_blocks=50, blocks_per_step=1000,
                   "C/N0 U[30,50] dB-Hz")
 
 
+def batch_parity(trk, raw, recs, inits, cstream, n, fs, cfg, taps, n_rec=4, per_rec=2):
+    """Untimed in-bench parity (oracle/replay.py): every epoch of `per_rec`
+    channels (the first and the last: a visible SV and, when fewer than 12
+    are visible, a noise-only channel) of each of the first `n_rec` local
+    recordings, re-run by the CPU oracle from the GPU's own pre-state --
+    sums within 1e-5 x max|E/P/L| and the 7 tap sums, NCO advance
+    bit-exact, loop outputs within 1e-5."""
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle
+    from oracle.replay import replay_channel
+    from paper_1907_00463_b200 import abi
+    t0 = time.perf_counter()
+    R = min(n_rec, len(recs))
+    picks = []
+    for j in range(R):
+        chans = [c for c in range(len(inits)) if cstream[c] == j]
+        picks += sorted({chans[0], chans[-1]})[:per_rec]
+    xs = {j: oracle.ingest(raw[j].cpu().numpy(), abi.FMT_INT16_IQ, fs) for j in range(R)}
+    got = {c: trk.records(c, tap_sums=True) for c in picks}
+
+    def one(c):
+        recs_c, ts = got[c]
+        return replay_channel(oracle, inits[c], recs_c, xs[cstream[c]], n, cfg, taps, fs, tap_sums=ts)
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        res = list(ex.map(one, picks))
+    worst = {k: max(r[0][k] for r in res) for k in ("sums", "taps", "loop", "cn0")}
+    n_bad = sum(r[1] for r in res)
+    first = next((r[2] for r in res if r[2]), None)
+    checked = int(sum(len(got[c][0]) for c in picks))
+    ok = worst["sums"] <= 1e-5 and worst["taps"] <= 1e-5 and worst["loop"] <= 1e-5 and n_bad == 0
+    return {"ok": bool(ok), "checked_channel_epochs": checked, "channels": picks,
+            "recordings": list(range(R)), "worst_sum": worst["sums"], "worst_tap_sum": worst["taps"],
+            "worst_loop": worst["loop"], "worst_cn0_rel": worst["cn0"], "exact_field_mismatches": n_bad,
+            "first_mismatch": first, "tolerance": {"sums": 1e-5, "loop": 1e-5, "nco": "bit-exact"},
+            "oracle": "oracle/l1rx_oracle.c track_epoch (tracking.hpp:520-618 restated; 3-tap instance "
+                      "pinned to the reference build), replayed from the GPU's own pre-state",
+            "seconds": round(time.perf_counter() - t0, 1)}
+
+
+def host_budget(need_local, world):
+    """Whether `need_local` bytes of pinned host memory per rank fit this host
+    with every local rank asking the same (ranks share the host's RAM)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        return False, 0
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    margin = 24 << 30  # the processes themselves, torch, page cache
+    return need_local * local_world + margin <= avail, avail
+
+
+def batch_e2e(ctx, raw, recs, inits, cstream, taps, cfg, fs, n, blocks, chunk_b, T, args, world, dist,
+              dev, barrier):
+    """e2e leg of config 4 through the public API: the local recordings
+    live in pinned host memory as `blocks / chunk_b` chunk buffers
+    [recording][chunk_b blocks]; each step resets a ring tracker, streams
+    every chunk with l1rxg_tracker_push_strided (H2D on the library's copy
+    stream into two alternating device staging blocks, overlapped with the
+    previous chunk's tracking) + run, and reads every epoch record back
+    into pinned host memory."""
+    import torch
+    from paper_1907_00463_b200 import abi
+    from paper_1907_00463_b200.tracking import Tracker
+    nrl = len(recs)
+    cb = chunk_b * n * 4
+    n_chunks = -(-blocks // chunk_b)
+    need = nrl * blocks * n * 4
+    fits, avail = host_budget(need, world)
+    e2e_recs = nrl
+    while not fits and e2e_recs > 1:  # never on the measured boxes (196 GB host, 134 GB input)
+        e2e_recs //= 2
+        fits, avail = host_budget(e2e_recs * blocks * n * 4, world)
+    if not fits:
+        return {"value": None, "unit": UNIT, "skipped": "host memory (%.0f GB available)" % (avail / 1e9)}
+    t_fill = time.perf_counter()
+    chunks = []
+    for c in range(n_chunks):
+        a, b = c * cb, min((c + 1) * cb, blocks * n * 4)
+        buf = ctx.host_alloc(e2e_recs * (b - a)).reshape(e2e_recs, b - a)
+        for j in range(e2e_recs):  # row by row: a strided device slice would stage a device copy
+            torch.from_numpy(buf[j]).copy_(raw[j, a:b])
+        chunks.append(buf)
+    torch.cuda.synchronize()
+    t_fill = time.perf_counter() - t_fill
+    nci = sum(1 for s_ in cstream if s_ < e2e_recs)
+    te = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits[:nci], chan_stream=cstream[:nci],
+                 n_streams=e2e_recs, taps=taps, cfg=cfg, ring_samples=(chunk_b + 4) * n,
+                 max_records=blocks, cta_mode=abi.CTA_SEGMENT)
+    rec_bytes = te.records_nbytes()
+    rec_pinned = ctx.host_alloc(rec_bytes)  # the step's records land in pinned host memory
+
+    def step_e2e():
+        te.reset(inits[:nci])
+        for buf in chunks:
+            te.push_strided(buf)
+            te.run()
+        te.records_raw(dst_ptr=rec_pinned.ctypes.data)
+        te.sync()
+
+    step_e2e()
+    te.timing()
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    e2e_ms = (time.perf_counter() - w0) * 1e3 / args.steps
+    _, _, e2e_launches = te.timing()
+    if dist:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_epochs_local = float(te.epoch_counts().sum())
+    e2e_epochs = e2e_epochs_local
+    if dist:  # every rank's channel-epochs of the step
+        tt = torch.tensor([e2e_epochs_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        e2e_epochs = float(tt.item())
+    out = {"value": e2e_epochs * n * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": int(e2e_recs * blocks * n * 4), "d2h_bytes_per_step": int(rec_bytes),
+           "blocks_per_step": blocks, "recordings_per_rank": e2e_recs, "channel_epochs_per_rank": e2e_epochs_local,
+           "h2d_gbs": e2e_recs * blocks * n * 4 / (e2e_ms * 1e-3) / 1e9,
+           "gpu_launches_per_step": e2e_launches / max(1, args.steps),
+           "pinned_source": "%d chunk buffers of %d blocks x %d recordings (%.1f GB each, %.1f GB pinned; "
+                            "filled in %.1f s, untimed)" % (n_chunks, chunk_b, e2e_recs, e2e_recs * cb / 1e9,
+                                                           e2e_recs * blocks * n * 4 / 1e9, t_fill),
+           "path": "pinned host chunk [recording][%d blocks] -> l1rxg_tracker_push_strided (H2D on the copy "
+                   "stream into one of two device staging blocks + one raw-ring copy launch) -> "
+                   "l1rxg_tracker_run (segment correlator over the chunk) -> ... -> records_raw to pinned "
+                   "host; wall clock per step, max over ranks" % chunk_b}
+    del te
+    del chunks
+    return out
+
+
 def run_batch(args, rank, world, local, dist, emit=True):
     """Config 4: many independent recordings, sharded by recording over the
     ranks (strong scaling: the 512 recordings are split, no data-path
@@ -494,58 +629,18 @@ def run_batch(args, rank, world, local, dist, emit=True):
         gathered = sum(int(o.numel()) for o in outs) if rank == 0 else None
         del rec_t, outs
 
-    # ---- e2e: the same step from pinned host memory (strided pushes)
+    # ---- untimed parity: oracle replay of a deterministic sample of epochs
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = batch_parity(trk, raw, recs, inits, cstream, n, fs, cfg, taps)
+
+    # ---- e2e: the same step from pinned host memory, every block of every
+    # local recording (bounded pinned chunks of chunk_b blocks, streamed
+    # through l1rxg_tracker_push_strided into a ring tracker)
     e2e = None
-    try:
-        import psutil
-        room = psutil.virtual_memory().available
-    except Exception:
-        room = 0
-    e2e_blocks = blocks
-    while e2e_blocks > chunk_b and len(recs) * e2e_blocks * n * 4 * 3 > room:
-        e2e_blocks //= 2
-    if not args.no_e2e and len(recs) * e2e_blocks * n * 4 * 3 <= room:
-        eb = e2e_blocks * n * 4
-        pinned = ctx.host_alloc(len(recs) * eb).reshape(len(recs), eb)
-        for j in range(len(recs)):  # row by row: a strided slice would stage a device copy
-            pinned[j] = raw[j, :eb].cpu().numpy()
-        # the segment correlator's device leg reads attached recordings; the
-        # host leg streams into its own rings
-        te = trk if not attached else Tracker(
-            ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(recs), taps=taps,
-            cfg=cfg, ring_samples=(chunk_b + 4) * n, max_records=blocks, cta_mode=abi.CTA_SEGMENT)
-        rec_bytes = te.records_nbytes()
-        rec_pinned = ctx.host_alloc(rec_bytes)  # the step's records land in pinned host memory
-
-        def step_e2e():
-            te.reset(inits)
-            for o in range(0, eb, chunk):
-                te.push_strided(pinned[:, o:o + chunk])
-                te.run()
-            te.records_raw(dst_ptr=rec_pinned.ctypes.data)
-            te.sync()
-            return rec_pinned
-
-        step_e2e()
-        barrier()
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            step_e2e()
-        e2e_ms = (time.perf_counter() - w0) * 1e3 / args.steps
-        if dist:
-            tt = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
-        e2e_epochs = float(te.epoch_counts().sum()) * (epochs_all / max(epochs_local, 1.0))
-        e2e = {"value": e2e_epochs * n * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(len(recs) * eb), "d2h_bytes_per_step": int(rec_bytes),
-               "blocks_per_step": e2e_blocks,
-               "path": "pinned host [recording][bytes] -> l1rxg_tracker_push_strided (one pitched "
-                       "H2D + one %s launch per %d-block chunk) -> run -> records_raw to pinned host" % (
-                           "raw-ring copy" if attached else "decode", chunk_b)}
-        del pinned
-        if te is not trk:
-            del te
+    if not args.no_e2e:
+        e2e = batch_e2e(ctx, raw, recs, inits, cstream, taps, cfg, fs, n, blocks, chunk_b, T, args,
+                        world, dist, dev, barrier)
     if rank != 0:
         if emit:
             dist.destroy_process_group()
@@ -570,13 +665,19 @@ def run_batch(args, rank, world, local, dist, emit=True):
         threads = os.cpu_count() or 1
         cb = min(args.cpu_blocks, blocks, 1000)
         R = min(8, len(recs))  # >= 8 recordings x 1000 blocks, scaled linearly
+        t_ing = time.perf_counter()
         xs = [oracle.ingest(raw[j, : cb * n * 4].cpu().numpy(), abi.FMT_INT16_IQ, fs) for j in range(R)]
+        t_ing = time.perf_counter() - t_ing
         nci = sum(1 for s_ in cstream if s_ < R)
         wall, ce = cpu_port_run(xs, inits[:nci], cfg, taps, fs, cb, threads, chan_stream=cstream[:nci])
         del xs
         cpu = {"value": float(ce) * n * T / wall / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+               "scope": "tracking stage only (correlator + loop update, bench.hpp:59-102); ingest "
+                        "(cint16 decode) timed separately",
+               "tracking_s": wall, "ingest_s": t_ing,
                "sample": f"recordings 0-{R - 1}: {nci} channels x {cb} blocks (oracle K-tap "
-                         f"restatement, {wall:.2f} s wall)"}
+                         f"restatement -- the reference has no 7-tap correlator -- on a {threads}-thread "
+                         f"channel pool, {wall:.2f} s)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -614,11 +715,17 @@ def run_batch(args, rank, world, local, dist, emit=True):
                                      ("unique float2 baseband bytes per step (each recording's ring read "
                                       "once; its 12 channels share it through L2)")}},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "parity": parity,
     }
     if gathered is not None:
         line["records_gathered_bytes"] = gathered
     if not emit:
         return line
+    if args.companion and world == 1:
+        trk.close()
+        del raw
+        torch.cuda.empty_cache()
+        line["companion_latency"] = companion_latency(args, local)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -657,6 +764,7 @@ def run_batch_reference(args, rank):
     threads = os.cpu_count() or 1
     walls, ces = [], []
     for step in range(args.warmup + args.steps):
+        # tracking stage only (bench.hpp:59-102); the cint16 decode ran above
         wall, ce = cpu_port_run(xs, inits, cfg, taps, fs, per_step, threads, chan_stream=cstream)
         if step >= args.warmup:
             walls.append(wall)
@@ -671,32 +779,34 @@ def run_batch_reference(args, rank):
                                             "parallelism": f"{threads} host threads"},
             "realtime_channels": statistics.mean(ces) / w / 1000.0,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{R} recordings ({len(inits)} channels) x {per_step} blocks per step"},
+                             "scope": "tracking stage only (correlator + loop update, bench.hpp:59-102)",
+                             "sample": f"{R} recordings ({len(inits)} channels) x {per_step} blocks per step "
+                                       f"(oracle K-tap restatement: the reference has no 7-tap correlator; "
+                                       f"its 3-tap instance equals the reference's scalar kernel)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return line
 
 
-def companion_config4(args, rank, world, local, dist):
-    """The throughput shape next to the latency-bound headline: config 4
-    (512 independent recordings x 1 000 blocks, 12 channels x 7 taps, cint16
-    at 65.472 MHz, the segment correlator on the resident recordings), its
-    value and roofline fraction; `bench.py --config 4` adds the e2e leg and
-    the CPU baseline."""
+def companion_latency(args, local):
+    """The latency view next to the throughput headline: config 2 (12
+    channels on one int8 real-IF stream, 10 000 strictly sequential 1-ms
+    epochs, the overlapped latency kernel), its value, e2e, per-epoch
+    critical path and roofline fraction; `bench.py --config 2` gives the
+    full line with its CPU baseline."""
     import copy
     import torch
     a = copy.copy(args)
-    a.recordings, a.blocks, a.steps, a.warmup = 0, 0, 3, 3
-    a.no_cpu_baseline, a.no_e2e, a.cta, a.ring_raw = True, True, "segment", False
+    a.blocks, a.steps, a.warmup = 0, 3, 3
+    a.no_cpu_baseline = True
     try:
-        ln = run_batch(a, rank, world, local, dist, emit=False)
         torch.cuda.empty_cache()
-        return {"workload": "config4: %d recordings x 12 channels x 7 taps x %d blocks (device-resident; "
-                            "bench.py --config 4 for the full line)" % (ln["config"]["recordings"],
-                                                                      ln["config"]["blocks_per_step"]),
-                "value": ln["value"], "unit": ln["unit"], "ms_per_step": ln["ms_per_step"],
-                "realtime_channels": ln["realtime_channels"], "roofline": ln["roofline"],
-                "clocks": ln["clocks"]}
+        ln = run_stream(a, 2, 0, 1, local, None, emit=False)
+        torch.cuda.empty_cache()
+        return {"workload": CONFIGS[2]["desc"], "value": ln["value"], "unit": ln["unit"],
+                "ms_per_step": ln["ms_per_step"], "epoch_latency_us": ln["epoch_latency_us"],
+                "realtime_channels": ln["realtime_channels"], "e2e": ln["e2e"], "roofline": ln["roofline"],
+                "gpu_launches": ln["gpu_launches"], "clocks": ln["clocks"]}
     except Exception as ex:  # reported, never fatal for the headline line
         return {"error": repr(ex)}
 
@@ -707,18 +817,20 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 4: the largest single-GPU workload)")
     ap.add_argument("--blocks", type=int, default=0, help="override the config's block count")
     ap.add_argument("--cpu-blocks", type=int, default=3000, help="CPU baseline sample (blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="config 4: skip the host-memory e2e leg")
+    ap.add_argument("--no-parity", action="store_true", help="config 4: skip the untimed oracle replay")
     ap.add_argument("--e2e-chunk-ms", type=int, default=1000)
     ap.add_argument("--recordings", type=int, default=0, help="config 4: override 512 recordings")
     ap.add_argument("--cta", default="segment", choices=["segment", "throughput", "latency"],
                     help="config 4 CTA shape: segment correlator (raw cint16 ring), throughput, latency")
     ap.add_argument("--ring-raw", action="store_true", help="config 4: keep cint16 raw in the rings")
     ap.add_argument("--no-companion", dest="companion", action="store_false",
-                    help="config 2: skip the config-4 throughput companion measurement")
+                    help="config 4: skip the config-2 latency companion measurement")
     args = ap.parse_args()
 
     import torch
@@ -726,18 +838,31 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    if args.impl == "reference":  # CPU arm: rank 0 alone runs and prints it
+        if rank != 0:
+            return None
+        if args.config == 5:
+            return run_grid(args, 0, 1, local, None)
+        if args.config == 4:
+            return run_batch_reference(args, 0)
+        return run_stream(args, args.config, 0, 1, local, None)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     if args.config == 5:
         return run_grid(args, rank, world, local, dist)
-    if args.config == 4 and args.impl == "gpu":
-        return run_batch(args, rank, world, local, dist)
     if args.config == 4:
-        return run_batch_reference(args, rank)
-    c, svs, chans = scenario(args.config, CONFIGS[args.config]["seed"] + rank)
+        return run_batch(args, rank, world, local, dist)
+    return run_stream(args, args.config, rank, world, local, dist)
+
+
+def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
+    """Configs 1-3: channels sharing one stream, closed loop over sequential
+    1-ms epochs (latency-bound by construction).  Weak scaling: each rank
+    tracks its own seeded recording."""
+    import torch
+    c, svs, chans = scenario(cfg_id, CONFIGS[cfg_id]["seed"] + rank)
     blocks = args.blocks or c["blocks"]
     fs = c["fs"]
     n = int(round(fs / 1000))
@@ -750,8 +875,6 @@ def main():
     sample_taps = float(blocks) * n * T * C_ch
 
     if args.impl == "reference":
-        if rank != 0:
-            return
         from paper_1907_00463_b200 import simsource as ss
         dev = "cuda" if torch.cuda.is_available() else "cpu"
         per_step = min(blocks, 1000)
@@ -759,34 +882,46 @@ def main():
                        device=dev).cpu().numpy()
         threads = os.cpu_count() or 1
         kind = "reference"
-        walls = []
+        walls, trks, ings = [], [], []
         for step in range(args.warmup + args.steps):
             if c["taps"] == "epl":
-                wall, _, ce = cpu_reference_run(raw, c, inits, cfg, per_step, threads)
+                # tracking stage only (bench.hpp:59-102): the pipeline's
+                # track_epoch rounds; the wall adds the SampleSource producer
+                wall, trk_s, ce = cpu_reference_run(raw, c, inits, cfg, per_step, threads)
+                ing = None
             else:
                 import oracle
-                fmtc = abi.FMT_INT16_IQ
-                x = oracle.ingest(raw, fmtc, fs)
                 t0 = time.perf_counter()
-                wall, ce = cpu_port_run(x, inits, cfg, taps, fs, per_step, threads)
-                wall = time.perf_counter() - t0
+                x = oracle.ingest(raw, abi.FMT_INT16_IQ, fs)
+                ing = time.perf_counter() - t0
+                trk_s, ce = cpu_port_run(x, inits, cfg, taps, fs, per_step, threads)
+                wall = trk_s + ing
                 kind = "port"
             if step >= args.warmup:
                 walls.append(wall)
+                trks.append(trk_s)
+                ings.append(ing)
         st_per = float(per_step) * n * T * C_ch
-        v = st_per / statistics.mean(walls) / 1e9
+        v = st_per / statistics.mean(trks) / 1e9
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
+                "ms_per_step": statistics.mean(trks) * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": c["desc"], "sample_blocks_per_step": per_step,
                            "parallelism": f"{threads} host threads"},
-                "realtime_channels": C_ch * per_step / statistics.mean(walls) / 1000.0,
+                "realtime_channels": C_ch * per_step / statistics.mean(trks) / 1000.0,
+                "tracking_stage_s": statistics.mean(trks),
+                "wall_incl_ingest": {"value": st_per / statistics.mean(walls) / 1e9, "unit": UNIT,
+                                     "s": statistics.mean(walls),
+                                     "note": "SampleSource producer thread (real-IF mixer + FIR) + "
+                                             "tracking, as the Receiver runs it" if kind == "reference"
+                                     else "ingest + tracking"},
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                                 "scope": "tracking stage only (bench.hpp:59-102)",
                                  "sample": f"{per_step} blocks x {C_ch} channels of the workload per step"},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
-        return
+        return line
 
     # ------------------------------------------------------------ GPU arm
     from paper_1907_00463_b200 import simsource as ss
@@ -892,7 +1027,7 @@ def main():
 
     if rank != 0:
         dist.destroy_process_group()
-        return
+        return None
 
     # ---- roofline of the dominant kernel (track_kernel, one launch/step)
     clk = clocks.summary()
@@ -904,7 +1039,7 @@ def main():
     peak = fp32_peak_tflops(sm_mhz)
     traffic = None
     traffic_kernel = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_config{cfg_id}.json")
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
@@ -979,11 +1114,14 @@ def main():
     }
     if gathered is not None:
         line["records_gathered_bytes"] = gathered
-    if args.config == 2 and args.companion and world == 1:
-        line["companion_throughput"] = companion_config4(args, rank, world, local, dist)
+    trk.close()
+    ctx.close()
+    if not emit:
+        return line
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    return line
 
 
 if __name__ == "__main__":

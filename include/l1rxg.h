@@ -302,6 +302,9 @@ int l1rxg_tracker_push_device_strided(l1rxg_tracker* trk, const void* dev_bytes,
  * (samples.hpp:136-211) for batch re-processing. */
 int l1rxg_tracker_attach_device(l1rxg_tracker* trk, const void* dev_bytes,
                                 int64_t samples_per_stream, int64_t stride_bytes);
+/* Ends an attachment: the tracker reads its own ring again, every stream
+ * restarts empty (pushes are refused while recordings are attached). */
+int l1rxg_tracker_detach(l1rxg_tracker* trk);
 /* Runs every channel over every epoch whose 1-ms window is fully
  * ingested (at most max_epochs per channel; <0 = unbounded).  Async. */
 int l1rxg_tracker_run(l1rxg_tracker* trk, int max_epochs);

@@ -21,7 +21,7 @@ EXPORTS = [
     "l1rxg_host_free", "l1rxg_correlate_epoch", "l1rxg_correlate_batch", "l1rxg_tracker_create",
     "l1rxg_tracker_destroy", "l1rxg_tracker_push", "l1rxg_tracker_push_device",
     "l1rxg_tracker_push_strided", "l1rxg_tracker_push_device_strided", "l1rxg_tracker_attach_device",
-    "l1rxg_tracker_run",
+    "l1rxg_tracker_detach", "l1rxg_tracker_run",
     "l1rxg_tracker_sync", "l1rxg_tracker_channels", "l1rxg_tracker_epoch_counts",
     "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_reset",
     "l1rxg_tracker_stream", "l1rxg_tracker_read_samples",
@@ -69,6 +69,7 @@ def lib():
     _sig(L, "l1rxg_tracker_push_strided", C.c_int, vp, vp, i64, i64)
     _sig(L, "l1rxg_tracker_push_device_strided", C.c_int, vp, vp, i64, i64)
     _sig(L, "l1rxg_tracker_attach_device", C.c_int, vp, vp, i64, i64)
+    _sig(L, "l1rxg_tracker_detach", C.c_int, vp)
     _sig(L, "l1rxg_tracker_run", C.c_int, vp, C.c_int)
     _sig(L, "l1rxg_tracker_sync", C.c_int, vp)
     _sig(L, "l1rxg_tracker_channels", C.c_int, vp, P(abi.Channel))

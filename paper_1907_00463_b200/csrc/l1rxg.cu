@@ -263,6 +263,59 @@ int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
     return 0;
 }
 
+// How many clusters of K CTAs (nt threads each) can be resident at once for
+// the latency kernels launch_track may pick (the smaller of track_kernel's
+// and the overlapped kernel's count).  Clusters of more than 8 CTAs are
+// limited by how many fit a GPC, not by the SM count, so the auto cluster
+// rule checks this before it keeps K = 16.
+template <int T>
+int cluster_capacity(int K, int nt, int nbuf, int len) {
+    auto cap = [&](const void* fn, size_t sm) -> int {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+            (K > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+            cudaGetLastError();
+            return 0;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(K));
+        cfg.blockDim = dim3(static_cast<unsigned>(nt));
+        cfg.dynamicSmemBytes = sm;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(K);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return nc;
+    };
+    const size_t xs = 2u * K * (2 * T + 2) * sizeof(double);
+    int c = cap(reinterpret_cast<const void*>(track_kernel<T, SK_F32, false>),
+                smem_bytes<T>(nt - 32, nbuf, 8) + xs);
+    const int nrun = (len + RUN - 1) / RUN;
+    const size_t sm_ovl = smem_bytes<T>(nrun, 2, 8) + ((xs + 15) & ~size_t(15)) + ovl_extra_bytes(nrun);
+    if (nbuf == 2 && sm_ovl <= 227u * 1024u)
+        c = std::min(c, cap(reinterpret_cast<const void*>(track_ovl_kernel<T>), sm_ovl));
+    return c;
+}
+
+int cluster_capacity_T(int T, int K, int nt, int nbuf, int len) {
+    switch (T) {
+    case 3: return cluster_capacity<3>(K, nt, nbuf, len);
+    case 5: return cluster_capacity<5>(K, nt, nbuf, len);
+    case 7: return cluster_capacity<7>(K, nt, nbuf, len);
+    case 9: return cluster_capacity<9>(K, nt, nbuf, len);
+    case 11: return cluster_capacity<11>(K, nt, nbuf, len);
+    case 13: return cluster_capacity<13>(K, nt, nbuf, len);
+    default: return cluster_capacity<16>(K, nt, nbuf, len);
+    }
+}
+
 template <int T>
 int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
     if (!a.thr) {
@@ -558,6 +611,15 @@ int ingest_launch(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nsamp,
     cudaEventRecord(b, st);
     t->timed.push_back({a, b, 0});
     r.pushed += nsamp;
+    return 0;
+}
+
+// pushes write the tracker's own ring: refused while recordings are attached
+// (the kernels read the attachment through the tensor map, not the ring)
+int refuse_if_attached(const l1rxg_tracker* t) {
+    if (t->att_samples > 0)
+        return set_err(L1RXG_EINVAL, "push on a tracker with attached device recordings "
+                                     "(l1rxg_tracker_detach first)");
     return 0;
 }
 
@@ -887,17 +949,26 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
                     K *= 2;
                 }
             }
-            const int share = ((n + K * RUN - 1) / (K * RUN)) * RUN;
-            while (K > 1 && (K - 1) * share >= n)
-                --K;
-            t->csize = K;
-            t->share = K > 1 ? share : n;
-            t->nt = pick_threads(t->share, nullptr, MAX_NT - 32) + 32;
-            // a second tile when it fits: the copy of epoch e+1 is then issued
-            // while epoch e is still being correlated (a full epoch ahead)
-            static const char* ev_nb1 = std::getenv("L1RXG_LAT_NBUF");
-            const size_t two = static_cast<size_t>(t->nt - 32) * RUN * 2 * sizeof(float2) + 40000;
-            t->nbuf = ev_nb1 ? std::atoi(ev_nb1) : (two <= 200000 ? 2 : 1);
+            const bool auto_k = d->cta_mode != L1RXG_CTA_SINGLE && d->cluster_size == 0 && !ev_cl;
+            for (;;) {
+                const int share = ((n + K * RUN - 1) / (K * RUN)) * RUN;
+                while (K > 1 && (K - 1) * share >= n)
+                    --K;
+                t->csize = K;
+                t->share = K > 1 ? share : n;
+                t->nt = pick_threads(t->share, nullptr, MAX_NT - 32) + 32;
+                // a second tile when it fits: the copy of epoch e+1 is then issued
+                // while epoch e is still being correlated (a full epoch ahead)
+                static const char* ev_nb1 = std::getenv("L1RXG_LAT_NBUF");
+                const size_t two = static_cast<size_t>(t->nt - 32) * RUN * 2 * sizeof(float2) + 40000;
+                t->nbuf = ev_nb1 ? std::atoi(ev_nb1) : (two <= 200000 ? 2 : 1);
+                // non-portable cluster sizes: every channel's cluster must be
+                // resident at once (GPC-limited), else fall back to 8
+                if (!auto_k || K <= 8 ||
+                    cluster_capacity_T(t->T, K, t->nt, t->nbuf, std::min(n, t->share)) >= d->n_channels)
+                    break;
+                K = 8;
+            }
         }
     }
     t->R = d->ring_samples;
@@ -1013,6 +1084,8 @@ int l1rxg_tracker_destroy(l1rxg_tracker* t) {
 int l1rxg_tracker_push_device(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nbytes) {
     if (!t || s < 0 || s >= (int)t->streams.size())
         return set_err(L1RXG_EINVAL, "bad stream");
+    if (int rc = refuse_if_attached(t))
+        return rc;
     const int bps = bytes_per_sample(t->d.format);
     if (nbytes <= 0)
         return 0;
@@ -1029,6 +1102,8 @@ int l1rxg_tracker_push_device_strided(l1rxg_tracker* t, const void* dev_bytes,
                                       int64_t nbytes_per_stream, int64_t stride_bytes) {
     if (!t || !dev_bytes)
         return set_err(L1RXG_EINVAL, "null argument");
+    if (int rc = refuse_if_attached(t))
+        return rc;
     const int bps = bytes_per_sample(t->d.format);
     if (nbytes_per_stream <= 0)
         return 0;
@@ -1094,6 +1169,8 @@ int l1rxg_tracker_push_strided(l1rxg_tracker* t, const void* bytes, int64_t nbyt
                                int64_t stride_bytes) {
     if (!t || !bytes)
         return set_err(L1RXG_EINVAL, "null argument");
+    if (int rc = refuse_if_attached(t))
+        return rc;
     if (nbytes_per_stream <= 0)
         return 0;
     const int bps = bytes_per_sample(t->d.format);
@@ -1156,9 +1233,31 @@ int l1rxg_tracker_attach_device(l1rxg_tracker* t, const void* dev_bytes, int64_t
     return 0;
 }
 
+int l1rxg_tracker_detach(l1rxg_tracker* t) {
+    if (!t)
+        return set_err(L1RXG_EINVAL, "null tracker");
+    if (t->att_samples == 0)
+        return 0;
+    CK(cudaSetDevice(t->ctx->device));
+    CK(cudaStreamSynchronize(t->ctx->compute));
+    // the tensor map describes the tracker's own ring again; streams restart empty
+    const int64_t stride = t->R + t->apron;
+    CUtensorMap m{};
+    if (int rc = encode_ring_map(&m, t->d_ring, stride / 32, stride * 4, static_cast<int>(t->streams.size())))
+        return rc;
+    t->tmap = m;
+    t->att_samples = 0;
+    for (auto& r : t->streams)
+        r.pushed = 0;
+    CK(cudaMemset(t->d_avail, 0, 8 * t->streams.size()));
+    return 0;
+}
+
 int l1rxg_tracker_push(l1rxg_tracker* t, int s, const void* bytes, int64_t nbytes) {
     if (!t || s < 0 || s >= (int)t->streams.size())
         return set_err(L1RXG_EINVAL, "bad stream");
+    if (int rc = refuse_if_attached(t))
+        return rc;
     const int bps = bytes_per_sample(t->d.format);
     if (nbytes <= 0)
         return 0;
@@ -1423,7 +1522,7 @@ int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
     CK(cudaMemsetAsync(t->d_ecount, 0, 8 * C, st));
     CK(cudaMemsetAsync(t->d_status, 0, 4 * C, st));
     for (auto& r : t->streams) {
-        r.pushed = 0;
+        r.pushed = t->att_samples;  // attached: every recorded sample stays available
         r.hist_cur = 0;
         for (int k = 0; k < 2; ++k) {
             CK(cudaMemsetAsync(r.hist8[k], 0, 32, st));

@@ -326,8 +326,9 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             float dw = (float)(c.w - wp[b]);
             // work warp 0: this epoch's rotator table (rate w_e), for phase A'
             // of e+1 (published by the barrier after the run totals) and the
-            // exact fallback -- off the control warp's update path
-            if (tid < 32)
+            // exact fallback -- off the control warp's update path.  Epoch 0's
+            // table is the prologue's (slower warps may still be reading it)
+            if (tid < 32 && e > 0)
                 ovl_fill_rot(rot2 + 32 * b, c.w, tid);
             if (fabsf(dw) * (float)RUN > a.ovl_dwmax) {  // rate moved too far: exact phase A
                 named_bar_sync(1, nwork);

@@ -195,6 +195,22 @@ __device__ __noinline__ float2 seg_slow_sum(const unsigned char* buf, int row, c
 // One run (32 samples of row `lane`), fast path: running sum with the
 // captures P(16) (static), P(q0) for q0 in [1, 16), P(q1) for q1 in (16, 32).
 // MASK: samples outside [jlo, jhi) (epoch edges) count as zero.
+//
+// The complex MAC is two packed FFMA2 per sample into one (re, im) register
+// pair: (re, im) += (xr, xi) * (c, c), then (re, im) += (xi, xr) * (s, -s)
+// -- the swapped operand and the one-sided negation are FFMA2 operand
+// modifiers (.LO_HI, .NP) and the rotator component a broadcast scalar, so
+// no moves; the same two roundings per component as fmaf(xi, s, fmaf(xr, c,
+// acc)) (L1RXG_SEG_SCALAR_FMA restores the four scalar FFMAs).
+__device__ __forceinline__ float2 seg_mac(float2 acc, float xr, float xi, float c, float s) {
+#ifdef L1RXG_SEG_SCALAR_FMA
+    return make_float2(fmaf(xi, s, fmaf(xr, c, acc.x)), fmaf(-xr, s, fmaf(xi, c, acc.y)));
+#else
+    acc = __ffma2_rn(make_float2(xr, xi), make_float2(c, c), acc);
+    return __ffma2_rn(make_float2(xi, xr), make_float2(s, -s), acc);
+#endif
+}
+
 template <bool MASK>
 __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, const float4* rot4, int q0,
                                         int q1, int jlo, int jhi, float2& p16, float2& c0, float2& c1,
@@ -203,8 +219,8 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
     // (16..31), interleaved for ILP: P(16 + j) = P(16) + B(j)
     const unsigned char* rowp = buf + lane * 128;
     const int sw = lane & 7;
-    float ar = 0.f, ai = 0.f, br = 0.f, bi = 0.f;
-    float c0r = 0.f, c0i = 0.f, c1r = 0.f, c1i = 0.f;
+    float2 A = make_float2(0.f, 0.f), B = make_float2(0.f, 0.f);
+    float2 C0 = make_float2(0.f, 0.f), C1 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
         const uint4 wa4 = *reinterpret_cast<const uint4*>(rowp + ((ch ^ sw) << 4));
@@ -225,26 +241,18 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
                 xa = (j >= jlo && j < jhi) ? xa : 0u;
                 xb = (j + 16 >= jlo && j + 16 < jhi) ? xb : 0u;
             }
-            if (j > 0 && j == q0) {
-                c0r = ar;
-                c0i = ai;
-            }
-            if (j > 0 && j + 16 == q1) {
-                c1r = br;
-                c1i = bi;
-            }
-            const float xar = seg_re(xa), xai = seg_im(xa);
-            const float xbr = seg_re(xb), xbi = seg_im(xb);
-            ar = fmaf(xai, as[t], fmaf(xar, ac[t], ar));
-            ai = fmaf(-xar, as[t], fmaf(xai, ac[t], ai));
-            br = fmaf(xbi, bs[t], fmaf(xbr, bc[t], br));
-            bi = fmaf(-xbr, bs[t], fmaf(xbi, bc[t], bi));
+            if (j > 0 && j == q0)
+                C0 = A;
+            if (j > 0 && j + 16 == q1)
+                C1 = B;
+            A = seg_mac(A, seg_re(xa), seg_im(xa), ac[t], as[t]);
+            B = seg_mac(B, seg_re(xb), seg_im(xb), bc[t], bs[t]);
         }
     }
-    p16 = make_float2(ar, ai);
-    c0 = make_float2(c0r, c0i);
-    c1 = make_float2(ar + c1r, ai + c1i);
-    tot = make_float2(ar + br, ai + bi);
+    p16 = A;
+    c0 = C0;
+    c1 = make_float2(A.x + C1.x, A.y + C1.y);
+    tot = make_float2(A.x + B.x, A.y + B.y);
 }
 
 #ifdef L1RXG_SEG_CHAINS4

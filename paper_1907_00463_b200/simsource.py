@@ -34,6 +34,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .tracking import llround
+
 CHIP_RATE = 1.023e6
 F_L1 = 1.57542e9
 NOISE_SIGMA = 0.25
@@ -94,7 +96,7 @@ def synth(n_ms: int, fs: float, svs, *, fmt: str = "int16_iq", if_hz: float = 0.
     the same chunk boundaries are used; the noise stream is seeded per
     chunk from (seed, chunk index))."""
     import torch
-    n = int(round(fs / 1000.0))
+    n = llround(fs / 1000.0)
     if abs(fs / 1000.0 - n) > 1e-9:
         raise ValueError("simulator requires an integer number of samples per ms")
     dev = torch.device(device)
@@ -176,7 +178,7 @@ def synth_gpu(ctx, n_ms: int, fs: float, recordings, *, fmt: str = "int16_iq", i
     fmts = {"int8_iq": (abi.FMT_INT8_IQ, 2), "int16_iq": (abi.FMT_INT16_IQ, 4),
             "int8_real_if": (abi.FMT_INT8_REAL_IF, 1)}
     f, bps = fmts[fmt]
-    n = int(round(fs / 1000.0))
+    n = llround(fs / 1000.0)
     n_rec = len(recordings)
     n_sv = len(recordings[0]) if n_rec else 0
     arr = (abi.SimSv * max(1, n_rec * n_sv))()

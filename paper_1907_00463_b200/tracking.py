@@ -40,6 +40,13 @@ KERNEL_SCALAR, KERNEL_BATCHED, KERNEL_NOOP = abi.KERNEL_SCALAR, abi.KERNEL_BATCH
 _dp = C.POINTER(C.c_double)
 
 
+def llround(x: float) -> int:
+    """std::llround: halves round away from zero (Python's round() rounds
+    them to even; tracking.hpp:634 and pipeline.hpp:330 use llround)."""
+    import math
+    return int(math.copysign(math.floor(abs(x) + 0.5), x))
+
+
 @dataclass
 class CaCode:
     """CaCode (cacode.hpp:15-18)."""
@@ -225,7 +232,7 @@ class Tracker:
         self.ctx = ctx
         self._lib = ctx._lib
         self.fmt, self.fs, self.if_hz = fmt, fs, if_hz
-        self.n = int(round(fs / 1000.0))
+        self.n = llround(fs / 1000.0)
         self.taps = taps or abi.Taps.epl(0.5)
         self.cfg = cfg or abi.TrackingCfg.default()
         chans = list(channels)
@@ -284,6 +291,11 @@ class Tracker:
         ingest pass (l1rxg_tracker_attach_device)."""
         check(self._lib.l1rxg_tracker_attach_device(self.handle, C.c_void_p(dev_ptr),
                                                     C.c_int64(samples_per_stream), C.c_int64(stride_bytes)))
+
+    def detach(self) -> None:
+        """Ends an attachment: the tracker reads its own ring again and its
+        streams restart empty (l1rxg_tracker_detach)."""
+        check(self._lib.l1rxg_tracker_detach(self.handle))
 
     def push_device_strided(self, dev_ptr: int, nbytes_per_stream: int, stride_bytes: int) -> None:
         """Same-length chunk for every stream in one launch (batched recordings)."""
@@ -371,7 +383,7 @@ def init_channel_from_acquisition(prn: int, doppler_hz: float, acq_buffer_start:
     ch.code_freq_hz = 1.023e6 * (1.0 + doppler_hz / 1.57542e9) + 0.0
     ch.pll_integrator = 2.0 * 3.14159265358979323846 * doppler_hz
     ch.fll_enabled = 1
-    spm = int(round(sample_rate_hz / 1000.0))
+    spm = llround(sample_rate_hz / 1000.0)
     boundary = acq_buffer_start + code_delay_samples
     start = boundary
     if start < start_offset_samples:

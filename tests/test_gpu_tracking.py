@@ -615,3 +615,38 @@ def test_segment_max_epochs_and_noop(ctx, oracle_mod):
     assert len(r) == 4 and np.all(r["ip"] == 0.0)
     for k in range(1, 4):
         assert abs((r[k]["chi_chips"] - r[k - 1]["chi_chips"]) - r[k - 1]["code_freq_hz"] / 1000.0) < 1e-9
+
+
+def test_attach_refuses_pushes_and_detach_restores_ring(ctx):
+    """Attached recordings are the rings: every push entry point is refused
+    while they are attached (the kernel reads the attachment, so a push would
+    silently advance availability past it), reset keeps the attachment with
+    every sample available, and detach hands the tracker its own ring back."""
+    import torch
+    fs, ms, n = 65.472e6, 6, 65472
+    svs = [[ss.Sv(prn=5, cn0_dbhz=46.0, doppler_hz=900.0, delay_chips=40.5)]]
+    dev = ss.synth_gpu(ctx, ms, fs, svs, seed=33)
+    inits = [_init(sv, fs) for sv in svs[0]]
+    taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+    t = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, taps=taps, ring_samples=(ms + 4) * n,
+                max_records=ms, cta_mode=abi.CTA_SEGMENT)
+    t.attach_device(dev.data_ptr(), dev.shape[1] // 4, dev.shape[1])
+    host = dev.cpu().numpy()
+    with pytest.raises(ValueError, match="attached"):
+        t.push(0, host[0, : 4 * n])
+    with pytest.raises(ValueError, match="attached"):
+        t.push_device(0, dev.data_ptr(), 4 * n)
+    with pytest.raises(ValueError, match="attached"):
+        t.push_strided(host[:, : 4 * n])
+    with pytest.raises(ValueError, match="attached"):
+        t.push_device_strided(dev.data_ptr(), 4 * n, dev.shape[1])
+    t.run()
+    first = t.records(0)
+    t.reset(inits)  # the attachment stays: same records again
+    t.run()
+    assert t.records(0).tobytes() == first.tobytes()
+    t.detach()
+    t.reset(inits)
+    t.push(0, host[0])  # now into the ring: the same samples, the same records
+    t.run()
+    assert t.records(0).tobytes() == first.tobytes()

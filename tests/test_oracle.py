@@ -255,7 +255,8 @@ def test_init_channel_equals_reference(orc):
     from paper_1907_00463_b200.tracking import init_channel_from_acquisition
     rng = np.random.default_rng(4)
     for _ in range(50):
-        fs = float(rng.choice([2.048e6, 5e6, 16.368e6, 65.472e6]))
+        # 2.0465 MHz: samples per ms 2046.5 -- llround rounds the half away from zero
+        fs = float(rng.choice([2.048e6, 2.0465e6, 5e6, 16.368e6, 65.472e6]))
         args = (int(rng.integers(1, 33)), rng.uniform(-5000, 5000), int(rng.integers(0, 10**6)),
                 int(rng.integers(0, 70000)), int(rng.integers(0, 2 * 10**6)), fs)
         a = orc.init_channel(*args, which="ref")
