@@ -325,9 +325,9 @@ def run_grid(args, rank, world, local, dist):
     from paper_1907_00463_b200.tracking import pick_peak
     det = []
     for p in prns_sv:
-        pb, pd, ratio = pick_peak(plane[int(p) - 1], bins, fs)
-        det.append({"prn": int(p), "bin_hz": float(bins[pb]), "delay_chips": pd * 0.5,
-                    "ratio": round(float(ratio), 2)})
+        r = pick_peak(plane[int(p) - 1], bins, fs, prn=int(p))
+        det.append({"prn": int(p), "bin_hz": r.doppler_hz, "delay_chips": r.code_delay_chips,
+                    "ratio": round(float(r.ratio), 2)})
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
     fp32_path = os.environ.get("L1RXG_GRID_FP32", "0") not in ("", "0")

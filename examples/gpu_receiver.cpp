@@ -12,8 +12,9 @@
 //
 // Prints one JSON object per detected channel and a summary object.
 // Reference behaviour mirrored: acquisition.hpp:114-149 (pick_peak: peak
-// cell, runner-up outside +-1 chip, threshold ratio 2.0), tracking.hpp:622-650
-// (init_channel_from_acquisition), pipeline.hpp:388-428 (block reader +
+// cell, runner-up outside +-1 chip, threshold ratio 2.0) and
+// tracking.hpp:622-650 (init_channel_from_acquisition) through the library's
+// l1rxg_pick_peak / l1rxg_init_channel, pipeline.hpp:388-428 (block reader +
 // paced mode with overflow counting).
 #include <chrono>
 #include <cmath>
@@ -40,65 +41,6 @@ void die(const char* what) {
     } while (0)
 
 constexpr double kChipRate = 1.023e6;
-constexpr double kFL1 = 1.57542e9;
-constexpr double kPi = 3.14159265358979323846;
-
-struct Detection {
-    int prn;
-    double ratio, doppler_hz;
-    int code_delay_samples;
-};
-
-// acquisition.hpp:114-149 on the half-chip delay grid (d = k * spc samples)
-Detection pick_peak(const double* plane, int n_bins, int n_delays, const std::vector<double>& bins,
-                    int prn, int spc, double fs) {
-    int best = 0;
-    for (int i = 1; i < n_bins * n_delays; ++i)
-        if (plane[i] > plane[best])
-            best = i;
-    const int pd = best % n_delays, pb = best / n_delays;
-    const int chip_samples = static_cast<int>(std::ceil(fs / kChipRate));
-    double runner = 0;
-    for (int b = 0; b < n_bins; ++b)
-        for (int d = 0; d < n_delays; ++d) {
-            int dist = std::abs(d - pd) * spc;
-            dist = std::min(dist, n_delays * spc - dist);
-            if (dist <= chip_samples)
-                continue;
-            runner = std::max(runner, plane[b * n_delays + d]);
-        }
-    Detection r;
-    r.prn = prn;
-    r.ratio = runner > 0 ? plane[best] / runner : INFINITY;
-    r.doppler_hz = bins[pb];
-    r.code_delay_samples = pd * spc;
-    return r;
-}
-
-// tracking.hpp:622-650
-l1rxg_channel init_channel(int prn, double doppler, int64_t acq_start, int64_t code_delay,
-                           int64_t start_offset, double fs) {
-    l1rxg_channel ch;
-    std::memset(&ch, 0, sizeof ch);
-    ch.prn = prn;
-    ch.state = L1RXG_ACQUIRED;
-    ch.carrier_doppler_hz = doppler;
-    ch.code_freq_hz = kChipRate * (1.0 + doppler / kFL1) + 0.0;
-    ch.pll_integrator = 2.0 * kPi * doppler;
-    ch.fll_enabled = 1;
-    const int64_t spm = std::llround(fs / 1000.0);
-    const int64_t boundary = acq_start + code_delay;
-    int64_t start = boundary;
-    if (start < start_offset) {
-        const int64_t gap = start_offset - boundary;
-        start = boundary + ((gap + spm - 1) / spm) * spm;
-    }
-    ch.sample_offset_next_epoch = start;
-    const double cps = ch.code_freq_hz / fs;
-    ch.code_phase_chips = std::fmod(static_cast<double>(start - boundary) * cps, 1023.0);
-    ch.chi_chips = ch.code_phase_chips;
-    return ch;
-}
 
 }  // namespace
 
@@ -164,10 +106,18 @@ int main(int argc, char** argv) {
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     std::vector<l1rxg_channel> chans;
     for (int p = 0; p < 32; ++p) {
-        const Detection d = pick_peak(plane.data() + static_cast<size_t>(p) * bins.size() * n_delays,
-                                      static_cast<int>(bins.size()), n_delays, bins, p + 1, spc, fs);
-        if (d.ratio >= 2.0)  // AcqConfig::threshold_ratio (acquisition.hpp:23)
-            chans.push_back(init_channel(d.prn, d.doppler_hz, 0, d.code_delay_samples, 0, fs));
+        // the reference's peak rule and hand-off, from the library (one
+        // implementation, pinned to acquisition.hpp:114-149 and
+        // tracking.hpp:622-650 by tests/test_acquisition_ref.py, test_oracle.py)
+        l1rxg_acq_result d;
+        OK(l1rxg_pick_peak(plane.data() + static_cast<size_t>(p) * bins.size() * n_delays,
+                           static_cast<int>(bins.size()), n_delays, bins.data(), spc, p + 1, fs,
+                           2.0 /* AcqConfig::threshold_ratio, acquisition.hpp:23 */, &d));
+        if (d.detected) {
+            l1rxg_channel ch;
+            OK(l1rxg_init_channel(d.prn, d.doppler_hz, 0, d.code_delay_samples, 0, fs, &ch));
+            chans.push_back(ch);
+        }
     }
     if (chans.empty()) {
         std::printf("{\"summary\": {\"detected\": 0}}\n");

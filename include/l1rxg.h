@@ -353,6 +353,32 @@ int l1rxg_search_grid(l1rxg_ctx* ctx, int format, const void* bytes,
 int l1rxg_search_grid_timing(l1rxg_ctx* ctx, double* ingest_fold_ms,
                              double* corr_ms);
 
+/* ---- acquisition hand-off (host functions, no GPU needed) -------------- */
+/* AcquisitionResult (acquisition.hpp:52-59). */
+typedef struct {
+    int32_t prn;
+    int32_t detected;
+    double ratio;
+    double doppler_hz;
+    int32_t code_delay_samples;
+    int32_t pad_;
+    double code_delay_chips;
+} l1rxg_acq_result;
+
+/* detail::pick_peak (acquisition.hpp:114-149) over one PRN's plane
+ * cells[bin][k] whose delays are d = k * delay_step samples (delay_step 1:
+ * the reference's full plane; the search grid's half-chip plane: delay_step
+ * = samples per half chip): peak cell; runner-up over every bin outside
+ * +-ceil(fs / chip rate) samples of the peak delay, with circular distance
+ * on the n_delays * delay_step sample axis; detected = ratio >= threshold. */
+int l1rxg_pick_peak(const double* cells, int n_bins, int n_delays, const double* bins,
+                    int delay_step, int prn, double sample_rate_hz,
+                    double threshold_ratio, l1rxg_acq_result* out);
+/* init_channel_from_acquisition (tracking.hpp:622-650). */
+int l1rxg_init_channel(int prn, double doppler_hz, int64_t acq_buffer_start,
+                       int64_t code_delay_samples, int64_t start_offset_samples,
+                       double sample_rate_hz, l1rxg_channel* out);
+
 /* ---- scenario synthesizer (test and benchmark corpora) ----------------- */
 /* SimSatellite in raw mode (simsource.hpp:24-40). */
 typedef struct {

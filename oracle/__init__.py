@@ -5,7 +5,10 @@ Two libraries, both loaded with ctypes:
 * ``port``  -- oracle/lib/libl1rx_oracle.so, the plain-C restatement of the
   reference's tracking path (oracle/l1rx_oracle.c);
 * ``ref``   -- oracle/_ref/libl1rx_ref.so, the UNMODIFIED reference headers
-  (/root/reference/proj/include) compiled in place behind ref_shim.cpp.
+  (/root/reference/proj/include) compiled in place behind ref_shim.cpp;
+* ``acq``   -- oracle/_ref/libl1rx_acq_ref.so, the unmodified reference
+  acquisition (acquisition.hpp, fft.hpp) behind acq_shim.cpp with FFTW's
+  API served by cuFFTW (executing a transform needs a GPU).
   Built only where /root/reference exists; the prebuilt .so travels to the
   GPU box with the gpurun snapshot.
 
@@ -39,8 +42,8 @@ def build(force: bool = False) -> None:
     targets = ["lib/libl1rx_oracle.so"]
     if os.path.isdir(REF_INC):
         targets.append("ref")
-    if force or not os.path.exists(PORT_SO) or (
-            os.path.isdir(REF_INC) and not os.path.exists(os.path.join(REF_DIR, "libl1rx_ref.so"))):
+    if force or not os.path.exists(PORT_SO) or (os.path.isdir(REF_INC) and not all(
+            os.path.exists(os.path.join(REF_DIR, f)) for f in ("libl1rx_ref.so", "libl1rx_acq_ref.so"))):
         subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
@@ -153,6 +156,74 @@ def ref():
          P(Channel), P(TrackingCfg), C.c_int, C.c_int, C.c_int64, _dp, _dp, P(C.c_int64),
          P(Channel))
     return lib
+
+
+def acq_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "libl1rx_acq_ref.so"))
+
+
+@lru_cache(maxsize=None)
+def acq():
+    from paper_1907_00463_b200.abi import AcqResult
+    path = os.path.join(REF_DIR, "libl1rx_acq_ref.so")
+    if not os.path.exists(path):
+        raise FileNotFoundError("reference acquisition not built: " + path)
+    lib = C.CDLL(path)
+    P = C.POINTER
+    _sig(lib, "acq_last_error", C.c_char_p)
+    _sig(lib, "acq_doppler_bins", C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, _dp, C.c_int)
+    for f in ("acq_acquire_pcs", "acq_acquire_fast"):
+        _sig(lib, f, C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+             C.c_int, C.c_double, P(AcqResult))
+    _sig(lib, "acq_pcs_plane", C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, C.c_int, _dp)
+    _sig(lib, "acq_pick_peak", C.c_int, _dp, C.c_int, C.c_int, _dp, C.c_int, C.c_double, C.c_double,
+         P(AcqResult))
+    return lib
+
+
+def ref_doppler_bins(dmin: float, dmax: float, step: float = 0.0, integration_ms: int = 4) -> np.ndarray:
+    """doppler_bins (acquisition.hpp:38-50)."""
+    out = np.zeros(4096)
+    n = acq().acq_doppler_bins(dmin, dmax, step, integration_ms, dptr(out), out.size)
+    if n < 0:
+        _raise(-n, acq().acq_last_error())
+    return out[:n].copy()
+
+
+def ref_acquire_pcs(iq: np.ndarray, prn: int, fs: float, dmin: float, dmax: float, step: float,
+                    integration_ms: int, threshold: float = 2.0, fast: bool = False):
+    """acquire_pcs / acquire_fast (acquisition.hpp:189-262): AcqResult."""
+    from paper_1907_00463_b200.abi import AcqResult
+    iq = np.ascontiguousarray(iq, np.complex128)
+    out = AcqResult()
+    fn = acq().acq_acquire_fast if fast else acq().acq_acquire_pcs
+    rc = fn(dptr(iq.view(np.float64)), iq.size, prn, fs, dmin, dmax, step, integration_ms, threshold,
+            C.byref(out))
+    _raise(rc, acq().acq_last_error())
+    return out
+
+
+def ref_pcs_plane(iq: np.ndarray, n_seg: int, prn: int, fs: float, bins) -> np.ndarray:
+    """The acquire_pcs plane cells[bin][sample delay] (acquisition.hpp:196-219)."""
+    iq = np.ascontiguousarray(iq, np.complex128)
+    b = np.ascontiguousarray(bins, np.float64)
+    N = int(round(fs / 1000))
+    cells = np.zeros((b.size, N))
+    rc = acq().acq_pcs_plane(dptr(iq.view(np.float64)), n_seg, prn, fs, dptr(b), b.size, dptr(cells))
+    _raise(rc, acq().acq_last_error())
+    return cells
+
+
+def ref_pick_peak(cells: np.ndarray, bins, prn: int, fs: float, threshold: float = 2.0):
+    """detail::pick_peak (acquisition.hpp:114-149) over a caller plane."""
+    from paper_1907_00463_b200.abi import AcqResult
+    cells = np.ascontiguousarray(cells, np.float64)
+    b = np.ascontiguousarray(bins, np.float64)
+    out = AcqResult()
+    rc = acq().acq_pick_peak(dptr(cells.reshape(-1)), cells.shape[0], cells.shape[1], dptr(b), prn, fs,
+                             threshold, C.byref(out))
+    _raise(rc, acq().acq_last_error())
+    return out
 
 
 # ---- numpy conveniences -------------------------------------------------

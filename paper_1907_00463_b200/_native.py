@@ -26,6 +26,7 @@ EXPORTS = [
     "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_reset",
     "l1rxg_tracker_stream", "l1rxg_tracker_read_samples",
     "l1rxg_tracker_timing", "l1rxg_search_grid", "l1rxg_search_grid_timing", "l1rxg_simulate",
+    "l1rxg_pick_peak", "l1rxg_init_channel",
 ]
 
 
@@ -83,6 +84,9 @@ def lib():
     _sig(L, "l1rxg_search_grid", C.c_int, vp, C.c_int, vp, C.c_int, i64, C.c_double, C.c_double,
          C.c_int, P(C.c_int32), C.c_int, dp, C.c_int, C.c_int, C.c_int, dp)
     _sig(L, "l1rxg_search_grid_timing", C.c_int, vp, dp, dp)
+    _sig(L, "l1rxg_pick_peak", C.c_int, dp, C.c_int, C.c_int, dp, C.c_int, C.c_int, C.c_double, C.c_double,
+         P(abi.AcqResult))
+    _sig(L, "l1rxg_init_channel", C.c_int, C.c_int, C.c_double, i64, i64, i64, C.c_double, P(abi.Channel))
     _sig(L, "l1rxg_simulate", C.c_int, vp, vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, i64,
          C.c_int, C.c_uint64, C.c_int, vp, i64)
     if L.l1rxg_abi_version() != abi.ABI_VERSION:

@@ -168,6 +168,13 @@ class SimSv(C.Structure):
                 ("cn0_dbhz", C.c_double), ("prn", C.c_int32), ("pad_", C.c_int32)]
 
 
+class AcqResult(C.Structure):
+    """l1rxg_acq_result: AcquisitionResult (acquisition.hpp:52-59)."""
+    _fields_ = [("prn", C.c_int32), ("detected", C.c_int32), ("ratio", C.c_double),
+                ("doppler_hz", C.c_double), ("code_delay_samples", C.c_int32), ("pad_", C.c_int32),
+                ("code_delay_chips", C.c_double)]
+
+
 RECORD_DTYPE_FIELDS = [f[0] for f in EpochRecord._fields_]
 
 

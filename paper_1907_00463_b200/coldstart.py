@@ -40,12 +40,10 @@ def acquire(ctx, raw, fmt: int, fs: float, if_hz: float, n_blocks: int, prns, bi
     plane = search_grid(ctx, raw, fmt, fs, if_hz, n_blocks, prns, bins, device_ptr=device_ptr)
     out = []
     for i, p in enumerate(np.asarray(prns, dtype=int)):
-        pb, pd, ratio = pick_peak(plane[i], bins, fs)
-        delay = int(pd * spc)
-        out.append(AcquisitionResult(prn=int(p), detected=bool(ratio >= threshold_ratio),
-                                     ratio=float(ratio), doppler_hz=float(bins[pb]),
-                                     code_delay_samples=delay,
-                                     code_delay_chips=delay * CHIP_RATE_HZ / fs))
+        r = pick_peak(plane[i], bins, fs, delay_step=spc, prn=int(p), threshold_ratio=threshold_ratio)
+        out.append(AcquisitionResult(prn=int(p), detected=bool(r.detected), ratio=float(r.ratio),
+                                     doppler_hz=float(r.doppler_hz), code_delay_samples=int(r.code_delay_samples),
+                                     code_delay_chips=float(r.code_delay_chips)))
     return out, plane
 
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -946,6 +947,11 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
                     if (!(ctas <= nsm ? per >= 32 * RUN
                                       : per >= 1024 && per <= 4096 && ctas <= 2 * nsm))
                         break;
+                    // 16-CTA clusters only up to 96 CTAs (measured, 16.368 MHz
+                    // real IF: 4 and 6 channels +3 % over K = 8, 8 and 9
+                    // channels -1.5 %; profiles/r2b,r2c_cluster_ab.txt)
+                    if (2 * K > 8 && d->n_channels * 2 * K > 96)
+                        break;
                     K *= 2;
                 }
             }
@@ -1747,6 +1753,69 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
     for (int64_t r = 0; r < static_cast<int64_t>(n_bins) * n_prns; ++r)
         for (int k = 0; k < n_delays; ++k)
             plane_out[r * n_delays + k] = pl[static_cast<size_t>(r * 2 * GRID_CHIPS + k)];
+    return 0;
+}
+
+int l1rxg_pick_peak(const double* cells, int n_bins, int n_delays, const double* bins, int delay_step, int prn,
+                    double fs, double threshold_ratio, l1rxg_acq_result* out) {
+    if (!cells || !bins || !out || n_bins < 1 || n_delays < 1 || delay_step < 1 || !(fs > 0))
+        return set_err(L1RXG_EINVAL, "bad pick_peak arguments");
+    const int64_t cells_n = static_cast<int64_t>(n_bins) * n_delays;
+    int64_t best = 0;  // first maximum in row-major order, as the reference's strict '>'
+    for (int64_t i = 1; i < cells_n; ++i)
+        if (cells[i] > cells[best])
+            best = i;
+    const int64_t pk = best % n_delays, pb = best / n_delays;
+    // distances on the sample axis (n_delays * delay_step samples, circular)
+    const int64_t n = static_cast<int64_t>(n_delays) * delay_step;
+    const int64_t chip_samples = static_cast<int64_t>(std::ceil(fs / CHIP_RATE_HZ));
+    double runner = 0;
+    for (int64_t b = 0; b < n_bins; ++b)
+        for (int64_t k = 0; k < n_delays; ++k) {
+            int64_t dist = (k > pk ? k - pk : pk - k) * delay_step;
+            dist = std::min(dist, n - dist);
+            if (dist <= chip_samples)
+                continue;
+            runner = std::max(runner, cells[b * n_delays + k]);
+        }
+    out->prn = prn;
+    out->ratio = runner > 0 ? cells[best] / runner : std::numeric_limits<double>::infinity();
+    out->detected = out->ratio >= threshold_ratio ? 1 : 0;
+    out->doppler_hz = bins[pb];
+    out->code_delay_samples = static_cast<int32_t>(pk * delay_step);
+    out->pad_ = 0;
+    out->code_delay_chips = static_cast<double>(pk * delay_step) * CHIP_RATE_HZ / fs;
+    return 0;
+}
+
+int l1rxg_init_channel(int prn, double doppler_hz, int64_t acq_buffer_start, int64_t code_delay_samples,
+                       int64_t start_offset_samples, double fs, l1rxg_channel* out) {
+    if (!out)
+        return set_err(L1RXG_EINVAL, "null out");
+    if (prn < 1 || prn > 32)
+        return set_err(L1RXG_ERANGE, "PRN must be in 1..32");
+    if (!(fs > 0))
+        return set_err(L1RXG_EINVAL, "sample_rate_hz must be positive");
+    l1rxg_channel ch;
+    std::memset(&ch, 0, sizeof ch);  // ChannelState{} (tracking.hpp:626)
+    ch.prn = prn;
+    ch.state = L1RXG_ACQUIRED;
+    ch.carrier_doppler_hz = doppler_hz;
+    ch.code_freq_hz = CHIP_RATE_HZ * (1.0 + doppler_hz / F_L1_HZ) + 0.0;  // carrier_aided_code_freq(f, 0)
+    ch.pll_integrator = 2.0 * PI_D * doppler_hz;
+    ch.fll_enabled = 1;
+    const int64_t spm = std::llround(fs / 1000.0);
+    const int64_t boundary = acq_buffer_start + code_delay_samples;
+    int64_t start = boundary;
+    if (start < start_offset_samples) {  // the first code boundary at or after the start offset
+        const int64_t gap = start_offset_samples - boundary;
+        start = boundary + ((gap + spm - 1) / spm) * spm;
+    }
+    ch.sample_offset_next_epoch = start;
+    const double cps = ch.code_freq_hz / fs;
+    ch.code_phase_chips = std::fmod(static_cast<double>(start - boundary) * cps, 1023.0);
+    ch.chi_chips = ch.code_phase_chips;
+    *out = ch;
     return 0;
 }
 

@@ -266,8 +266,11 @@ __device__ __forceinline__ void seg_run4(const unsigned char* buf, int lane, con
                                          float2& tot) {
     const unsigned char* rowp = buf + lane * 128;
     const int sw = lane & 7;
-    float pr[4] = {0.f, 0.f, 0.f, 0.f}, pi[4] = {0.f, 0.f, 0.f, 0.f};
-    float car = 0.f, cai = 0.f, cbr = 0.f, cbi = 0.f, ccr = 0.f, cci = 0.f, cdr = 0.f, cdi = 0.f;
+    float2 P[4];
+#pragma unroll
+    for (int Q = 0; Q < 4; ++Q)
+        P[Q] = make_float2(0.f, 0.f);
+    float2 CA = P[0], CB = P[0], CC = P[0], CD = P[0];
     const int q1r = q1 - 16;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // chunk h of each quarter: samples 8Q + 4h + u
@@ -282,10 +285,10 @@ __device__ __forceinline__ void seg_run4(const unsigned char* buf, int lane, con
             const float rc[4] = {r01.x, r01.z, r23.x, r23.z};
             const float rs[4] = {r01.y, r01.w, r23.y, r23.w};
             // captures before adding step t: A at q0, B at q0 - 8, C at q1 - 16, D at q1 - 24
-            if (t > 0 && t == q0) { car = pr[0]; cai = pi[0]; }
-            if (t == q0 - 8) { cbr = pr[1]; cbi = pi[1]; }
-            if (t > 0 && t == q1r) { ccr = pr[2]; cci = pi[2]; }
-            if (t == q1r - 8) { cdr = pr[3]; cdi = pi[3]; }
+            if (t > 0 && t == q0) CA = P[0];
+            if (t == q0 - 8) CB = P[1];
+            if (t > 0 && t == q1r) CC = P[2];
+            if (t == q1r - 8) CD = P[3];
 #pragma unroll
             for (int Q = 0; Q < 4; ++Q) {
                 const uint32_t wv[4] = {wq[Q].x, wq[Q].y, wq[Q].z, wq[Q].w};
@@ -293,19 +296,17 @@ __device__ __forceinline__ void seg_run4(const unsigned char* buf, int lane, con
                 const int j = 8 * Q + t;
                 if (MASK)
                     x = (j >= jlo && j < jhi) ? x : 0u;
-                const float xr = seg_re(x), xi = seg_im(x);
-                pr[Q] = fmaf(xi, rs[Q], fmaf(xr, rc[Q], pr[Q]));
-                pi[Q] = fmaf(-xr, rs[Q], fmaf(xi, rc[Q], pi[Q]));
+                P[Q] = seg_mac(P[Q], seg_re(x), seg_im(x), rc[Q], rs[Q]);
             }
         }
     }
-    const float a8r = pr[0], a8i = pi[0];
-    const float h16r = a8r + pr[1], h16i = a8i + pi[1];
-    const float c24r = h16r + pr[2], c24i = h16i + pi[2];
-    p16 = make_float2(h16r, h16i);
-    c0 = q0 < 8 ? make_float2(car, cai) : make_float2(a8r + cbr, a8i + cbi);
-    c1 = q1r < 8 ? make_float2(h16r + ccr, h16i + cci) : make_float2(c24r + cdr, c24i + cdi);
-    tot = make_float2(c24r + pr[3], c24i + pi[3]);
+    const float2 a8 = P[0];
+    const float2 h16 = make_float2(a8.x + P[1].x, a8.y + P[1].y);
+    const float2 c24 = make_float2(h16.x + P[2].x, h16.y + P[2].y);
+    p16 = h16;
+    c0 = q0 < 8 ? CA : make_float2(a8.x + CB.x, a8.y + CB.y);
+    c1 = q1r < 8 ? make_float2(h16.x + CC.x, h16.y + CC.y) : make_float2(c24.x + CD.x, c24.y + CD.y);
+    tot = make_float2(c24.x + P[3].x, c24.y + P[3].y);
 }
 #endif
 
@@ -387,6 +388,8 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         g0k = seg_trans_count(s, tap_index(0, c.cps, c.base, dk));  // transitions in (idx(0), idx(n-1)]
         cntk = seg_trans_count(s, tap_index(n - 1, c.cps, c.base, dk)) - g0k;
     }
+    const float inv_L = 1.f / (float)L;  // p = g / L exactly for g < 2^13 (the +0.5 keeps off integers)
+#ifdef L1RXG_SEG_FILL_FLAT  // experiment switch: one flattened loop decoding (tap, transition)
     int g0[T], pre[T + 1];
     pre[0] = 0;
 #pragma unroll
@@ -394,7 +397,6 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         g0[k] = __shfl_sync(0xffffffffu, g0k, k);
         pre[k + 1] = pre[k] + __shfl_sync(0xffffffffu, cntk, k);
     }
-    const float inv_L = 1.f / (float)L;  // p = g / L exactly for g < 2^13 (the +0.5 keeps off integers)
     for (int f = tid; f < pre[T]; f += nthr) {
         int k = 0, g = 0;
 #pragma unroll
@@ -410,10 +412,38 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         const double dist = fabs(e - rint(e));
         const bool tie = !(dist > 1e-9);
         const int b = tie ? tap_boundary(m, dk, c, 1, n - 1) : __double2loint(__dadd_ru(e, 6755399441055744.0));
-        // checked within 1e-7 of a tie: steps of one residue differ in e by
-        // ~1e-11, so a step near a tie and its partner are both checked
         seg_enter<T>(tab, b + lead, k, !(dist > 1e-7) || !fast_geom);
     }
+#else
+    // one loop per tap (k a compile-time constant inside: no (tap,
+    // transition) decode, constant entry shifts), started where the
+    // flattened order would put it (thread (pre_k + i) mod nthr takes
+    // transition i of tap k) so every thread keeps the same share
+    int pre = 0;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const int g0 = __shfl_sync(0xffffffffu, g0k, k);
+        const int cnt = __shfl_sync(0xffffffffu, cntk, k);
+        const double dk = s->d[k];
+        const double off = -dk - c.base;
+        int i = tid - pre % nthr;
+        if (i < 0)
+            i += nthr;
+        pre += cnt;
+        for (; i < cnt; i += nthr) {
+            const int g = g0 + i;
+            const int p = (int)(((float)g + 0.5f) * inv_L);
+            const int m = p * 1023 + s->tm[g - p * L];
+            const double e = ((double)m + off) * c.inv_cps;
+            const double dist = fabs(e - rint(e));
+            const bool tie = !(dist > 1e-9);
+            const int b = tie ? tap_boundary(m, dk, c, 1, n - 1) : __double2loint(__dadd_ru(e, 6755399441055744.0));
+            // checked within 1e-7 of a tie: steps of one residue differ in e by
+            // ~1e-11, so a step near a tie and its partner are both checked
+            seg_enter<T>(tab, b + lead, k, !(dist > 1e-7) || !fast_geom);
+        }
+    }
+#endif
 }
 
 template <int T>

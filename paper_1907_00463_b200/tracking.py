@@ -172,19 +172,21 @@ def search_grid_timing(ctx: "Context"):
     return a.value, b.value
 
 
-def pick_peak(plane_row: np.ndarray, bins, fs: float):
+def pick_peak(plane_row: np.ndarray, bins, fs: float, delay_step: int | None = None,
+              prn: int = 0, threshold_ratio: float = 2.0) -> abi.AcqResult:
     """detail::pick_peak (acquisition.hpp:114-149) over one PRN's plane
-    [bin][delay] on the half-chip delay grid: (bin, delay index, ratio) with
-    the runner-up taken outside +-1 chip of the peak's code phase."""
-    nb, nd = plane_row.shape
-    best = int(np.argmax(plane_row))
-    pb, pd = divmod(best, nd)
-    d = np.arange(nd)
-    dist = np.minimum(np.abs(d - pd), nd - np.abs(d - pd))
-    mask = dist > 2  # half-chip grid: +-1 chip = 2 delay steps
-    runner = plane_row[:, mask].max() if mask.any() else 0.0
-    ratio = plane_row[pb, pd] / runner if runner > 0 else float("inf")
-    return pb, pd, ratio
+    [bin][k] with delays d = k * delay_step samples (default: the search
+    grid's half-chip step), by the library's l1rxg_pick_peak: the peak cell
+    and the runner-up over every bin outside +-ceil(fs / chip rate) samples
+    of the peak delay.  Returns AcquisitionResult (acquisition.hpp:52-59)."""
+    cells = np.ascontiguousarray(plane_row, np.float64)
+    b = np.ascontiguousarray(bins, np.float64)
+    nb, nd = cells.shape
+    step = delay_step if delay_step is not None else int(round(fs / 1.023e6 / 2.0))
+    out = abi.AcqResult()
+    check(lib().l1rxg_pick_peak(cells.ctypes.data_as(_dp), nb, nd, b.ctypes.data_as(_dp), step, prn, fs,
+                                threshold_ratio, C.byref(out)))
+    return out
 
 
 def _store_nco(ch, nco: abi.Nco) -> None:
@@ -373,24 +375,9 @@ class Tracker:
 def init_channel_from_acquisition(prn: int, doppler_hz: float, acq_buffer_start: int,
                                   code_delay_samples: int, start_offset_samples: int,
                                   sample_rate_hz: float) -> abi.Channel:
-    """init_channel_from_acquisition (tracking.hpp:622-650): host-side
-    channel hand-off (once per channel; not on the hot path)."""
-    import math
+    """init_channel_from_acquisition (tracking.hpp:622-650) by the library's
+    l1rxg_init_channel: host-side channel hand-off (once per channel)."""
     ch = abi.Channel()
-    ch.prn = prn
-    ch.state = abi.ACQUIRED
-    ch.carrier_doppler_hz = doppler_hz
-    ch.code_freq_hz = 1.023e6 * (1.0 + doppler_hz / 1.57542e9) + 0.0
-    ch.pll_integrator = 2.0 * 3.14159265358979323846 * doppler_hz
-    ch.fll_enabled = 1
-    spm = llround(sample_rate_hz / 1000.0)
-    boundary = acq_buffer_start + code_delay_samples
-    start = boundary
-    if start < start_offset_samples:
-        gap = start_offset_samples - boundary
-        start = boundary + ((gap + spm - 1) // spm) * spm
-    ch.sample_offset_next_epoch = start
-    cps = ch.code_freq_hz / sample_rate_hz
-    ch.code_phase_chips = math.fmod(float(start - boundary) * cps, 1023.0)
-    ch.chi_chips = ch.code_phase_chips
+    check(lib().l1rxg_init_channel(prn, doppler_hz, acq_buffer_start, code_delay_samples,
+                                   start_offset_samples, sample_rate_hz, C.byref(ch)))
     return ch

@@ -70,11 +70,12 @@ LAYOUT_C = r"""
 #define O(T, f) printf(#T "." #f " %zu\n", offsetof(T, f));
 int main(void) {
   S(l1rxg_nco) S(l1rxg_corr) S(l1rxg_tracking_cfg) S(l1rxg_taps) S(l1rxg_channel)
-  S(l1rxg_epoch_record) S(l1rxg_tracker_desc) S(l1rxg_sim_sv)
+  S(l1rxg_epoch_record) S(l1rxg_tracker_desc) S(l1rxg_sim_sv) S(l1rxg_acq_result)
   O(l1rxg_channel, sample_offset_next_epoch) O(l1rxg_channel, win_qp) O(l1rxg_channel, mu_smoothed)
   O(l1rxg_epoch_record, ie) O(l1rxg_epoch_record, pll_prev_error) O(l1rxg_tracker_desc, cfg)
   O(l1rxg_tracker_desc, taps) O(l1rxg_taps, offsets_chips) O(l1rxg_tracking_cfg, carrier_lock_drop)
-  O(l1rxg_sim_sv, cn0_dbhz) O(l1rxg_sim_sv, prn)
+  O(l1rxg_sim_sv, cn0_dbhz) O(l1rxg_sim_sv, prn) O(l1rxg_acq_result, code_delay_samples)
+  O(l1rxg_acq_result, code_delay_chips)
   return 0;
 }
 """
@@ -89,7 +90,8 @@ def test_struct_layout_matches_header(tmp_path):
     got = dict(line.split() for line in lines if line)
     py = {"l1rxg_nco": abi.Nco, "l1rxg_corr": abi.Corr, "l1rxg_tracking_cfg": abi.TrackingCfg,
           "l1rxg_taps": abi.Taps, "l1rxg_channel": abi.Channel, "l1rxg_epoch_record": abi.EpochRecord,
-          "l1rxg_tracker_desc": abi.TrackerDesc, "l1rxg_sim_sv": abi.SimSv}
+          "l1rxg_tracker_desc": abi.TrackerDesc, "l1rxg_sim_sv": abi.SimSv,
+          "l1rxg_acq_result": abi.AcqResult}
     for k, v in got.items():
         if "." in k:
             t, f = k.split(".")

@@ -48,10 +48,10 @@ def test_grid_matches_oracle(ctx, oracle_mod, fs, fmt, ifz, grid_path):
     for i, p in enumerate(prns):
         assert np.unravel_index(np.argmax(gpu[i]), gpu[i].shape) == \
             np.unravel_index(np.argmax(want[i]), want[i].shape)
-    pb, pd, ratio = pick_peak(gpu[0], bins, fs)
+    r = pick_peak(gpu[0], bins, fs)
     # real IF: the 23-tap half-band FIR delays the stream by 11 samples
     true_delay = 200.3 + (11 * 1.023e6 / fs if fmt == abi.FMT_INT8_REAL_IF else 0.0)
-    assert bins[pb] == 1500.0 and abs(pd * 0.5 - true_delay) < 0.6 and ratio > 2.0
+    assert r.doppler_hz == 1500.0 and abs(r.code_delay_chips - true_delay) < 0.6 and r.ratio > 2.0
 
 
 def test_grid_rejects_unsupported_rates(ctx):
@@ -60,3 +60,40 @@ def test_grid_rejects_unsupported_rates(ctx):
         search_grid(ctx, raw, abi.FMT_INT8_IQ, 5e6, 0.0, 1, [1], [0.0])
     with pytest.raises(IndexError):
         search_grid(ctx, np.zeros(2046 * 4, np.int8), abi.FMT_INT16_IQ, 2.046e6, 0.0, 1, [33], [0.0])
+
+
+def test_grid_plane_and_detections_equal_reference_acquire_pcs(ctx, oracle_mod, grid_path):
+    """Config-5 shape pinned to the UNMODIFIED reference acquisition
+    (acquisition.hpp + fft.hpp over cuFFTW, oracle/acq_shim.cpp): the GPU
+    plane equals acquire_pcs's own plane (FFT circular correlation, the
+    unnormalised inverse: cells = N |corr|) on the half-chip delay grid
+    d = 8k within 1e-5 of the largest cell, and the GPU hand-off
+    (l1rxg_pick_peak on that grid) agrees with the reference's acquire_pcs
+    result: detection, Doppler bin, and code delay within half a grid step."""
+    if not oracle_mod.acq_available():
+        pytest.skip("reference acquisition shim not built")
+    fs, ifz, N, n_seg = 16.368e6, 4.092e6, 16368, 4
+    rng = np.random.default_rng(55)
+    svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(40, 46), doppler_hz=rng.uniform(-9000, 9000),
+                 delay_chips=rng.uniform(0, 1023)) for p in (6, 14, 27)]
+    raw = ss.synth(n_seg, fs, svs, fmt="int8_real_if", if_hz=ifz, seed=56, device="cuda").cpu().numpy()
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, ifz)
+    bins = oracle_mod.ref_doppler_bins(-10000, 10000, 500, n_seg)  # config 5's 41 bins
+    prns = [6, 14, 27, 2]  # three present, one absent
+    gpu = search_grid(ctx, raw, abi.FMT_INT8_REAL_IF, fs, ifz, n_seg, prns, bins)
+    for i, p in enumerate(prns):
+        sel = [int(np.argmin(np.abs(bins - b))) for b in (bins if p == 2 else [svs[i].doppler_hz])]
+        if p != 2:  # the plane at the satellite's bin and its neighbours (FFTs through cuFFTW are slow)
+            sel = sorted({max(0, min(bins.size - 1, sel[0] + o)) for o in (-1, 0, 1)})
+        else:
+            sel = [0, 20, 40]
+        ref_plane = oracle_mod.ref_pcs_plane(x, n_seg, p, fs, bins[sel])
+        want = ref_plane[:, ::8]
+        err = np.abs(gpu[i][sel] - want).max() / want.max()
+        assert err < 1e-5, (p, err)
+        want_det = oracle_mod.ref_acquire_pcs(x, p, fs, -10000, 10000, 500, n_seg)
+        got_det = pick_peak(gpu[i], bins, fs, prn=p)
+        assert bool(want_det.detected) == bool(got_det.detected) == (p != 2), (p, want_det.ratio, got_det.ratio)
+        if p != 2:
+            assert want_det.doppler_hz == got_det.doppler_hz
+            assert abs(want_det.code_delay_samples - got_det.code_delay_samples) <= 4
