@@ -247,46 +247,61 @@ GRID = dict(fs=16.368e6, if_hz=4.092e6, n_prns=32, bins=np.arange(-10000.0, 1000
 
 
 def run_grid(args, rank, world, local, dist):
-    """Config 5: the correlator-bank search grid, PRNs sharded over ranks
-    (weak: each rank searches all 32 PRNs of its own recording)."""
+    """Config 5: the correlator-bank search grid over one recording, its 32
+    PRNs sharded over the ranks (strong scaling: shard_list of PRNs 1-32),
+    every rank's plane gathered to rank 0 over NCCL inside the e2e leg."""
     import torch
     from paper_1907_00463_b200 import abi, simsource as ss
+    from paper_1907_00463_b200.shard import shard_list
     g = GRID
-    rng = np.random.default_rng(g["seed"] + rank)
+    rng = np.random.default_rng(g["seed"])
     prns_sv = rng.choice(np.arange(1, 33), 6, replace=False)
     svs = [ss.Sv(prn=int(p), cn0_dbhz=rng.uniform(25, 45), doppler_hz=rng.uniform(-9000, 9000),
                  delay_chips=rng.uniform(0, 1023)) for p in prns_sv]
     fs, N, blocks = g["fs"], 16368, g["blocks"]
-    prns = np.arange(1, 33, dtype=np.int32)
+    all_prns = np.arange(1, 33, dtype=np.int32)
+    prns = np.array(shard_list(list(all_prns), world, rank), dtype=np.int32)
     bins = g["bins"]
-    direct_st = float(len(prns)) * bins.size * 2046 * N * blocks  # direct-equivalent sample-taps
+    direct_st = float(all_prns.size) * bins.size * 2046 * N * blocks  # direct-equivalent sample-taps, all ranks
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    raw = ss.synth(blocks, fs, svs, fmt="int8_real_if", if_hz=g["if_hz"], seed=g["seed"] + rank,
-                   device=dev)
+    raw = ss.synth(blocks, fs, svs, fmt="int8_real_if", if_hz=g["if_hz"], seed=g["seed"], device=dev)
     if args.impl == "reference":
         if rank != 0:
             return
         import oracle
         x = oracle.ingest(raw.cpu().numpy(), abi.FMT_INT8_REAL_IF, fs, g["if_hz"])
-        # bounded sample: 2 PRNs x 4 bins x 1 block of the direct restatement
-        # (acquire_pcs needs FFTW, absent on the box), scaled per cell
-        walls = []
-        for step in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            for p in (int(prns_sv[0]), 7):
-                oracle.search_grid(x[:N], N, 1, p, fs, bins[18:22], 8, 2046)
-            if step >= args.warmup:
-                walls.append(time.perf_counter() - t0)
-        st = 2 * 4 * 2046 * N * 1.0
+        walls, kind = [], "port"
+        if oracle.acq_available() and torch.cuda.is_available():
+            # the reference's own acquire_pcs (acquisition.hpp:189-222; FFTW's
+            # API served by cuFFTW): 2 PRNs x 41 bins x 20 blocks per step,
+            # scaled per direct-equivalent cell
+            kind = "reference"
+            for step in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                for p in (int(prns_sv[0]), 7):
+                    oracle.ref_acquire_pcs(x, p, fs, -10000, 10000, 500, blocks)
+                if step >= args.warmup:
+                    walls.append(time.perf_counter() - t0)
+            st = 2 * bins.size * 2046 * N * blocks * 1.0
+            sample = ("2 PRNs x 41 bins x 20 blocks: the reference's acquire_pcs (FFT circular correlation, "
+                      "acquisition.hpp:189-222) with FFTW's API served by cuFFTW (FFTW3 absent)")
+        else:
+            # bounded sample of the direct restatement: 2 PRNs x 4 bins x 1 block
+            for step in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                for p in (int(prns_sv[0]), 7):
+                    oracle.search_grid(x[:N], N, 1, p, fs, bins[18:22], 8, 2046)
+                if step >= args.warmup:
+                    walls.append(time.perf_counter() - t0)
+            st = 2 * 4 * 2046 * N * 1.0
+            sample = "2 PRNs x 4 bins x 1 block, direct time-domain restatement of acquire_pcs"
         v = st / statistics.mean(walls) / 1e9
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
                           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                           "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
-                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                           "config": {"workload": g["desc"]},
-                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                                           "sample": "2 PRNs x 4 bins x 1 block, direct time-domain "
-                                                     "restatement of acquire_pcs (FFTW absent)"},
+                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
                           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
@@ -298,67 +313,90 @@ def run_grid(args, rank, world, local, dist):
                     device_ptr=raw.data_ptr())
     clocks = ClockSampler(local)
     fold_ms = corr_ms = 0.0
+    if dist:
+        dist.barrier()
     with clocks:
-        w0 = time.perf_counter()
         for _ in range(args.steps):
             plane = search_grid(ctx, nbytes, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns,
                                 bins, device_ptr=raw.data_ptr())
             a, b = search_grid_timing(ctx)
             fold_ms += a
             corr_ms += b
-        wall = (time.perf_counter() - w0) * 1e3 / args.steps
     dev_ms = (fold_ms + corr_ms) / args.steps
     t_max = dev_ms
     if dist:
         tt = torch.tensor([dev_ms], device=torch.device("cuda", local))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    # e2e: host bytes in, plane out
-    host = raw.cpu().numpy()
+
+    # e2e: host bytes in, this rank's PRN planes out, gathered to rank 0 (NCCL)
+    host = ctx.host_alloc(nbytes)
+    host[:] = raw.cpu().numpy()
+
+    def step_e2e():
+        pl = search_grid(ctx, host, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns, bins)
+        if not dist:
+            return pl
+        from paper_1907_00463_b200.shard import gather_bytes
+        t = torch.from_numpy(pl.reshape(-1).view(np.uint8)).to(torch.device("cuda", local))
+        outs = gather_bytes(t, dist, dst=0)
+        if rank != 0:
+            return None
+        return np.concatenate([o.cpu().numpy().view(np.float64) for o in outs]).reshape(
+            all_prns.size, bins.size, 2046)
+    step_e2e()
+    if dist:
+        dist.barrier()
     w0 = time.perf_counter()
     for _ in range(args.steps):
-        plane = search_grid(ctx, host, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns, bins)
+        full = step_e2e()
     e2e_ms = (time.perf_counter() - w0) * 1e3 / args.steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device=torch.device("cuda", local))
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
     if rank != 0:
+        dist.destroy_process_group()
         return
-    # detections (acquisition.hpp:114-149) for the record
+    # detections (acquisition.hpp:114-149) from the gathered full plane
     from paper_1907_00463_b200.tracking import pick_peak
     det = []
     for p in prns_sv:
-        r = pick_peak(plane[int(p) - 1], bins, fs, prn=int(p))
+        r = pick_peak(full[int(p) - 1], bins, fs, prn=int(p))
         det.append({"prn": int(p), "bin_hz": r.doppler_hz, "delay_chips": r.code_delay_chips,
-                    "ratio": round(float(r.ratio), 2)})
+                    "ratio": round(float(r.ratio), 2), "detected": bool(r.detected)})
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
     fp32_path = os.environ.get("L1RXG_GRID_FP32", "0") not in ("", "0")
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     if fp32_path:  # FP32-pipe circulant kernel: 2 FFMA x 2 flop per cell-chip
-        corr_flops = float(len(prns)) * bins.size * blocks * 2 * 1023 * 1023 * 4
+        corr_flops = float(prns.size) * bins.size * blocks * 2 * 1023 * 1023 * 4
         peak = fp32_peak_tflops(sm_mhz)
         bound, note = "fp32", ("executed algorithm: two 1023-point circulant +-1 correlations per "
                                "(PRN, bin, block) on the FP32 pipes; direct-equivalent rate in value")
     else:  # bf16x3 tensor-core GEMM: M=1024 delays, N=2*2*bins*blocks rows, K=3*1024
-        corr_flops = 2.0 * 1024 * (4 * bins.size * blocks) * 3072 * len(prns)
+        corr_flops = 2.0 * 1024 * (4 * bins.size * blocks) * 3072 * prns.size
         peak = peaks.get("bf16_tflops", 2250.0)
         bound, note = "tensor", ("executed algorithm: per PRN one bf16 GEMM (fp32 folds split into "
                                  "three bf16 terms, +-1 circulant code matrix, fp32 accumulate) via "
                                  "cuBLAS on tcgen05; peak = MEASURED_PEAKS bf16_tflops (burst); the "
                                  "corr time also holds the split, circulant-build and |.| kernels")
     achieved = corr_flops / (corr_ms / args.steps * 1e-3) / 1e12
-    line = {"metric": METRIC, "value": world * direct_st / (t_max * 1e-3) / 1e9, "unit": UNIT,
+    line = {"metric": METRIC, "value": direct_st / (t_max * 1e-3) / 1e9, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; 6 SVs)",
             "config": {"workload": g["desc"], "delay_grid": "d = 8k samples, k < 2046",
                        "value_basis": "direct-equivalent sample-taps (PRN x bin x delay x sample)",
-                       "parallelism": f"weak: {world} rank(s)"},
+                       "parallelism": f"strong: 32 PRNs over {world} rank(s) ({prns.size} on rank 0), "
+                                      f"planes gathered to rank 0 (NCCL) in the e2e leg"},
             "kernel_ms_per_step": {"ingest_fold": fold_ms / args.steps, "corr": corr_ms / args.steps},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "note": note},
-            "e2e": {"value": world * direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes),
-                    "d2h_bytes_per_step": int(plane.size * 4)},
+            "e2e": {"value": direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes) * world,
+                    "d2h_bytes_per_step": int(full.size * 8)},
             "detections": det, "gpu_launches": (3 if fp32_path else 6) * args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
     if dist:
@@ -862,7 +900,12 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     1-ms epochs (latency-bound by construction).  Weak scaling: each rank
     tracks its own seeded recording."""
     import torch
-    c, svs, chans = scenario(cfg_id, CONFIGS[cfg_id]["seed"] + rank)
+    # configs 2/3 partition their channels over the ranks (one recording,
+    # broadcast from rank 0; strong scaling); config 1 -- one sequential
+    # channel -- runs a replica per rank on its own seeded recording (weak)
+    batch = cfg_id in (2, 3) and world > 1
+    seed = CONFIGS[cfg_id]["seed"] + (0 if batch or cfg_id != 1 else rank)
+    c, svs, chans = scenario(cfg_id, seed)
     blocks = args.blocks or c["blocks"]
     fs = c["fs"]
     n = int(round(fs / 1000))
@@ -871,8 +914,11 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     cfg.lock_fail_limit = 2**31 - 1
     taps = make_taps(c["taps"])
     inits = channel_inits(chans, fs)
+    C_all = len(inits)
+    if batch and args.impl != "reference":
+        from paper_1907_00463_b200.shard import shard_list
+        inits = shard_list(inits, world, rank)  # this rank's channel batch
     C_ch, T = len(inits), taps.n_counted
-    sample_taps = float(blocks) * n * T * C_ch
 
     if args.impl == "reference":
         from paper_1907_00463_b200 import simsource as ss
@@ -928,8 +974,14 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     from paper_1907_00463_b200.tracking import Context, Tracker
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    raw = ss.synth(blocks, fs, svs, fmt=c["fmt"], if_hz=c["if_hz"], seed=c["seed"] + rank,
-                   device=str(dev))
+    if batch:  # one stream for every channel batch: synthesized on rank 0, broadcast over NCCL
+        from paper_1907_00463_b200.shard import broadcast_stream
+        nbytes_stream = blocks * n * {"int8_real_if": 1, "int16_iq": 4}[c["fmt"]]
+        raw = (ss.synth(blocks, fs, svs, fmt=c["fmt"], if_hz=c["if_hz"], seed=seed, device=str(dev))
+               if rank == 0 else torch.empty(nbytes_stream, dtype=torch.uint8, device=dev))
+        raw = broadcast_stream(raw.view(torch.uint8).reshape(-1), dist, src=0)
+    else:
+        raw = ss.synth(blocks, fs, svs, fmt=c["fmt"], if_hz=c["if_hz"], seed=seed, device=str(dev))
     torch.cuda.synchronize()
     fmt = {"int8_real_if": abi.FMT_INT8_REAL_IF, "int16_iq": abi.FMT_INT16_IQ}[c["fmt"]]
     ctx = Context(local)
@@ -974,8 +1026,14 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     ms_per_step = t_max / args.steps
     counts = trk.epoch_counts()
     assert int(counts.min()) >= blocks - 1, counts
-    sample_taps = float(counts.sum()) * n * T  # every channel-epoch actually tracked
-    value = world * sample_taps / (ms_per_step * 1e-3) / 1e9
+    sample_taps = float(counts.sum()) * n * T  # every channel-epoch actually tracked (this rank)
+    epochs_all = float(counts.sum())
+    if dist:  # every rank's channel-epochs (batches or replicas)
+        tt = torch.tensor([epochs_all], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        epochs_all = float(tt.item())
+    sample_taps_all = epochs_all * n * T
+    value = sample_taps_all / (ms_per_step * 1e-3) / 1e9
 
     # ---- e2e through the public API from pinned host memory
     pinned = ctx.host_alloc(nbytes)
@@ -1013,7 +1071,7 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = world * sample_taps / (e2e_ms * 1e-3) / 1e9
+    e2e_value = sample_taps_all / (e2e_ms * 1e-3) / 1e9
     _, _, e2e_launches = trk.timing()
 
     # ---- end-of-run gather of the records to rank 0 over NCCL
@@ -1082,15 +1140,18 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if batch else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded, paper_1907_00463_b200/simsource.py; loops start from truth)",
         "config": {"workload": c["desc"], "blocks": blocks, "channels": C_ch, "taps_counted": T,
-                   "samples_per_block": n, "parallelism": f"weak: {world} rank(s) x own recording",
+                   "samples_per_block": n,
+                   "parallelism": (f"strong: {C_all} channels in batches over {world} ranks, one stream "
+                                   f"broadcast from rank 0 (NCCL), records gathered to rank 0" if batch else
+                                   f"weak: {world} replica(s), each rank its own seeded recording"),
                    "l2": "inputs larger than L2 (raw %.0f MB + baseband ring %.2f GB per step)" % (
                        nbytes / 1e6, blocks * n * 8 / 1e9),
                    "lock_fail_limit": "INT_MAX (every channel computes every epoch)",
                    "manifest": stream_manifest(raw, c["seed"] + rank, svs, c["fmt"])},
-        "realtime_channels": world * float(counts.sum()) / (ms_per_step * 1e-3) / 1000.0,
+        "realtime_channels": epochs_all / (ms_per_step * 1e-3) / 1000.0,
         # the per-epoch critical path of a channel (track launch time / epochs),
         # the latency view SURVEY 8d asks for on the sequential configs
         "epoch_latency_us": track_launch_ms * 1e3 / max(1.0, float(counts.max())),

@@ -205,7 +205,11 @@ int l1rxg_host_free(l1rxg_ctx* ctx, void* p);
 /* correlate_epoch_scalar / _batched / _noop (tracking.hpp:226-230,
  * 288-292, 434-436): one epoch of n complex<double> samples (interleaved
  * re,im), NCO state advanced in place (tracking.hpp:275-280),
- * CorrelatorOutputs returned.  n == 0 -> L1RXG_EINVAL ("empty epoch view"). */
+ * CorrelatorOutputs returned.  n == 0 -> L1RXG_EINVAL ("empty epoch view").
+ * Re-entrant: each calling host thread gets its own CUDA stream and device
+ * buffers (created on its first call, freed by l1rxg_destroy), so the
+ * reference's ChannelPool workers (pipeline.hpp:584-588) call it
+ * concurrently, one channel each. */
 int l1rxg_correlate_epoch(l1rxg_ctx* ctx, int kernel, const double* iq,
                           int n, l1rxg_nco* state_inout, int prn,
                           double el_spacing_chips, double sample_rate_hz,

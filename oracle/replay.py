@@ -110,3 +110,25 @@ def replay_channel(oracle, init, recs, x, n, cfg, taps, fs, tap_sums=None, kerne
             if first is None:
                 first = f"epoch {k}: " + ", ".join(bad)
     return worst, n_bad, first
+
+
+def replay_sampled(oracle, trk, picks, inits, x_of, n, cfg, taps, fs, every=1, threads=None):
+    """Replays channel c's epochs k = 0, every, 2 every, ... for every c in
+    `picks` (trk: a paper_1907_00463_b200.tracking.Tracker; x_of(c): the
+    oracle's complex128 stream of channel c), in parallel over host threads.
+    Returns the worst errors, the number of replayed channel-epochs, the
+    exact-field mismatch count and the first mismatch."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    got = {c: trk.records(c, tap_sums=True) for c in picks}
+
+    def one(c):
+        recs, ts = got[c]
+        return replay_channel(oracle, inits[c], recs, x_of(c), n, cfg, taps, fs, tap_sums=ts,
+                              epochs=range(0, len(recs), every)), len(range(0, len(recs), every))
+    with ThreadPoolExecutor(max_workers=threads or os.cpu_count() or 1) as ex:
+        res = list(ex.map(one, picks))
+    worst = {k: max(r[0][0][k] for r in res) for k in ("sums", "taps", "loop", "cn0")}
+    return {"worst": worst, "checked": int(sum(r[1] for r in res)),
+            "mismatches": int(sum(r[0][1] for r in res)),
+            "first_mismatch": next((r[0][2] for r in res if r[0][2]), None)}

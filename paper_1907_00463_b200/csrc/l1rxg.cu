@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -484,11 +485,23 @@ struct DevBuf {
 
 }  // namespace
 
+// Per-thread state of the per-call path (l1rxg_correlate_epoch/_batch): its
+// own stream and device buffers, so calls from many host threads -- the
+// reference's ChannelPool workers, pipeline.hpp:584-588 -- run concurrently.
+struct CallScratch {
+    cudaStream_t s = nullptr;
+    DevBuf iq64, iq32, states, prns, sums, corr;
+    std::vector<double> hsums;
+};
+
 struct l1rxg_ctx {
     int device = 0;
+    uint64_t id = 0;  // unique per context (keys the threads' CallScratch)
     cudaStream_t compute = nullptr, copy = nullptr;
     int8_t* d_codes = nullptr;
     DevBuf iq64, iq32, states, prns, sums, corr;
+    std::mutex scratch_mu;                    // guards `scratch` (registration, destroy)
+    std::vector<CallScratch*> scratch;        // every thread's per-call state
     DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
     DevBuf gsim;  // simulator scenario
     DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
@@ -496,7 +509,7 @@ struct l1rxg_ctx {
     cublasHandle_t blas = nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     double grid_ms[2] = {0, 0};
-    std::mutex mu;  // serialises the per-call path
+    std::mutex mu;  // serialises the search grid and simulator scratch
     int64_t launches = 0;
 };
 
@@ -546,6 +559,25 @@ struct l1rxg_tracker {
 };
 
 namespace {
+
+// This thread's per-call state for context c (created on first use).
+CallScratch* call_scratch(l1rxg_ctx* c) {
+    thread_local std::vector<std::pair<uint64_t, CallScratch*>> mine;
+    for (auto& e : mine)
+        if (e.first == c->id)
+            return e.second;
+    auto* cs = new CallScratch();
+    if (cudaStreamCreateWithFlags(&cs->s, cudaStreamNonBlocking) != cudaSuccess) {
+        delete cs;
+        return nullptr;
+    }
+    {
+        std::lock_guard<std::mutex> lk(c->scratch_mu);
+        c->scratch.push_back(cs);
+    }
+    mine.emplace_back(c->id, cs);
+    return cs;
+}
 
 cudaEvent_t get_event(l1rxg_tracker* t) {
     if (!t->ev_pool.empty()) {
@@ -689,6 +721,8 @@ int l1rxg_create(int device, l1rxg_ctx** out) {
     if (upload_constants())
         return set_err(L1RXG_ECUDA, "constant upload failed");
     auto* c = new l1rxg_ctx();
+    static std::atomic<uint64_t> next_id{1};
+    c->id = next_id++;
     c->device = device;
     std::vector<int8_t> codes(33 * 1023, 0);
     for (int p = 1; p <= 32; ++p)
@@ -720,6 +754,12 @@ int l1rxg_destroy(l1rxg_ctx* c) {
                       &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist, &c->gA,
                       &c->gMt, &c->gC})
         b->release();
+    for (CallScratch* cs : c->scratch) {
+        for (DevBuf* b : {&cs->iq64, &cs->iq32, &cs->states, &cs->prns, &cs->sums, &cs->corr})
+            b->release();
+        cudaStreamDestroy(cs->s);
+        delete cs;
+    }
     if (c->blas)
         cublasDestroy(c->blas);
     cudaFree(c->d_codes);
@@ -768,29 +808,31 @@ int l1rxg_correlate_batch(l1rxg_ctx* c, const double* iq, int n, int n_jobs,
             return set_err(L1RXG_EINVAL, "code NCO state out of the correlator's domain "
                                          "(0 <= code_phase, code_freq > 0, replica span < 4096 chips)");
     }
-    std::lock_guard<std::mutex> lk(c->mu);
     CK(cudaSetDevice(c->device));
+    CallScratch* cs = call_scratch(c);
+    if (!cs)
+        return set_err(L1RXG_ECUDA, "per-thread stream creation failed");
     const int T = pick_T(taps->n_taps);
     const size_t ns = static_cast<size_t>(n) * n_jobs;
-    if (c->iq64.ensure(ns * 16) || c->iq32.ensure(ns * 8) ||
-        c->states.ensure(sizeof(l1rxg_nco) * n_jobs) || c->prns.ensure(4 * (size_t)n_jobs) ||
-        c->sums.ensure(sizeof(double) * 2 * T * (size_t)n_jobs) ||
-        c->corr.ensure(sizeof(l1rxg_corr) * n_jobs))
+    if (cs->iq64.ensure(ns * 16) || cs->iq32.ensure(ns * 8) ||
+        cs->states.ensure(sizeof(l1rxg_nco) * n_jobs) || cs->prns.ensure(4 * (size_t)n_jobs) ||
+        cs->sums.ensure(sizeof(double) * 2 * T * (size_t)n_jobs) ||
+        cs->corr.ensure(sizeof(l1rxg_corr) * n_jobs))
         return L1RXG_ENOMEM;
-    cudaStream_t s = c->compute;
-    CK(cudaMemcpyAsync(c->iq64.p, iq, ns * 16, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->states.p, states, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->prns.p, prns, 4 * (size_t)n_jobs, cudaMemcpyHostToDevice, s));
+    cudaStream_t s = cs->s;
+    CK(cudaMemcpyAsync(cs->iq64.p, iq, ns * 16, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cs->states.p, states, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cs->prns.p, prns, 4 * (size_t)n_jobs, cudaMemcpyHostToDevice, s));
     cf64_to_f32_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(
-        static_cast<const double2*>(c->iq64.p), static_cast<float2*>(c->iq32.p), (int64_t)ns);
+        static_cast<const double2*>(cs->iq64.p), static_cast<float2*>(cs->iq32.p), (int64_t)ns);
     CK(cudaGetLastError());
     JobArgs a{};
-    a.samples = static_cast<const float2*>(c->iq32.p);
-    a.states = static_cast<l1rxg_nco*>(c->states.p);
-    a.prns = static_cast<const int32_t*>(c->prns.p);
+    a.samples = static_cast<const float2*>(cs->iq32.p);
+    a.states = static_cast<l1rxg_nco*>(cs->states.p);
+    a.prns = static_cast<const int32_t*>(cs->prns.p);
     a.codes = c->d_codes;
-    a.tap_sums = static_cast<double*>(c->sums.p);
-    a.corr = static_cast<l1rxg_corr*>(c->corr.p);
+    a.tap_sums = static_cast<double*>(cs->sums.p);
+    a.corr = static_cast<l1rxg_corr*>(cs->corr.p);
     a.n = n;
     a.kp = taps->prompt;
     a.ke = taps->early;
@@ -804,16 +846,15 @@ int l1rxg_correlate_batch(l1rxg_ctx* c, const double* iq, int n, int n_jobs,
     rc = go();
     if (rc)
         return rc;
-    c->launches += 2;
-    CK(cudaMemcpyAsync(states, c->states.p, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyDeviceToHost, s));
-    std::vector<double> sums(static_cast<size_t>(2 * T) * n_jobs);
-    CK(cudaMemcpyAsync(sums.data(), c->sums.p, sums.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(states, cs->states.p, sizeof(l1rxg_nco) * n_jobs, cudaMemcpyDeviceToHost, s));
+    cs->hsums.resize(static_cast<size_t>(2 * T) * n_jobs);
+    CK(cudaMemcpyAsync(cs->hsums.data(), cs->sums.p, cs->hsums.size() * 8, cudaMemcpyDeviceToHost, s));
     if (corr_out)
-        CK(cudaMemcpyAsync(corr_out, c->corr.p, sizeof(l1rxg_corr) * n_jobs, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(corr_out, cs->corr.p, sizeof(l1rxg_corr) * n_jobs, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (tap_sums)
         for (int j = 0; j < n_jobs; ++j)
-            std::memcpy(tap_sums + (size_t)j * 2 * taps->n_taps, sums.data() + (size_t)j * 2 * T,
+            std::memcpy(tap_sums + (size_t)j * 2 * taps->n_taps, cs->hsums.data() + (size_t)j * 2 * T,
                         sizeof(double) * 2 * taps->n_taps);
     return 0;
 }

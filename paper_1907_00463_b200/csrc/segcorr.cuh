@@ -221,6 +221,9 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
     const int sw = lane & 7;
     float2 A = make_float2(0.f, 0.f), B = make_float2(0.f, 0.f);
     float2 C0 = make_float2(0.f, 0.f), C1 = make_float2(0.f, 0.f);
+#ifdef L1RXG_SEG_SPLIT2
+    float2 As = C0, Bs = C0, C0s = C0, C1s = C0;
+#endif
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
         const uint4 wa4 = *reinterpret_cast<const uint4*>(rowp + ((ch ^ sw) << 4));
@@ -241,14 +244,38 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
                 xa = (j >= jlo && j < jhi) ? xa : 0u;
                 xb = (j + 16 >= jlo && j + 16 < jhi) ? xb : 0u;
             }
+#ifdef L1RXG_SEG_SPLIT2  // experiment: the two FFMA2 of a sample into separate accumulators (ILP)
+            if (j > 0 && j == q0) {
+                C0 = A;
+                C0s = As;
+            }
+            if (j > 0 && j + 16 == q1) {
+                C1 = B;
+                C1s = Bs;
+            }
+            {
+                const float xr = seg_re(xa), xi = seg_im(xa), yr = seg_re(xb), yi = seg_im(xb);
+                A = __ffma2_rn(make_float2(xr, xi), make_float2(ac[t], ac[t]), A);
+                As = __ffma2_rn(make_float2(xi, xr), make_float2(as[t], -as[t]), As);
+                B = __ffma2_rn(make_float2(yr, yi), make_float2(bc[t], bc[t]), B);
+                Bs = __ffma2_rn(make_float2(yi, yr), make_float2(bs[t], -bs[t]), Bs);
+            }
+#else
             if (j > 0 && j == q0)
                 C0 = A;
             if (j > 0 && j + 16 == q1)
                 C1 = B;
             A = seg_mac(A, seg_re(xa), seg_im(xa), ac[t], as[t]);
             B = seg_mac(B, seg_re(xb), seg_im(xb), bc[t], bs[t]);
+#endif
         }
     }
+#ifdef L1RXG_SEG_SPLIT2
+    A = make_float2(A.x + As.x, A.y + As.y);
+    B = make_float2(B.x + Bs.x, B.y + Bs.y);
+    C0 = make_float2(C0.x + C0s.x, C0.y + C0s.y);
+    C1 = make_float2(C1.x + C1s.x, C1.y + C1s.y);
+#endif
     p16 = A;
     c0 = C0;
     c1 = make_float2(A.x + C1.x, A.y + C1.y);
@@ -420,7 +447,7 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
     // flattened order would put it (thread (pre_k + i) mod nthr takes
     // transition i of tap k) so every thread keeps the same share
     int pre = 0;
-#pragma unroll
+#pragma unroll 1  // unrolled (k constant) it ran 5 % fewer instructions but missed the instruction cache
     for (int k = 0; k < T; ++k) {
         const int g0 = __shfl_sync(0xffffffffu, g0k, k);
         const int cnt = __shfl_sync(0xffffffffu, cntk, k);

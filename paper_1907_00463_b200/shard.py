@@ -6,9 +6,10 @@ The path has no per-epoch exchange -- channels never share mutable state
 only collective is the end-of-run gather of records to rank 0 (NCCL over
 NVLink on GPUs, gloo in the CPU tests).
 
-Units per config: recordings (config 4, weak or strong), channel batches
-(configs 2/3), PRNs (config 5).  Config 1 (a single sequential channel)
-does not shard: N ranks run N replicas.
+Units per config: recordings (config 4, strong), channel batches of one
+stream broadcast from rank 0 (configs 2/3, strong), PRNs of one recording
+(config 5, strong; the planes are gathered).  Config 1 (a single sequential
+channel) does not shard: N ranks run N replicas.
 """
 from __future__ import annotations
 
@@ -27,6 +28,15 @@ def shard_range(n_units: int, world: int, rank: int) -> range:
 
 def shard_list(units: Sequence, world: int, rank: int) -> List:
     return [units[i] for i in shard_range(len(units), world, rank)]
+
+
+def broadcast_stream(buf, dist, src: int = 0):
+    """Broadcasts a recording (1-D uint8 tensor, same size on every rank)
+    from `src` to every rank: the stream that all channel batches of a run
+    share (configs 2/3).  NCCL over NVLink on GPUs, gloo in the CPU tests."""
+    if dist is not None and dist.get_world_size() > 1:
+        dist.broadcast(buf, src=src)
+    return buf
 
 
 def gather_bytes(local, dist, dst: int = 0):

