@@ -1395,6 +1395,14 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             sa.n_channels = t->d.n_channels;
             sa.chunk_epochs = chunk;
             sa.fast_geom = seg_geometry_ok(&t->d) ? 1 : 0;
+            sa.qgrid = 1;  // start-chip LUT when every (padded) tap offset is k/4 chip, |k| <= 4
+            for (int k = 0; k < t->T; ++k) {
+                const double q4 = a.taps.offsets_chips[k] * 4.0;
+                if (!(q4 == std::rint(q4) && std::fabs(q4) <= 4.0))
+                    sa.qgrid = 0;
+            }
+            if (const char* ev = std::getenv("L1RXG_SEG_QGRID"))  // tests: force the exact per-tap path
+                sa.qgrid = sa.qgrid && ev[0] != '0';
             CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels)), st));
             DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
         }

@@ -77,6 +77,7 @@ struct __align__(64) SegArgs {
     int* ready;         // [n_channels] chunks finished (zeroed before the launch)
     int n_items, n_channels, chunk_epochs;
     int fast_geom;      // seg_geometry_ok: unchecked step-table entries away from ties
+    int qgrid;          // every tap offset a multiple of 1/4 chip in [-1, 1]: start chips by the LUT
 };
 
 template <int T>
@@ -107,6 +108,10 @@ struct SegSmem {
     int16_t cum[1024];       // transitions at indices <= r within one period
 #endif
     int L;                   // transitions per period
+    // quarter-grid start chips: bit t of qlut[4 qq + c] = chip of tap t at
+    // a run's first sample, for qq = floor(4 frac(ph)) and c = the chips at
+    // floor(ph) - 1 .. + 1 (bits 0..2)
+    uint8_t qlut[32];
 };
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
@@ -337,9 +342,24 @@ __device__ __forceinline__ void seg_run4(const unsigned char* buf, int lane, con
 }
 #endif
 
-// anchored value z * conj(anchor), anchor = (cos, sin) of theta(i0)
+// anchored value z * conj(anchor), anchor = (cos, sin) of theta(i0):
+// (fma(zr, c, zi s), fma(zi, c, -(zr s))) -- one FMUL2 (swapped operand,
+// one-sided negation) and one FFMA2, the same roundings as the scalar form
 __device__ __forceinline__ float2 seg_anchor(float2 z, float ca, float sa) {
+#ifdef L1RXG_SEG_SCALAR_FMA
     return make_float2(fmaf(z.x, ca, z.y * sa), fmaf(z.y, ca, -(z.x * sa)));
+#else
+    return __ffma2_rn(z, make_float2(ca, ca), __fmul2_rn(make_float2(z.y, z.x), make_float2(sa, -sa)));
+#endif
+}
+
+// 2 p - t (the run sum when the chip flips where p was captured)
+__device__ __forceinline__ float2 seg_flip(float2 p, float2 t) {
+#ifdef L1RXG_SEG_SCALAR_FMA
+    return make_float2(fmaf(2.f, p.x, -t.x), fmaf(2.f, p.y, -t.y));
+#else
+    return __ffma2_rn(p, make_float2(2.f, 2.f), make_float2(-t.x, -t.y));
+#endif
 }
 
 // Enters the step of tap k at epoch run position pos (= b + lead).  A step
@@ -518,6 +538,15 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
     }
     for (int k = tid; k < T; k += blockDim.x)
         s->d[k] = a.taps.offsets_chips[k];
+    if (tid < 32) {  // quarter-grid LUT (used when sa.qgrid): floor(ph + d_t) = floor(ph) + ((qq + 4 d_t) >> 2)
+        const int qq = tid >> 3, c3 = tid & 7;  // c3 bit 0, 1, 2: the chips at floor(ph) - 1, 0, + 1
+        uint32_t pat = 0;
+        for (int t = 0; t < T; ++t) {
+            const int D = (int)rint(a.taps.offsets_chips[t] * 4.0);
+            pat |= ((uint32_t)(c3 >> (1 + ((qq + D) >> 2))) & 1u) << t;
+        }
+        s->qlut[tid] = (uint8_t)pat;
+    }
     for (int r = tid; r < truns; r += blockDim.x)
         tab[r] = 0;  // every later epoch leaves the table clean (owners clear their entries)
     // per-warp TMA unit counters: persistent across work items (every item
@@ -723,11 +752,32 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     // 32 chip bits from m0 hold them all
                     const int m0 = floor_idx(phs) - 2;
                     const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
-                    // start chip of tap t: its chip bit moved to bit 31, then +1.0f / -1.0f
+                    // start chips of the taps as bits of `spat` (bit t: the chip of
+                    // tap t at the run's first sample, floor(fl(ph + d_t)))
+                    uint32_t spat = 0;
+                    bool exact = !sa.qgrid;
+                    if (!exact) {
+                        // quarter grid: fl(ph + d_t) = ph + d_t exactly (both are
+                        // multiples of ulp(ph) < 2^-40), so floor(ph + d_t) =
+                        // floor(ph) + ((qq + 4 d_t) >> 2), qq = floor(4 frac(ph)); the
+                        // fraction goes to fp32 rounding toward zero (qq exact); within
+                        // 1e-6 of a quarter (or of a binade edge) the exact path decides
+                        const double fl = __dsub_rn(__dadd_rd(phs, 6755399441055744.0), 6755399441055744.0);
+                        const float f4 = __double2float_rz(__dsub_rn(phs, fl)) * 4.f;
+                        const int qq = (int)f4;
+                        exact = f4 - (float)qq < 1e-6f || (float)(qq + 1) - f4 < 1e-6f;
+                        spat = s->qlut[qq * 8 + ((win >> 1) & 7)];
+                    }
+                    if (exact) {
+                        spat = 0;
+                        for (int t = 0; t < T; ++t) {
+                            const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
+                            spat |= ((win >> (ms - m0)) & 1u) << t;
+                        }
+                    }
+                    // start chip of tap t: its bit moved to bit 31, then +1.0f / -1.0f
                     auto start_chip = [&](int t) -> float {
-                        const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
-                        const uint32_t hb = win << (31 - (ms - m0));
-                        return __uint_as_float((hb & 0x80000000u) ^ 0xBF800000u);
+                        return __uint_as_float(((spat << (31 - t)) & 0x80000000u) ^ 0xBF800000u);
                     };
                     // run anchor e^{-j theta(i0)}, theta as the reference (fma(w, i, phi))
                     const double th = __fma_rn(c.w, (double)i0, c.phi);
@@ -769,9 +819,9 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
                     // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
                     const float2 v0 = seg_anchor(tot, ca_, sa_);
-                    const float2 v1 = seg_anchor(make_float2(fmaf(2.f, p16.x, -tot.x), fmaf(2.f, p16.y, -tot.y)), ca_, sa_);
-                    const float2 v2 = seg_anchor(make_float2(fmaf(2.f, pc0.x, -tot.x), fmaf(2.f, pc0.y, -tot.y)), ca_, sa_);
-                    const float2 v3 = seg_anchor(make_float2(fmaf(2.f, pc1.x, -tot.x), fmaf(2.f, pc1.y, -tot.y)), ca_, sa_);
+                    const float2 v1 = seg_anchor(seg_flip(p16, tot), ca_, sa_);
+                    const float2 v2 = seg_anchor(seg_flip(pc0, tot), ca_, sa_);
+                    const float2 v3 = seg_anchor(seg_flip(pc1, tot), ca_, sa_);
     #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int code = (int)(w >> (10 + 2 * t)) & 3;
@@ -779,8 +829,14 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         const float2 hi2 = (code & 1) ? v3 : v2;
                         const float2 v = (code & 2) ? hi2 : lo;
                         const float cs = start_chip(t);
+    #ifdef L1RXG_SEG_SCALAR_FMA
                         acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
                         acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
+    #else
+                        const float2 at = __ffma2_rn(v, make_float2(cs, cs), make_float2(acc[2 * t], acc[2 * t + 1]));
+                        acc[2 * t] = at.x;
+                        acc[2 * t + 1] = at.y;
+    #endif
                     }
                     if (slow) {  // exact per-sample sums replace the fast ones
     #pragma unroll
