@@ -367,21 +367,37 @@ def run_grid(args, rank, world, local, dist):
                     "ratio": round(float(r.ratio), 2), "detected": bool(r.detected)})
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
-    fp32_path = os.environ.get("L1RXG_GRID_FP32", "0") not in ("", "0")
+    path = os.environ.get("L1RXG_GRID", "mma")
+    if os.environ.get("L1RXG_GRID_FP32", "0") not in ("", "0"):
+        path = "fp32"
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    if fp32_path:  # FP32-pipe circulant kernel: 2 FFMA x 2 flop per cell-chip
+    n_rows = 32 * ((blocks + 4) // 5)
+    if path == "fp32":  # FP32-pipe circulant kernel: 2 FFMA x 2 flop per cell-chip
         corr_flops = float(prns.size) * bins.size * blocks * 2 * 1023 * 1023 * 4
         peak = fp32_peak_tflops(sm_mhz)
         bound, note = "fp32", ("executed algorithm: two 1023-point circulant +-1 correlations per "
                                "(PRN, bin, block) on the FP32 pipes; direct-equivalent rate in value")
-    else:  # bf16x3 tensor-core GEMM: M=1024 delays, N=2*2*bins*blocks rows, K=3*1024
+        launches = 3
+    elif path == "gemm":  # cuBLAS bf16x3 GEMM: M=1024 delays, N=2*2*bins*blocks rows, K=3*1024
         corr_flops = 2.0 * 1024 * (4 * bins.size * blocks) * 3072 * prns.size
         peak = peaks.get("bf16_tflops", 2250.0)
         bound, note = "tensor", ("executed algorithm: per PRN one bf16 GEMM (fp32 folds split into "
                                  "three bf16 terms, +-1 circulant code matrix, fp32 accumulate) via "
                                  "cuBLAS on tcgen05; peak = MEASURED_PEAKS bf16_tflops (burst); the "
                                  "corr time also holds the split, circulant-build and |.| kernels")
+        launches = 6
+    else:  # K4c: hand-written tcgen05 int8 GEMM, M=1024 delays x N=n_rows digit rows per group x K=1024
+        corr_flops = 2.0 * 1024 * n_rows * (2 * bins.size) * 1024 * prns.size
+        peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+        bound, note = "tensor", ("executed algorithm: grid_mma_kernel, one tcgen05 kind::i8 GEMM (folds as "
+                                 "three signed base-256 digits of 24-bit row-quantised integers x the "
+                                 "+-1 circulant generated in shared memory, exact int32 accumulation in "
+                                 "TMEM) with the digit recombination, |.| and the 20-block noncoherent sum "
+                                 "fused into the epilogue; %d digit rows per (bin, parity) group; peak = "
+                                 "2 x MEASURED_PEAKS bf16_tflops (B200 dense int8 rate = 2 x bf16); the "
+                                 "corr time also holds the digit split and its memset" % n_rows)
+        launches = 4
     achieved = corr_flops / (corr_ms / args.steps * 1e-3) / 1e12
     line = {"metric": METRIC, "value": direct_st / (t_max * 1e-3) / 1e9, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
@@ -397,7 +413,7 @@ def run_grid(args, rank, world, local, dist):
             "e2e": {"value": direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes) * world,
                     "d2h_bytes_per_step": int(full.size * 8)},
-            "detections": det, "gpu_launches": (3 if fp32_path else 6) * args.steps, "clocks": clk}
+            "detections": det, "gpu_launches": launches * args.steps, "clocks": clk, "grid_path": path}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -25,6 +25,7 @@
 #include "search.cuh"
 #include "ovlcorr.cuh"
 #include "segcorr.cuh"
+#include "gridmma.cuh"
 #include "simgen.cuh"
 #include "l1rxg.h"
 
@@ -427,6 +428,30 @@ int encode_ring_map(CUtensorMap* map, void* ring, int64_t rows, int64_t stride_b
     return 0;
 }
 
+// 2-D uint8 tensor {cols, rows} (row pitch = cols bytes), box {box_cols,
+// box_rows}, 128-byte swizzle: the search grid's digit rows for K4c.
+int encode_u8_2d(CUtensorMap* map, void* base, int64_t cols, int64_t rows, int box_cols, int box_rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            return set_err(L1RXG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return set_err(L1RXG_ECUDA, "cuTensorMapEncodeTiled (grid digits) failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
 int validate_taps(const l1rxg_taps* t) {
     if (!t || t->n_taps < 1 || t->n_taps > L1RXG_MAX_TAPS)
         return set_err(L1RXG_EINVAL, "n_taps must be in 1..16");
@@ -505,6 +530,7 @@ struct l1rxg_ctx {
     DevBuf graw, gbase, gF, gplane, gbins, gprns, ghist;  // search grid scratch
     DevBuf gsim;  // simulator scenario
     DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
+    DevBuf gQ, gS;                                        // K4c: int8 digit rows, row steps
     std::vector<int32_t> gMt_prns;                        // PRNs whose circulants gMt holds
     cublasHandle_t blas = nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
@@ -752,7 +778,7 @@ int l1rxg_destroy(l1rxg_ctx* c) {
             cudaEventDestroy(e);
     for (DevBuf* b : {&c->gsim, &c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
                       &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist, &c->gA,
-                      &c->gMt, &c->gC})
+                      &c->gMt, &c->gC, &c->gQ, &c->gS})
         b->release();
     for (CallScratch* cs : c->scratch) {
         for (DevBuf* b : {&cs->iq64, &cs->iq32, &cs->states, &cs->prns, &cs->sums, &cs->corr})
@@ -1738,8 +1764,52 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         static_cast<float2*>(c->gF.p));
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->gev[1], st));
-    const char* ev_fp32 = std::getenv("L1RXG_GRID_FP32");  // per call: tests compare both
-    if (ev_fp32 && std::atoi(ev_fp32)) {  // FP32-pipe circulant correlation (reference kernel)
+    const char* ev_fp32 = std::getenv("L1RXG_GRID_FP32");  // per call: tests compare the paths
+    const char* ev_path = std::getenv("L1RXG_GRID");          // "mma" (default) | "gemm" (cuBLAS) | "fp32"
+    const bool use_fp32 = (ev_fp32 && std::atoi(ev_fp32)) || (ev_path && std::strcmp(ev_path, "fp32") == 0);
+    const bool use_gemm = !use_fp32 && ev_path && std::strcmp(ev_path, "gemm") == 0;
+    if (!use_fp32 && !use_gemm) {  // K4c: hand-written tcgen05 int8 GEMM + fused |.| epilogue
+        const int G = n_bins * 2;
+        const int NR = gm_rows(n_blocks);
+        if (c->gQ.ensure(static_cast<size_t>(G) * NR * 1024) || c->gS.ensure(sizeof(float) * G * n_blocks * 2))
+            return L1RXG_ENOMEM;
+        CK(cudaMemsetAsync(c->gQ.p, 0, static_cast<size_t>(G) * NR * 1024, st));  // padding rows
+        grid_digits_kernel<<<G * n_blocks, 256, 0, st>>>(static_cast<const float2*>(c->gF.p), n_blocks, NR,
+                                                         static_cast<int8_t*>(c->gQ.p), static_cast<float*>(c->gS.p));
+        CK(cudaGetLastError());
+        GridMmaArgs ga;
+        std::memset(&ga, 0, sizeof ga);
+        if (int rc = encode_u8_2d(&ga.bmap, c->gQ.p, 1024, static_cast<int64_t>(G) * NR, GM_KB, NR))
+            return rc;
+        ga.codes = c->d_codes;
+        ga.prns = static_cast<const int32_t*>(c->gprns.p);
+        ga.scales = static_cast<const float*>(c->gS.p);
+        ga.plane = static_cast<float*>(c->gplane.p);
+        ga.n_prns = n_prns;
+        ga.n_groups = G;
+        ga.n_seg = n_blocks;
+        ga.n_rows = NR;
+        ga.out_scale = static_cast<float>(N);
+        // shape knobs (defaults measured, DESIGN.md section 3 K4c)
+        const char* ev_a = std::getenv("L1RXG_GRID_A");    // "smem" | "tmem"
+        const char* ev_ks = std::getenv("L1RXG_GRID_KS");  // K blocks per stage
+        const char* ev_epi = std::getenv("L1RXG_GRID_EPI");
+        ga.a_smem = ev_a ? (std::strcmp(ev_a, "smem") == 0) : 1;
+        ga.ks = ev_ks ? std::max(1, std::min(8, std::atoi(ev_ks))) : 2;
+        while (GM_NKB % ga.ks)
+            --ga.ks;
+        ga.epi = ev_epi ? std::atoi(ev_epi) != 0 : 1;
+        if (gm_stages(NR, ga.ks, ga.a_smem) < 2)
+            return set_err(L1RXG_EINVAL, "search grid: too many blocks for the B ring");
+        const size_t sm = gm_smem_bytes_rt(NR, ga.ks, ga.a_smem);
+        CK(cudaFuncSetAttribute(grid_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int nsm = 148;
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        const int units = n_prns * GM_TILES * G;
+        grid_mma_kernel<<<std::min(nsm, units), GM_THREADS, sm, st>>>(ga);
+        CK(cudaGetLastError());
+        c->launches += 3;
+    } else if (use_fp32) {  // FP32-pipe circulant correlation (reference kernel)
         const size_t sm = 2 * 1024 * sizeof(float) + sizeof(float2) * GRID_CHIPS * n_blocks;
         CK(cudaFuncSetAttribute(grid_corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         grid_corr_kernel<<<n_prns * n_bins * 2, GRID_TPB, sm, st>>>(

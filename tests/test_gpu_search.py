@@ -15,13 +15,12 @@ def _plane_oracle(oracle_mod, x, N, n_seg, prns, fs, bins, spc):
                      for p in prns])
 
 
-@pytest.fixture(params=["tensor", "fp32"])
+@pytest.fixture(params=["mma", "gemm", "fp32"])
 def grid_path(request, monkeypatch):
-    """The bf16x3 tensor-core GEMM (default) and the FP32-pipe kernel."""
-    if request.param == "fp32":
-        monkeypatch.setenv("L1RXG_GRID_FP32", "1")
-    else:
-        monkeypatch.delenv("L1RXG_GRID_FP32", raising=False)
+    """The hand-written tcgen05 int8 GEMM with the fused |.| epilogue
+    (default, K4c), the cuBLAS bf16x3 GEMM, and the FP32-pipe kernel."""
+    monkeypatch.delenv("L1RXG_GRID_FP32", raising=False)
+    monkeypatch.setenv("L1RXG_GRID", request.param)
     return request.param
 
 

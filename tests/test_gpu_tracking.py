@@ -533,6 +533,30 @@ def test_simulator_superposition_chunking_and_reproducibility(ctx):
     assert np.concatenate([c0, c1], axis=1).tobytes() == a.tobytes()
 
 
+@pytest.mark.parametrize("fmt,fs", [("int16_iq", 16.368e6), ("int8_iq", 16.368e6), ("int16_iq", 65.472e6)])
+def test_simulator_bytes_match_reference_simstream(ctx, oracle_mod, fmt, fs):
+    """Byte-level parity with the reference simulator itself: the unmodified
+    SimStream (simsource.hpp:253-331, oracle/_ref) renders the same noise-free
+    satellites, quantised as generate_recording does (lround, clamp to
+    +-127 / +-32767, simsource.hpp:393-413); the CUDA generator's bytes equal
+    them except at rounding ties of its fp32 cos/sin (at most one LSB)."""
+    if not oracle_mod.ref_available():
+        pytest.skip("reference build absent")
+    ms = 4
+    svs = _sim_svs()
+    g = ss.synth_gpu(ctx, ms, fs, [svs], fmt=fmt, noise=False).cpu().numpy()[0]
+    ref = oracle_mod.ref_sim_baseband(
+        [dict(prn=sv.prn, cn0=sv.cn0_dbhz, doppler=sv.doppler_hz, doppler_rate=sv.doppler_rate,
+              delay_chips=sv.delay_chips, phase0=sv.phase0) for sv in svs], ms / 1000.0, fs, False, 0)
+    scale, lim, dt = (32768.0, 32767, np.int16) if fmt == "int16_iq" else (128.0, 127, np.int8)
+    v = np.stack([ref.real, ref.imag], -1).reshape(-1) * scale
+    want = np.clip(np.sign(v) * np.floor(np.abs(v) + 0.5), -lim, lim).astype(np.int64)  # std::lround
+    got = g.view(dt).astype(np.int64)
+    assert got.size == want.size
+    d = np.abs(got - want)
+    assert d.max() <= 1 and (d == 0).mean() > 0.999, (d.max(), (d == 0).mean())
+
+
 def test_simulator_noise_and_post_correlation_snr(ctx):
     """Noise of sigma/sqrt(2) per component (simsource.hpp:325-327) and the
     post-correlation SNR over 1 ms = C/N0 - 30 dB (test_simsource.cpp:149-179),
