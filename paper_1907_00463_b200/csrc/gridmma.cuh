@@ -52,7 +52,7 @@ constexpr int GM_TILES = 8;                // 8 x 128 = 1024 >= 1023 delays
 constexpr int GM_KB = 128;                 // K bytes per pipeline stage (one 128-B swizzle row)
 constexpr int GM_NKB = 8;                  // K = 1024 (1023 chips + a zero)
 constexpr int GM_A_BYTES = GM_M * 1024;    // the circulant tile, all of K
-constexpr int GM_THREADS = 256;
+constexpr int GM_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warps 4-11 epilogue (two per TMEM lane quarter)
 constexpr int GM_SEG_PER_CHUNK = 5;        // 5 segments x (re, im) x 3 digits = 30 of 32 columns
 
 __host__ __device__ constexpr int gm_rows(int n_seg) { return 32 * ((n_seg + GM_SEG_PER_CHUNK - 1) / GM_SEG_PER_CHUNK); }
@@ -64,7 +64,7 @@ struct __align__(64) GridMmaArgs {
     CUtensorMap bmap;        // digits [n_groups * n_rows][1024] int8, box {128 B, n_rows}, 128B swizzle
     const int8_t* codes;     // [33][1023]
     const int32_t* prns;     // [n_prns]
-    const float* scales;     // [n_groups][n_seg][2]: the quantisation step of each fold row
+    const float* scales;     // [n_groups][n_seg]: the quantisation step of each fold vector
     float* plane;            // [n_prns][n_bins][2046]
     int n_prns, n_groups, n_seg, n_rows;
     float out_scale;         // N: FFTW's unnormalised inverse
@@ -179,13 +179,14 @@ __global__ void __launch_bounds__(256) grid_digits_kernel(const float2* __restri
         mr = fmaxf(mr, red[0][w]);
         mi = fmaxf(mi, red[1][w]);
     }
-    // quantisation step: the row's largest |F| maps to QMAX = 2^23 - 2^16, so
-    // the top balanced digit stays in [-127, 127]
+    // quantisation step (one per fold vector, re and im alike): its largest
+    // |component| maps to QMAX = 2^23 - 2^16, so the top balanced digit stays
+    // in [-127, 127]
     constexpr float QMAX = 8323072.f;
-    const float st[2] = {mr / QMAX, mi / QMAX};
-    const float inv[2] = {st[0] > 0.f ? 1.f / st[0] : 0.f, st[1] > 0.f ? 1.f / st[1] : 0.f};
-    if (threadIdx.x < 2)
-        scales[((int64_t)g * n_seg + seg) * 2 + threadIdx.x] = st[threadIdx.x];
+    const float stv = fmaxf(mr, mi) / QMAX;
+    const float inv[2] = {stv > 0.f ? 1.f / stv : 0.f, stv > 0.f ? 1.f / stv : 0.f};
+    if (threadIdx.x == 0)
+        scales[(int64_t)g * n_seg + seg] = stv;
     int8_t* rows = Bq + (int64_t)g * n_rows * 1024;
     for (int k = threadIdx.x; k < 1024; k += blockDim.x) {
         const float2 v = k < GRID_CHIPS ? f[k] : make_float2(0.f, 0.f);
@@ -271,16 +272,16 @@ __host__ __device__ inline int gm_stages(int n_rows, int ks, int a_smem) {
 }
 __host__ __device__ inline size_t gm_smem_bytes_rt(int n_rows, int ks, int a_smem) {
     return 1024 + (a_smem ? (size_t)GM_A_BYTES : 0) + (size_t)gm_stages(n_rows, ks, a_smem) * n_rows * GM_KB * ks +
-           2304 + 512;
+           2304 + 256 + 2 * GM_M * sizeof(float);
 }
 
+template <bool A_SMEM, int KS>
 __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_constant__ GridMmaArgs ga) {
     extern __shared__ unsigned char gm_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gm_raw) + 1023) & ~uintptr_t(1023));
     const int NR = ga.n_rows;
-    const int KS = ga.ks;                // K blocks per stage
-    const bool a_smem = ga.a_smem != 0;
-    const int NS = gm_stages(NR, KS, ga.a_smem);
+    constexpr bool a_smem = A_SMEM;
+    const int NS = gm_stages(NR, KS, A_SMEM);
     const int box_bytes = NR * GM_KB;
     const int stage_bytes = box_bytes * KS;
     unsigned char* A = sm;                               // a_smem: the circulant tile
@@ -290,9 +291,10 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
     uint64_t* full = bars;                       // [NS] TMA landed
     uint64_t* empty = bars + 12;                 // [NS] MMAs done with the stage
     uint64_t* tfull = bars + 24;                 // [2] accumulator ready
-    uint64_t* tempty = bars + 26;                // [2] accumulator drained (4 epilogue warps)
+    uint64_t* tempty = bars + 26;                // [2] accumulator drained (8 epilogue warps)
     uint64_t* adone = bars + 28;                 // MMAs of a (p, tile) run complete (A reusable)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
+    float* pairsum = reinterpret_cast<float*>(bars + 32);  // [2][128]: the epilogue pairs' partial sums
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_units = ga.n_prns * GM_TILES * ga.n_groups;
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
+            mbar_init(&tempty[b], 8);
         }
         mbar_init(adone, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
         if (a_smem) {
             gm_build_a_smem(A, cext, mt * GM_M, tid, GM_THREADS);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-        } else if (warp >= 4) {  // A into TMEM: lane j = delay, 8 stores of 32 columns (128 chips)
+        } else if (warp >= 4 && warp < 8) {  // A into TMEM: lane j = delay, 8 stores of 32 columns (128 chips)
             const int q = warp - 4, j = q * 32 + lane;
             const int J = mt * GM_M + j;
             const uint32_t* cw = reinterpret_cast<const uint32_t*>(cext);
@@ -386,63 +388,62 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
                 }
             __syncwarp();
         } else if (warp == 1) {
-            // ---- MMA issuer (one lane): D[abuf] = A . B^T over K = 1024
-            const uint32_t abase = smem_u32(A);
-            for (int u = u0; u < u1; ++u) {
-                if (lane == 0)
+            // ---- MMA issuer: lane 0 alone walks the run (descriptors advanced
+            // by adding (byte offset >> 4) to the start-address field)
+            if (lane == 0) {
+                const uint64_t adesc0 = gm_desc(smem_u32(A));
+                const uint64_t bdesc0 = gm_desc(smem_u32(Bst));
+                for (int u = u0; u < u1; ++u) {
                     gm_wait(&tempty[abuf], (uint32_t)(aphase ^ 1));
-                __syncwarp();
-                gm_fence_after();
-                const uint32_t dacc = tacc + (uint32_t)(abuf * NR);
-                for (int ks = 0; ks < nkst; ++ks) {
-                    if (lane == 0)
-                        gm_wait(&full[stage], (uint32_t)phase);
-                    __syncwarp();
                     gm_fence_after();
-                    if (lane == 0) {
-                        const uint32_t sbase = smem_u32(Bst + stage * stage_bytes);
+                    const uint32_t dacc = tacc + (uint32_t)(abuf * NR);
+                    for (int ks = 0; ks < nkst; ++ks) {
+                        gm_wait(&full[stage], (uint32_t)phase);
+                        gm_fence_after();
+                        const uint64_t bst = bdesc0 + (uint64_t)((stage * stage_bytes) >> 4);
+#pragma unroll
                         for (int j = 0; j < KS; ++j) {
-                            const int kb = ks * KS + j;
 #pragma unroll
                             for (int kk = 0; kk < GM_KB / 32; ++kk) {
-                                const uint64_t bd = gm_desc(sbase + j * box_bytes + kk * 32);
-                                const uint32_t acc = (kb | kk) != 0;
-                                if (a_smem)
-                                    gm_mma(dacc, gm_desc(abase + kb * 16384 + kk * 32), bd, idesc, acc);
+                                const int kb = ks * KS + j;
+                                const uint64_t bd = bst + (uint64_t)((j * box_bytes + kk * 32) >> 4);
+                                const uint32_t acc = (ks | j | kk) != 0;
+                                if (A_SMEM)
+                                    gm_mma(dacc, adesc0 + (uint64_t)((kb * 16384 + kk * 32) >> 4), bd, idesc, acc);
                                 else
                                     gm_mma_ts(dacc, tmem + (uint32_t)(kb * 32 + kk * 8), bd, idesc, acc);
                             }
                         }
                         gm_commit(&empty[stage]);  // the stage is free once these MMAs finish
-                        if (ks == nkst - 1)
-                            gm_commit(&tfull[abuf]);
+                        if (++stage == NS) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
-                    __syncwarp();
-                    if (++stage == NS) {
-                        stage = 0;
-                        phase ^= 1;
+                    gm_commit(&tfull[abuf]);
+                    if (++abuf == nacc) {
+                        abuf = 0;
+                        aphase ^= 1;
                     }
                 }
-                if (++abuf == nacc) {
-                    abuf = 0;
-                    aphase ^= 1;
-                }
-            }
-            if (lane == 0)
                 gm_commit(adone);  // every MMA of this run done -> A may be rebuilt
+            }
             __syncwarp();
         } else if (warp >= 4) {
-            // ---- epilogue: thread = delay lane of this warp's TMEM quarter
-            const int q = warp - 4;
+            // ---- epilogue: two warps per TMEM lane quarter (thread = delay
+            // lane), each over half of the group's 32-column chunks; the pair
+            // adds its partial sums through shared memory
+            const int q = warp & 3, h = (warp - 4) >> 2;
             const int J = mt * GM_M + q * 32 + lane;
             const int n_bins = ga.n_groups >> 1;
+            const int nch = (ga.n_seg + GM_SEG_PER_CHUNK - 1) / GM_SEG_PER_CHUNK;
             for (int u = u0; u < u1; ++u) {
                 const int g = u - pt * ga.n_groups;
                 gm_wait(&tfull[abuf], (uint32_t)aphase);
                 gm_fence_after();
-                const float* sc = ga.scales + (int64_t)g * ga.n_seg * 2;
+                const float* sc = ga.scales + (int64_t)g * ga.n_seg;
                 float acc = 0.f;
-                for (int ch = 0; ga.epi && ch * GM_SEG_PER_CHUNK < ga.n_seg; ++ch) {
+                for (int ch = h; ga.epi && ch < nch; ch += 2) {
                     uint32_t v[32];
                     GM_LD32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * NR + ch * 32), v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -450,13 +451,11 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
                     for (int sl = 0; sl < GM_SEG_PER_CHUNK; ++sl) {
                         const int seg = ch * GM_SEG_PER_CHUNK + sl;
                         if (seg < ga.n_seg) {
-                            const float re = __ldg(sc + 2 * seg) *
-                                             fmaf(65536.f, (float)(int)v[sl * 6 + 2],
-                                                  fmaf(256.f, (float)(int)v[sl * 6 + 1], (float)(int)v[sl * 6 + 0]));
-                            const float im = __ldg(sc + 2 * seg + 1) *
-                                             fmaf(65536.f, (float)(int)v[sl * 6 + 5],
-                                                  fmaf(256.f, (float)(int)v[sl * 6 + 4], (float)(int)v[sl * 6 + 3]));
-                            acc += sqrtf(fmaf(re, re, im * im));
+                            // 65536 c2 + (256 c1 + c0): the low part exact in int32
+                            const int* c = reinterpret_cast<const int*>(v) + sl * 6;
+                            const float re = fmaf(65536.f, (float)c[2], (float)(256 * c[1] + c[0]));
+                            const float im = fmaf(65536.f, (float)c[5], (float)(256 * c[4] + c[3]));
+                            acc = fmaf(__ldg(sc + seg), sqrtf(fmaf(re, re, im * im)), acc);
                         }
                     }
                 }
@@ -464,23 +463,28 @@ __global__ void __launch_bounds__(GM_THREADS, 1) grid_mma_kernel(const __grid_co
                 __syncwarp();
                 if (lane == 0)
                     gm_mbar_arrive(&tempty[abuf]);
-                if (J < GRID_CHIPS)
-                    ga.plane[((int64_t)pi * n_bins + (g >> 1)) * (2 * GRID_CHIPS) + 2 * J + (g & 1)] = ga.out_scale * acc;
+                float* slot = pairsum + (u & 1) * GM_M + q * 32 + lane;
+                if (h == 1)
+                    *slot = acc;
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+                if (h == 0 && J < GRID_CHIPS)
+                    ga.plane[((int64_t)pi * n_bins + (g >> 1)) * (2 * GRID_CHIPS) + 2 * J + (g & 1)] =
+                        ga.out_scale * (acc + *slot);
                 if (++abuf == nacc) {
                     abuf = 0;
                     aphase ^= 1;
                 }
             }
         }
-        // keep every role's ring counters in step (each role advanced only its own)
-        if ((warp != 0 || lane != 0) && warp != 1)
+        // keep every thread's ring counters in step (each role's lane advanced only its own)
+        if (warp >= 2 || lane != 0)
             for (int u = u0; u < u1; ++u)
                 for (int ks = 0; ks < nkst; ++ks)
                     if (++stage == NS) {
                         stage = 0;
                         phase ^= 1;
                     }
-        if (warp < 4 && warp != 1)
+        if (warp < 4 && !(warp == 1 && lane == 0))
             for (int u = u0; u < u1; ++u)
                 if (++abuf == nacc) {
                     abuf = 0;

@@ -1771,7 +1771,7 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
     if (!use_fp32 && !use_gemm) {  // K4c: hand-written tcgen05 int8 GEMM + fused |.| epilogue
         const int G = n_bins * 2;
         const int NR = gm_rows(n_blocks);
-        if (c->gQ.ensure(static_cast<size_t>(G) * NR * 1024) || c->gS.ensure(sizeof(float) * G * n_blocks * 2))
+        if (c->gQ.ensure(static_cast<size_t>(G) * NR * 1024) || c->gS.ensure(sizeof(float) * G * n_blocks))
             return L1RXG_ENOMEM;
         CK(cudaMemsetAsync(c->gQ.p, 0, static_cast<size_t>(G) * NR * 1024, st));  // padding rows
         grid_digits_kernel<<<G * n_blocks, 256, 0, st>>>(static_cast<const float2*>(c->gF.p), n_blocks, NR,
@@ -1795,19 +1795,31 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         const char* ev_ks = std::getenv("L1RXG_GRID_KS");  // K blocks per stage
         const char* ev_epi = std::getenv("L1RXG_GRID_EPI");
         ga.a_smem = ev_a ? (std::strcmp(ev_a, "smem") == 0) : 1;
-        ga.ks = ev_ks ? std::max(1, std::min(8, std::atoi(ev_ks))) : 2;
-        while (GM_NKB % ga.ks)
-            --ga.ks;
+        ga.ks = ev_ks ? std::max(1, std::min(4, std::atoi(ev_ks))) : 2;
+        if (ga.ks == 3)
+            ga.ks = 2;
         ga.epi = ev_epi ? std::atoi(ev_epi) != 0 : 1;
         if (gm_stages(NR, ga.ks, ga.a_smem) < 2)
             return set_err(L1RXG_EINVAL, "search grid: too many blocks for the B ring");
         const size_t sm = gm_smem_bytes_rt(NR, ga.ks, ga.a_smem);
-        CK(cudaFuncSetAttribute(grid_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int nsm = 148;
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
         const int units = n_prns * GM_TILES * G;
-        grid_mma_kernel<<<std::min(nsm, units), GM_THREADS, sm, st>>>(ga);
-        CK(cudaGetLastError());
+        auto launch = [&](auto kern) -> int {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<std::min(nsm, units), GM_THREADS, sm, st>>>(ga);
+            CK(cudaGetLastError());
+            return 0;
+        };
+        int lrc = 0;
+        if (ga.a_smem)
+            lrc = ga.ks == 1 ? launch(grid_mma_kernel<true, 1>) : ga.ks == 2 ? launch(grid_mma_kernel<true, 2>)
+                                                                             : launch(grid_mma_kernel<true, 4>);
+        else
+            lrc = ga.ks == 1 ? launch(grid_mma_kernel<false, 1>) : ga.ks == 2 ? launch(grid_mma_kernel<false, 2>)
+                                                                              : launch(grid_mma_kernel<false, 4>);
+        if (lrc)
+            return lrc;
         c->launches += 3;
     } else if (use_fp32) {  // FP32-pipe circulant correlation (reference kernel)
         const size_t sm = 2 * 1024 * sizeof(float) + sizeof(float2) * GRID_CHIPS * n_blocks;
