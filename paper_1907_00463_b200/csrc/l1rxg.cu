@@ -1794,8 +1794,10 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         const char* ev_a = std::getenv("L1RXG_GRID_A");    // "smem" | "tmem"
         const char* ev_ks = std::getenv("L1RXG_GRID_KS");  // K blocks per stage
         const char* ev_epi = std::getenv("L1RXG_GRID_EPI");
-        ga.a_smem = ev_a ? (std::strcmp(ev_a, "smem") == 0) : 1;
-        ga.ks = ev_ks ? std::max(1, std::min(4, std::atoi(ev_ks))) : 2;
+        // measured (profiles/r2k_grid_shapes.txt, config 5): A in TMEM with 4 K
+        // blocks per stage 0.306 ms; A in shared memory (2 per stage) 0.332 ms
+        ga.a_smem = ev_a ? (std::strcmp(ev_a, "smem") == 0) : 0;
+        ga.ks = ev_ks ? std::max(1, std::min(4, std::atoi(ev_ks))) : 4;
         if (ga.ks == 3)
             ga.ks = 2;
         ga.epi = ev_epi ? std::atoi(ev_epi) != 0 : 1;
