@@ -7,7 +7,7 @@
 // overflow accounting, the analogue of the paper's Table 6 real-time run).
 //
 //   gpu_receiver FILE FORMAT FS_HZ IF_HZ [--acq-ms N] [--chunk-ms N]
-//                [--paced] [--max-ms N]
+//                [--paced] [--max-ms N] [--queue N] [--consumer-delay-ms N]
 //   FORMAT: int8_real_if | int8_iq | int16_iq
 //
 // Prints one JSON object per detected channel and a summary object.
@@ -18,6 +18,9 @@
 // paced mode with overflow counting).
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -46,14 +49,15 @@ constexpr double kChipRate = 1.023e6;
 
 int main(int argc, char** argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: %s FILE FORMAT FS_HZ IF_HZ [--acq-ms N] [--chunk-ms N] [--paced] [--max-ms N]\n",
+        std::fprintf(stderr, "usage: %s FILE FORMAT FS_HZ IF_HZ [--acq-ms N] [--chunk-ms N] [--paced] [--max-ms N] "
+                             "[--queue N] [--consumer-delay-ms N]\n",
                      argv[0]);
         return 1;
     }
     const char* path = argv[1];
     const std::string fmt_s = argv[2];
     const double fs = std::atof(argv[3]), if_hz = std::atof(argv[4]);
-    int acq_ms = 10, chunk_ms = 100, max_ms = 1 << 30;
+    int acq_ms = 10, chunk_ms = 100, max_ms = 1 << 30, queue_cap = 4, consumer_delay_ms = 0;
     bool paced = false;
     for (int k = 5; k < argc; ++k) {
         const std::string a = argv[k];
@@ -65,6 +69,10 @@ int main(int argc, char** argv) {
             max_ms = std::atoi(argv[++k]);
         else if (a == "--paced")
             paced = true;
+        else if (a == "--queue" && k + 1 < argc)
+            queue_cap = std::max(1, std::atoi(argv[++k]));
+        else if (a == "--consumer-delay-ms" && k + 1 < argc)  // test hook: a slow consumer
+            consumer_delay_ms = std::atoi(argv[++k]);
     }
     const int fmt = fmt_s == "int8_real_if" ? L1RXG_FMT_INT8_REAL_IF
                     : fmt_s == "int16_iq"   ? L1RXG_FMT_INT16_IQ
@@ -141,32 +149,88 @@ int main(int argc, char** argv) {
     std::vector<int32_t> cs(chans.size(), 0);
     l1rxg_tracker* trk = nullptr;
     OK(l1rxg_tracker_create(ctx, &desc, chans.data(), cs.data(), &trk));
+    // ---- streaming: a producer thread reads the recording in chunk_ms blocks
+    // into a bounded queue of pinned buffers (BlockQueue, pipeline.hpp:30-86);
+    // paced, it releases each block at its stream time (samples.hpp:162-170)
+    // and a block that finds the queue full is dropped and counted as an
+    // overflow, the run marked degraded (pipeline.hpp:393-397: never silent
+    // loss) -- the consumer pushes zeros in its place, so sample accounting and
+    // every later epoch's timing stay exact.  Offline, the producer blocks.
     const int64_t chunk_bytes = chunk_ms * n * bps;
-    void* pinned[2] = {nullptr, nullptr};
-    OK(l1rxg_host_alloc(ctx, chunk_bytes, &pinned[0]));
-    OK(l1rxg_host_alloc(ctx, chunk_bytes, &pinned[1]));
+    const int n_buf = queue_cap + 1;  // queue slots + the one being consumed
+    std::vector<void*> pinned(static_cast<size_t>(n_buf), nullptr);
+    for (auto& pb : pinned)
+        OK(l1rxg_host_alloc(ctx, chunk_bytes, &pb));
+    void* zeros = nullptr;
+    OK(l1rxg_host_alloc(ctx, chunk_bytes, &zeros));
+    std::memset(zeros, 0, static_cast<size_t>(chunk_bytes));
+    struct Item {
+        int buf;        // pinned buffer, or -1: a dropped block (zeros)
+        int64_t bytes;
+    };
+    std::mutex mu;
+    std::condition_variable cv_item, cv_free;
+    std::deque<Item> q;
+    std::vector<int> free_bufs;
+    for (int k = 0; k < n_buf; ++k)
+        free_bufs.push_back(k);
+    bool closed = false;
+    int64_t overflows = 0;
     std::fseek(f, 0, SEEK_SET);
-    int64_t overflows = 0, ms_done = 0;
     const auto start = std::chrono::steady_clock::now();
-    for (int k = 0; ms_done < total_ms; ++k) {
-        const int64_t ms = std::min<int64_t>(chunk_ms, total_ms - ms_done);
-        void* buf = pinned[k & 1];
-        // the previous push from this buffer has been copied once the push
-        // two chunks ago is done: sync keeps the double buffer safe
-        if (k >= 2)
-            OK(l1rxg_tracker_sync(trk));
-        if (std::fread(buf, 1, static_cast<size_t>(ms * n * bps), f) != static_cast<size_t>(ms * n * bps))
-            break;
-        OK(l1rxg_tracker_push(trk, 0, buf, ms * n * bps));
-        OK(l1rxg_tracker_run(trk, -1));
-        ms_done += ms;
-        if (paced) {  // hold real time; a chunk finishing late is an overflow (pipeline.hpp:412-428)
-            const auto due = start + std::chrono::milliseconds(ms_done);
-            if (std::chrono::steady_clock::now() > due + std::chrono::milliseconds(chunk_ms))
+    std::thread producer([&] {
+        std::vector<unsigned char> tmp(static_cast<size_t>(chunk_bytes));
+        for (int64_t done = 0; done < total_ms;) {
+            const int64_t ms = std::min<int64_t>(chunk_ms, total_ms - done);
+            const size_t want = static_cast<size_t>(ms * n * bps);
+            if (std::fread(tmp.data(), 1, want, f) != want)
+                break;
+            done += ms;
+            if (paced)  // the block is due at its stream time
+                std::this_thread::sleep_until(start + std::chrono::milliseconds(done));
+            std::unique_lock<std::mutex> lk(mu);
+            if (!paced)
+                cv_free.wait(lk, [&] { return !free_bufs.empty() && (int)q.size() < queue_cap; });
+            if (free_bufs.empty() || (int)q.size() >= queue_cap) {  // paced: try_push failed
                 ++overflows;
-            std::this_thread::sleep_until(due);
+                q.push_back({-1, static_cast<int64_t>(want)});  // a gap marker, not data
+                cv_item.notify_one();
+                continue;
+            }
+            const int b = free_bufs.back();
+            free_bufs.pop_back();
+            std::memcpy(pinned[static_cast<size_t>(b)], tmp.data(), want);
+            q.push_back({b, static_cast<int64_t>(want)});
+            cv_item.notify_one();
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        closed = true;
+        cv_item.notify_all();
+    });
+    int64_t ms_done = 0;
+    for (;;) {
+        Item it;
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv_item.wait(lk, [&] { return !q.empty() || closed; });
+            if (q.empty())
+                break;
+            it = q.front();
+            q.pop_front();
+        }
+        OK(l1rxg_tracker_push(trk, 0, it.buf >= 0 ? pinned[static_cast<size_t>(it.buf)] : zeros, it.bytes));
+        OK(l1rxg_tracker_run(trk, -1));
+        OK(l1rxg_tracker_sync(trk));  // the pinned buffer's copy is done: back to the pool
+        ms_done += it.bytes / (n * bps);
+        if (consumer_delay_ms > 0)
+            std::this_thread::sleep_for(std::chrono::milliseconds(consumer_delay_ms));
+        if (it.buf >= 0) {
+            std::lock_guard<std::mutex> lk(mu);
+            free_bufs.push_back(it.buf);
+            cv_free.notify_one();
         }
     }
+    producer.join();
     OK(l1rxg_tracker_sync(trk));
     const double wall_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
@@ -184,12 +248,13 @@ int main(int argc, char** argv) {
     }
     std::printf("{\"summary\": {\"detected\": %zu, \"recording_ms\": %lld, \"acquisition_wall_ms\": %.2f, "
                 "\"tracking_wall_s\": %.4f, \"real_time_factor\": %.2f, \"channel_epochs_per_s\": %.0f, "
-                "\"paced\": %s, \"overflows\": %lld}}\n",
+                "\"paced\": %s, \"overflows\": %lld, \"degraded\": %s, \"queue\": %d}}\n",
                 chans.size(), static_cast<long long>(ms_done), acq_wall_ms, wall_s,
                 (ms_done / 1000.0) / wall_s, ch_epochs / wall_s, paced ? "true" : "false",
-                static_cast<long long>(overflows));
-    l1rxg_host_free(ctx, pinned[0]);
-    l1rxg_host_free(ctx, pinned[1]);
+                static_cast<long long>(overflows), overflows > 0 ? "true" : "false", queue_cap);
+    for (auto pb : pinned)
+        l1rxg_host_free(ctx, pb);
+    l1rxg_host_free(ctx, zeros);
     l1rxg_tracker_destroy(trk);
     l1rxg_destroy(ctx);
     std::fclose(f);

@@ -822,22 +822,6 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     const float2 v1 = seg_anchor(seg_flip(p16, tot), ca_, sa_);
                     const float2 v2 = seg_anchor(seg_flip(pc0, tot), ca_, sa_);
                     const float2 v3 = seg_anchor(seg_flip(pc1, tot), ca_, sa_);
-    #pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int code = (int)(w >> (10 + 2 * t)) & 3;
-                        const float2 lo = (code & 1) ? v1 : v0;
-                        const float2 hi2 = (code & 1) ? v3 : v2;
-                        const float2 v = (code & 2) ? hi2 : lo;
-                        const float cs = start_chip(t);
-    #ifdef L1RXG_SEG_SCALAR_FMA
-                        acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
-                        acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
-    #else
-                        const float2 at = __ffma2_rn(v, make_float2(cs, cs), make_float2(acc[2 * t], acc[2 * t + 1]));
-                        acc[2 * t] = at.x;
-                        acc[2 * t + 1] = at.y;
-    #endif
-                    }
                     if (slow) {  // exact per-sample sums replace the fast ones
     #pragma unroll
                         for (int t = 0; t < T; ++t)
@@ -859,6 +843,48 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         hr += z.x;
                         hi += z.y;
                     }
+#ifdef L1RXG_SEG_SELCOMB  // experiment switch: the tap combine by register selects
+    #pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int code = (int)(w >> (10 + 2 * t)) & 3;
+                        const float2 lo = (code & 1) ? v1 : v0;
+                        const float2 hi2 = (code & 1) ? v3 : v2;
+                        const float2 v = (code & 2) ? hi2 : lo;
+                        const float cs = start_chip(t);
+    #ifdef L1RXG_SEG_SCALAR_FMA
+                        acc[2 * t] = fmaf(cs, v.x, acc[2 * t]);
+                        acc[2 * t + 1] = fmaf(cs, v.y, acc[2 * t + 1]);
+    #else
+                        const float2 at = __ffma2_rn(v, make_float2(cs, cs), make_float2(acc[2 * t], acc[2 * t + 1]));
+                        acc[2 * t] = at.x;
+                        acc[2 * t + 1] = at.y;
+    #endif
+                    }
+#else
+                    // the tap combine: v0..v3 go to this lane's own row of the
+                    // consumed unit buffer (thread-private scratch; slot (4 i +
+                    // lane) mod 16 puts a warp's 8-byte accesses on two wavefronts)
+                    // and every tap loads its value by code -- one LDS.64 per tap
+                    // instead of three float2 selects
+                    {
+                        unsigned char* rowv = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES + lane * 128;
+                        *reinterpret_cast<float2*>(rowv + ((lane + 0) & 15) * 8) = v0;
+                        *reinterpret_cast<float2*>(rowv + ((lane + 4) & 15) * 8) = v1;
+                        *reinterpret_cast<float2*>(rowv + ((lane + 8) & 15) * 8) = v2;
+                        *reinterpret_cast<float2*>(rowv + ((lane + 12) & 15) * 8) = v3;
+    #pragma unroll
+                        for (int t = 0; t < T; ++t) {
+                            const int code = (int)(w >> (10 + 2 * t)) & 3;
+                            const float2 v = *reinterpret_cast<const float2*>(rowv + ((4 * code + lane) & 15) * 8);
+                            const float cs = start_chip(t);
+                            const float2 at = __ffma2_rn(v, make_float2(cs, cs), make_float2(acc[2 * t], acc[2 * t + 1]));
+                            acc[2 * t] = at.x;
+                            acc[2 * t + 1] = at.y;
+                        }
+                        // these generic writes precede the next TMA into the buffer
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+#endif
                     __syncwarp();
                     ++consumed;
                     if (issued < consumed + SEG_NBUF)
