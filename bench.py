@@ -329,21 +329,28 @@ def run_grid(args, rank, world, local, dist):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
 
-    # e2e: host bytes in, this rank's PRN planes out, gathered to rank 0 (NCCL)
+    # e2e: host bytes in (pinned), this rank's PRN planes out as float32 --
+    # into pinned host memory at N = 1; into device memory, gathered to rank
+    # 0 over NCCL and read back there, at N > 1
     host = ctx.host_alloc(nbytes)
     host[:] = raw.cpu().numpy()
+    plane_bytes = prns.size * bins.size * 2046 * 4
+    out_host = ctx.host_alloc(all_prns.size * bins.size * 2046 * 4).view(np.float32)
+    out_dev = torch.empty(plane_bytes, dtype=torch.uint8, device=torch.device("cuda", local)) if dist else None
 
     def step_e2e():
-        pl = search_grid(ctx, host, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns, bins)
         if not dist:
-            return pl
+            return search_grid(ctx, host, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns, bins, out=out_host,
+                               dtype=np.float32)
         from paper_1907_00463_b200.shard import gather_bytes
-        t = torch.from_numpy(pl.reshape(-1).view(np.uint8)).to(torch.device("cuda", local))
-        outs = gather_bytes(t, dist, dst=0)
+        search_grid(ctx, host, abi.FMT_INT8_REAL_IF, fs, g["if_hz"], blocks, prns, bins,
+                    out_device_ptr=out_dev.data_ptr(), dtype=np.float32)
+        outs = gather_bytes(out_dev, dist, dst=0)
         if rank != 0:
             return None
-        return np.concatenate([o.cpu().numpy().view(np.float64) for o in outs]).reshape(
-            all_prns.size, bins.size, 2046)
+        allp = torch.cat(outs)
+        torch.from_numpy(out_host.view(np.uint8)).copy_(allp)
+        return out_host.reshape(all_prns.size, bins.size, 2046)
     step_e2e()
     if dist:
         dist.barrier()
@@ -391,12 +398,13 @@ def run_grid(args, rank, world, local, dist):
         corr_flops = 2.0 * 1024 * n_rows * (2 * bins.size) * 1024 * prns.size
         peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
         bound, note = "tensor", ("executed algorithm: grid_mma_kernel, one tcgen05 kind::i8 GEMM (folds as "
-                                 "three signed base-256 digits of 24-bit row-quantised integers x the "
-                                 "+-1 circulant generated in shared memory, exact int32 accumulation in "
+                                 "three signed base-256 digits of 24-bit vector-quantised integers x the "
+                                 "+-1 circulant generated on chip into TMEM, exact int32 accumulation in "
                                  "TMEM) with the digit recombination, |.| and the 20-block noncoherent sum "
                                  "fused into the epilogue; %d digit rows per (bin, parity) group; peak = "
-                                 "2 x MEASURED_PEAKS bf16_tflops (B200 dense int8 rate = 2 x bf16); the "
-                                 "corr time also holds the digit split and its memset" % n_rows)
+                                 "2 x MEASURED_PEAKS bf16_tflops (B200 dense int8 rate = 2 x bf16; against "
+                                 "the nominal 4.5 POPS the fraction is frac_vs_nominal); the corr time also "
+                                 "holds the digit split and its memset" % n_rows)
         launches = 4
     achieved = corr_flops / (corr_ms / args.steps * 1e-3) / 1e12
     line = {"metric": METRIC, "value": direct_st / (t_max * 1e-3) / 1e9, "unit": UNIT,
@@ -409,10 +417,12 @@ def run_grid(args, rank, world, local, dist):
                                       f"planes gathered to rank 0 (NCCL) in the e2e leg"},
             "kernel_ms_per_step": {"ingest_fold": fold_ms / args.steps, "corr": corr_ms / args.steps},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None, "note": note},
+                         "frac": achieved / peak, "traffic": None, "note": note,
+                         "frac_vs_nominal": (None if path == "fp32" else
+                                             achieved / (4500.0 if path == "mma" else 2250.0))},
             "e2e": {"value": direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes) * world,
-                    "d2h_bytes_per_step": int(full.size * 8)},
+                    "d2h_bytes_per_step": int(full.size * 4)},
             "detections": det, "gpu_launches": launches * args.steps, "clocks": clk, "grid_path": path}
     print(json.dumps(line), flush=True)
     if dist:

@@ -353,6 +353,17 @@ int l1rxg_search_grid(l1rxg_ctx* ctx, int format, const void* bytes,
                       int n_blocks, const int32_t* prns, int n_prns,
                       const double* doppler_bins_hz, int n_bins,
                       int delay_step, int n_delays, double* plane_out);
+/* Same plane into float32 or float64 (plane_f32 = 1 / 0) at host or device
+ * memory (plane_on_device): the GPU converts and trims the plane, so a pinned
+ * host buffer or a device buffer (e.g. for an NCCL gather) receives it with
+ * one copy.  l1rxg_search_grid = float64, host. */
+int l1rxg_search_grid_ex(l1rxg_ctx* ctx, int format, const void* bytes,
+                         int bytes_on_device, int64_t nbytes,
+                         double sample_rate_hz, double if_frequency_hz,
+                         int n_blocks, const int32_t* prns, int n_prns,
+                         const double* doppler_bins_hz, int n_bins,
+                         int delay_step, int n_delays, void* plane_out,
+                         int plane_f32, int plane_on_device);
 /* Device time of the last l1rxg_search_grid: ingest + fold, correlation. */
 int l1rxg_search_grid_timing(l1rxg_ctx* ctx, double* ingest_fold_ms,
                              double* corr_ms);

@@ -25,7 +25,7 @@ EXPORTS = [
     "l1rxg_tracker_sync", "l1rxg_tracker_channels", "l1rxg_tracker_epoch_counts",
     "l1rxg_tracker_records", "l1rxg_tracker_records_raw", "l1rxg_tracker_reset",
     "l1rxg_tracker_stream", "l1rxg_tracker_read_samples",
-    "l1rxg_tracker_timing", "l1rxg_search_grid", "l1rxg_search_grid_timing", "l1rxg_simulate",
+    "l1rxg_tracker_timing", "l1rxg_search_grid", "l1rxg_search_grid_ex", "l1rxg_search_grid_timing", "l1rxg_simulate",
     "l1rxg_pick_peak", "l1rxg_init_channel",
 ]
 
@@ -83,6 +83,8 @@ def lib():
     _sig(L, "l1rxg_tracker_timing", C.c_int, vp, dp, dp, P(i64))
     _sig(L, "l1rxg_search_grid", C.c_int, vp, C.c_int, vp, C.c_int, i64, C.c_double, C.c_double,
          C.c_int, P(C.c_int32), C.c_int, dp, C.c_int, C.c_int, C.c_int, dp)
+    _sig(L, "l1rxg_search_grid_ex", C.c_int, vp, C.c_int, vp, C.c_int, i64, C.c_double, C.c_double,
+         C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int)
     _sig(L, "l1rxg_search_grid_timing", C.c_int, vp, dp, dp)
     _sig(L, "l1rxg_pick_peak", C.c_int, dp, C.c_int, C.c_int, dp, C.c_int, C.c_int, C.c_double, C.c_double,
          P(abi.AcqResult))

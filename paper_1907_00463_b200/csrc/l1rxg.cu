@@ -531,6 +531,7 @@ struct l1rxg_ctx {
     DevBuf gsim;  // simulator scenario
     DevBuf gA, gMt, gC;                                   // tensor-core grid: operands, products
     DevBuf gQ, gS;                                        // K4c: int8 digit rows, row steps
+    DevBuf gout;                                          // the trimmed, converted plane
     std::vector<int32_t> gMt_prns;                        // PRNs whose circulants gMt holds
     cublasHandle_t blas = nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
@@ -778,7 +779,7 @@ int l1rxg_destroy(l1rxg_ctx* c) {
             cudaEventDestroy(e);
     for (DevBuf* b : {&c->gsim, &c->iq64, &c->iq32, &c->states, &c->prns, &c->sums, &c->corr, &c->graw,
                       &c->gbase, &c->gF, &c->gplane, &c->gbins, &c->gprns, &c->ghist, &c->gA,
-                      &c->gMt, &c->gC, &c->gQ, &c->gS})
+                      &c->gMt, &c->gC, &c->gQ, &c->gS, &c->gout})
         b->release();
     for (CallScratch* cs : c->scratch) {
         for (DevBuf* b : {&cs->iq64, &cs->iq32, &cs->states, &cs->prns, &cs->sums, &cs->corr})
@@ -1684,6 +1685,14 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
                       int64_t nbytes, double fs, double if_hz, int n_blocks, const int32_t* prns,
                       int n_prns, const double* bins, int n_bins, int delay_step, int n_delays,
                       double* plane_out) {
+    return l1rxg_search_grid_ex(c, format, bytes, bytes_on_device, nbytes, fs, if_hz, n_blocks, prns, n_prns, bins,
+                                n_bins, delay_step, n_delays, plane_out, 0, 0);
+}
+
+int l1rxg_search_grid_ex(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_device,
+                         int64_t nbytes, double fs, double if_hz, int n_blocks, const int32_t* prns,
+                         int n_prns, const double* bins, int n_bins, int delay_step, int n_delays,
+                         void* plane_out, int plane_f32, int plane_on_device) {
     if (!c || !bytes || !prns || !bins || !plane_out)
         return set_err(L1RXG_EINVAL, "null argument");
     const int bps = bytes_per_sample(format);
@@ -1874,18 +1883,27 @@ int l1rxg_search_grid(l1rxg_ctx* c, int format, const void* bytes, int bytes_on_
         c->launches += 3;
     }
     CK(cudaEventRecord(c->gev[2], st));
-    std::vector<float> pl(static_cast<size_t>(2 * GRID_CHIPS) * n_bins * n_prns);
-    CK(cudaMemcpyAsync(pl.data(), c->gplane.p, pl.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    // the plane trimmed to n_delays and converted on the GPU, one copy out
+    const int64_t cells = static_cast<int64_t>(n_bins) * n_prns * n_delays;
+    const size_t ebytes = plane_f32 ? sizeof(float) : sizeof(double);
+    void* dst = plane_out;
+    if (!plane_on_device) {
+        if (c->gout.ensure(static_cast<size_t>(cells) * ebytes))
+            return L1RXG_ENOMEM;
+        dst = c->gout.p;
+    }
+    grid_plane_out_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(
+        static_cast<const float*>(c->gplane.p), n_delays, cells, dst, plane_f32);
+    CK(cudaGetLastError());
+    if (!plane_on_device)
+        CK(cudaMemcpyAsync(plane_out, dst, static_cast<size_t>(cells) * ebytes, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     float ms0 = 0, ms1 = 0;
     cudaEventElapsedTime(&ms0, c->gev[0], c->gev[1]);
     cudaEventElapsedTime(&ms1, c->gev[1], c->gev[2]);
     c->grid_ms[0] = ms0;
     c->grid_ms[1] = ms1;
-    c->launches += 3;
-    for (int64_t r = 0; r < static_cast<int64_t>(n_bins) * n_prns; ++r)
-        for (int k = 0; k < n_delays; ++k)
-            plane_out[r * n_delays + k] = pl[static_cast<size_t>(r * 2 * GRID_CHIPS + k)];
+    c->launches += 4;
     return 0;
 }
 

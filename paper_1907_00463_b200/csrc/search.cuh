@@ -224,4 +224,18 @@ __global__ void grid_mag_kernel(const float* __restrict__ C, int n_rows, int n_b
     }
 }
 
+// plane [prn][bin][2046] fp32 -> [prn][bin][n_delays] fp32 or fp64
+__global__ void grid_plane_out_kernel(const float* __restrict__ plane, int n_delays, int64_t cells, void* out,
+                                      int f32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cells)
+        return;
+    const int64_t r = i / n_delays, k = i - r * n_delays;
+    const float v = plane[r * (2 * GRID_CHIPS) + k];
+    if (f32)
+        static_cast<float*>(out)[i] = v;
+    else
+        static_cast<double*>(out)[i] = (double)v;
+}
+
 }  // namespace l1rxg

@@ -144,26 +144,36 @@ class Context:
 
 
 def search_grid(ctx: "Context", raw, fmt: int, fs: float, if_hz: float, n_blocks: int, prns, bins,
-                n_delays: int | None = None, device_ptr: int | None = None) -> np.ndarray:
+                n_delays: int | None = None, device_ptr: int | None = None, out=None,
+                out_device_ptr: int | None = None, dtype=np.float64):
     """acquire_pcs plane semantics (acquisition.hpp:170-222) on the GPU:
     returns plane[prn][bin][delay] for delays d = k * (samples per half chip),
     cells N * |sum_n wiped[n] code[(n - d) mod N]| summed over n_blocks
-    1-ms segments.  raw: host bytes, or device_ptr for bytes in HBM."""
+    1-ms segments.  raw: host bytes, or device_ptr for bytes in HBM.  The
+    plane lands in `out` (a host array, pinned is fastest) or at
+    out_device_ptr (device memory), as float64 or float32 (`dtype`)."""
     spc = int(round(fs / 1.023e6 / 2.0))
     nd = n_delays or 2046
     prns = np.ascontiguousarray(prns, np.int32)
     bins = np.ascontiguousarray(bins, np.float64)
-    plane = np.zeros((prns.size, bins.size, nd), np.float64)
+    f32 = np.dtype(dtype) == np.float32
     if device_ptr is not None:
         ptr, on_dev, nbytes = C.c_void_p(device_ptr), 1, int(raw)
     else:
         a = np.ascontiguousarray(raw).view(np.uint8)
         ptr, on_dev, nbytes = a.ctypes.data_as(C.c_void_p), 0, a.nbytes
-    check(ctx._lib.l1rxg_search_grid(ctx.handle, fmt, ptr, on_dev, nbytes, fs, if_hz, n_blocks,
-                                     prns.ctypes.data_as(C.POINTER(C.c_int32)), prns.size,
-                                     bins.ctypes.data_as(_dp), bins.size, spc, nd,
-                                     plane.ctypes.data_as(_dp)))
-    return plane
+    if out_device_ptr is not None:
+        dst, dst_dev, plane = C.c_void_p(out_device_ptr), 1, None
+    else:
+        plane = out if out is not None else np.zeros((prns.size, bins.size, nd), np.float32 if f32 else np.float64)
+        if plane.dtype != (np.float32 if f32 else np.float64) or plane.size != prns.size * bins.size * nd:
+            raise ValueError("out: wrong dtype or size")
+        dst, dst_dev = C.c_void_p(plane.ctypes.data), 0
+    check(ctx._lib.l1rxg_search_grid_ex(ctx.handle, fmt, ptr, on_dev, nbytes, fs, if_hz, n_blocks,
+                                        prns.ctypes.data_as(C.c_void_p), prns.size,
+                                        bins.ctypes.data_as(C.c_void_p), bins.size, spc, nd, dst, int(f32),
+                                        dst_dev))
+    return plane.reshape(prns.size, bins.size, nd) if plane is not None else None
 
 
 def search_grid_timing(ctx: "Context"):
