@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         hr += z.x;
                         hi += z.y;
                     }
-#ifdef L1RXG_SEG_SELCOMB  // experiment switch: the tap combine by register selects
+#ifndef L1RXG_SEG_LDSCOMB  // the tap combine by register selects (measured faster than the LDS variant below)
     #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int code = (int)(w >> (10 + 2 * t)) & 3;
@@ -861,11 +861,11 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
     #endif
                     }
 #else
-                    // the tap combine: v0..v3 go to this lane's own row of the
-                    // consumed unit buffer (thread-private scratch; slot (4 i +
-                    // lane) mod 16 puts a warp's 8-byte accesses on two wavefronts)
-                    // and every tap loads its value by code -- one LDS.64 per tap
-                    // instead of three float2 selects
+                    // experiment (L1RXG_SEG_LDSCOMB, measured -1.7 %): v0..v3 go to
+                    // this lane's own row of the consumed unit buffer (thread-private
+                    // scratch; slot (4 i + lane) mod 16 puts a warp's 8-byte accesses
+                    // on two wavefronts) and every tap loads its value by code -- one
+                    // LDS.64 per tap instead of three float2 selects
                     {
                         unsigned char* rowv = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES + lane * 128;
                         *reinterpret_cast<float2*>(rowv + ((lane + 0) & 15) * 8) = v0;
