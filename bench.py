@@ -515,8 +515,7 @@ def batch_e2e(ctx, raw, recs, inits, cstream, taps, cfg, fs, n, blocks, chunk_b,
     for c in range(n_chunks):
         a, b = c * cb, min((c + 1) * cb, blocks * n * 4)
         buf = ctx.host_alloc(e2e_recs * (b - a)).reshape(e2e_recs, b - a)
-        for j in range(e2e_recs):  # row by row: a strided device slice would stage a device copy
-            torch.from_numpy(buf[j]).copy_(raw[j, a:b])
+        torch.from_numpy(buf).copy_(raw[:e2e_recs, a:b])  # one D2H per chunk (a device-side gather first)
         chunks.append(buf)
     torch.cuda.synchronize()
     t_fill = time.perf_counter() - t_fill

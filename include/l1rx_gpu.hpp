@@ -108,7 +108,9 @@ inline CorrelatorOutputs correlate_epoch_gpu(std::span<const cplx> view, Channel
 }
 
 // ChannelState <-> l1rxg_channel (NavDecodeState stays on the host).
-inline l1rxg_channel to_c(const ChannelState& ch) {
+// window_ms > L1RXG_WIN_MAX: the C/N0 window travels as its running sums
+// (see l1rxg_channel in l1rxg.h), accumulated in the reference's order
+inline l1rxg_channel to_c(const ChannelState& ch, int window_ms = 0) {
     l1rxg_channel p;
     std::memset(&p, 0, sizeof p);
     p.prn = ch.prn;
@@ -137,6 +139,19 @@ inline l1rxg_channel to_c(const ChannelState& ch) {
     p.metrics_valid = ch.metrics_valid;
     p.sample_offset_next_epoch = ch.sample_offset_next_epoch;
     p.win_len = static_cast<int32_t>(ch.win_ip.size());
+    if (window_ms > L1RXG_WIN_MAX) {
+        double nbi = 0, nbq = 0, wbp = 0;
+        for (std::size_t k = 0; k < ch.win_ip.size(); ++k) {
+            const double sg = ch.win_ip[k] >= 0 ? 1.0 : -1.0;
+            nbi += sg * ch.win_ip[k];
+            nbq += sg * ch.win_qp[k];
+            wbp += ch.win_ip[k] * ch.win_ip[k] + ch.win_qp[k] * ch.win_qp[k];
+        }
+        p.win_ip[0] = nbi;
+        p.win_qp[0] = nbq;
+        p.win_ip[1] = wbp;
+        return p;
+    }
     for (std::size_t k = 0; k < ch.win_ip.size() && k < L1RXG_WIN_MAX; ++k) {
         p.win_ip[k] = ch.win_ip[k];
         p.win_qp[k] = ch.win_qp[k];
@@ -144,7 +159,10 @@ inline l1rxg_channel to_c(const ChannelState& ch) {
     return p;
 }
 
-inline void from_c(const l1rxg_channel& p, ChannelState& ch) {
+// window_ms > L1RXG_WIN_MAX: the device state holds the open window's sums,
+// not its samples, so the reference-side window restarts empty (its C/N0
+// estimate resumes at the next full window)
+inline void from_c(const l1rxg_channel& p, ChannelState& ch, int window_ms = 0) {
     ch.state = static_cast<ChannelRunState>(p.state);
     ch.code_phase_chips = p.code_phase_chips;
     ch.code_freq_hz = p.code_freq_hz;
@@ -169,6 +187,11 @@ inline void from_c(const l1rxg_channel& p, ChannelState& ch) {
     ch.lock_fail_count = p.lock_fail_count;
     ch.metrics_valid = p.metrics_valid;
     ch.sample_offset_next_epoch = p.sample_offset_next_epoch;
+    if (window_ms > L1RXG_WIN_MAX) {
+        ch.win_ip.clear();
+        ch.win_qp.clear();
+        return;
+    }
     ch.win_ip.assign(p.win_ip, p.win_ip + p.win_len);
     ch.win_qp.assign(p.win_qp, p.win_qp + p.win_len);
 }
@@ -194,7 +217,8 @@ public:
         d.cfg = to_c(cfg);
         std::vector<l1rxg_channel> c;
         for (const auto& ch : chans)
-            c.push_back(to_c(ch));
+            c.push_back(to_c(ch, cfg.cn0_window_ms));
+        window_ms_ = cfg.cn0_window_ms;
         std::vector<int32_t> s(chans.size(), 0);
         check(l1rxg_tracker_create(context(), &d, c.data(), s.data(), &trk_));
         n_ = chans.size();
@@ -212,7 +236,7 @@ public:
         out.resize(n_);
         for (std::size_t k = 0; k < n_; ++k) {
             out[k].prn = c[k].prn;
-            from_c(c[k], out[k]);
+            from_c(c[k], out[k], window_ms_);
         }
     }
     std::vector<l1rxg_epoch_record> records(int channel, int64_t e0, int64_t count) {
@@ -223,6 +247,7 @@ public:
 
 private:
     l1rxg_tracker* trk_ = nullptr;
+    int window_ms_ = 0;
     std::size_t n_ = 0;
 };
 

@@ -122,7 +122,11 @@ typedef struct {
 
 /* Full ChannelState (tracking.hpp:177-207) as POD, minus NavDecodeState
  * (host-side consumer) and KernelScratch.  The C/N0
- * window vectors (tracking.hpp:203) are a fixed array of win_len entries. */
+ * window vectors (tracking.hpp:203) are a fixed array of win_len entries;
+ * for cn0_window_ms > L1RXG_WIN_MAX the window carries its running sums
+ * instead (win_ip[0] = sum sign(ip) ip, win_qp[0] = sum sign(ip) qp,
+ * win_ip[1] = sum ip^2 + qp^2 over its win_len epochs, accumulated in push
+ * order -- the reference's sums bit for bit). */
 typedef struct {
     int32_t prn;
     int32_t state; /* l1rxg_run_state */

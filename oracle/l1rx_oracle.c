@@ -335,18 +335,44 @@ void orc_update_quality_metrics(l1rxg_channel* ch, const l1rxg_corr* o,
     const double clr = pwr > 0 ? (o->ip * o->ip - o->qp * o->qp) / pwr : 0.0;
     const double alpha = 1.0 / (double)cfg->cn0_window_ms;
     ch->carrier_lock_ratio += alpha * (clr - ch->carrier_lock_ratio);
-    ch->win_ip[ch->win_len] = o->ip;
-    ch->win_qp[ch->win_len] = o->qp;
-    ch->win_len++;
     const int m = cfg->cn0_window_ms;
-    if (ch->win_len >= m) {
-        double nbi = 0, nbq = 0, wbp = 0;
-        for (int k = 0; k < m; ++k) {
-            const double sg = ch->win_ip[k] >= 0 ? 1.0 : -1.0;
-            nbi += sg * ch->win_ip[k];
-            nbq += sg * ch->win_qp[k];
-            wbp += ch->win_ip[k] * ch->win_ip[k] + ch->win_qp[k] * ch->win_qp[k];
+    double nbi = 0, nbq = 0, wbp = 0;
+    int full = 0;
+    if (m <= L1RXG_WIN_MAX) {
+        ch->win_ip[ch->win_len] = o->ip;
+        ch->win_qp[ch->win_len] = o->qp;
+        ch->win_len++;
+        if (ch->win_len >= m) {
+            for (int k = 0; k < m; ++k) {
+                const double sg = ch->win_ip[k] >= 0 ? 1.0 : -1.0;
+                nbi += sg * ch->win_ip[k];
+                nbq += sg * ch->win_qp[k];
+                wbp += ch->win_ip[k] * ch->win_ip[k] + ch->win_qp[k] * ch->win_qp[k];
+            }
+            full = 1;
         }
+    } else {
+        /* windows longer than the POD's arrays: the same sums accumulated in
+           push order (win_ip[0], win_qp[0], win_ip[1]) -- the reference's
+           loop over the window vectors sums in exactly this order */
+        if (ch->win_len > 0) {
+            nbi = ch->win_ip[0];
+            nbq = ch->win_qp[0];
+            wbp = ch->win_ip[1];
+        }
+        const double sg = o->ip >= 0 ? 1.0 : -1.0;
+        nbi += sg * o->ip;
+        nbq += sg * o->qp;
+        wbp += o->ip * o->ip + o->qp * o->qp;
+        ch->win_len++;
+        full = ch->win_len >= m;
+        if (!full) {
+            ch->win_ip[0] = nbi;
+            ch->win_qp[0] = nbq;
+            ch->win_ip[1] = wbp;
+        }
+    }
+    if (full) {
         ch->win_len = 0;
         const double mu = wbp > 0 ? (nbi * nbi + nbq * nbq) / wbp : 0.0;
         ch->mu_smoothed = ch->metrics_valid ? ch->mu_smoothed + 0.2 * (mu - ch->mu_smoothed) : mu;

@@ -58,10 +58,22 @@ def pre_state(init: abi.Channel, recs, k: int, win: int) -> abi.Channel:
     ch.metrics_valid = 1 if (init.metrics_valid or total >= win) else 0
     wl = total % win
     ch.win_len = wl
-    for j in range(wl):
-        src = recs[k - wl + j] if k - wl + j >= 0 else None
-        ch.win_ip[j] = float(src["ip"]) if src is not None else init.win_ip[j]
-        ch.win_qp[j] = float(src["qp"]) if src is not None else init.win_qp[j]
+    if win <= len(ch.win_ip):
+        for j in range(wl):
+            src = recs[k - wl + j] if k - wl + j >= 0 else None
+            ch.win_ip[j] = float(src["ip"]) if src is not None else init.win_ip[j]
+            ch.win_qp[j] = float(src["qp"]) if src is not None else init.win_qp[j]
+    elif wl > 0:  # longer windows carry their running sums (loop_metrics), rebuilt in push order
+        if k - wl < 0:
+            raise ValueError("replay of a long C/N0 window needs the records since the window opened")
+        nbi = nbq = wbp = 0.0
+        for j in range(wl):
+            ip, qp = float(recs[k - wl + j]["ip"]), float(recs[k - wl + j]["qp"])
+            sg = 1.0 if ip >= 0 else -1.0
+            nbi += sg * ip
+            nbq += sg * qp
+            wbp += ip * ip + qp * qp
+        ch.win_ip[0], ch.win_qp[0], ch.win_ip[1] = nbi, nbq, wbp
     ch.sample_offset_next_epoch = int(cur["sample_offset_start"])
     return ch
 

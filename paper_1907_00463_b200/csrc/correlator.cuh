@@ -717,19 +717,42 @@ __device__ void loop_metrics(l1rxg_channel& ch, const l1rxg_corr& o, const LoopC
     const double pwr = __dadd_rn(ii, qq);
     const double clr = pwr > 0 ? __ddiv_rn(__dsub_rn(ii, qq), pwr) : 0.0;
     clr_s = __dadd_rn(clr_s, __dmul_rn(lc.alpha, __dsub_rn(clr, clr_s)));
-    ch.win_ip[win_len] = o.ip;
-    ch.win_qp[win_len] = o.qp;
-    win_len++;
     const int m = cfg.cn0_window_ms;
-    if (win_len >= m) {
-        double nbi = 0, nbq = 0, wbp = 0;
-        for (int k = 0; k < m; ++k) {
-            const double wi = ch.win_ip[k], wq = ch.win_qp[k];
-            const double sg = wi >= 0 ? 1.0 : -1.0;
-            nbi = __dadd_rn(nbi, __dmul_rn(sg, wi));
-            nbq = __dadd_rn(nbq, __dmul_rn(sg, wq));
-            wbp = __dadd_rn(wbp, __dadd_rn(__dmul_rn(wi, wi), __dmul_rn(wq, wq)));
+    double nbi = 0, nbq = 0, wbp = 0;
+    bool full = false;
+    if (m <= L1RXG_WIN_MAX) {  // the window's samples, summed when it is full
+        ch.win_ip[win_len] = o.ip;
+        ch.win_qp[win_len] = o.qp;
+        win_len++;
+        if (win_len >= m) {
+            for (int k = 0; k < m; ++k) {
+                const double wi = ch.win_ip[k], wq = ch.win_qp[k];
+                const double sg = wi >= 0 ? 1.0 : -1.0;
+                nbi = __dadd_rn(nbi, __dmul_rn(sg, wi));
+                nbq = __dadd_rn(nbq, __dmul_rn(sg, wq));
+                wbp = __dadd_rn(wbp, __dadd_rn(__dmul_rn(wi, wi), __dmul_rn(wq, wq)));
+            }
+            full = true;
         }
+    } else {  // longer windows: the same sums accumulated in push order (bit-identical)
+        if (win_len > 0) {
+            nbi = ch.win_ip[0];
+            nbq = ch.win_qp[0];
+            wbp = ch.win_ip[1];
+        }
+        const double sg = o.ip >= 0 ? 1.0 : -1.0;
+        nbi = __dadd_rn(nbi, __dmul_rn(sg, o.ip));
+        nbq = __dadd_rn(nbq, __dmul_rn(sg, o.qp));
+        wbp = __dadd_rn(wbp, __dadd_rn(__dmul_rn(o.ip, o.ip), __dmul_rn(o.qp, o.qp)));
+        win_len++;
+        full = win_len >= m;
+        if (!full) {
+            ch.win_ip[0] = nbi;
+            ch.win_qp[0] = nbq;
+            ch.win_ip[1] = wbp;
+        }
+    }
+    if (full) {
         win_len = 0;
         const double mu =
             wbp > 0 ? __ddiv_rn(__dadd_rn(__dmul_rn(nbi, nbi), __dmul_rn(nbq, nbq)), wbp) : 0.0;

@@ -474,8 +474,6 @@ int validate_cfg(const l1rxg_tracking_cfg* c) {
         return set_err(L1RXG_EINVAL, "only 1 ms epochs are supported");
     if (c->cn0_window_ms < 2)
         return set_err(L1RXG_EINVAL, "cn0_window_ms must be >= 2");
-    if (c->cn0_window_ms > L1RXG_WIN_MAX)
-        return set_err(L1RXG_EINVAL, "cn0_window_ms must be <= 64 on the GPU path");
     return 0;
 }
 
@@ -949,7 +947,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         if (!(chans[k].code_phase_chips >= 0.0) || !(chans[k].code_phase_chips < 1023.0) ||
             !(chans[k].code_freq_hz > 0) || !(chans[k].code_freq_hz < 1.1 * CHIP_RATE_HZ))
             return set_err(L1RXG_EINVAL, "channel code NCO out of domain");
-        if (chans[k].win_len < 0 || chans[k].win_len >= d->cfg.cn0_window_ms)
+        if (chans[k].win_len < 0 || chans[k].win_len >= d->cfg.cn0_window_ms)  // (sums mode: any count < m)
             return set_err(L1RXG_EINVAL, "channel C/N0 window length out of range");
     }
     CK(cudaSetDevice(c->device));

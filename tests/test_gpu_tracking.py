@@ -700,3 +700,33 @@ def test_segment_quarter_grid_start_chips_bit_identical(ctx, oracle_mod, monkeyp
     x = oracle_mod.ingest(dev.cpu().numpy()[0], abi.FMT_INT16_IQ, fs)
     replay_check(oracle_mod, inits[1], out[0][1][0], x, n, abi.TrackingCfg.default(), taps, fs,
                  tap_sums=out[0][1][1])
+
+
+@pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SEGMENT])
+def test_long_cn0_window_replay(ctx, oracle_mod, cta_mode):
+    """cn0_window_ms beyond the POD's 64-entry window arrays (the reference
+    allows any value >= 2, tracking.hpp:55-56): the device carries the window
+    as running sums accumulated in push order; every epoch replays against the
+    oracle (whose own window equals the reference's, test_oracle.py), C/N0 and
+    the lock-fail counting included."""
+    cfg = abi.TrackingCfg.default()
+    cfg.cn0_window_ms = 100
+    if cta_mode == abi.CTA_SEGMENT:
+        fs, n, fmt, tag = 65.472e6, 65472, abi.FMT_INT16_IQ, "int16_iq"
+        taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+        ms = 260
+    else:
+        fs, n, fmt, tag = IF_FS, 16368, abi.FMT_INT8_REAL_IF, "int8_real_if"
+        taps = abi.Taps.epl(0.5)
+        ms = 400
+    sv = ss.Sv(prn=11, cn0_dbhz=44.0, doppler_hz=-1800.0, delay_chips=222.2)
+    raw = _raw(ms, fs, [sv], tag, IF_HZ if tag == "int8_real_if" else 0.0, seed=91)
+    init = _init(sv, fs)
+    trk = Tracker(ctx, fmt, fs, IF_HZ if tag == "int8_real_if" else 0.0, [init], taps=taps, cfg=cfg,
+                  ring_samples=(ms + 8) * n, max_records=ms, cta_mode=cta_mode)
+    trk.push(0, raw)
+    trk.run()
+    recs, ts = trk.records(0, tap_sums=True)
+    assert len(recs) >= ms - 2 and np.count_nonzero(recs["cn0_dbhz"]) > 0
+    x = oracle_mod.ingest(raw, fmt, fs, IF_HZ if tag == "int8_real_if" else 0.0)
+    replay_check(oracle_mod, init, recs, x, n, cfg, taps, fs, tap_sums=ts)

@@ -265,9 +265,12 @@ def test_init_channel_equals_reference(orc):
         assert bytes(a) == bytes(b) == bytes(c)
 
 
-def test_closed_loop_equals_reference(orc):
+@pytest.mark.parametrize("window_ms", [20, 100])
+def test_closed_loop_equals_reference(orc, window_ms):
     """track_epoch restatement vs the reference over a 1.5 s closed loop
-    (test_tracking.cpp:403-417 scenario)."""
+    (test_tracking.cpp:403-417 scenario); at cn0_window_ms = 100 the
+    restatement carries the window as running sums (longer than the POD's
+    64-entry arrays, l1rxg.h) and must still equal the reference's vectors."""
     need_ref(orc)
     fs = 2.048e6
     sig = orc.ref_sim_baseband([dict(prn=7, cn0=45, doppler=320.0, delay_chips=100.25)], 1.5, fs,
@@ -275,6 +278,7 @@ def test_closed_loop_equals_reference(orc):
     b = int(round(100.25 / 1.023e6 * fs))
     ch = orc.init_channel(7, 0.0, 0, b - 1, 0, fs, "ref")
     cfg = abi.TrackingCfg.default()
+    cfg.cn0_window_ms = window_ms
     _, r = orc.ref_track_buffer(ch, sig, 2048, cfg, fs, kernel=0)
     _, done, p, _ = orc.track_run([ch], [0], [sig], 2048, cfg, abi.Taps.epl(0.5), fs, 2000)
     p = p[0][: done[0]]
