@@ -318,6 +318,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     } else {
         // ---- work warps: correlation of epoch e, then phase A' of epoch e+1
         for (;;) {
+            if (tid == 0)
+                PROF_STAMP(0);  // (profiling builds: CTA 0, thread 0's stage clocks per epoch)
             const int b = e & 1;
             const EpochConsts cc = s->c;
             EpochConsts c = cc;
@@ -348,12 +350,20 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
                     ovl_run_totals<T>(c, s->ct, s->d, a.kp, i0, cnt, ptot[tid], mtot[tid], pm0 + tid * RUN,
                                       mm0 + tid * RUN, dw, acc, &anchors[tid]);
             }
+            if (tid == 0)
+                PROF_STAMP(1);
             named_bar_sync(1, nwork);  // anchors visible
+            if (tid == 0)
+                PROF_STAMP(2);
             ovl_phase_b<T>(pb, c, pm0, mm0, anchors, s->ct, u0, len, dw);
             phase_b_fold<T>(pb, acc);
+            if (tid == 0)
+                PROF_STAMP(3);
             warp_partials<V>(acc, s->red, lane, warp);
             named_bar_sync(1, nwork);  // tile b consumed; partials written
             named_bar_arrive(2, nthr);  // X
+            if (tid == 0)
+                PROF_STAMP(4);
             if (tid == 0) {  // the copy of epoch e+2 into tile b, after X (off the update's path)
                 s->inflight[b] = 0;
                 try_issue(e + 2);
@@ -366,7 +376,13 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
                 if (tid == 0)
                     wp[b ^ 1] = cc.w;
             }
+            if (tid == 0)
+                PROF_STAMP(5);
             named_bar_sync(3, nthr);  // Y
+            if (tid == 0)
+                PROF_STAMP(6);
+            if (tid == 0)
+                PROF_STAMP(7);
             if (s->stop || !next_ok)
                 break;
             ++e;
