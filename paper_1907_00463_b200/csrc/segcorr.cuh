@@ -81,6 +81,11 @@ struct __align__(64) SegArgs {
 };
 
 template <int T>
+struct SegEntry {
+    typedef typename std::conditional<(3 * T + 10 <= 32), uint32_t, unsigned long long>::type type;
+};
+
+template <int T>
 struct SegSmem {
     l1rxg_channel ch;
     EpochConsts c;
@@ -112,6 +117,10 @@ struct SegSmem {
     // a run's first sample, for qq = floor(4 frac(ph)) and c = the chips at
     // floor(ph) - 1 .. + 1 (bits 0..2)
     uint8_t qlut[32];
+    // step-table entry pieces of a step at run position q: bits 0-7 the
+    // capture-position field, bits 8-9 the tap code (q = 0: no entry); tap k's
+    // entry is (entq & 0xff) | (entq >> 8) << (10 + 2 k)
+    uint16_t entq[32];
 };
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
@@ -122,10 +131,6 @@ struct SegSmem {
 //               every tap stepping in that half takes the slow path
 //   bits 10+2k..: tap k's step in the run: 0 none, 1 at 16, 2 at q0, 3 at q1
 //   bit 10+2T+k: tap k takes the exact slow path in this run (two steps)
-template <int T>
-struct SegEntry {
-    typedef typename std::conditional<(3 * T + 10 <= 32), uint32_t, unsigned long long>::type type;
-};
 // runs per epoch table: every row a unit of the epoch can cover
 __host__ __device__ constexpr int seg_table_runs(int n) { return (((n + 62) >> 5) + 31) / 32 * 32; }
 
@@ -266,10 +271,17 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
                 Bs = __ffma2_rn(make_float2(yi, yr), make_float2(bs[t], -bs[t]), Bs);
             }
 #else
+#ifdef L1RXG_SEG_CAP1  // experiment switch: a capture compare at every position
             if (j > 0 && j == q0)
                 C0 = A;
             if (j > 0 && j + 16 == q1)
                 C1 = B;
+#else  // captures at even positions only (the odd ones add their last sample after the run)
+            if ((j & 1) == 0 && j > 0 && j == (q0 & ~1))
+                C0 = A;
+            if ((j & 1) == 0 && j > 0 && j + 16 == (q1 & ~1))
+                C1 = B;
+#endif
             A = seg_mac(A, seg_re(xa), seg_im(xa), ac[t], as[t]);
             B = seg_mac(B, seg_re(xb), seg_im(xb), bc[t], bs[t]);
 #endif
@@ -280,6 +292,19 @@ __device__ __forceinline__ void seg_run(const unsigned char* buf, int lane, cons
     B = make_float2(B.x + Bs.x, B.y + Bs.y);
     C0 = make_float2(C0.x + C0s.x, C0.y + C0s.y);
     C1 = make_float2(C1.x + C1s.x, C1.y + C1s.y);
+#endif
+#if !defined(L1RXG_SEG_CAP1) && !defined(L1RXG_SEG_SPLIT2)
+    {  // odd capture positions: P(q) = P(q - 1) + the rotated sample q - 1 (masked like the run)
+        const int ja = (q0 - 1) & 15, jb = 16 + ((q1 - 1) & 15);
+        uint32_t xa = seg_sample(buf, lane, ja), xb = seg_sample(buf, lane, jb);
+        xa = (q0 & 1) && (!MASK || (ja >= jlo && ja < jhi)) ? xa : 0u;
+        xb = (q1 & 1) && (!MASK || (jb >= jlo && jb < jhi)) ? xb : 0u;
+        const float4 r2 = rot4[ja >> 1], r3 = rot4[jb >> 1];
+        const float ca = (ja & 1) ? r2.z : r2.x, sa = (ja & 1) ? r2.w : r2.y;
+        const float cb = (jb & 1) ? r3.z : r3.x, sb = (jb & 1) ? r3.w : r3.y;
+        C0 = seg_mac(C0, seg_re(xa), seg_im(xa), ca, sa);
+        C1 = seg_mac(C1, seg_re(xb), seg_im(xb), cb, sb);
+    }
 #endif
     p16 = A;
     c0 = C0;
@@ -477,17 +502,31 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         if (i < 0)
             i += nthr;
         pre += cnt;
+        // transition g = g0 + i is chip p * 1023 + tm[gp], gp = g - p * L,
+        // advanced incrementally (nthr < L: at most one period per step)
+        int p = (int)(((float)(g0 + i) + 0.5f) * inv_L);
+        int gp = g0 + i - p * L;
         for (; i < cnt; i += nthr) {
-            const int g = g0 + i;
-            const int p = (int)(((float)g + 0.5f) * inv_L);
-            const int m = p * 1023 + s->tm[g - p * L];
+            const int m = p * 1023 + s->tm[gp];
             const double e = ((double)m + off) * c.inv_cps;
             const double dist = fabs(e - rint(e));
             const bool tie = !(dist > 1e-9);
             const int b = tie ? tap_boundary(m, dk, c, 1, n - 1) : __double2loint(__dadd_ru(e, 6755399441055744.0));
             // checked within 1e-7 of a tie: steps of one residue differ in e by
             // ~1e-11, so a step near a tie and its partner are both checked
-            seg_enter<T>(tab, b + lead, k, !(dist > 1e-7) || !fast_geom);
+            const int pos = b + lead;
+            if (!(dist > 1e-7) || !fast_geom)
+                seg_enter<T>(tab, pos, k, true);
+            else if (pos & 31) {
+                typedef typename SegEntry<T>::type E;
+                const uint32_t eq = s->entq[pos & 31];
+                atomicOr(&tab[pos >> 5], (E)(eq & 0xffu) | ((E)(eq >> 8) << (10 + 2 * k)));  // result unused: RED
+            }
+            gp += nthr;
+            if (gp >= L) {
+                gp -= L;
+                ++p;
+            }
         }
     }
 #endif
@@ -546,6 +585,14 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             pat |= ((uint32_t)(c3 >> (1 + ((qq + D) >> 2))) & 1u) << t;
         }
         s->qlut[tid] = (uint8_t)pat;
+    }
+    if (tid < 32) {  // step-table entry pieces by position (seg_enter's fields)
+        const int q = tid;
+        const int h = q >> 4 & (q != 16);
+        const bool mid = q == 16;
+        const uint32_t qf = mid ? 0u : (uint32_t)(q & 15) << (4 * h);
+        const uint32_t code = mid ? 1u : 2u + (uint32_t)h;
+        s->entq[q] = q == 0 ? (uint16_t)0 : (uint16_t)(qf | (code << 8));
     }
     for (int r = tid; r < truns; r += blockDim.x)
         tab[r] = 0;  // every later epoch leaves the table clean (owners clear their entries)
