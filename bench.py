@@ -372,6 +372,29 @@ def run_grid(args, rank, world, local, dist):
         r = pick_peak(full[int(p) - 1], bins, fs, prn=int(p))
         det.append({"prn": int(p), "bin_hz": r.doppler_hz, "delay_chips": r.code_delay_chips,
                     "ratio": round(float(r.ratio), 2), "detected": bool(r.detected)})
+    # untimed parity: the full plane against the reference's own acquire_pcs
+    # plane (acquisition.hpp over cuFFTW) at three bins of three PRNs (two
+    # present, one absent), within 1e-5 of the largest cell
+    parity = None
+    if not args.no_parity:
+        try:
+            import oracle
+            if oracle.acq_available():
+                t0p = time.perf_counter()
+                x = oracle.ingest(raw.cpu().numpy(), abi.FMT_INT8_REAL_IF, fs, g["if_hz"])
+                absent = next(p for p in range(1, 33) if p not in set(int(q) for q in prns_sv))
+                worst = 0.0
+                for sv_i, p in ((0, int(prns_sv[0])), (1, int(prns_sv[1])), (None, absent)):
+                    k = int(np.argmin(np.abs(bins - svs[sv_i].doppler_hz))) if sv_i is not None else 20
+                    sel = sorted({max(0, min(bins.size - 1, k + o)) for o in (-1, 0, 1)})
+                    want = oracle.ref_pcs_plane(x, blocks, p, fs, bins[sel])[:, ::8]
+                    worst = max(worst, float(np.abs(full[p - 1][sel] - want).max() / want.max()))
+                parity = {"ok": worst <= 1e-5, "worst_cell": worst, "tolerance": 1e-5,
+                          "sample": "3 bins x 3 PRNs (2 present, 1 absent) of the full 32-PRN plane",
+                          "reference": "acquire_pcs plane, acquisition.hpp + fft.hpp over cuFFTW",
+                          "seconds": round(time.perf_counter() - t0p, 1)}
+        except Exception as ex:  # reported, not fatal
+            parity = {"ok": None, "error": repr(ex)}
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
     path = os.environ.get("L1RXG_GRID", "mma")
@@ -423,7 +446,8 @@ def run_grid(args, rank, world, local, dist):
             "e2e": {"value": direct_st / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(nbytes) * world,
                     "d2h_bytes_per_step": int(full.size * 4)},
-            "detections": det, "gpu_launches": launches * args.steps, "clocks": clk, "grid_path": path}
+            "detections": det, "gpu_launches": launches * args.steps, "clocks": clk, "grid_path": path,
+            "parity": parity}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -862,6 +886,7 @@ def companion_latency(args, local):
     a = copy.copy(args)
     a.blocks, a.steps, a.warmup = 0, 3, 3
     a.no_cpu_baseline = True
+    a.no_parity = True
     try:
         torch.cuda.empty_cache()
         ln = run_stream(a, 2, 0, 1, local, None, emit=False)
@@ -918,6 +943,35 @@ def main():
     if args.config == 4:
         return run_batch(args, rank, world, local, dist)
     return run_stream(args, args.config, rank, world, local, dist)
+
+
+def stream_parity(trk, raw, inits, fmt, if_hz, n, fs, cfg, taps, every=25, head=200):
+    """Untimed in-bench parity for configs 1-3 (oracle/replay.py): every
+    `every`-th epoch of every channel plus the first `head` epochs of channel
+    0, re-run by the CPU oracle from the GPU's own pre-state (sums 1e-5 x
+    max|E/P/L| and every tap, NCO advance bit-exact, loop outputs 1e-5)."""
+    import oracle
+    from oracle.replay import replay_channel
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    x = oracle.ingest(raw.cpu().numpy(), fmt, fs, if_hz)
+    got = {c: trk.records(c, tap_sums=True) for c in range(len(inits))}
+
+    def one(c):
+        recs, ts = got[c]
+        ks = sorted(set(range(0, len(recs), every)) | (set(range(min(head, len(recs)))) if c == 0 else set()))
+        return replay_channel(oracle, inits[c], recs, x, n, cfg, taps, fs, tap_sums=ts, epochs=ks) + (len(ks),)
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        res = list(ex.map(one, range(len(inits))))
+    worst = {k: max(r[0][k] for r in res) for k in ("sums", "taps", "loop", "cn0")}
+    n_bad = sum(r[1] for r in res)
+    ok = worst["sums"] <= 1e-5 and worst["taps"] <= 1e-5 and worst["loop"] <= 1e-5 and n_bad == 0
+    return {"ok": bool(ok), "checked_channel_epochs": int(sum(r[3] for r in res)),
+            "sample": f"every {every}th epoch of every channel + epochs 0-{head - 1} of channel 0",
+            "worst_sum": worst["sums"], "worst_tap_sum": worst["taps"], "worst_loop": worst["loop"],
+            "exact_field_mismatches": n_bad, "first_mismatch": next((r[2] for r in res if r[2]), None),
+            "tolerance": {"sums": 1e-5, "loop": 1e-5, "nco": "bit-exact"},
+            "seconds": round(time.perf_counter() - t0, 1)}
 
 
 def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
@@ -1138,6 +1192,11 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     bytes_per_sample = {"int8_real_if": 1, "int16_iq": 4}[c["fmt"]]
     alg_bytes = blocks * n * (8 if real_if else bytes_per_sample)  # track_kernel reads the baseband
 
+    # ---- untimed parity: oracle replay of a deterministic sample of epochs
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = stream_parity(trk, raw, inits, fmt, c["if_hz"], n, fs, cfg, taps)
+
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -1191,6 +1250,7 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
                      "hbm": {"achieved_gbs": alg_bytes / (track_launch_ms * 1e-3) / 1e9,
                              "peak_gbs": hbm_peak}},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": rec_bytes,
                 "path": "pinned host -> l1rxg_tracker_push (%d ms chunks, H2D overlapped with "
