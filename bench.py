@@ -551,7 +551,7 @@ def batch_e2e(ctx, raw, recs, inits, cstream, taps, cfg, fs, n, blocks, chunk_b,
     rec_pinned = ctx.host_alloc(rec_bytes)  # the step's records land in pinned host memory
 
     def step_e2e():
-        te.reset(inits[:nci])
+        te.reset()
         for buf in chunks:
             te.push_strided(buf)
             te.run()
@@ -659,7 +659,7 @@ def run_batch(args, rank, world, local, dist, emit=True):
         trk.attach_device(raw.data_ptr(), bytes_rec // 4, bytes_rec)
 
     def step_device():
-        trk.reset(inits)
+        trk.reset()
         if attached:
             trk.run()
             return
@@ -1070,7 +1070,7 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     nbytes = raw.numel()
 
     def step_device():
-        trk.reset(inits)
+        trk.reset()
         trk.push_device(0, raw.data_ptr(), nbytes)
         trk.run()
 
@@ -1124,7 +1124,7 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     rec_pinned = ctx.host_alloc(rec_bytes)  # the step's records land in pinned host memory
 
     def step_e2e():
-        trk.reset(inits)
+        trk.reset()
         for o in range(0, nbytes, chunk):
             trk.push(0, pinned[o:o + chunk])
             trk.run()

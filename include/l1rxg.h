@@ -331,7 +331,9 @@ int l1rxg_tracker_records_raw(l1rxg_tracker* trk, void* dst, int dst_is_device,
                               int64_t* bytes_out);
 /* Restarts every stream at sample 0 (empty ring, zero FIR history, like a
  * fresh SampleSource) and resets the channels to `channels` with zero epoch
- * counts: one more pass over a recording without reallocating. */
+ * counts: one more pass over a recording without reallocating.  channels ==
+ * NULL restores the channels given to l1rxg_tracker_create (a device-side
+ * copy: no host transfer). */
 int l1rxg_tracker_reset(l1rxg_tracker* trk, const l1rxg_channel* channels);
 /* The CUDA stream (cudaStream_t) the tracker's kernels run on, so a caller
  * can bracket work with its own events. */

@@ -564,7 +564,10 @@ struct l1rxg_tracker {
     std::vector<StreamRing> streams;
     unsigned char* d_ring = nullptr;
     int64_t* d_avail = nullptr;
+    unsigned char* d_hist = nullptr;  // every stream's FIR histories, one allocation (zeroed by reset)
+    size_t hist_bytes = 0;
     l1rxg_channel* d_chans = nullptr;
+    l1rxg_channel* d_chans0 = nullptr;  // the channels given at creation (reset(NULL) restores them)
     int32_t* d_chan_stream = nullptr;
     l1rxg_epoch_record* d_recs = nullptr;
     double* d_tapsums = nullptr;
@@ -1080,19 +1083,26 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             return set_err(rc, msg);
         }
     }
-    for (auto& r : t->streams) {
-        for (int k = 0; k < 2; ++k) {
-            if ((e = cudaMalloc(&r.hist8[k], 32)) != cudaSuccess ||
-                (e = cudaMalloc(&r.histf[k], 32 * sizeof(float2))) != cudaSuccess)
-                return fail(e);
-            cudaMemset(r.hist8[k], 0, 32);
-            cudaMemset(r.histf[k], 0, 32 * sizeof(float2));
+    {  // per stream: two int8 histories (32 B) and two float2 histories (256 B)
+        const size_t per = 2 * 32 + 2 * 32 * sizeof(float2);
+        t->hist_bytes = per * t->streams.size();
+        if ((e = cudaMalloc(&t->d_hist, t->hist_bytes)) != cudaSuccess)
+            return fail(e);
+        cudaMemset(t->d_hist, 0, t->hist_bytes);
+        for (size_t q = 0; q < t->streams.size(); ++q) {
+            unsigned char* b = t->d_hist + q * per;
+            auto& r = t->streams[q];
+            r.histf[0] = reinterpret_cast<float2*>(b);
+            r.histf[1] = reinterpret_cast<float2*>(b + 32 * sizeof(float2));
+            r.hist8[0] = reinterpret_cast<int8_t*>(b + 64 * sizeof(float2));
+            r.hist8[1] = reinterpret_cast<int8_t*>(b + 64 * sizeof(float2) + 32);
         }
     }
     const size_t C = static_cast<size_t>(std::max(1, d->n_channels));
     const size_t nrec = C * static_cast<size_t>(d->max_records);
     if ((e = cudaMalloc(&t->d_avail, 8 * t->streams.size())) != cudaSuccess ||
         (e = cudaMalloc(&t->d_chans, sizeof(l1rxg_channel) * C)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_chans0, sizeof(l1rxg_channel) * C)) != cudaSuccess ||
         (e = cudaMalloc(&t->d_chan_stream, 4 * C)) != cudaSuccess ||
         (e = cudaMalloc(&t->d_recs, sizeof(l1rxg_epoch_record) * nrec)) != cudaSuccess ||
         (e = cudaMalloc(&t->d_tapsums, sizeof(double) * 2 * t->T * nrec)) != cudaSuccess ||
@@ -1105,6 +1115,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     cudaMemset(t->d_status, 0, 4 * C);
     if (d->n_channels > 0) {
         cudaMemcpy(t->d_chans, chans, sizeof(l1rxg_channel) * d->n_channels, cudaMemcpyHostToDevice);
+        cudaMemcpy(t->d_chans0, chans, sizeof(l1rxg_channel) * d->n_channels, cudaMemcpyHostToDevice);
         cudaMemcpy(t->d_chan_stream, chan_stream, 4 * (size_t)d->n_channels, cudaMemcpyHostToDevice);
     }
     for (int k = 0; k < 2; ++k) {
@@ -1124,14 +1135,10 @@ int l1rxg_tracker_destroy(l1rxg_tracker* t) {
     cudaDeviceSynchronize();
     cudaFree(t->d_ring);
     cudaFree(t->d_segq);
-    for (auto& r : t->streams) {
-        for (int k = 0; k < 2; ++k) {
-            cudaFree(r.hist8[k]);
-            cudaFree(r.histf[k]);
-        }
-    }
+    cudaFree(t->d_hist);
     cudaFree(t->d_avail);
     cudaFree(t->d_chans);
+    cudaFree(t->d_chans0);
     cudaFree(t->d_chan_stream);
     cudaFree(t->d_recs);
     cudaFree(t->d_tapsums);
@@ -1585,7 +1592,7 @@ int l1rxg_tracker_records_raw(l1rxg_tracker* t, void* dst, int dst_is_device, in
 }
 
 int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
-    if (!t || (!chans && t->d.n_channels > 0))
+    if (!t)
         return set_err(L1RXG_EINVAL, "null argument");
     CK(cudaSetDevice(t->ctx->device));
     CK(cudaStreamSynchronize(t->ctx->copy));
@@ -1604,14 +1611,16 @@ int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
     for (auto& r : t->streams) {
         r.pushed = t->att_samples;  // attached: every recorded sample stays available
         r.hist_cur = 0;
-        for (int k = 0; k < 2; ++k) {
-            CK(cudaMemsetAsync(r.hist8[k], 0, 32, st));
-            CK(cudaMemsetAsync(r.histf[k], 0, 32 * sizeof(float2), st));
-        }
     }
-    if (t->d.n_channels > 0)
-        CK(cudaMemcpyAsync(t->d_chans, chans, sizeof(l1rxg_channel) * t->d.n_channels,
-                           cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(t->d_hist, 0, t->hist_bytes, st));  // every stream's FIR history, one memset
+    if (t->d.n_channels > 0) {
+        if (chans)
+            CK(cudaMemcpyAsync(t->d_chans, chans, sizeof(l1rxg_channel) * t->d.n_channels,
+                               cudaMemcpyHostToDevice, st));
+        else  // the creation-time channels, device to device
+            CK(cudaMemcpyAsync(t->d_chans, t->d_chans0, sizeof(l1rxg_channel) * t->d.n_channels,
+                               cudaMemcpyDeviceToDevice, st));
+    }
     CK(cudaStreamSynchronize(st));
     return 0;
 }

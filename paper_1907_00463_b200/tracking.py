@@ -359,8 +359,12 @@ class Tracker:
                                                   C.byref(nb)))
         return nb.value
 
-    def reset(self, channels) -> None:
-        """Restart all streams at sample 0 with fresh channel states."""
+    def reset(self, channels=None) -> None:
+        """Restart all streams at sample 0 with fresh channel states
+        (channels=None: the ones given at creation, restored on the device)."""
+        if channels is None:
+            check(self._lib.l1rxg_tracker_reset(self.handle, None))
+            return
         chans = list(channels)
         arr = (abi.Channel * max(1, len(chans)))(*chans)
         check(self._lib.l1rxg_tracker_reset(self.handle, arr))

@@ -669,6 +669,9 @@ def test_attach_refuses_pushes_and_detach_restores_ring(ctx):
     t.reset(inits)  # the attachment stays: same records again
     t.run()
     assert t.records(0).tobytes() == first.tobytes()
+    t.reset()  # the creation-time channels, restored on the device
+    t.run()
+    assert t.records(0).tobytes() == first.tobytes()
     t.detach()
     t.reset(inits)
     t.push(0, host[0])  # now into the ring: the same samples, the same records
