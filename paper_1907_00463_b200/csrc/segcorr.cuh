@@ -63,6 +63,10 @@ namespace l1rxg {
 constexpr int SEG_NW = L1RXG_SEG_NW;         // warps per CTA, all correlate
 constexpr int SEG_NT = 32 * SEG_NW;
 constexpr int SEG_NBUF = 2;                  // TMA buffers per work warp
+#ifndef L1RXG_SEG_FILL_UNR
+#define L1RXG_SEG_FILL_UNR 2
+#endif
+constexpr int SEG_FILL_UNR = L1RXG_SEG_FILL_UNR;  // step-table transitions located per fill iteration
 constexpr int SEG_UNIT_BYTES = 32 * 128;     // 32 rows x 32 cint16 samples
 constexpr int SEG_MIN_N = 32 * 32 * (SEG_NW - 1) + 1;  // every warp has >= 1 unit per epoch
 constexpr int SEG_TRANS_P = 576;             // transitions per code period (<= 544 for C/A codes)
@@ -99,6 +103,9 @@ struct SegSmem {
         long long pos;                // ring position of epoch e's first sample
         int e, k, nwu, e_adm;         // next unit: epoch, warp-unit, units of that epoch; admitted epochs
     } q[SEG_NW];
+#ifdef L1RXG_SEG_DYN
+    int ucnt[2];                      // units of epoch e claimed so far (ucnt[e & 1])
+#endif
     uint64_t pbar[2];                 // (cluster exchange: unused, csize == 1)
     l1rxg_epoch_record rec;
     int64_t rec_slot;
@@ -506,6 +513,51 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
         // advanced incrementally (nthr < L: at most one period per step)
         int p = (int)(((float)(g0 + i) + 0.5f) * inv_L);
         int gp = g0 + i - p * L;
+#ifndef L1RXG_SEG_FILL_SERIAL
+        // SEG_FILL_UNR transitions per iteration: the fp64 locate chains
+        // (LDS -> I2F.F64 -> DADD -> DMUL -> FRND -> DADD) of different
+        // transitions are independent, so they overlap instead of running
+        // back to back
+        for (; i < cnt; i += SEG_FILL_UNR * nthr) {
+            int m[SEG_FILL_UNR];
+            bool has[SEG_FILL_UNR];
+#pragma unroll
+            for (int u = 0; u < SEG_FILL_UNR; ++u) {
+                has[u] = i + u * nthr < cnt;
+                m[u] = p * 1023 + s->tm[gp];  // gp < L always: in bounds even past cnt
+                gp += nthr;
+                if (gp >= L) {
+                    gp -= L;
+                    ++p;
+                }
+            }
+            double dist[SEG_FILL_UNR];
+            int b[SEG_FILL_UNR];
+#pragma unroll
+            for (int u = 0; u < SEG_FILL_UNR; ++u) {
+                const double e = ((double)m[u] + off) * c.inv_cps;
+                dist[u] = fabs(e - rint(e));
+                b[u] = __double2loint(__dadd_ru(e, 6755399441055744.0));
+            }
+#pragma unroll
+            for (int u = 0; u < SEG_FILL_UNR; ++u) {
+                if (!has[u])
+                    break;
+                if (!(dist[u] > 1e-9))  // a tie: the reference expression decides
+                    b[u] = tap_boundary(m[u], dk, c, 1, n - 1);
+                // checked within 1e-7 of a tie: steps of one residue differ in e by
+                // ~1e-11, so a step near a tie and its partner are both checked
+                const int pos = b[u] + lead;
+                if (!(dist[u] > 1e-7) || !fast_geom)
+                    seg_enter<T>(tab, pos, k, true);
+                else if (pos & 31) {
+                    typedef typename SegEntry<T>::type E;
+                    const uint32_t eq = s->entq[pos & 31];
+                    atomicOr(&tab[pos >> 5], (E)(eq & 0xffu) | ((E)(eq >> 8) << (10 + 2 * k)));  // result unused: RED
+                }
+            }
+        }
+#else
         for (; i < cnt; i += nthr) {
             const int m = p * 1023 + s->tm[gp];
             const double e = ((double)m + off) * c.inv_cps;
@@ -528,6 +580,7 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
                 ++p;
             }
         }
+#endif
     }
 #endif
 }
@@ -630,6 +683,9 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             for (int q = 0; q < (int)(sizeof(l1rxg_channel) / 8); ++q)
                 dst[q] = __ldcg(src + q);
             s->pending = 0;
+#ifdef L1RXG_SEG_DYN
+            s->ucnt[0] = s->ucnt[1] = 0;
+#endif
         }
         __syncthreads();
         if (max_e <= 0 || s->stop) {  // past the launch's epoch budget (or the wait gave up)
@@ -706,6 +762,46 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
         }
         // lane 0 issues the warp's next unit (if admitted) and advances its
         // stream; the warp learns whether a copy was issued
+#ifdef L1RXG_SEG_DYN
+        // dynamic units: the warps of the CTA claim the units of an epoch
+        // from one shared counter (a warp that starts its runs late -- the
+        // control warp finishes the previous epoch first -- takes fewer), so
+        // the warps reach the end-of-runs barrier together.  ubuf0/ubuf1: the
+        // (epoch << 12 | unit) each of the warp's two buffers holds.
+        int ubuf0 = -1, ubuf1 = -1;
+        auto issue_one = [&]() -> bool {
+            int got = -1;
+            if (lane == 0) {
+                auto& Q = s->q[warp];
+                while (Q.e < Q.e_adm) {
+                    const int u = atomicAdd(&s->ucnt[Q.e & 1], 1);
+                    if (u < Q.nwu) {
+                        const int b = issued & (SEG_NBUF - 1);
+                        uint64_t* bar = &s->fbar[warp][b];
+                        mbar_expect_tx(bar, SEG_UNIT_BYTES);
+                        tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
+                                      (int)(Q.pos >> 5) + 32 * u, strm, bar);
+                        got = (Q.e << 12) | u;
+                        break;
+                    }
+                    ++Q.e;  // the epoch's units are all claimed: the next epoch's
+                    Q.pos += n;
+                    if (Q.pos >= R)
+                        Q.pos -= R;
+                    Q.nwu = (((((int)(Q.pos & 31)) + n + 31) >> 5) + 31) >> 5;
+                }
+            }
+            got = __shfl_sync(0xffffffffu, got, 0);
+            if (got < 0)
+                return false;
+            if (issued & 1)
+                ubuf1 = got;
+            else
+                ubuf0 = got;
+            ++issued;
+            return true;
+        };
+#else
         auto issue_one = [&]() -> bool {
             int ok = 0;
             if (lane == 0) {
@@ -732,6 +828,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             issued += ok;
             return ok != 0;
         };
+#endif
         if (warp < SEG_NW)
             while (issued < consumed + SEG_NBUF && issue_one()) {
             }
@@ -775,7 +872,18 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                 const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
                 bool snapped = false;
                 float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
+#ifdef L1RXG_SEG_DYN
+                (void)nwu;
+                for (;;) {
+                    if (consumed == issued && !issue_one())
+                        break;
+                    const int ub = (consumed & 1) ? ubuf1 : ubuf0;
+                    if ((ub >> 12) != e)  // the warp's next unit belongs to a later epoch
+                        break;
+                    const int k = ub & 4095;
+#else
                 for (int k = warp; k < nwu && !noop; k += SEG_NW) {
+#endif
                     const int r = 32 * k + lane;  // the lane's run: epoch run index
                     const int i0 = 32 * r - lead;  // epoch index of its first sample
                     const int jlo = max(0, -i0);
@@ -964,8 +1072,12 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
 #else
                 warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
 #endif
-                if (lane == 0)
+                if (lane == 0) {
                     s->c.inv_cps = fast_rcp(s->c.cps);
+#ifdef L1RXG_SEG_DYN
+                    s->ucnt[e & 1] = 0;  // epoch e + 2's counter (epoch e's claims all ended before the barrier)
+#endif
+                }
                 float sn, co;
                 sincosf((float)(s->c.w * (double)lane), &sn, &co);
                 s->rot[lane] = make_float2(co * scale, sn * scale);
