@@ -103,9 +103,6 @@ struct SegSmem {
         long long pos;                // ring position of epoch e's first sample
         int e, k, nwu, e_adm;         // next unit: epoch, warp-unit, units of that epoch; admitted epochs
     } q[SEG_NW];
-#ifdef L1RXG_SEG_DYN
-    int ucnt[2];                      // units of epoch e claimed so far (ucnt[e & 1])
-#endif
     uint64_t pbar[2];                 // (cluster exchange: unused, csize == 1)
     l1rxg_epoch_record rec;
     int64_t rec_slot;
@@ -683,9 +680,6 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             for (int q = 0; q < (int)(sizeof(l1rxg_channel) / 8); ++q)
                 dst[q] = __ldcg(src + q);
             s->pending = 0;
-#ifdef L1RXG_SEG_DYN
-            s->ucnt[0] = s->ucnt[1] = 0;
-#endif
         }
         __syncthreads();
         if (max_e <= 0 || s->stop) {  // past the launch's epoch budget (or the wait gave up)
@@ -762,46 +756,6 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
         }
         // lane 0 issues the warp's next unit (if admitted) and advances its
         // stream; the warp learns whether a copy was issued
-#ifdef L1RXG_SEG_DYN
-        // dynamic units: the warps of the CTA claim the units of an epoch
-        // from one shared counter (a warp that starts its runs late -- the
-        // control warp finishes the previous epoch first -- takes fewer), so
-        // the warps reach the end-of-runs barrier together.  ubuf0/ubuf1: the
-        // (epoch << 12 | unit) each of the warp's two buffers holds.
-        int ubuf0 = -1, ubuf1 = -1;
-        auto issue_one = [&]() -> bool {
-            int got = -1;
-            if (lane == 0) {
-                auto& Q = s->q[warp];
-                while (Q.e < Q.e_adm) {
-                    const int u = atomicAdd(&s->ucnt[Q.e & 1], 1);
-                    if (u < Q.nwu) {
-                        const int b = issued & (SEG_NBUF - 1);
-                        uint64_t* bar = &s->fbar[warp][b];
-                        mbar_expect_tx(bar, SEG_UNIT_BYTES);
-                        tma_load_rows(sbase + boff + (uint32_t)((warp * SEG_NBUF + b) * SEG_UNIT_BYTES), &sa.tmap,
-                                      (int)(Q.pos >> 5) + 32 * u, strm, bar);
-                        got = (Q.e << 12) | u;
-                        break;
-                    }
-                    ++Q.e;  // the epoch's units are all claimed: the next epoch's
-                    Q.pos += n;
-                    if (Q.pos >= R)
-                        Q.pos -= R;
-                    Q.nwu = (((((int)(Q.pos & 31)) + n + 31) >> 5) + 31) >> 5;
-                }
-            }
-            got = __shfl_sync(0xffffffffu, got, 0);
-            if (got < 0)
-                return false;
-            if (issued & 1)
-                ubuf1 = got;
-            else
-                ubuf0 = got;
-            ++issued;
-            return true;
-        };
-#else
         auto issue_one = [&]() -> bool {
             int ok = 0;
             if (lane == 0) {
@@ -828,7 +782,6 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             issued += ok;
             return ok != 0;
         };
-#endif
         if (warp < SEG_NW)
             while (issued < consumed + SEG_NBUF && issue_one()) {
             }
@@ -872,18 +825,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                 const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
                 bool snapped = false;
                 float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
-#ifdef L1RXG_SEG_DYN
-                (void)nwu;
-                for (;;) {
-                    if (consumed == issued && !issue_one())
-                        break;
-                    const int ub = (consumed & 1) ? ubuf1 : ubuf0;
-                    if ((ub >> 12) != e)  // the warp's next unit belongs to a later epoch
-                        break;
-                    const int k = ub & 4095;
-#else
                 for (int k = warp; k < nwu && !noop; k += SEG_NW) {
-#endif
                     const int r = 32 * k + lane;  // the lane's run: epoch run index
                     const int i0 = 32 * r - lead;  // epoch index of its first sample
                     const int jlo = max(0, -i0);
@@ -1072,12 +1014,8 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
 #else
                 warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
 #endif
-                if (lane == 0) {
+                if (lane == 0)
                     s->c.inv_cps = fast_rcp(s->c.cps);
-#ifdef L1RXG_SEG_DYN
-                    s->ucnt[e & 1] = 0;  // epoch e + 2's counter (epoch e's claims all ended before the barrier)
-#endif
-                }
                 float sn, co;
                 sincosf((float)(s->c.w * (double)lane), &sn, &co);
                 s->rot[lane] = make_float2(co * scale, sn * scale);
