@@ -330,25 +330,33 @@ int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
                  : launch_track_thr<T, false>(a, n_ch, nt, s, sk);
 }
 
-// Segment correlator: one CTA per channel, four per SM.
-template <int T>
-int launch_seg(const SegArgs& sa, int n_ch, cudaStream_t s) {
-    (void)n_ch;
-    const size_t sm = seg_smem_bytes<T>(sa.t.n);
-    CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(track_seg_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+// Segment correlator: persistent CTAs over (chunk, channel) work items.
+template <int T, bool QD>
+int launch_seg_k(const SegArgs& sa, cudaStream_t s) {
+    const size_t sm = seg_smem_bytes<T, QD>(sa.t.n);
+    CK(cudaFuncSetAttribute(track_seg_kernel<T, QD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_seg_kernel<T, QD>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     // persistent: as many CTAs as fit, each looping over work items
     int per_sm = 0, nsm = 148, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_seg_kernel<T>, SEG_NT, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_seg_kernel<T, QD>, SEG_NT, sm));
     int grid = std::max(1, std::min(sa.n_items, std::max(1, per_sm) * nsm));
     if (const char* ev = std::getenv("L1RXG_SEG_GRID"))  // tests: many work items per CTA
         grid = std::max(1, std::min(grid, std::atoi(ev)));
-    track_seg_kernel<T><<<grid, SEG_NT, sm, s>>>(sa);
+    track_seg_kernel<T, QD><<<grid, SEG_NT, sm, s>>>(sa);
     CK(cudaGetLastError());
     return 0;
+}
+template <int T>
+int launch_seg(const SegArgs& sa, int n_ch, cudaStream_t s) {
+    (void)n_ch;
+    if constexpr (3 * T <= 32 && T <= 9) {  // (the quarter grid has at most 9 distinct taps)
+        if (sa.qdirect)
+            return launch_seg_k<T, true>(sa, s);
+    }
+    return launch_seg_k<T, false>(sa, s);
 }
 
 template <int T>
@@ -1435,6 +1443,12 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             }
             if (const char* ev = std::getenv("L1RXG_SEG_QGRID"))  // tests: force the exact per-tap path
                 sa.qgrid = sa.qgrid && ev[0] != '0';
+            // direct quarter-crossing kernel (no step table): the quarter grid at >= 62 samples
+            // per chip (nominal rate with 0.1 % margin; the device re-checks every epoch's rate)
+            sa.qdirect = sa.qgrid && sa.fast_geom && t->T <= 9 && a.n < 500000 &&
+                         4.0 * CHIP_RATE_HZ / t->d.sample_rate_hz * 1.001 <= 2.0 / 31.0;
+            if (const char* ev = std::getenv("L1RXG_SEG_QDIRECT"))  // tests: force the step-table kernel
+                sa.qdirect = sa.qdirect && ev[0] != '0';
             CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels)), st));
             DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
         }

@@ -82,6 +82,7 @@ struct __align__(64) SegArgs {
     int n_items, n_channels, chunk_epochs;
     int fast_geom;      // seg_geometry_ok: unchecked step-table entries away from ties
     int qgrid;          // every tap offset a multiple of 1/4 chip in [-1, 1]: start chips by the LUT
+    int qdirect;        // quarter grid + >= 62 samples per chip: per-run crossings, no step table (QD kernel)
 };
 
 template <int T>
@@ -125,6 +126,17 @@ struct SegSmem {
     // capture-position field, bits 8-9 the tap code (q = 0: no entry); tap k's
     // entry is (entq & 0xff) | (entq >> 8) << (10 + 2 k)
     uint16_t entq[32];
+    // QD (direct quarter-crossing) kernel: per-epoch constants in quarter-chip
+    // units (x 4 is exact) and the crossing LUT: qdlut[4 c4 + qq], c4 = the
+    // chips at floor(ph) - 1 .. + 2, qq = floor(4 ph) & 3; bits [0, T) the
+    // taps' start chips, [T, 2T) the taps whose chip flips at the run's first
+    // quarter crossing, [2T, 3T) at its second
+    struct __align__(16) {
+        double cps4, base4;  // 4 cps, 4 base: fma(i, cps4, base4) = 4 fl(fma(i, cps, base)) exactly
+        double omb, inv4;    // 1 - base4; 1 / cps4 (estimate)
+        int ok;              // cps4 <= 2/31: at most two crossings per run, >= 15 samples apart
+    } qd;
+    uint32_t qdlut[64];
 };
 
 // Per-epoch step table, one entry per 32-sample run of the epoch (runs
@@ -138,12 +150,13 @@ struct SegSmem {
 // runs per epoch table: every row a unit of the epoch can cover
 __host__ __device__ constexpr int seg_table_runs(int n) { return (((n + 62) >> 5) + 31) / 32 * 32; }
 
-template <int T>
+template <int T, bool QD = false>
 __host__ __device__ constexpr size_t seg_smem_bytes(int n) {
     // header, step table, then up to 1 KB of padding to the 1024-B aligned unit buffers
     // (L1RXG_SEG_NOPAD: the buffers first, at the 1024-B aligned dynamic base)
     return ((sizeof(SegSmem<T>) + 15) & ~size_t(15)) +
-           ((static_cast<size_t>(seg_table_runs(n)) * sizeof(typename SegEntry<T>::type) + 15) & ~size_t(15)) +
+           (QD ? size_t(0)
+               : ((static_cast<size_t>(seg_table_runs(n)) * sizeof(typename SegEntry<T>::type) + 15) & ~size_t(15))) +
 #ifndef L1RXG_SEG_NOPAD
            1024 +
 #endif
@@ -582,17 +595,33 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
 #endif
 }
 
-template <int T>
 #ifndef L1RXG_SEG_MINB
 #define L1RXG_SEG_MINB (SEG_NW == 4 ? 5 : 4)
 #endif  // (CTAs per SM the registers are budgeted for)
-__global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const __grid_constant__ SegArgs sa) {
+#ifndef L1RXG_SEG_MINB_QD
+#define L1RXG_SEG_MINB_QD L1RXG_SEG_MINB
+#endif
+// QD = true: the direct quarter-crossing variant (sa.qdirect).  Every tap
+// offset is k/4 chip, so fl(ph + d_t) = ph + d_t and every replica step of
+// every tap happens where 4 ph(i) = fma(i, 4 cps, 4 base) crosses an integer;
+// with >= 62 samples per chip a 32-sample run holds at most two such
+// crossings, >= 15 samples apart (never two in one half-run).  Each run
+// locates its own crossings (fp64 estimate; within 2^-28 samples of a tie
+// the whole run takes the exact per-sample path) and a 64-entry LUT gives
+// the taps' start chips and which taps flip at each crossing from the four
+// chips around floor(ph): no per-epoch step table, no fill, one barrier
+// fewer per epoch, 8 KB less shared memory.  Same captures and the same
+// arithmetic as the table path: records are byte-identical away from ties.
+template <int T, bool QD = false>
+__global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MINB)
+    track_seg_kernel(const __grid_constant__ SegArgs sa) {
     typedef typename SegEntry<T>::type E;
+    static_assert(!QD || 3 * T <= 32, "QD packs three T-bit fields into one LUT word");
     const TrackArgs& a = sa.t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.n;
     const uint32_t sbase = smem_u32(smem_raw);
-    const int truns = seg_table_runs(n);
+    const int truns = QD ? 0 : seg_table_runs(n);
 #ifdef L1RXG_SEG_NOPAD
     if (sbase & 1023u)
         __trap();  // the unit buffers need the 1024-B alignment of the 128-B swizzle
@@ -646,6 +675,17 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
     }
     for (int r = tid; r < truns; r += blockDim.x)
         tab[r] = 0;  // every later epoch leaves the table clean (owners clear their entries)
+    if (QD && tid < 64) {  // crossing LUT: chip index of tap t at quarter K = 4 m + qq is m + ((qq + D_t) >> 2)
+        const int qq = tid & 3, c4 = tid >> 2;  // c4 bit b: the chip at m - 1 + b
+        uint32_t pat = 0;
+        for (int t = 0; t < T; ++t) {
+            const int D = (int)rint(a.taps.offsets_chips[t] * 4.0);
+            const int s0 = (qq + D) >> 2, s1 = (qq + 1 + D) >> 2, s2 = (qq + 2 + D) >> 2;  // -1 .. 2
+            const uint32_t b0 = (c4 >> (s0 + 1)) & 1u, b1 = (c4 >> (s1 + 1)) & 1u, b2 = (c4 >> (s2 + 1)) & 1u;
+            pat |= b0 << t | (b0 ^ b1) << (T + t) | (b1 ^ b2) << (2 * T + t);
+        }
+        s->qdlut[tid] = pat;
+    }
     // per-warp TMA unit counters: persistent across work items (every item
     // waits for its last copies, so the mbarrier parities continue)
     int issued = 0, consumed = 0;
@@ -731,6 +771,13 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz,
                         ch.carrier_phase_rad, a.lc.fs, n);
             s->c.inv_cps = fast_rcp(s->c.cps);  // tap_boundary's estimate
+            if (QD) {
+                s->qd.cps4 = 4.0 * s->c.cps;
+                s->qd.base4 = 4.0 * s->c.base;
+                s->qd.omb = 1.0 - 4.0 * s->c.base;
+                s->qd.inv4 = 0.25 * s->c.inv_cps;
+                s->qd.ok = s->c.cps > 0.0 && 4.0 * s->c.cps <= 2.0 / 31.0;
+            }
         }
         __syncthreads();
         if (tid < 32) {
@@ -803,7 +850,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
             // until the loop update) rather than in registers across the runs
             const EpochConsts& c = s->c;
             // the step table of this epoch: every thread (the control warp too)
-            if (!noop) {
+            if (!QD && !noop) {
                 seg_fill<T>(tab, s, c, (int)(off & 31), tid, SEG_NT, sa.fast_geom != 0);
                 __syncthreads();
             }
@@ -825,51 +872,86 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                 const int nwu = (((lead + n + 31) >> 5) + 31) >> 5;
                 bool snapped = false;
                 float hr = 0.f, hi = 0.f;  // first-half prompt (tracking.hpp:265-271)
+                const bool qd_ok = !QD || s->qd.ok != 0;
                 for (int k = warp; k < nwu && !noop; k += SEG_NW) {
                     const int r = 32 * k + lane;  // the lane's run: epoch run index
                     const int i0 = 32 * r - lead;  // epoch index of its first sample
                     const int jlo = max(0, -i0);
                     const int jhi = max(jlo, min(32, n - i0));
-                    const E w = tab[r];
-                    tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
-                    uint32_t slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
-                    if (w & 0x300u) {  // a half with two positions: its steppers take the slow path
-    #pragma unroll
-                        for (int t = 0; t < T; ++t) {
-                            const int code = (int)(w >> (10 + 2 * t)) & 3;
-                            if ((code == 2 && (w & 0x100u)) || (code == 3 && (w & 0x200u)))
-                                slow |= 1u << t;
+                    E w = 0;
+                    uint32_t slow = 0, spat = 0;
+                    // QD: crossing positions x1 < x2 (run positions, >= jlo + 1), the LUT word and
+                    // whether the run takes the exact per-sample path for every tap
+                    int x1 = 0, x2 = 0;
+                    bool slow_all = false;
+                    if constexpr (QD) {
+                        // 4 ph at the run's first counted sample, its floor K0 (quarter index), and
+                        // the samples where 4 ph reaches K0 + 1 and K0 + 2: e = (K - base4) / cps4.
+                        // z = e + 1.5 * 2^20 holds floor(e) in the high word's low 20 bits and
+                        // frac(e) * 2^32 in the low word; the first sample at or past the crossing
+                        // is floor(e) + 1 unless e is within 2^-28 of an integer (a tie: the
+                        // reference's own rounding decides, so the run goes per-sample)
+                        const double q4 = __fma_rn((double)(i0 + jlo), s->qd.cps4, s->qd.base4);
+                        const double rk = __dadd_rd(q4, 6755399441055744.0);
+                        const int K0 = __double2loint(rk);
+                        const double inv4 = s->qd.inv4;
+                        const double e1 = __dmul_rn(__dadd_rn(__dsub_rn(rk, 6755399441055744.0), s->qd.omb), inv4);
+                        const double z1 = __dadd_rn(e1, 1572864.0);
+                        const double z2 = __dadd_rn(z1, inv4);
+                        x1 = (__double2hiint(z1) & 0xfffff) - 0x7ffff - i0;
+                        x2 = (__double2hiint(z2) & 0xfffff) - 0x7ffff - i0;
+                        slow_all = (uint32_t)__double2loint(z1) + 16u < 32u || (uint32_t)__double2loint(z2) + 16u < 32u ||
+                                   (x1 >= 16 && x2 <= 31) || !qd_ok;
+                        const int m0 = (K0 >> 2) - 2;
+                        const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
+                        spat = s->qdlut[((win >> 1) & 15u) * 4u + (uint32_t)(K0 & 3)];
+                        // a crossing past the run's last sample flips nothing here
+                        if (x1 > 31)
+                            spat &= ~(((1u << T) - 1u) << T);
+                        if (x2 > 31)
+                            spat &= ~(((1u << T) - 1u) << (2 * T));
+                    } else {
+                        w = tab[r];
+                        tab[r] = 0;  // clean for the next epoch (each entry is read once, by its owner)
+                        slow = (uint32_t)(w >> (10 + 2 * T)) & ((1u << T) - 1u);
+                        if (w & 0x300u) {  // a half with two positions: its steppers take the slow path
+        #pragma unroll
+                            for (int t = 0; t < T; ++t) {
+                                const int code = (int)(w >> (10 + 2 * t)) & 3;
+                                if ((code == 2 && (w & 0x100u)) || (code == 3 && (w & 0x200u)))
+                                    slow |= 1u << t;
+                            }
                         }
-                    }
-                    // start chips of the taps (the reference's chip index at i0)
-                    // (the first run of an epoch starts before sample 0: its
-                    // start chip is the one at the first sample it counts)
-                    const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
-                    // |d| <= 1 chip: every tap's index is in [m0, m0 + 4]; the
-                    // 32 chip bits from m0 hold them all
-                    const int m0 = floor_idx(phs) - 2;
-                    const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
-                    // start chips of the taps as bits of `spat` (bit t: the chip of
-                    // tap t at the run's first sample, floor(fl(ph + d_t)))
-                    uint32_t spat = 0;
-                    bool exact = !sa.qgrid;
-                    if (!exact) {
-                        // quarter grid: fl(ph + d_t) = ph + d_t exactly (both are
-                        // multiples of ulp(ph) < 2^-40), so floor(ph + d_t) =
-                        // floor(ph) + ((qq + 4 d_t) >> 2), qq = floor(4 frac(ph)); the
-                        // fraction goes to fp32 rounding toward zero (qq exact); within
-                        // 1e-6 of a quarter (or of a binade edge) the exact path decides
-                        const double fl = __dsub_rn(__dadd_rd(phs, 6755399441055744.0), 6755399441055744.0);
-                        const float f4 = __double2float_rz(__dsub_rn(phs, fl)) * 4.f;
-                        const int qq = (int)f4;
-                        exact = f4 - (float)qq < 1e-6f || (float)(qq + 1) - f4 < 1e-6f;
-                        spat = s->qlut[qq * 8 + ((win >> 1) & 7)];
-                    }
-                    if (exact) {
+                        // start chips of the taps (the reference's chip index at i0)
+                        // (the first run of an epoch starts before sample 0: its
+                        // start chip is the one at the first sample it counts)
+                        const double phs = __fma_rn((double)(i0 + jlo), c.cps, c.base);
+                        // |d| <= 1 chip: every tap's index is in [m0, m0 + 4]; the
+                        // 32 chip bits from m0 hold them all
+                        const int m0 = floor_idx(phs) - 2;
+                        const uint32_t win = __funnelshift_r(s->chipw[m0 >> 5], s->chipw[(m0 >> 5) + 1], m0 & 31);
+                        // start chips of the taps as bits of `spat` (bit t: the chip of
+                        // tap t at the run's first sample, floor(fl(ph + d_t)))
                         spat = 0;
-                        for (int t = 0; t < T; ++t) {
-                            const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
-                            spat |= ((win >> (ms - m0)) & 1u) << t;
+                        bool exact = !sa.qgrid;
+                        if (!exact) {
+                            // quarter grid: fl(ph + d_t) = ph + d_t exactly (both are
+                            // multiples of ulp(ph) < 2^-40), so floor(ph + d_t) =
+                            // floor(ph) + ((qq + 4 d_t) >> 2), qq = floor(4 frac(ph)); the
+                            // fraction goes to fp32 rounding toward zero (qq exact); within
+                            // 1e-6 of a quarter (or of a binade edge) the exact path decides
+                            const double fl = __dsub_rn(__dadd_rd(phs, 6755399441055744.0), 6755399441055744.0);
+                            const float f4 = __double2float_rz(__dsub_rn(phs, fl)) * 4.f;
+                            const int qq = (int)f4;
+                            exact = f4 - (float)qq < 1e-6f || (float)(qq + 1) - f4 < 1e-6f;
+                            spat = s->qlut[qq * 8 + ((win >> 1) & 7)];
+                        }
+                        if (exact) {
+                            spat = 0;
+                            for (int t = 0; t < T; ++t) {
+                                const int ms = floor_idx(__dadd_rn(phs, s->d[t]));
+                                spat |= ((win >> (ms - m0)) & 1u) << t;
+                            }
                         }
                     }
                     // start chip of tap t: its bit moved to bit 31, then +1.0f / -1.0f
@@ -900,7 +982,14 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     mbar_wait(&s->fbar[warp][b], (uint32_t)((consumed / SEG_NBUF) & 1));
                     const unsigned char* buf = smem_raw + boff + (warp * SEG_NBUF + b) * SEG_UNIT_BYTES;
                     float2 p16, pc0, pc1, tot;
-                    const int q0 = (int)(w & 15), q1 = (w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0;
+                    // capture positions: first half (1..15), second half (17..31), 0 = none.  QD: the
+                    // first crossing in the first half (case A; the second one is then in 16..32), or
+                    // no crossing before 16 (the first one takes the second-half capture; position 16
+                    // is C1 = 0, i.e. P(16))
+                    const bool caseA = QD && x1 <= 15;
+                    const int qb = caseA ? x2 : x1;
+                    const int q0 = QD ? (caseA ? x1 : 0) : (int)(w & 15);
+                    const int q1 = QD ? ((qb >= 17 && qb <= 31) ? qb : 0) : ((w & 0xf0u) ? (int)((w >> 4) & 15) + 16 : 0);
     #ifdef L1RXG_SEG_CHAINS4
                     const float4* rq4 = reinterpret_cast<const float4*>(s->rotq);
                     if (__all_sync(0xffffffffu, jlo == 0 && jhi == 32))
@@ -913,25 +1002,49 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                     else
                         seg_run<true>(buf, lane, rot4, q0, q1, jlo, jhi, p16, pc0, pc1, tot);
     #endif
-                    // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
-                    // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
-                    const float2 v0 = seg_anchor(tot, ca_, sa_);
-                    const float2 v1 = seg_anchor(seg_flip(p16, tot), ca_, sa_);
-                    const float2 v2 = seg_anchor(seg_flip(pc0, tot), ca_, sa_);
-                    const float2 v3 = seg_anchor(seg_flip(pc1, tot), ca_, sa_);
-                    if (slow) {  // exact per-sample sums replace the fast ones
-    #pragma unroll
-                        for (int t = 0; t < T; ++t)
-                            if ((slow >> t) & 1u) {
-                                const int code = (int)(w >> (10 + 2 * t)) & 3;
-                                const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
+                    float2 v0, v1, v2, v3;
+                    if constexpr (QD) {
+                        // V0 = P(32) (no step); V1 / V2 = the chip flips at the first / second crossing
+                        v0 = seg_anchor(tot, ca_, sa_);
+                        const float2 w1 = caseA ? pc0 : pc1;
+                        v1 = seg_anchor(seg_flip(w1, tot), ca_, sa_);
+                        v2 = seg_anchor(seg_flip(pc1, tot), ca_, sa_);
+                        v3 = v2;
+                        if (slow_all) {  // exact per-sample sums of every tap; the fast combine adds zeros
+#pragma unroll 1
+                            for (int t = 0; t < T; ++t) {
                                 const float2 z = seg_anchor(
                                     seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[t], i0, jlo, jhi, c.cps, c.base),
                                     ca_, sa_);
-                                const float cs = start_chip(t);
-                                acc[2 * t] += fmaf(-cs, v.x, z.x);
-                                acc[2 * t + 1] += fmaf(-cs, v.y, z.y);
+#pragma unroll
+                                for (int u = 0; u < T; ++u) {  // (no dynamic index into acc)
+                                    acc[2 * u] += u == t ? z.x : 0.f;
+                                    acc[2 * u + 1] += u == t ? z.y : 0.f;
+                                }
                             }
+                            v0 = v1 = v2 = make_float2(0.f, 0.f);
+                        }
+                    } else {
+                        // tap k's run sum is start_chip * V[code_k]: V0 = P(32) (no step),
+                        // V_s = P(q_s) - (P(32) - P(q_s)) (the chip flips at q_s)
+                        v0 = seg_anchor(tot, ca_, sa_);
+                        v1 = seg_anchor(seg_flip(p16, tot), ca_, sa_);
+                        v2 = seg_anchor(seg_flip(pc0, tot), ca_, sa_);
+                        v3 = seg_anchor(seg_flip(pc1, tot), ca_, sa_);
+                        if (slow) {  // exact per-sample sums replace the fast ones
+        #pragma unroll
+                            for (int t = 0; t < T; ++t)
+                                if ((slow >> t) & 1u) {
+                                    const int code = (int)(w >> (10 + 2 * t)) & 3;
+                                    const float2 v = code == 0 ? v0 : (code == 1 ? v1 : (code == 2 ? v2 : v3));
+                                    const float2 z = seg_anchor(
+                                        seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[t], i0, jlo, jhi, c.cps, c.base),
+                                        ca_, sa_);
+                                    const float cs = start_chip(t);
+                                    acc[2 * t] += fmaf(-cs, v.x, z.x);
+                                    acc[2 * t + 1] += fmaf(-cs, v.y, z.y);
+                                }
+                        }
                     }
                     if (i0 < nh && i0 + 32 > nh) {  // the run holding the n/2 split
                         const float2 z = seg_anchor(seg_slow_sum(buf, lane, s->rot, s->chipw, s->d[a.kp], i0,
@@ -940,6 +1053,18 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         hr += z.x;
                         hi += z.y;
                     }
+                    if constexpr (QD) {
+    #pragma unroll
+                        for (int t = 0; t < T; ++t) {
+                            const bool f1 = (spat >> (T + t)) & 1u, f2 = (spat >> (2 * T + t)) & 1u;
+                            float2 v = f2 ? v2 : v0;
+                            v = f1 ? v1 : v;
+                            const float cs = start_chip(t);
+                            const float2 at = __ffma2_rn(v, make_float2(cs, cs), make_float2(acc[2 * t], acc[2 * t + 1]));
+                            acc[2 * t] = at.x;
+                            acc[2 * t + 1] = at.y;
+                        }
+                    } else {
 #ifndef L1RXG_SEG_LDSCOMB  // the tap combine by register selects (measured faster than the LDS variant below)
     #pragma unroll
                     for (int t = 0; t < T; ++t) {
@@ -982,6 +1107,7 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     }
 #endif
+                    }
                     __syncwarp();
                     ++consumed;
                     if (issued < consumed + SEG_NBUF)
@@ -1014,8 +1140,16 @@ __global__ void __launch_bounds__(SEG_NT, L1RXG_SEG_MINB) track_seg_kernel(const
 #else
                 warp0_update<T>(s, a, cc, off, cidx, done, SEG_NW, lane, 0, e, nullptr, rec_i);
 #endif
-                if (lane == 0)
+                if (lane == 0) {
                     s->c.inv_cps = fast_rcp(s->c.cps);
+                    if (QD) {
+                        s->qd.cps4 = 4.0 * s->c.cps;
+                        s->qd.base4 = 4.0 * s->c.base;
+                        s->qd.omb = 1.0 - 4.0 * s->c.base;
+                        s->qd.inv4 = 0.25 * s->c.inv_cps;
+                        s->qd.ok = s->c.cps > 0.0 && 4.0 * s->c.cps <= 2.0 / 31.0;
+                    }
+                }
                 float sn, co;
                 sincosf((float)(s->c.w * (double)lane), &sn, &co);
                 s->rot[lane] = make_float2(co * scale, sn * scale);

@@ -680,10 +680,12 @@ def test_attach_refuses_pushes_and_detach_restores_ring(ctx):
 
 
 def test_segment_quarter_grid_start_chips_bit_identical(ctx, oracle_mod, monkeypatch):
-    """The quarter-grid start-chip LUT (every tap offset k/4 chip: floor(ph +
-    d_t) from floor(ph) and floor(4 frac ph)) gives byte-identical records to
-    the exact per-tap fp64 path (L1RXG_SEG_QGRID=0), including at Doppler
-    offsets that walk the code phase across quarter-chip boundaries."""
+    """On the quarter grid (every tap offset k/4 chip) three formulations give
+    byte-identical records: the direct quarter-crossing kernel (default: every
+    run locates its own crossings, no step table), the step-table kernel with
+    the start-chip LUT (L1RXG_SEG_QDIRECT=0) and the step-table kernel with
+    the exact per-tap fp64 start chips (L1RXG_SEG_QGRID=0) -- including at
+    Doppler offsets that walk the code phase across quarter-chip boundaries."""
     fs, ms, n = 65.472e6, 30, 65472
     svs = [[ss.Sv(prn=p, cn0_dbhz=45.0, doppler_hz=dop, delay_chips=dl)
             for p, dop, dl in ((4, 4999.0, 100.25), (15, -3700.0, 512.5), (28, 120.0, 1000.75))]]
@@ -691,18 +693,21 @@ def test_segment_quarter_grid_start_chips_bit_identical(ctx, oracle_mod, monkeyp
     inits = [_init(sv, fs) for sv in svs[0]]
     taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
     out = []
-    for env in ("1", "0"):
-        monkeypatch.setenv("L1RXG_SEG_QGRID", env)
+    for qd, qg in (("1", "1"), ("0", "1"), ("0", "0")):
+        monkeypatch.setenv("L1RXG_SEG_QDIRECT", qd)
+        monkeypatch.setenv("L1RXG_SEG_QGRID", qg)
         t = Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, taps=taps, ring_samples=(ms + 4) * n,
                     max_records=ms, cta_mode=abi.CTA_SEGMENT)
         t.attach_device(dev.data_ptr(), dev.shape[1] // 4, dev.shape[1])
         t.run()
         out.append([t.records(c, tap_sums=True) for c in range(3)])
-    for (ra, sa), (rb, sb) in zip(*out):
-        assert ra.tobytes() == rb.tobytes() and sa.tobytes() == sb.tobytes()
+    for other in out[1:]:
+        for (ra, sa), (rb, sb) in zip(out[0], other):
+            assert ra.tobytes() == rb.tobytes() and sa.tobytes() == sb.tobytes()
     x = oracle_mod.ingest(dev.cpu().numpy()[0], abi.FMT_INT16_IQ, fs)
-    replay_check(oracle_mod, inits[1], out[0][1][0], x, n, abi.TrackingCfg.default(), taps, fs,
-                 tap_sums=out[0][1][1])
+    for c in range(3):
+        replay_check(oracle_mod, inits[c], out[0][c][0], x, n, abi.TrackingCfg.default(), taps, fs,
+                     tap_sums=out[0][c][1])
 
 
 @pytest.mark.parametrize("cta_mode", [abi.CTA_AUTO, abi.CTA_SEGMENT])
