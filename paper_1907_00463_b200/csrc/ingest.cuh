@@ -29,8 +29,34 @@ __device__ __forceinline__ void ring_put(float2* ring, int64_t R, int64_t apron,
 // 2*sum_t h[t] mixed(g-t) (samples.hpp:234-240) is a 23-tap real
 // convolution per output phase with coefficient tables cre/cim[4][23]
 // folded on the host (includes the 2/128 scale).
-__constant__ float c_if4_re[4][23];
-__constant__ float c_if4_im[4][23];
+// The same filter with its structure used: of the 46 products per output
+// only 13 matter -- the mixer zeroes one component of every sample, and the
+// half-band taps at odd t != 11 are 1e-17 (sin(m pi) in floating point).
+// For g = ph mod 4 the component fed by the even taps is
+//   B = sum_{k<12} a[k] v(g - 2k),  a[k] = 2 h[2k] / 128 * (-1)^k  (phase 0's signs),
+// negated for the phases in big_neg, and the other component is c * v(g - 11),
+// negated for the phases in c_neg; even phases give (re, im) = (B, C), odd
+// phases (C, B).  Same ascending-t FMA chain as the full tables minus the
+// terms below 1e-15 of the result.  One definition for the ingest kernel
+// (float2 rings) and the FIR warps of the overlapped kernel (raw rings).
+struct If4Fir {
+    float a[12];
+    float c;
+    uint32_t big_neg, c_neg;
+};
+__constant__ If4Fir c_if4f;
+
+// x[0] = v(g), x[-t] = v(g - t) as floats (the raw int8 values); ph = g & 3.
+__device__ __forceinline__ float2 if4_fir(const float* x, int ph) {
+    float b = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; ++k)
+        b = fmaf(c_if4f.a[k], x[-2 * k], b);
+    float c = c_if4f.c * x[-11];
+    b = (c_if4f.big_neg >> ph) & 1u ? -b : b;
+    c = (c_if4f.c_neg >> ph) & 1u ? -c : c;
+    return (ph & 1) ? make_float2(c, b) : make_float2(b, c);
+}
 
 constexpr int ING_TPB = 256;
 constexpr int ING_OUT_PER_THREAD = 4;
@@ -61,18 +87,11 @@ __global__ void __launch_bounds__(ING_TPB) ingest_if4_kernel(
         const int64_t idx = t0 + q + u;
         if (idx >= count)
             break;
-        const int ph = (int)((g0 + idx) & 3);
-        float re = 0.f, im = 0.f;
-#pragma unroll
-        for (int t = 0; t < 23; ++t) {
-            const float x = v[q + u + 22 - t];
-            re = fmaf(c_if4_re[ph][t], x, re);
-            im = fmaf(c_if4_im[ph][t], x, im);
-        }
+        const float2 y = if4_fir(&v[q + u + 22], (int)((g0 + idx) & 3));
         int64_t pos = pos0 + idx;
         if (pos >= R)
             pos -= R;
-        ring_put(ring, R, apron, pos, make_float2(re, im));
+        ring_put(ring, R, apron, pos, y);
     }
     if (blockIdx.x == 0 && threadIdx.x < 22) {
         const int64_t idx = count - 22 + threadIdx.x;
@@ -80,6 +99,43 @@ __global__ void __launch_bounds__(ING_TPB) ingest_if4_kernel(
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
         *avail_slot = g0 + count;
+}
+
+// Raw real-IF ring (overlapped kernel with FIR warps): the bytes themselves,
+// ring[g mod R], the head mirrored behind the tail (apron) and the last
+// RAWIF_PAD bytes mirrored in front of the head, so every window
+// [pos - 22, pos + n) is contiguous.  The pad reads zero at stream start.
+constexpr int RAWIF_PAD = 32;
+__global__ void copy_rawif_kernel(const int8_t* __restrict__ src, int64_t count, int8_t* ring, int64_t R,
+                                  int64_t apron, int64_t pos0, int64_t* avail_slot, int64_t avail_value) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        const int8_t v = src[i];
+        int64_t pos = pos0 + i;
+        if (pos >= R)
+            pos -= R;
+        ring[pos] = v;
+        if (pos < apron)
+            ring[R + pos] = v;
+        if (pos >= R - RAWIF_PAD)
+            ring[pos - R] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && avail_slot)
+        *avail_slot = avail_value;
+}
+// Baseband samples [g0, g0 + count) of a raw real-IF ring (read_samples).
+__global__ void rawif_window_kernel(const int8_t* __restrict__ ring, int64_t R, int64_t g0, int64_t count,
+                                    float2* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count)
+        return;
+    float x[23];
+#pragma unroll
+    for (int t = 0; t < 23; ++t) {
+        const int64_t g = g0 + i - t;
+        x[22 - t] = g >= 0 ? (float)ring[g % R] : 0.f;
+    }
+    out[i] = if4_fir(&x[22], (int)((g0 + i) & 3));
 }
 
 // Generic real IF: pass 1, mixer at the global index in fp64

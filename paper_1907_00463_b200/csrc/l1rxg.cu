@@ -103,9 +103,21 @@ int upload_constants() {
             }
         for (int t = 0; t < 23; ++t)
             h2[t] = static_cast<float>(2.0 * h[t]);
-        if (cudaMemcpyToSymbol(c_if4_re, re, sizeof re) != cudaSuccess ||
-            cudaMemcpyToSymbol(c_if4_im, im, sizeof im) != cudaSuccess ||
-            cudaMemcpyToSymbol(c_halfband2, h2, sizeof h2) != cudaSuccess)
+        If4Fir f{};
+        for (int k = 0; k < 12; ++k)
+            f.a[k] = re[0][2 * k];
+        f.c = im[0][11];
+        for (int r = 0; r < 4; ++r) {
+            const float big = (r & 1) ? im[r][0] : re[r][0];
+            const float cc = (r & 1) ? re[r][11] : im[r][11];
+            if (std::fabs(big) != std::fabs(f.a[0]) || std::fabs(cc) != std::fabs(f.c))
+                g_const_rc = 1;
+            f.big_neg |= (big != f.a[0] ? 1u : 0u) << r;
+            f.c_neg |= (cc != f.c ? 1u : 0u) << r;
+        }
+        if (cudaMemcpyToSymbol(c_if4f, &f, sizeof f) != cudaSuccess)
+            g_const_rc = 1;
+        if (cudaMemcpyToSymbol(c_halfband2, h2, sizeof h2) != cudaSuccess)
             g_const_rc = 1;
     });
     return g_const_rc;
@@ -217,22 +229,26 @@ int launch_track_thr(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int s
 // Overlapped latency kernel (ovlcorr.cuh): float2 rings, two tiles, one unit
 // per epoch, and its P'/M' tiles within the shared-memory budget.  Returns
 // -1 when not applicable (the caller then runs track_kernel).
+// Shared memory of track_ovl_kernel<T, RAW> for nt main threads (0: does not fit / not applicable).
 template <int T>
-int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
-    static const char* ev = std::getenv("L1RXG_OVL");
-    if ((ev && ev[0] == '0') || a.thr || sk != SK_F32 || a.nbuf != 2 ||
-        a.lc.kernel == L1RXG_KERNEL_NOOP)
-        return -1;
+size_t ovl_smem(const TrackArgs& a, int nt, bool raw) {
     const int len = a.csize > 1 ? std::min(a.n, a.share) : a.n;  // rank 0's unit: the largest
     if (len > (nt - 32) * RUN)
-        return -1;
+        return 0;
     const int nrun = (len + RUN - 1) / RUN;  // the kernel's layout unit
-    const size_t xsl = (2u * a.csize * (2 * T + 2) * sizeof(double) + 15) & ~size_t(15);
-    const size_t sm = smem_bytes<T>(nrun, 2, 8) + xsl + ovl_extra_bytes(nrun);
-    if (sm > 227u * 1024u)
+    const size_t xsl = ovl_xslot_bytes(a.csize, 2 * T + 2, (nt - 32) / 32, a.xd);
+    const size_t sm = smem_bytes<T>(nrun, 2, 8) + xsl + ovl_extra_bytes(nrun) + (raw ? ovl_raw_bytes(nrun) : 0);
+    return sm > 227u * 1024u ? 0 : sm;
+}
+
+template <int T, bool RAW>
+int launch_ovl_k(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, bool check_only) {
+    const size_t sm = ovl_smem<T>(a, nt, RAW);
+    const int block = nt + (RAW ? 32 * OVL_NF : 0);
+    if (!sm || block > MAX_NT)
         return -1;
-    CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    CK(cudaFuncSetAttribute(track_ovl_kernel<T, RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(track_ovl_kernel<T, RAW>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     // the P'/M' tiles must not cost co-residency: every CTA of the launch
     // resident at once, as with track_kernel (measured: config 3's paired
@@ -240,17 +256,19 @@ int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
     int per_sm = 0, nsm = 148, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_ovl_kernel<T>, nt, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, track_ovl_kernel<T, RAW>, block, sm));
     if (static_cast<long long>(n_ch) * a.csize > static_cast<long long>(per_sm) * nsm)
         return -1;
+    if (check_only)
+        return 0;
     if (a.csize <= 1) {
-        track_ovl_kernel<T><<<n_ch, nt, sm, s>>>(a);
+        track_ovl_kernel<T, RAW><<<n_ch, block, sm, s>>>(a);
     } else {
         if (a.csize > 8)
-            CK(cudaFuncSetAttribute(track_ovl_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            CK(cudaFuncSetAttribute(track_ovl_kernel<T, RAW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(n_ch * a.csize));
-        cfg.blockDim = dim3(static_cast<unsigned>(nt));
+        cfg.blockDim = dim3(static_cast<unsigned>(block));
         cfg.dynamicSmemBytes = sm;
         cfg.stream = s;
         cudaLaunchAttribute at[1];
@@ -260,10 +278,29 @@ int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, track_ovl_kernel<T>, a));
+        CK(cudaLaunchKernelEx(&cfg, track_ovl_kernel<T, RAW>, a));
     }
     CK(cudaGetLastError());
     return 0;
+}
+
+// Overlapped latency kernel (ovlcorr.cuh): float2 rings (or the raw real-IF
+// byte ring, sk == SK_R8), two tiles, one unit per epoch, and its P'/M' tiles
+// within the shared-memory budget.  Returns -1 when not applicable (the caller
+// then runs track_kernel; a raw real-IF ring is only created when it applies).
+template <int T>
+int launch_ovl(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk, bool check_only = false) {
+    static const char* ev = std::getenv("L1RXG_OVL");
+    if ((ev && ev[0] == '0') || a.thr || (sk != SK_F32 && sk != SK_R8) || a.nbuf != 2 ||
+        a.lc.kernel == L1RXG_KERNEL_NOOP)
+        return -1;
+    return sk == SK_R8 ? launch_ovl_k<T, true>(a, n_ch, nt, s, check_only)
+                       : launch_ovl_k<T, false>(a, n_ch, nt, s, check_only);
+}
+// create-time probe: would the RAW variant run this tracker's shape?
+template <int T>
+int ovl_raw_applicable(const TrackArgs& a, int n_ch, int nt) {
+    return launch_ovl<T>(a, n_ch, nt, nullptr, SK_R8, true);
 }
 
 // How many clusters of K CTAs (nt threads each) can be resident at once for
@@ -301,9 +338,12 @@ int cluster_capacity(int K, int nt, int nbuf, int len) {
     int c = cap(reinterpret_cast<const void*>(track_kernel<T, SK_F32, false>),
                 smem_bytes<T>(nt - 32, nbuf, 8) + xs);
     const int nrun = (len + RUN - 1) / RUN;
-    const size_t sm_ovl = smem_bytes<T>(nrun, 2, 8) + ((xs + 15) & ~size_t(15)) + ovl_extra_bytes(nrun);
+    const size_t sm_ovl = smem_bytes<T>(nrun, 2, 8) +
+                          std::max(ovl_xslot_bytes(K, 2 * T + 2, (nt - 32) / 32, 0),
+                                   ovl_xslot_bytes(K, 2 * T + 2, (nt - 32) / 32, 1)) +
+                          ovl_extra_bytes(nrun);
     if (nbuf == 2 && sm_ovl <= 227u * 1024u)
-        c = std::min(c, cap(reinterpret_cast<const void*>(track_ovl_kernel<T>), sm_ovl));
+        c = std::min(c, cap(reinterpret_cast<const void*>(track_ovl_kernel<T, false>), sm_ovl));
     return c;
 }
 
@@ -326,6 +366,8 @@ int launch_track(const TrackArgs& a, int n_ch, int nt, cudaStream_t s, int sk) {
         if (rc != -1)
             return rc;
     }
+    if (sk == SK_R8)
+        return set_err(L1RXG_EINVAL, "raw real-IF ring without the overlapped kernel (L1RXG_OVL changed after create?)");
     return a.thr ? launch_track_thr<T, true>(a, n_ch, nt, s, sk)
                  : launch_track_thr<T, false>(a, n_ch, nt, s, sk);
 }
@@ -530,6 +572,7 @@ struct l1rxg_ctx {
     uint64_t id = 0;  // unique per context (keys the threads' CallScratch)
     cudaStream_t compute = nullptr, copy = nullptr;
     int8_t* d_codes = nullptr;
+    uint32_t* d_chipw = nullptr;  // [33][CHIP_EXT / 32 + 1]: bit m % 32 of word m / 32 = chip[m mod 1023] > 0
     DevBuf iq64, iq32, states, prns, sums, corr;
     std::mutex scratch_mu;                    // guards `scratch` (registration, destroy)
     std::vector<CallScratch*> scratch;        // every thread's per-call state
@@ -565,9 +608,14 @@ struct l1rxg_tracker {
     int seg = 0;     // segment correlator (track_seg_kernel) over a raw cint16 ring
     CUtensorMap tmap{};  // seg: the ring as [stream][row][32 samples] for TMA tensor copies
     int64_t att_samples = 0;  // seg: > 0 while device recordings are attached in place of the ring
-    int* d_segq = nullptr;    // seg: work-item counter + per-channel chunks done
+    int* d_segq = nullptr;    // seg: work-item counter + per-channel chunks done + progress + class counters
+    int* d_gangs = nullptr;   // seg: [2][n_gangs] first channel and channel count of each gang (same-stream run)
+    int n_gangs = 0, gang_max = 0;
+    DevBuf seg_ctab;          // seg: per-class ticket table of a launch
     int share = 0;   // samples of each epoch per cluster CTA
     int64_t R = 0, apron = 0;
+    int64_t pad = 0; // raw real-IF ring: bytes in front of every stream's ring (mirror of its tail)
+    int rawif = 0;   // raw real-IF byte ring filtered inside the overlapped kernel (no ingest pass)
     int esz = 8;     // ring element bytes (ring_esz)
     std::vector<StreamRing> streams;
     unsigned char* d_ring = nullptr;
@@ -637,7 +685,13 @@ int ingest_launch(l1rxg_tracker* t, int s, const void* dev_bytes, int64_t nsamp,
     cudaEventRecord(a, st);
     if (fmt == L1RXG_FMT_INT8_REAL_IF) {
         const double w = -2.0 * PI_D * t->d.if_frequency_hz / t->d.sample_rate_hz;
-        if (w == -PI_D / 2.0) {
+        if (t->rawif) {  // the bytes themselves; the overlapped kernel's FIR warps filter them
+            const unsigned blocks = static_cast<unsigned>((nsamp + 255) / 256);
+            copy_rawif_kernel<<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(dev_bytes), nsamp,
+                                                      reinterpret_cast<int8_t*>(r.ring), t->R, t->apron, pos0,
+                                                      slot, g0 + nsamp);
+            t->launches += 1;
+        } else if (w == -PI_D / 2.0) {
             const int cur = r.hist_cur;
             const int64_t blocks = (nsamp + ING_TILE - 1) / ING_TILE;
             ingest_if4_kernel<<<(unsigned)blocks, ING_TPB, 0, st>>>(
@@ -766,6 +820,18 @@ int l1rxg_create(int device, l1rxg_ctx** out) {
     cudaError_t e = cudaMalloc(&c->d_codes, codes.size());
     if (e == cudaSuccess)
         e = cudaMemcpy(c->d_codes, codes.data(), codes.size(), cudaMemcpyHostToDevice);
+    {
+        constexpr int W = CHIP_EXT / 32 + 1;
+        std::vector<uint32_t> cw(33 * W, 0u);
+        for (int p = 1; p <= 32; ++p)
+            for (int q = 0; q < W; ++q)
+                for (int b = 0; b < 32; ++b)
+                    cw[p * W + q] |= (codes[p * 1023 + (32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
+        if (e == cudaSuccess)
+            e = cudaMalloc(&c->d_chipw, cw.size() * 4);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(c->d_chipw, cw.data(), cw.size() * 4, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess)
         e = cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking);
     if (e == cudaSuccess)
@@ -799,6 +865,7 @@ int l1rxg_destroy(l1rxg_ctx* c) {
     if (c->blas)
         cublasDestroy(c->blas);
     cudaFree(c->d_codes);
+    cudaFree(c->d_chipw);
     cudaStreamDestroy(c->compute);
     cudaStreamDestroy(c->copy);
     delete c;
@@ -1056,6 +1123,31 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
     }
     t->R = d->ring_samples;
     t->esz = ring_esz(d->format, d->ring_raw);
+    {   // raw real-IF byte ring filtered by the overlapped kernel's FIR warps (RAW variant), opt-in with
+        // L1RXG_OVL_RAWIF=1: it removes the ingest pass and the float2 ring (config 2: 1.36 GB -> ~0.2 GB of
+        // DRAM traffic per 10 000 blocks), but the FIR warps share the SM with the per-epoch critical path and
+        // the latency-bound epoch gets 4 % longer (profiles/r3e_rawif_ab.txt), so the float2 ring stays default
+        static const char* ev_raw = std::getenv("L1RXG_OVL_RAWIF");
+        const double w = -2.0 * PI_D * d->if_frequency_hz / d->sample_rate_hz;
+        if (!t->seg && !t->thr && d->format == L1RXG_FMT_INT8_REAL_IF && w == -PI_D / 2.0 &&
+            ev_raw && ev_raw[0] == '1' && d->n_channels > 0) {
+            TrackArgs pa{};
+            pa.n = n;
+            pa.csize = t->csize;
+            pa.share = t->share;
+            pa.nbuf = t->nbuf;
+            pa.thr = 0;
+            pa.xd = 0;
+            pa.lc.kernel = d->kernel;
+            auto probe = [&]() -> int { DISPATCH_T(t->T, ovl_raw_applicable, pa, d->n_channels, t->nt); };
+            if (probe() == 0) {
+                t->rawif = 1;
+                t->esz = 1;
+                t->pad = RAWIF_PAD;
+            }
+            cudaGetLastError();
+        }
+    }
     if (t->seg) {
         // raw cint16 in rows of 32 samples: R and the apron whole rows; the
         // apron covers an epoch plus the last unit's row overhang
@@ -1076,14 +1168,33 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
                        std::string("tracker alloc: ") + cudaGetErrorString(e));
     };
     cudaError_t e;
-    const int64_t stride = t->R + t->apron;
+    const int64_t stride = t->R + t->apron + t->pad;
     if ((e = cudaMalloc(&t->d_ring, static_cast<size_t>(t->esz) * static_cast<size_t>(stride) * t->streams.size())) !=
         cudaSuccess)
         return fail(e);
+    if (t->rawif)  // the pad in front of the head reads as the zero FIR history of a stream's start
+        cudaMemset(t->d_ring, 0, static_cast<size_t>(stride) * t->streams.size());
     for (size_t k = 0; k < t->streams.size(); ++k)
-        t->streams[k].ring = t->d_ring + static_cast<int64_t>(k) * stride * t->esz;
-    if (t->seg && (e = cudaMalloc(&t->d_segq, 4 * (1 + std::max(1, d->n_channels)))) != cudaSuccess)
+        t->streams[k].ring = t->d_ring + (static_cast<int64_t>(k) * stride + t->pad) * t->esz;
+    if (t->seg && (e = cudaMalloc(&t->d_segq, 4 * (1 + 2 * static_cast<size_t>(std::max(1, d->n_channels)) + SEG_CLASSES))) != cudaSuccess)
         return fail(e);
+    if (t->seg && d->n_channels > 0) {  // gangs: runs of consecutive channels on the same stream
+        std::vector<int> first, count;
+        for (int c = 0; c < d->n_channels; ++c) {
+            if (c > 0 && chan_stream[c] == chan_stream[c - 1])
+                count.back() += 1;
+            else {
+                first.push_back(c);
+                count.push_back(1);
+            }
+        }
+        t->n_gangs = static_cast<int>(first.size());
+        t->gang_max = *std::max_element(count.begin(), count.end());
+        first.insert(first.end(), count.begin(), count.end());
+        if ((e = cudaMalloc(&t->d_gangs, 4 * first.size())) != cudaSuccess)
+            return fail(e);
+        cudaMemcpy(t->d_gangs, first.data(), 4 * first.size(), cudaMemcpyHostToDevice);
+    }
     if (t->seg) {
         if (int rc = encode_ring_map(&t->tmap, t->d_ring, stride / 32, stride * 4, d->n_streams)) {
             const std::string msg = g_err;
@@ -1143,6 +1254,8 @@ int l1rxg_tracker_destroy(l1rxg_tracker* t) {
     cudaDeviceSynchronize();
     cudaFree(t->d_ring);
     cudaFree(t->d_segq);
+    cudaFree(t->d_gangs);
+    t->seg_ctab.release();
     cudaFree(t->d_hist);
     cudaFree(t->d_avail);
     cudaFree(t->d_chans);
@@ -1376,8 +1489,8 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
         return 0;
     CK(cudaSetDevice(t->ctx->device));
     TrackArgs a{};
-    a.ring = t->d_ring;
-    a.ring_stride = t->R + t->apron;
+    a.ring = t->d_ring + t->pad * t->esz;
+    a.ring_stride = t->R + t->apron + t->pad;
     a.ring_cap = t->att_samples > 0 ? t->att_samples : t->R;
     a.avail = t->d_avail;
     a.chans = t->d_chans;
@@ -1401,6 +1514,10 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.thr = t->thr;
     static const char* ev_dw = std::getenv("L1RXG_OVL_DWMAX");
     a.ovl_dwmax = ev_dw ? static_cast<float>(std::atof(ev_dw)) : 1e-3f;
+    // direct exchange of the warp partials (overlapped kernel, clusters): L1RXG_OVL_XD=0/1 overrides
+    static const char* ev_xd = std::getenv("L1RXG_OVL_XD");
+    a.xd = ev_xd && ev_xd[0] == '1' && t->csize > 1 && 2 * t->T + 2 <= 32 &&
+           t->csize * ((t->nt - 32) / 32) <= 64;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
@@ -1412,7 +1529,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
         CK(cudaMemsetAsync(dprof, 0, 4 * 64 * 8 * sizeof(long long), st));
     }
     a.prof = dprof;
-    const int sk = t->esz == 4 ? SK_I16 : t->esz == 2 ? SK_I8 : SK_F32;
+    const int sk = t->rawif ? SK_R8 : t->esz == 4 ? SK_I16 : t->esz == 2 ? SK_I8 : SK_F32;
     SegArgs sa;
     auto go = [&]() -> int {
         if (t->seg) {
@@ -1424,7 +1541,10 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             for (const auto& r : t->streams)
                 most = std::max(most, r.pushed);
             const int64_t max_e = std::min<int64_t>(a.max_epochs, most / a.n + 1);
-            const int chunk = static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
+            // L1RXG_SEG_CHUNK: epochs per work item (experiments)
+            static const char* ev_chunk = std::getenv("L1RXG_SEG_CHUNK");
+            const int chunk = ev_chunk ? std::max(1, std::atoi(ev_chunk))
+                                       : static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
             const int64_t nchunk = std::max<int64_t>(1, (max_e + chunk - 1) / chunk);
             const int64_t items = nchunk * t->d.n_channels;
             if (items > 0x7fffffff)
@@ -1449,7 +1569,53 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
                          4.0 * CHIP_RATE_HZ / t->d.sample_rate_hz * 1.001 <= 2.0 / 31.0;
             if (const char* ev = std::getenv("L1RXG_SEG_QDIRECT"))  // tests: force the step-table kernel
                 sa.qdirect = sa.qdirect && ev[0] != '0';
-            CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels)), st));
+            // gang pacing (experiment, measured slower: profiles/r3a): siblings within L1RXG_SEG_PACE epochs; 0 = off (default)
+            static const char* ev_pace = std::getenv("L1RXG_SEG_PACE");
+            sa.prog = t->d_segq + 1 + t->d.n_channels;
+            sa.pace = ev_pace ? std::atoi(ev_pace) : 0;
+            CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + 2 * static_cast<size_t>(t->d.n_channels) + SEG_CLASSES), st));
+            // gang tickets when streams are shared (L1RXG_SEG_GANGS=0: the single item queue)
+            static const char* ev_gangs = std::getenv("L1RXG_SEG_GANGS");
+            sa.gang_first = nullptr;
+            sa.gang_count = nullptr;
+            sa.n_gangs = t->n_gangs;
+            sa.gang_max = t->gang_max;
+            sa.cnext = t->d_segq + 1 + 2 * t->d.n_channels;
+            sa.ctab = nullptr;
+            sa.ctab_stride = 0;
+            if (t->gang_max > 1 && !(ev_gangs && ev_gangs[0] == '0') && nchunk * t->n_gangs < 0x3fffffff) {
+                sa.ctab_stride = static_cast<int>(nchunk * t->n_gangs) + 1024;
+                const size_t tb = 4 * static_cast<size_t>(SEG_CLASSES) * sa.ctab_stride;
+                if (t->seg_ctab.ensure(tb))
+                    return L1RXG_ENOMEM;
+                CK(cudaMemsetAsync(t->seg_ctab.p, 0xff, tb, st));
+                sa.ctab = static_cast<int*>(t->seg_ctab.p);
+                sa.gang_first = t->d_gangs;
+                sa.gang_count = t->d_gangs + t->n_gangs;
+            }
+            sa.chipw = t->ctx->d_chipw;
+            // L1RXG_SEG_TRACE=<file>: globaltimer at every work item's start and end, written as
+            // "item channel chunk start_ns end_ns smid warp_slot" lines after the launch (diagnostics)
+            static const char* ev_trace = std::getenv("L1RXG_SEG_TRACE");
+            sa.trace = nullptr;
+            if (ev_trace) {
+                CK(cudaMalloc(&sa.trace, 24 * static_cast<size_t>(items)));
+                CK(cudaMemsetAsync(sa.trace, 0, 24 * static_cast<size_t>(items), st));
+                if (int rc = [&]() -> int { DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st); }())
+                    return rc;
+                std::vector<unsigned long long> h(3 * static_cast<size_t>(items));
+                CK(cudaMemcpyAsync(h.data(), sa.trace, 24 * static_cast<size_t>(items), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                cudaFree(sa.trace);
+                if (FILE* f = std::fopen(ev_trace, "w")) {
+                    for (int64_t i = 0; i < items; ++i)
+                        std::fprintf(f, "%lld %lld %lld %llu %llu %llu %llu\n", (long long)i,
+                                     (long long)(i % t->d.n_channels), (long long)(i / t->d.n_channels), h[3 * i],
+                                     h[3 * i + 1], h[3 * i + 2] >> 32, h[3 * i + 2] & 0xffffffffull);
+                    std::fclose(f);
+                }
+                return 0;
+            }
             DISPATCH_T(t->T, launch_seg, sa, t->d.n_channels, st);
         }
         DISPATCH_T(t->T, launch_track, a, t->d.n_channels, t->nt, st, sk);
@@ -1627,6 +1793,9 @@ int l1rxg_tracker_reset(l1rxg_tracker* t, const l1rxg_channel* chans) {
         r.hist_cur = 0;
     }
     CK(cudaMemsetAsync(t->d_hist, 0, t->hist_bytes, st));  // every stream's FIR history, one memset
+    if (t->rawif)  // and the raw rings' front pads
+        CK(cudaMemset2DAsync(t->d_ring, static_cast<size_t>(t->R + t->apron + t->pad), 0,
+                             static_cast<size_t>(t->pad), t->streams.size(), st));
     if (t->d.n_channels > 0) {
         if (chans)
             CK(cudaMemcpyAsync(t->d_chans, chans, sizeof(l1rxg_channel) * t->d.n_channels,
@@ -1649,6 +1818,26 @@ int l1rxg_tracker_read_samples(l1rxg_tracker* t, int s, int64_t s0, int64_t coun
     const StreamRing& r = t->streams[static_cast<size_t>(s)];
     if (s0 < 0 || count < 0 || s0 + count > r.pushed || s0 < r.pushed - t->R)
         return set_err(L1RXG_EINVAL, "samples not in the ring");
+    if (t->rawif) {  // the baseband the FIR warps see: the same if4_fir over the ring's bytes
+        if (s0 >= 22 && s0 - 22 < r.pushed - t->R)
+            return set_err(L1RXG_EINVAL, "samples (with their FIR history) not in the ring");
+        if (count == 0)
+            return 0;
+        float2* dout = nullptr;
+        CK(cudaMalloc(&dout, sizeof(float2) * static_cast<size_t>(count)));
+        rawif_window_kernel<<<static_cast<unsigned>((count + 255) / 256), 256>>>(
+            reinterpret_cast<const int8_t*>(r.ring), t->R, s0, count, dout);
+        std::vector<float2> h(static_cast<size_t>(count));
+        const cudaError_t ce = cudaMemcpy(h.data(), dout, sizeof(float2) * h.size(), cudaMemcpyDeviceToHost);
+        cudaFree(dout);
+        if (ce != cudaSuccess)
+            return set_err(L1RXG_ECUDA, cudaGetErrorString(ce));
+        for (int64_t k = 0; k < count; ++k) {
+            iq_out[2 * k] = h[static_cast<size_t>(k)].x;
+            iq_out[2 * k + 1] = h[static_cast<size_t>(k)].y;
+        }
+        return 0;
+    }
     const int esz = t->esz;
     std::vector<unsigned char> tmp(static_cast<size_t>(count) * esz);
     for (int64_t k = 0; k < count;) {

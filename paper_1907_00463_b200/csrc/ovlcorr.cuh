@@ -24,8 +24,13 @@
 #pragma once
 
 #include "correlator.cuh"
+#include "ingest.cuh"
 
 namespace l1rxg {
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ void named_bar_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -45,6 +50,30 @@ __host__ __device__ inline size_t ovl_extra_bytes(int nrun) {
     const size_t cap = (size_t)nrun * RUN;
     return 2 * cap * sizeof(float2) + 2 * (size_t)nrun * sizeof(float2) + 2 * 32 * sizeof(float2) +
            4 * sizeof(double) + 64;
+}
+
+// Cluster exchange slots: [2 (epoch parity)][csize][V] fp64 CTA totals, or with
+// the direct exchange (TrackArgs::xd) [2][csize][work warps][V] fp32 warp partials.
+__host__ __device__ inline size_t ovl_xslot_bytes(int csize, int V, int wwarps, int xd) {
+    const size_t b = xd ? 2u * (size_t)csize * wwarps * V * sizeof(float) : 2u * (size_t)csize * V * sizeof(double);
+    return (b + 15) & ~size_t(15);
+}
+
+// RAW variant (real int8 IF at fs/4, raw byte ring): OVL_NF extra warps turn each
+// epoch's unit of raw bytes (bulk copy, 1 B per sample instead of the 8 B of a
+// float2 ring) into the float2 tile the work warps read -- the fs/4 mixer and the
+// 23-tap half-band FIR of SampleSource (samples.hpp:215-253, if4_fir) -- one
+// epoch ahead of phase A', so the ingest pass and its float2 ring are gone.
+// Extra shared memory: two raw unit buffers, one float staging row, six mbarriers.
+#ifndef L1RXG_OVL_NF
+#define L1RXG_OVL_NF 2
+#endif
+constexpr int OVL_NF = L1RXG_OVL_NF;
+__host__ __device__ inline size_t ovl_raw_unit_bytes(int nrun) {  // + copy alignment (16) + staging shift (4)
+    return ((size_t)nrun * RUN + 22 + 16 + 12 + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t ovl_raw_bytes(int nrun) {
+    return 16 + 2 * ovl_raw_unit_bytes(nrun) + 4 * ovl_raw_unit_bytes(nrun) + 8 * 8;
 }
 
 // Phase A' of one run: exclusive prefixes P'(j), M'(j) into pp/mp, totals out.
@@ -157,10 +186,10 @@ __device__ __forceinline__ void ovl_fill_rot(float2* rot, double w, int lane) {
 
 // Latency shape only: float2 rings, two sample tiles, one unit per epoch
 // (the host selects it), Scalar/Batched kernels (Noop stays on track_kernel).
-template <int T>
+template <int T, bool RAW>
 __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
-    constexpr int esz = 8;
-    constexpr int A = 2;  // samples per 16-byte bulk-copy granule
+    constexpr int esz = 8;  // tile element: float2 (the RAW variant's ring holds bytes)
+    constexpr int A = 2;    // samples per 16-byte bulk-copy granule
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CorrSmem<T>* s = reinterpret_cast<CorrSmem<T>*>(smem_raw);
     const int csize = a.csize;
@@ -169,10 +198,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     const bool writer = crank == 0;
     const int strm = a.chan_stream[cidx];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = (blockDim.x + 31) >> 5;
+    const int nfir = RAW ? 32 * OVL_NF : 0;  // FIR warps sit after the control warp
+    const int nthr = blockDim.x - nfir;
+    const int nwarps = (nthr + 31) >> 5;
     const int ctl = nwarps - 1;
-    const int nwork = blockDim.x - 32;
-    const int nthr = blockDim.x;
+    const int nwork = nthr - 32;
     const int nwork_warps = nwarps - 1;
     constexpr int V = 2 * T + 2;
     const int n = a.n;
@@ -185,10 +215,12 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     const int nrun = ((csize > 1 ? min(n, a.share) : n) + RUN - 1) / RUN;
     const int cap = nrun * RUN;
     const int64_t avail = a.avail[strm];
-    const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * esz;
+    const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * (RAW ? 1 : esz);
     float2* anchors = anchors_of(s);
     double* xs = xslots_of(s, nrun, 2, esz);
-    unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ((2 * csize * V * sizeof(double) + 15) & ~size_t(15));
+    const bool xd = a.xd != 0;  // direct exchange: warp partials straight into every CTA's slots
+    float* const xf = reinterpret_cast<float*>(xs);
+    unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ovl_xslot_bytes(csize, V, nwork_warps, a.xd);
     float2* const pm0 = reinterpret_cast<float2*>(xb);  // P' tile [cap]
     float2* const mm0 = pm0 + cap;                       // M' tile [cap]
     float2* ptot = mm0 + cap;
@@ -197,8 +229,18 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     double* wp = reinterpret_cast<double*>(rot2 + 64);  // [2]: the rate each buffer's P'/M' were made with
     int* ie = reinterpret_cast<int*>(wp + 2);            // [2]: epoch whose copy was issued into each tile
     long long* dn = reinterpret_cast<long long*>(ie + 2); // epochs done (control warp -> writeback)
+    // RAW: raw unit buffers [2], float staging row, mbarriers, stop flag
+    unsigned char* const rawb = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(dn + 1) + 15) & ~uintptr_t(15));
+    const size_t rub = ovl_raw_unit_bytes(nrun);
+    float* const xfl = reinterpret_cast<float*>(rawb + 2 * rub);
+    uint64_t* const rbar = reinterpret_cast<uint64_t*>(rawb + 6 * rub);  // [2] raw unit landed
+    uint64_t* const fbar = rbar + 2;                                     // [2] float2 tile filled
+    uint64_t* const ebar = rbar + 4;                                     // [2] float2 tile consumed
+    volatile int* const fstop = reinterpret_cast<volatile int*>(rbar + 6);
     const int64_t off0 = a.chans[cidx].sample_offset_next_epoch;
-    const bool ring_ok = off0 >= 0 && off0 >= avail - a.ring_cap;
+    // (RAW: the 22 samples of FIR history before the window must still be in the ring)
+    const bool ring_ok = off0 >= 0 && off0 - (RAW ? 22 : 0) >= avail - a.ring_cap;
     // epoch v's unit into tile v & 1 (range admission only; an Idle channel's
     // speculative copies are drained at exit)
     auto try_issue = [&](int v) {
@@ -224,7 +266,14 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             mbar_init(&s->bars[b][1], 1);
             mbar_init(&s->pbar[b], 1);
             s->inflight[b] = 0;
+            if (RAW) {
+                mbar_init(&rbar[b], 1);
+                mbar_init(&fbar[b], (uint32_t)nfir);
+                mbar_init(&ebar[b], 1);
+            }
         }
+        if (RAW)
+            fstop[0] = fstop[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         s->pending = 0;
         s->stop = 0;
@@ -242,8 +291,10 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
         const l1rxg_channel& ch = s->ch;
         make_consts(s->c, ch.code_phase_chips, ch.code_freq_hz, ch.carrier_doppler_hz, ch.carrier_phase_rad,
                     a.lc.fs, n);
-        try_issue(0);
-        try_issue(1);
+        if (!RAW) {
+            try_issue(0);
+            try_issue(1);
+        }
         wp[0] = s->c.w;
     }
     __syncthreads();
@@ -254,7 +305,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     // prologue: phase A' of epoch 0 with its own rate (dw = 0)
     auto phase_a_epoch = [&](int v, const float2* rot) {
         const int b = v & 1;
-        const int delta = (int)(unit_pos(v) & (A - 1));
+        const int delta = RAW ? 0 : (int)(unit_pos(v) & (A - 1));
         const int h = A * ((len + delta) / (2 * A));
         const float2* rawt = reinterpret_cast<const float2*>(tile_of(s, nrun, b, esz)) + delta;
         const int i0 = r0 + tid * RUN;
@@ -262,10 +313,14 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
         const int r0t = delta + tid * RUN;
         const uint32_t par = (uint32_t)(v >> 1) & 1u;
         if (cnt > 0) {
-            if (r0t < h)
-                mbar_wait(&s->bars[b][0], par);
-            if (r0t + RUN > h)
-                mbar_wait(&s->bars[b][1], par);
+            if (RAW) {
+                mbar_wait(&fbar[b], par);  // the FIR warps filled tile b
+            } else {
+                if (r0t < h)
+                    mbar_wait(&s->bars[b][0], par);
+                if (r0t + RUN > h)
+                    mbar_wait(&s->bars[b][1], par);
+            }
             if (cnt == RUN)
                 ovl_phase_a<true>(rawt + tid * RUN, pm0 + tid * RUN, mm0 + tid * RUN, rot, cnt, ptot[tid],
                                   mtot[tid]);
@@ -283,7 +338,89 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     int e = 0;
     int64_t done = a.ecount[cidx];
     int rec_i = (int)(done % a.max_records);
-    if (!first_ok) {  // nothing admitted (also: overwritten window)
+    if (RAW && tid >= nthr) {
+        // ---- FIR warps: raw unit of epoch v -> float2 tile v & 1, ahead of phase A'
+        const int ftid = tid - nthr;
+        auto adm = [&](int v) { return first_ok && v < a.max_epochs && off0 + (int64_t)(v + 1) * n <= avail; };
+        auto issue_raw = [&](int v) {  // window [pos - 22, pos + len) from the 16-byte boundary below it
+            const int64_t pos = (off0 + r0 + (int64_t)v * n) % a.ring_cap;
+            const int dl = (int)((pos - 22) & 15);
+            const uint32_t bytes = (uint32_t)((dl + len + 22 + 15) & ~15);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&rbar[v & 1], bytes);
+            tma_load_1d(rawb + (size_t)(v & 1) * rub, ring + (pos - 22 - dl), bytes, &rbar[v & 1]);
+        };
+        if (ftid == 0 && adm(0))
+            issue_raw(0);
+        int pend = adm(0) ? 0 : -1;  // newest epoch whose raw copy was issued
+        for (int v = 0; adm(v); ++v) {
+            const int b = v & 1;
+            named_bar_sync(4, nfir);  // every FIR warp is done with epoch v-1 (raw buffer b^1, staging row)
+            if (adm(v + 1)) {
+                if (ftid == 0)
+                    issue_raw(v + 1);
+                pend = v + 1;
+            }
+            mbar_wait(&rbar[b], (uint32_t)(v >> 1) & 1u);
+            const int64_t pos = (off0 + r0 + (int64_t)v * n) % a.ring_cap;
+            const int dl = (int)((pos - 22) & 15);
+            const unsigned char* rw = rawb + (size_t)b * rub;
+            // bytes -> floats, a word at a time, shifted so that sample 4q - 24 of the unit sits at a
+            // 16-byte aligned staging index: sample i <-> byte dl + 22 + i <-> float dl + 22 + i + sh
+            const int sh = (4 - ((dl + 22) & 3)) & 3;
+            for (int j = 4 * ftid; j < dl + len + 22; j += 4 * nfir) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(rw + j);
+                float* o = xfl + j + sh;
+                o[0] = (float)(int8_t)(w & 0xffu);
+                o[1] = (float)(int8_t)((w >> 8) & 0xffu);
+                o[2] = (float)(int8_t)((w >> 16) & 0xffu);
+                o[3] = (float)(int8_t)(w >> 24);
+            }
+            if (ftid == 0) {  // one thread decides (uniformly for the named barrier) whether to go on
+                if (v >= 2)
+                    mbar_wait(&ebar[b], (uint32_t)((v - 2) >> 1) & 1u);  // epoch v-2 is done with tile b
+                fstop[1] = fstop[0];
+            }
+            named_bar_sync(4, nfir);
+            if (fstop[1])
+                break;
+            float2* tl = reinterpret_cast<float2*>(tile_of(s, nrun, b, esz));
+            const int ph0 = (int)((off0 + r0 + (int64_t)v * n) & 3);
+            // four consecutive outputs per task from 28 staged floats (samples 4q - 24 .. 4q + 3) held in
+            // registers; the mixer phase of output u is (ph0 + u) & 3 for every task
+            const float4* x4 = reinterpret_cast<const float4*>(xfl + dl + sh - 2);  // sample -24
+            for (int q = ftid; 4 * q < len; q += nfir) {
+                float x[28];
+#pragma unroll
+                for (int k = 0; k < 7; ++k) {
+                    const float4 v4 = x4[q + k];
+                    x[4 * k] = v4.x;
+                    x[4 * k + 1] = v4.y;
+                    x[4 * k + 2] = v4.z;
+                    x[4 * k + 3] = v4.w;
+                }
+                float2 y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    y[u] = if4_fir(&x[24 + u], (ph0 + u) & 3);
+                if (4 * q + 4 <= len) {
+                    float4* o = reinterpret_cast<float4*>(tl + 4 * q);
+                    o[0] = make_float4(y[0].x, y[0].y, y[1].x, y[1].y);
+                    o[1] = make_float4(y[2].x, y[2].y, y[3].x, y[3].y);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * q + u < len)
+                            tl[4 * q + u] = y[u];
+                }
+            }
+            mbar_arrive(&fbar[b]);
+            if (pend == v)
+                pend = -1;
+        }
+        if (pend >= 0)  // never leave a bulk copy in flight into freed smem
+            mbar_wait(&rbar[pend & 1], (uint32_t)(pend >> 1) & 1u);
+    } else if (!first_ok) {  // nothing admitted (also: overwritten window)
         if (tid == 0 && s->ch.state != L1RXG_IDLE && a.max_epochs > 0 && off0 + n <= avail && !ring_ok)
             a.status[cidx] = 1;
     } else if (warp == ctl) {
@@ -292,8 +429,18 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             const EpochConsts c = s->c;  // epoch e's constants (written by the previous update)
             const int64_t off = s->ch.sample_offset_next_epoch;
             nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
-            named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
-            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
+            if (xd) {  // every work warp of the cluster stores its partials here: no X barrier, no CTA totals
+                const int par = e & 1;
+                const int KW = csize * nwork_warps;
+                if (lane == 0)
+                    mbar_expect_tx(&s->pbar[par], (uint32_t)(KW * V * 4));
+                mbar_wait_cluster(&s->pbar[par], (uint32_t)(e >> 1) & 1u);
+                gather_direct<V>(xf + (size_t)par * KW * V, KW, s->sums, lane);
+                __syncwarp();
+            } else {
+                named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
+            }
+            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i, xd);
             const bool stop = s->stop != 0;
             named_bar_arrive(3, nthr);  // Y: epoch e+1's constants (or stop)
             if (s->pending) {           // epoch e's metrics and record, while e+1 correlates
@@ -359,14 +506,34 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             phase_b_fold<T>(pb, acc);
             if (tid == 0)
                 PROF_STAMP(3);
-            warp_partials<V>(acc, s->red, lane, warp);
+            if constexpr (V <= 32) {
+                if (xd) {
+                    float val;
+                    int idx;
+                    if (warp_partials_reg<V>(acc, lane, val, idx)) {
+                        const int par = e & 1;
+                        float* slot = xf + ((size_t)(par * csize + crank) * nwork_warps + warp) * V + idx;
+                        for (int q = 0; q < csize; ++q)
+                            st_async_f32(cluster_map(slot, q), val, cluster_map(&s->pbar[par], q));
+                    }
+                } else {
+                    warp_partials<V>(acc, s->red, lane, warp);
+                }
+            } else {
+                warp_partials<V>(acc, s->red, lane, warp);
+            }
             named_bar_sync(1, nwork);  // tile b consumed; partials written
-            named_bar_arrive(2, nthr);  // X
+            if (!xd)
+                named_bar_arrive(2, nthr);  // X
             if (tid == 0)
                 PROF_STAMP(4);
             if (tid == 0) {  // the copy of epoch e+2 into tile b, after X (off the update's path)
-                s->inflight[b] = 0;
-                try_issue(e + 2);
+                if (RAW) {
+                    mbar_arrive(&ebar[b]);  // the FIR warps may refill tile b
+                } else {
+                    s->inflight[b] = 0;
+                    try_issue(e + 2);
+                }
             }
             // speculative phase A' of epoch e+1 with this epoch's rate
             const int64_t offn = off0 + (int64_t)(e + 1) * n;
@@ -387,6 +554,11 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
                 break;
             ++e;
         }
+    }
+    if (RAW && tid == 0) {  // release FIR warps waiting for a tile no epoch will consume
+        fstop[0] = 1;
+        mbar_arrive(&ebar[0]);
+        mbar_arrive(&ebar[1]);
     }
     __syncthreads();
     if (tid == 0) {

@@ -70,6 +70,7 @@ constexpr int SEG_FILL_UNR = L1RXG_SEG_FILL_UNR;  // step-table transitions loca
 constexpr int SEG_UNIT_BYTES = 32 * 128;     // 32 rows x 32 cint16 samples
 constexpr int SEG_MIN_N = 32 * 32 * (SEG_NW - 1) + 1;  // every warp has >= 1 unit per epoch
 constexpr int SEG_TRANS_P = 576;             // transitions per code period (<= 544 for C/A codes)
+constexpr int SEG_CLASSES = 8;               // CTA classes by warp slot (CTAs per SM, capped)
 
 struct __align__(64) SegArgs {
     TrackArgs t;
@@ -83,6 +84,25 @@ struct __align__(64) SegArgs {
     int fast_geom;      // seg_geometry_ok: unchecked step-table entries away from ties
     int qgrid;          // every tap offset a multiple of 1/4 chip in [-1, 1]: start chips by the LUT
     int qdirect;        // quarter grid + >= 62 samples per chip: per-run crossings, no step table (QD kernel)
+    // gang pacing: the channels of one stream (consecutive channel indices) read the same
+    // samples; a channel starts its next epoch only when every sibling is within `pace`
+    // epochs of it, so the stream's window stays in L2 (one DRAM read per sample instead of
+    // one per channel).  prog[c] = epochs of this launch channel c has behind it.
+    int* prog;          // [n_channels] (zeroed before the launch)
+    int pace;           // allowed lead in epochs (0: no pacing)
+    // gang tickets: the warp scheduler favours a CTA by the age of its warp slots (measured: the CTA in
+    // slots 0-3 of an SM runs 2.2x faster than the one in slots 16-19, profiles/r3e_seg_item_trace_chunk32.txt),
+    // so CTAs are classed by slot and every class takes whole gang-chunks (one chunk of every channel of
+    // one stream): siblings run on equally fast CTAs, start together and stay together, and the stream's
+    // window is read from DRAM once.  gang_first == nullptr: single queue of (chunk, channel) items.
+    const int* gang_first;        // [n_gangs] first channel of the gang
+    const int* gang_count;        // [n_gangs] channels of the gang (<= gang_max)
+    int n_gangs, gang_max;
+    int* cnext;                   // [SEG_CLASSES] per-class sub-item counters (zeroed before the launch)
+    int* ctab;                    // [SEG_CLASSES][ctab_stride] gang-chunk of each class ticket (-1: not yet drawn)
+    int ctab_stride;
+    const uint32_t* chipw;        // [33][CHIP_EXT / 32 + 1] chip bits per PRN (built once per context)
+    unsigned long long* trace;    // optional [n_items][3]: globaltimer at item start / end, smid << 32 | warp slot (L1RXG_SEG_TRACE)
 };
 
 template <int T>
@@ -692,8 +712,40 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
 
     for (;;) {
         // ---- next work item
-        if (tid == 0)
-            s->item = atomicAdd(sa.next, 1);
+        if (tid == 0) {
+            if (sa.gang_first) {
+                unsigned wslot;
+                asm volatile("mov.u32 %0, %%warpid;" : "=r"(wslot));
+                const int k = min((int)(wslot / SEG_NW), SEG_CLASSES - 1);
+                const int n_gc = sa.n_items / sa.n_channels * sa.n_gangs;  // gang-chunks of the launch
+                int item = sa.n_items;
+                for (;;) {
+                    const int i = atomicAdd(&sa.cnext[k], 1);
+                    const int ticket = i / sa.gang_max, member = i - ticket * sa.gang_max;
+                    if (ticket >= sa.ctab_stride)  // (cannot happen: one spare ticket per CTA of the grid)
+                        break;
+                    volatile int* slot = sa.ctab + (size_t)k * sa.ctab_stride + ticket;
+                    int g;
+                    if (member == 0) {  // first of its ticket: draws the class's next gang-chunk
+                        g = atomicAdd(sa.next, 1);
+                        *slot = g;
+                    } else {
+                        while ((g = *slot) < 0)
+                            __nanosleep(100);
+                    }
+                    if (g >= n_gc)
+                        break;
+                    const int gang = g % sa.n_gangs;
+                    if (member >= sa.gang_count[gang])
+                        continue;
+                    item = (g / sa.n_gangs) * sa.n_channels + sa.gang_first[gang] + member;
+                    break;
+                }
+                s->item = item;
+            } else {
+                s->item = atomicAdd(sa.next, 1);
+            }
+        }
         __syncthreads();
         const int item = s->item;
         if (item >= sa.n_items)
@@ -714,35 +766,56 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
                 }
                 __threadfence();
             }
-            // state written by another SM: read around L1
+            s->pending = 0;
+            if (sa.trace) {
+                unsigned long long tn;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                sa.trace[3 * (size_t)item] = tn;
+                unsigned smid, wid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+                sa.trace[3 * (size_t)item + 2] = ((unsigned long long)smid << 32) | wid;
+            }
+        }
+        __syncthreads();  // (orders the ready wait before every thread's loads)
+        {   // state written by another SM: read around L1, every thread a share
             const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.chans + cidx);
             unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s->ch);
-            for (int q = 0; q < (int)(sizeof(l1rxg_channel) / 8); ++q)
+            for (int q = tid; q < (int)(sizeof(l1rxg_channel) / 8); q += blockDim.x)
                 dst[q] = __ldcg(src + q);
-            s->pending = 0;
         }
         __syncthreads();
         if (max_e <= 0 || s->stop) {  // past the launch's epoch budget (or the wait gave up)
             __syncthreads();
-            if (tid == 0)
+            if (tid == 0) {
+                if (sa.pace > 0)
+                    *(volatile int*)&sa.prog[cidx] = 0x3fffffff;  // never holds a sibling back
                 atomicExch(&sa.ready[cidx], chunk + 1);
+            }
             continue;
         }
         const int strm = a.chan_stream[cidx];
+        // the gang: up to 32 consecutive channels around cidx on the same stream
+        int g_lo = cidx, g_n = 1;
+        if (sa.pace > 0) {
+            while (g_lo > 0 && cidx - g_lo < 31 && a.chan_stream[g_lo - 1] == strm)
+                --g_lo;
+            int g_hi = cidx;
+            while (g_hi + 1 < sa.n_channels && g_hi + 1 - g_lo < 32 && a.chan_stream[g_hi + 1] == strm)
+                ++g_hi;
+            g_n = g_hi - g_lo + 1;
+        }
+        const int ge0 = chunk * sa.chunk_epochs;  // this item's first epoch within the launch
         const int64_t avail = a.avail[strm];
         const int64_t off0 = s->ch.sample_offset_next_epoch;
         if (s->prn_cached != s->ch.prn) {  // the PRN's chip bits and transition list
-            // stage the code in the (drained) unit buffers, then build from shared memory
+            // stage the code in the (drained) unit buffers; the chip bits come from the context's table
             int8_t* cc = reinterpret_cast<int8_t*>(smem_raw + boff);
             for (int j = tid; j < 1023; j += blockDim.x)
                 cc[j] = a.codes[s->ch.prn * 1023 + j];
+            for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x)
+                s->chipw[q] = sa.chipw[s->ch.prn * (CHIP_EXT / 32 + 1) + q];
             __syncthreads();
-            for (int q = tid; q <= CHIP_EXT / 32; q += blockDim.x) {
-                uint32_t wv = 0;
-                for (int b = 0; b < 32; ++b)
-                    wv |= (cc[(32 * q + b) % 1023] > 0 ? 1u : 0u) << b;
-                s->chipw[q] = wv;
-            }
             if (warp == ctl) {  // ballot-scan of the code's transitions
                 int running = 0;
                 for (int base = 0; base < 1023; base += 32) {
@@ -1129,6 +1202,10 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
             __syncthreads();
             if (warp == 0) {
                 const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
+                // sibling progress, loaded now and looked at after the update
+                int sib = 0x7fffffff;
+                if (g_n > 1 && lane < g_n)
+                    sib = __ldcg(sa.prog + g_lo + lane);
 #ifdef L1RXG_SEG_XSKIP_UPDATE  // experiment: bound on hiding the loop update (wrong results)
                 if (lane == 0) {
                     s->c.phi = cc.phi;
@@ -1154,6 +1231,17 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
                 sincosf((float)(s->c.w * (double)lane), &sn, &co);
                 s->rot[lane] = make_float2(co * scale, sn * scale);
                 s->rotq[(lane & 7) * 4 + (lane >> 3)] = make_float2(co * scale, sn * scale);
+                if (g_n > 1) {  // publish this epoch, then wait for the slowest sibling (bounded: a hint, never a dependency)
+                    const int mine = ge0 + e + 1;
+                    if (lane == 0)
+                        *(volatile int*)&sa.prog[cidx] = mine;
+                    int spins = 0;
+                    while (__reduce_min_sync(0xffffffffu, sib) < mine - sa.pace && ++spins < 256) {
+                        __nanosleep(400);
+                        if (lane < g_n)
+                            sib = __ldcg(sa.prog + g_lo + lane);
+                    }
+                }
             }
             __syncthreads();
             if (s->stop)
@@ -1172,14 +1260,27 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
             consumed = issued;
         }
         __syncthreads();
+        {
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s->ch);
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.chans + cidx);
+            for (int q = tid; q < (int)(sizeof(l1rxg_channel) / 8); q += blockDim.x)
+                dst[q] = src[q];
+        }
         if (tid == 0) {
-            a.chans[cidx] = s->ch;
             a.ecount[cidx] = done;
+            if (sa.trace) {
+                unsigned long long tn;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                sa.trace[3 * (size_t)item + 1] = tn;
+            }
         }
         __threadfence();  // records, tap sums and state visible before the chunk is marked done
         __syncthreads();
-        if (tid == 0)
+        if (tid == 0) {
+            if (sa.pace > 0)  // an item that ended early (Idle, out of samples) must not hold its siblings back
+                *(volatile int*)&sa.prog[cidx] = e < max_e ? 0x3fffffff : ge0 + max_e;
             atomicExch(&sa.ready[cidx], chunk + 1);
+        }
     }
 }
 

@@ -147,6 +147,37 @@ def test_twelve_channel_shared_stream(ctx, oracle_mod, cta_mode):
         replay_check(oracle_mod, inits[c], recs, x, n, cfg, taps, fs)
 
 
+@pytest.mark.parametrize("chunk_blocks", [13, 7])
+def test_real_if_ring_wraps(ctx, oracle_mod, chunk_blocks):
+    """Real-IF stream through a ring of 40 blocks that wraps many times
+    (chunked pushes + runs over 300 blocks): windows that straddle the ring's
+    end, and FIR histories that reach back across it (carried by the ingest
+    pass; in the raw byte ring of L1RXG_OVL_RAWIF=1 the front pad mirrors
+    the tail), give the same epochs as the oracle's
+    SampleSource on the whole stream; read_samples returns its baseband."""
+    fs, n = IF_FS, 16368
+    svs = [ss.Sv(prn=7, cn0_dbhz=46.0, doppler_hz=-1850.0, delay_chips=77.3),
+           ss.Sv(prn=19, cn0_dbhz=41.0, doppler_hz=3300.0, delay_chips=903.6)]
+    raw = _raw(300, fs, svs, "int8_real_if", IF_HZ, seed=17)
+    inits = [_init(sv, fs) for sv in svs]
+    cfg, taps = abi.TrackingCfg.default(), abi.Taps.epl(0.5)
+    trk = Tracker(ctx, abi.FMT_INT8_REAL_IF, fs, IF_HZ, inits, ring_samples=40 * n + 5,
+                  max_records=300)
+    x = oracle_mod.ingest(raw, abi.FMT_INT8_REAL_IF, fs, IF_HZ)
+    for c0 in range(0, raw.size, chunk_blocks * n + 3):
+        c1 = min(raw.size, c0 + chunk_blocks * n + 3)
+        trk.push(0, raw[c0:c1])
+        trk.run()
+        k0 = max(0, c1 - 2 * n)
+        got = trk.read_samples(0, k0, c1 - k0)
+        assert np.abs(got - x[k0:c1]).max() < 2e-6
+    counts = trk.epoch_counts()
+    for c in range(2):
+        recs = trk.records(c)
+        assert len(recs) == counts[c] >= 297
+        replay_check(oracle_mod, inits[c], recs, x, n, cfg, taps, fs)
+
+
 @pytest.mark.parametrize("shape", ["monitor", "wideband"])
 def test_multitap_replay_parity(ctx, oracle_mod, shape):
     """Configs 3 and 4 shapes (scaled): 11 taps at 0.1 chip (+2 loop taps)
@@ -377,12 +408,16 @@ def test_raw_ring_matches_decoded_ring(ctx, oracle_mod, fmt, fs, cta_mode):
 @pytest.mark.parametrize("env,sel", [
     ({"L1RXG_OVL": "0"}, "raw_ring_matches_decoded_ring or cluster_sizes"),
     ({"L1RXG_OVL_DWMAX": "-1"}, "cluster_sizes or odd_epoch_lengths or config1_shape or twelve_channel or multitap"),
-], ids=["no_overlap", "overlap_exact_every_epoch"])
+    ({"L1RXG_OVL_RAWIF": "1"}, "config1_shape or twelve_channel or real_if_ring_wraps or cluster_sizes"),
+], ids=["no_overlap", "overlap_exact_every_epoch", "raw_byte_ring_real_if"])
 def test_latency_shape_variants(env, sel):
     """In a child process (the switches are read once per process): the
     non-overlapped kernel (L1RXG_OVL=0: raw-vs-decoded bit identity, replay
-    parity), and the overlapped kernel's exact phase-A recompute forced on
-    every epoch (L1RXG_OVL_DWMAX=-1: replay parity through that path)."""
+    parity), the overlapped kernel's exact phase-A recompute forced on
+    every epoch (L1RXG_OVL_DWMAX=-1: replay parity through that path), and
+    the real-IF stream as a raw byte ring filtered by the overlapped
+    kernel's FIR warps (L1RXG_OVL_RAWIF=1; by default the ingest pass fills
+    a float2 ring)."""
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
