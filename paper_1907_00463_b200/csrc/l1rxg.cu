@@ -1541,10 +1541,16 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             for (const auto& r : t->streams)
                 most = std::max(most, r.pushed);
             const int64_t max_e = std::min<int64_t>(a.max_epochs, most / a.n + 1);
-            // L1RXG_SEG_CHUNK: epochs per work item (experiments)
+            // gang tickets when streams are shared (L1RXG_SEG_GANGS=0: the single item queue); with them a
+            // work item is 16 epochs (measured at full size, profiles/r3f_seg_gang_tickets.txt: DRAM reads 1.14x
+            // the unique bytes; 32 epochs 1.7x, 64 epochs 3.6x, same time), else an eighth of the launch
+            // (L1RXG_SEG_CHUNK overrides)
+            static const char* ev_gangs = std::getenv("L1RXG_SEG_GANGS");
             static const char* ev_chunk = std::getenv("L1RXG_SEG_CHUNK");
+            const bool use_gangs = t->gang_max > 1 && !(ev_gangs && ev_gangs[0] == '0');
             const int chunk = ev_chunk ? std::max(1, std::atoi(ev_chunk))
-                                       : static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
+                              : use_gangs ? 16
+                                          : static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
             const int64_t nchunk = std::max<int64_t>(1, (max_e + chunk - 1) / chunk);
             const int64_t items = nchunk * t->d.n_channels;
             if (items > 0x7fffffff)
@@ -1574,8 +1580,6 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             sa.prog = t->d_segq + 1 + t->d.n_channels;
             sa.pace = ev_pace ? std::atoi(ev_pace) : 0;
             CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + 2 * static_cast<size_t>(t->d.n_channels) + SEG_CLASSES), st));
-            // gang tickets when streams are shared (L1RXG_SEG_GANGS=0: the single item queue)
-            static const char* ev_gangs = std::getenv("L1RXG_SEG_GANGS");
             sa.gang_first = nullptr;
             sa.gang_count = nullptr;
             sa.n_gangs = t->n_gangs;
@@ -1583,7 +1587,7 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             sa.cnext = t->d_segq + 1 + 2 * t->d.n_channels;
             sa.ctab = nullptr;
             sa.ctab_stride = 0;
-            if (t->gang_max > 1 && !(ev_gangs && ev_gangs[0] == '0') && nchunk * t->n_gangs < 0x3fffffff) {
+            if (use_gangs && nchunk * t->n_gangs < 0x3fffffff) {
                 sa.ctab_stride = static_cast<int>(nchunk * t->n_gangs) + 1024;
                 const size_t tb = 4 * static_cast<size_t>(SEG_CLASSES) * sa.ctab_stride;
                 if (t->seg_ctab.ensure(tb))

@@ -619,7 +619,7 @@ __device__ __forceinline__ void seg_fill(typename SegEntry<T>::type* tab, const 
 #define L1RXG_SEG_MINB (SEG_NW == 4 ? 5 : 4)
 #endif  // (CTAs per SM the registers are budgeted for)
 #ifndef L1RXG_SEG_MINB_QD
-#define L1RXG_SEG_MINB_QD L1RXG_SEG_MINB
+#define L1RXG_SEG_MINB_QD (SEG_NW == 4 ? 6 : L1RXG_SEG_MINB)  // QD, 4 warps: 80 registers, six CTAs per SM (+2 %, profiles/r3g)
 #endif
 // QD = true: the direct quarter-crossing variant (sa.qdirect).  Every tap
 // offset is k/4 chip, so fl(ph + d_t) = ph + d_t and every replica step of

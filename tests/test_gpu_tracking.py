@@ -332,6 +332,55 @@ def test_batched_recordings_throughput_mode(ctx, oracle_mod, mode):
         replay_check(oracle_mod, inits[c], ra, x, n, cfg, taps, fs, tap_sums=ta)
 
 
+@pytest.mark.parametrize("layout", ["uneven", "interleaved"])
+def test_segment_gang_tickets_uneven_and_interleaved(ctx, oracle_mod, layout):
+    """The segment correlator's gang tickets (work drawn per recording by
+    CTAs of one warp-slot class): recordings with 5, 1 and 3 channels (a
+    ticket's spare members are skipped), and channels of three recordings
+    interleaved (every gang a single channel: the plain item queue); 40
+    epochs in work items of 16 (several chunks per channel); per-epoch replay
+    parity and the attached run equal to the pushed one byte for byte."""
+    import torch
+    fs, ms, n = 65.472e6, 40, 65472
+    rng = np.random.default_rng(97)
+    per = [5, 1, 3] if layout == "uneven" else [3, 3, 3]
+    raws, inits, cstream = [], [], []
+    for r, k in enumerate(per):
+        prns = rng.choice(np.arange(1, 33), k, replace=False)
+        svs = [ss.Sv(prn=int(p), cn0_dbhz=rng.uniform(40, 50), doppler_hz=rng.uniform(-5000, 5000),
+                     delay_chips=rng.uniform(0, 1023)) for p in prns]
+        raws.append(_raw(ms, fs, svs, "int16_iq", seed=970 + r))
+        inits += [_init(sv, fs) for sv in svs]
+        cstream += [r] * k
+    if layout == "interleaved":
+        order = [0, 3, 6, 1, 4, 7, 2, 5, 8]
+        inits = [inits[i] for i in order]
+        cstream = [cstream[i] for i in order]
+    raw = np.stack(raws)
+    taps = abi.Taps.make([-0.75 + 0.25 * k for k in range(7)], early=4, prompt=3, late=2)
+    cfg = abi.TrackingCfg.default()
+
+    def make():
+        return Tracker(ctx, abi.FMT_INT16_IQ, fs, 0.0, inits, chan_stream=cstream, n_streams=len(per),
+                       taps=taps, cfg=cfg, ring_samples=(ms + 4) * n, max_records=ms,
+                       cta_mode=abi.CTA_SEGMENT)
+    a = make()
+    a.push_strided(raw)
+    a.run()
+    b = make()
+    dev = torch.from_numpy(raw).cuda()
+    b.attach_device(dev.data_ptr(), raw.shape[1] // 4, raw.shape[1])
+    b.run()
+    b.sync()
+    ca = a.epoch_counts()
+    assert np.array_equal(ca, b.epoch_counts()) and ca.min() >= ms - 2
+    for c in range(len(inits)):
+        ra, ta = a.records(c, tap_sums=True)
+        assert ra.tobytes() == b.records(c).tobytes()
+        x = oracle_mod.ingest(raw[cstream[c]], abi.FMT_INT16_IQ, fs)
+        replay_check(oracle_mod, inits[c], ra, x, n, cfg, taps, fs, tap_sums=ta)
+
+
 def test_bad_cta_mode_rejected(ctx):
     init = init_channel_from_acquisition(7, 0.0, 0, 0, 0, 2.048e6)
     with pytest.raises(ValueError):

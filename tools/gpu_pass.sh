@@ -12,6 +12,8 @@ timeout 600 python bench.py --config 5 --impl reference > gpurun_out/$T/ref_conf
 timeout 600 python bench.py --config 2 --impl reference > gpurun_out/$T/ref_config2.json 2> gpurun_out/$T/ref_config2.err
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:grid_mma_kernel -c 1 -o gpurun_out/$T/grid_mma \
   python bench.py --config 5 --steps 1 --warmup 1 > gpurun_out/$T/ncu_grid.log 2>&1
+# (gpurun brings back at most 64 MiB: keep the raw page of this report, not the report)
+ncu -i gpurun_out/$T/grid_mma.ncu-rep --page raw --csv > gpurun_out/$T/grid_mma_raw.csv 2>/dev/null && rm -f gpurun_out/$T/grid_mma.ncu-rep
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$T/launches5.csv \
   python bench.py --config 5 --steps 2 --warmup 1 > gpurun_out/$T/ncu_l5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:track_seg_kernel -c 1 -o gpurun_out/$T/seg_steady \
