@@ -497,12 +497,6 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double x, uin
                  "d"(x), "r"(remote_bar)
                  : "memory");
 }
-__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float x, uint32_t remote_bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
-                     remote_addr),
-                 "r"(__float_as_uint(x)), "r"(remote_bar)
-                 : "memory");
-}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -916,68 +910,6 @@ __device__ __forceinline__ void warp_partials(const float* acc, float* red, int 
     }
 }
 
-// The same butterfly, result left in registers: returns true on the lanes
-// that hold a finished value (val = the warp's sum of value idx).  V <= 32.
-template <int V>
-__device__ __forceinline__ bool warp_partials_reg(const float* acc, int lane, float& val, int& idx) {
-    constexpr int P = (V <= 8) ? 8 : (V <= 16) ? 16 : 32;
-    static_assert(V <= 32, "register butterfly covers V <= 32");
-    float x[P];
-#pragma unroll
-    for (int v = 0; v < P; ++v)
-        x[v] = v < V ? acc[v] : 0.f;
-    int base = 0;
-#pragma unroll
-    for (int lv = 0, o = 16; lv < 5; ++lv, o >>= 1) {
-        const int c = P >> lv;
-        if (c > 1) {
-            const int h = c / 2;
-            const bool upper = (lane & o) != 0;
-#pragma unroll
-            for (int i = 0; i < h; ++i) {
-                const float send = upper ? x[i] : x[i + h];
-                const float keep = upper ? x[i + h] : x[i];
-                x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-            if (upper)
-                base += h;
-        } else {
-            x[0] += __shfl_xor_sync(0xffffffffu, x[0], o);
-        }
-    }
-    val = x[0];
-    idx = base;
-    return base < V && (lane & (32 / P - 1)) == 0;
-}
-
-// Direct exchange (overlapped kernel): every work warp of every CTA of the
-// cluster has stored its V fp32 partials into this CTA's slots x[KW][V]
-// (KW = cluster CTAs x work warps).  Lane (g, v) adds the slots g, g+G, ...
-// of value v in two fp64 chains, then the G groups are folded by shuffles:
-// a fixed order, identical in every CTA.  Totals to sums[0..V).
-template <int V>
-__device__ __forceinline__ void gather_direct(const float* x, int KW, double* sums, int lane) {
-    constexpr int P = (V <= 8) ? 8 : (V <= 16) ? 16 : 32;
-    constexpr int G = 32 / P;
-    const int v = lane & (P - 1), g = lane / P;
-    double t0 = 0.0, t1 = 0.0;
-    if (v < V) {
-        int i = g;
-        for (; i + G < KW; i += 2 * G) {
-            t0 += (double)x[i * V + v];
-            t1 += (double)x[(i + G) * V + v];
-        }
-        if (i < KW)
-            t0 += (double)x[i * V + v];
-    }
-    double t = t0 + t1;
-#pragma unroll
-    for (int o = P; o < 32; o <<= 1)
-        t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (v < V && g == 0)
-        sums[v] = t;
-}
-
 // fp64 cross-warp totals (by warp 0): lane v adds the nwarps partials of
 // value v into four interleaved fp64 chains, then pairs them -- a fixed,
 // deterministic order; only the live warps are converted and added.
@@ -1028,7 +960,6 @@ struct TrackArgs {
     int share;        // samples of each epoch per cluster CTA (multiple of RUN)
     int thr;          // throughput-shape instantiation (track_kernel<..., true>)
     float ovl_dwmax;  // overlapped kernel: |dw| * RUN above this recomputes phase A exactly
-    int xd;           // overlapped kernel: work warps store their partials straight into every CTA
 };
 
 // Stage clocks (profiling builds only: -DL1RXG_PROFILE, run with
@@ -1166,16 +1097,13 @@ __device__ __forceinline__ void finish_epoch(S* s, const TrackArgs& a, int lane,
 template <int T, typename S>
 __device__ __forceinline__ void warp0_update(S* s, const TrackArgs& a, const EpochConsts& c,
                                              int64_t off, int cidx, int64_t done, int nwork_warps,
-                                             int lane, int crank, int ep, double* xs, int rec_i,
-                                             bool gathered = false) {
+                                             int lane, int crank, int ep, double* xs, int rec_i) {
     constexpr int V = 2 * T + 2;
     PROF_W(0);
-    if (!gathered) {
-        warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
-        __syncwarp();
-    }
+    warp0_totals<V>(s->red, s->sums, lane, nwork_warps);
+    __syncwarp();
     PROF_W(1);
-    if (a.csize > 1 && !gathered) {
+    if (a.csize > 1) {
         // every CTA of the cluster sends its fp64 totals to every CTA
         // (st.async completing bytes on the receiver's mbarrier), then each
         // sums the csize slots in rank order: identical cluster totals (and

@@ -236,7 +236,7 @@ size_t ovl_smem(const TrackArgs& a, int nt, bool raw) {
     if (len > (nt - 32) * RUN)
         return 0;
     const int nrun = (len + RUN - 1) / RUN;  // the kernel's layout unit
-    const size_t xsl = ovl_xslot_bytes(a.csize, 2 * T + 2, (nt - 32) / 32, a.xd);
+    const size_t xsl = ovl_xslot_bytes(a.csize, 2 * T + 2);
     const size_t sm = smem_bytes<T>(nrun, 2, 8) + xsl + ovl_extra_bytes(nrun) + (raw ? ovl_raw_bytes(nrun) : 0);
     return sm > 227u * 1024u ? 0 : sm;
 }
@@ -338,10 +338,7 @@ int cluster_capacity(int K, int nt, int nbuf, int len) {
     int c = cap(reinterpret_cast<const void*>(track_kernel<T, SK_F32, false>),
                 smem_bytes<T>(nt - 32, nbuf, 8) + xs);
     const int nrun = (len + RUN - 1) / RUN;
-    const size_t sm_ovl = smem_bytes<T>(nrun, 2, 8) +
-                          std::max(ovl_xslot_bytes(K, 2 * T + 2, (nt - 32) / 32, 0),
-                                   ovl_xslot_bytes(K, 2 * T + 2, (nt - 32) / 32, 1)) +
-                          ovl_extra_bytes(nrun);
+    const size_t sm_ovl = smem_bytes<T>(nrun, 2, 8) + ovl_xslot_bytes(K, 2 * T + 2) + ovl_extra_bytes(nrun);
     if (nbuf == 2 && sm_ovl <= 227u * 1024u)
         c = std::min(c, cap(reinterpret_cast<const void*>(track_ovl_kernel<T, false>), sm_ovl));
     return c;
@@ -608,7 +605,7 @@ struct l1rxg_tracker {
     int seg = 0;     // segment correlator (track_seg_kernel) over a raw cint16 ring
     CUtensorMap tmap{};  // seg: the ring as [stream][row][32 samples] for TMA tensor copies
     int64_t att_samples = 0;  // seg: > 0 while device recordings are attached in place of the ring
-    int* d_segq = nullptr;    // seg: work-item counter + per-channel chunks done + progress + class counters
+    int* d_segq = nullptr;    // seg: work-item counter + per-channel chunks done + class counters
     int* d_gangs = nullptr;   // seg: [2][n_gangs] first channel and channel count of each gang (same-stream run)
     int n_gangs = 0, gang_max = 0;
     DevBuf seg_ctab;          // seg: per-class ticket table of a launch
@@ -1137,7 +1134,6 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
             pa.share = t->share;
             pa.nbuf = t->nbuf;
             pa.thr = 0;
-            pa.xd = 0;
             pa.lc.kernel = d->kernel;
             auto probe = [&]() -> int { DISPATCH_T(t->T, ovl_raw_applicable, pa, d->n_channels, t->nt); };
             if (probe() == 0) {
@@ -1176,7 +1172,7 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
         cudaMemset(t->d_ring, 0, static_cast<size_t>(stride) * t->streams.size());
     for (size_t k = 0; k < t->streams.size(); ++k)
         t->streams[k].ring = t->d_ring + (static_cast<int64_t>(k) * stride + t->pad) * t->esz;
-    if (t->seg && (e = cudaMalloc(&t->d_segq, 4 * (1 + 2 * static_cast<size_t>(std::max(1, d->n_channels)) + SEG_CLASSES))) != cudaSuccess)
+    if (t->seg && (e = cudaMalloc(&t->d_segq, 4 * (1 + static_cast<size_t>(std::max(1, d->n_channels)) + SEG_CLASSES))) != cudaSuccess)
         return fail(e);
     if (t->seg && d->n_channels > 0) {  // gangs: runs of consecutive channels on the same stream
         std::vector<int> first, count;
@@ -1514,10 +1510,6 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
     a.thr = t->thr;
     static const char* ev_dw = std::getenv("L1RXG_OVL_DWMAX");
     a.ovl_dwmax = ev_dw ? static_cast<float>(std::atof(ev_dw)) : 1e-3f;
-    // direct exchange of the warp partials (overlapped kernel, clusters): L1RXG_OVL_XD=0/1 overrides
-    static const char* ev_xd = std::getenv("L1RXG_OVL_XD");
-    a.xd = ev_xd && ev_xd[0] == '1' && t->csize > 1 && 2 * t->T + 2 <= 32 &&
-           t->csize * ((t->nt - 32) / 32) <= 64;
     cudaStream_t st = t->ctx->compute;
     cudaEvent_t e0 = get_event(t), e1 = get_event(t);
     cudaEventRecord(e0, st);
@@ -1575,16 +1567,12 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
                          4.0 * CHIP_RATE_HZ / t->d.sample_rate_hz * 1.001 <= 2.0 / 31.0;
             if (const char* ev = std::getenv("L1RXG_SEG_QDIRECT"))  // tests: force the step-table kernel
                 sa.qdirect = sa.qdirect && ev[0] != '0';
-            // gang pacing (experiment, measured slower: profiles/r3a): siblings within L1RXG_SEG_PACE epochs; 0 = off (default)
-            static const char* ev_pace = std::getenv("L1RXG_SEG_PACE");
-            sa.prog = t->d_segq + 1 + t->d.n_channels;
-            sa.pace = ev_pace ? std::atoi(ev_pace) : 0;
-            CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + 2 * static_cast<size_t>(t->d.n_channels) + SEG_CLASSES), st));
+            CK(cudaMemsetAsync(t->d_segq, 0, 4 * (1 + static_cast<size_t>(t->d.n_channels) + SEG_CLASSES), st));
             sa.gang_first = nullptr;
             sa.gang_count = nullptr;
             sa.n_gangs = t->n_gangs;
             sa.gang_max = t->gang_max;
-            sa.cnext = t->d_segq + 1 + 2 * t->d.n_channels;
+            sa.cnext = t->d_segq + 1 + t->d.n_channels;
             sa.ctab = nullptr;
             sa.ctab_stride = 0;
             if (use_gangs && nchunk * t->n_gangs < 0x3fffffff) {

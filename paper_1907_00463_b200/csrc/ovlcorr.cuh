@@ -52,11 +52,9 @@ __host__ __device__ inline size_t ovl_extra_bytes(int nrun) {
            4 * sizeof(double) + 64;
 }
 
-// Cluster exchange slots: [2 (epoch parity)][csize][V] fp64 CTA totals, or with
-// the direct exchange (TrackArgs::xd) [2][csize][work warps][V] fp32 warp partials.
-__host__ __device__ inline size_t ovl_xslot_bytes(int csize, int V, int wwarps, int xd) {
-    const size_t b = xd ? 2u * (size_t)csize * wwarps * V * sizeof(float) : 2u * (size_t)csize * V * sizeof(double);
-    return (b + 15) & ~size_t(15);
+// Cluster exchange slots: [2 (epoch parity)][csize][V] fp64 CTA totals.
+__host__ __device__ inline size_t ovl_xslot_bytes(int csize, int V) {
+    return (2u * (size_t)csize * V * sizeof(double) + 15) & ~size_t(15);
 }
 
 // RAW variant (real int8 IF at fs/4, raw byte ring): OVL_NF extra warps turn each
@@ -218,9 +216,7 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
     const unsigned char* ring = a.ring + (int64_t)strm * a.ring_stride * (RAW ? 1 : esz);
     float2* anchors = anchors_of(s);
     double* xs = xslots_of(s, nrun, 2, esz);
-    const bool xd = a.xd != 0;  // direct exchange: warp partials straight into every CTA's slots
-    float* const xf = reinterpret_cast<float*>(xs);
-    unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ovl_xslot_bytes(csize, V, nwork_warps, a.xd);
+    unsigned char* xb = reinterpret_cast<unsigned char*>(xs) + ovl_xslot_bytes(csize, V);
     float2* const pm0 = reinterpret_cast<float2*>(xb);  // P' tile [cap]
     float2* const mm0 = pm0 + cap;                       // M' tile [cap]
     float2* ptot = mm0 + cap;
@@ -429,18 +425,8 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             const EpochConsts c = s->c;  // epoch e's constants (written by the previous update)
             const int64_t off = s->ch.sample_offset_next_epoch;
             nco_advance_lanes(s->nco_ph1, s->nco_cp1, c, s->ch, lane);
-            if (xd) {  // every work warp of the cluster stores its partials here: no X barrier, no CTA totals
-                const int par = e & 1;
-                const int KW = csize * nwork_warps;
-                if (lane == 0)
-                    mbar_expect_tx(&s->pbar[par], (uint32_t)(KW * V * 4));
-                mbar_wait_cluster(&s->pbar[par], (uint32_t)(e >> 1) & 1u);
-                gather_direct<V>(xf + (size_t)par * KW * V, KW, s->sums, lane);
-                __syncwarp();
-            } else {
-                named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
-            }
-            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i, xd);
+            named_bar_sync(2, nthr);  // X: epoch e's partial sums are in s->red
+            warp0_update<T>(s, a, c, off, cidx, done, nwork_warps, lane, crank, e, xs, rec_i);
             const bool stop = s->stop != 0;
             named_bar_arrive(3, nthr);  // Y: epoch e+1's constants (or stop)
             if (s->pending) {           // epoch e's metrics and record, while e+1 correlates
@@ -506,25 +492,9 @@ __global__ void __launch_bounds__(MAX_NT, 1) track_ovl_kernel(TrackArgs a) {
             phase_b_fold<T>(pb, acc);
             if (tid == 0)
                 PROF_STAMP(3);
-            if constexpr (V <= 32) {
-                if (xd) {
-                    float val;
-                    int idx;
-                    if (warp_partials_reg<V>(acc, lane, val, idx)) {
-                        const int par = e & 1;
-                        float* slot = xf + ((size_t)(par * csize + crank) * nwork_warps + warp) * V + idx;
-                        for (int q = 0; q < csize; ++q)
-                            st_async_f32(cluster_map(slot, q), val, cluster_map(&s->pbar[par], q));
-                    }
-                } else {
-                    warp_partials<V>(acc, s->red, lane, warp);
-                }
-            } else {
-                warp_partials<V>(acc, s->red, lane, warp);
-            }
+            warp_partials<V>(acc, s->red, lane, warp);
             named_bar_sync(1, nwork);  // tile b consumed; partials written
-            if (!xd)
-                named_bar_arrive(2, nthr);  // X
+            named_bar_arrive(2, nthr);  // X
             if (tid == 0)
                 PROF_STAMP(4);
             if (tid == 0) {  // the copy of epoch e+2 into tile b, after X (off the update's path)

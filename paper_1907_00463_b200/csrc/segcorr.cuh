@@ -84,12 +84,6 @@ struct __align__(64) SegArgs {
     int fast_geom;      // seg_geometry_ok: unchecked step-table entries away from ties
     int qgrid;          // every tap offset a multiple of 1/4 chip in [-1, 1]: start chips by the LUT
     int qdirect;        // quarter grid + >= 62 samples per chip: per-run crossings, no step table (QD kernel)
-    // gang pacing: the channels of one stream (consecutive channel indices) read the same
-    // samples; a channel starts its next epoch only when every sibling is within `pace`
-    // epochs of it, so the stream's window stays in L2 (one DRAM read per sample instead of
-    // one per channel).  prog[c] = epochs of this launch channel c has behind it.
-    int* prog;          // [n_channels] (zeroed before the launch)
-    int pace;           // allowed lead in epochs (0: no pacing)
     // gang tickets: the warp scheduler favours a CTA by the age of its warp slots (measured: the CTA in
     // slots 0-3 of an SM runs 2.2x faster than the one in slots 16-19, profiles/r3e_seg_item_trace_chunk32.txt),
     // so CTAs are classed by slot and every class takes whole gang-chunks (one chunk of every channel of
@@ -787,25 +781,11 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
         __syncthreads();
         if (max_e <= 0 || s->stop) {  // past the launch's epoch budget (or the wait gave up)
             __syncthreads();
-            if (tid == 0) {
-                if (sa.pace > 0)
-                    *(volatile int*)&sa.prog[cidx] = 0x3fffffff;  // never holds a sibling back
+            if (tid == 0)
                 atomicExch(&sa.ready[cidx], chunk + 1);
-            }
             continue;
         }
         const int strm = a.chan_stream[cidx];
-        // the gang: up to 32 consecutive channels around cidx on the same stream
-        int g_lo = cidx, g_n = 1;
-        if (sa.pace > 0) {
-            while (g_lo > 0 && cidx - g_lo < 31 && a.chan_stream[g_lo - 1] == strm)
-                --g_lo;
-            int g_hi = cidx;
-            while (g_hi + 1 < sa.n_channels && g_hi + 1 - g_lo < 32 && a.chan_stream[g_hi + 1] == strm)
-                ++g_hi;
-            g_n = g_hi - g_lo + 1;
-        }
-        const int ge0 = chunk * sa.chunk_epochs;  // this item's first epoch within the launch
         const int64_t avail = a.avail[strm];
         const int64_t off0 = s->ch.sample_offset_next_epoch;
         if (s->prn_cached != s->ch.prn) {  // the PRN's chip bits and transition list
@@ -1202,10 +1182,6 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
             __syncthreads();
             if (warp == 0) {
                 const EpochConsts cc = s->c;  // this epoch's (warp0_update writes the next one's)
-                // sibling progress, loaded now and looked at after the update
-                int sib = 0x7fffffff;
-                if (g_n > 1 && lane < g_n)
-                    sib = __ldcg(sa.prog + g_lo + lane);
 #ifdef L1RXG_SEG_XSKIP_UPDATE  // experiment: bound on hiding the loop update (wrong results)
                 if (lane == 0) {
                     s->c.phi = cc.phi;
@@ -1231,17 +1207,6 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
                 sincosf((float)(s->c.w * (double)lane), &sn, &co);
                 s->rot[lane] = make_float2(co * scale, sn * scale);
                 s->rotq[(lane & 7) * 4 + (lane >> 3)] = make_float2(co * scale, sn * scale);
-                if (g_n > 1) {  // publish this epoch, then wait for the slowest sibling (bounded: a hint, never a dependency)
-                    const int mine = ge0 + e + 1;
-                    if (lane == 0)
-                        *(volatile int*)&sa.prog[cidx] = mine;
-                    int spins = 0;
-                    while (__reduce_min_sync(0xffffffffu, sib) < mine - sa.pace && ++spins < 256) {
-                        __nanosleep(400);
-                        if (lane < g_n)
-                            sib = __ldcg(sa.prog + g_lo + lane);
-                    }
-                }
             }
             __syncthreads();
             if (s->stop)
@@ -1276,11 +1241,8 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
         }
         __threadfence();  // records, tap sums and state visible before the chunk is marked done
         __syncthreads();
-        if (tid == 0) {
-            if (sa.pace > 0)  // an item that ended early (Idle, out of samples) must not hold its siblings back
-                *(volatile int*)&sa.prog[cidx] = e < max_e ? 0x3fffffff : ge0 + max_e;
+        if (tid == 0)
             atomicExch(&sa.ready[cidx], chunk + 1);
-        }
     }
 }
 
