@@ -64,34 +64,74 @@ constexpr int ING_TILE = ING_TPB * ING_OUT_PER_THREAD;  // outputs per block
 
 // raw: bytes of samples [g0, g0+count); hist: the 22 bytes before g0
 // (zeros at stream start); writes hist_out = the last 22 bytes of the run.
+// A block stages its 1024 + 24 input samples as floats (sample t0 - 24 + k at
+// v[k]); a thread then holds the 28 samples of four consecutive outputs in
+// registers (seven LDS.128) and stores the outputs as two 16-byte vectors
+// where the ring position allows it.
 __global__ void __launch_bounds__(ING_TPB) ingest_if4_kernel(
     const int8_t* __restrict__ raw, const int8_t* __restrict__ hist, int8_t* hist_out,
     int64_t g0, int64_t count, float2* ring, int64_t R, int64_t apron, int64_t pos0,
     int64_t* avail_slot) {
-    __shared__ float v[ING_TILE + 24];
+    __shared__ __align__(16) float v[ING_TILE + 24];
     const int64_t t0 = (int64_t)blockIdx.x * ING_TILE;  // run-relative first output
-    // inputs t0-22 .. t0+ING_TILE-1
-    for (int k = threadIdx.x; k < ING_TILE + 22; k += ING_TPB) {
-        const int64_t idx = t0 - 22 + k;
+    for (int k = threadIdx.x; k < ING_TILE + 24; k += ING_TPB) {
+        const int64_t idx = t0 - 24 + k;
         int8_t b = 0;
         if (idx < 0)
-            b = hist[22 + idx];
+            b = idx >= -22 ? hist[22 + idx] : (int8_t)0;
         else if (idx < count)
             b = raw[idx];
         v[k] = (float)b;
     }
     __syncthreads();
     const int q = threadIdx.x * ING_OUT_PER_THREAD;
+    const int64_t idx0 = t0 + q;
+    if (idx0 < count) {
+        float x[28];
+        const float4* v4 = reinterpret_cast<const float4*>(v + q);
 #pragma unroll
-    for (int u = 0; u < ING_OUT_PER_THREAD; ++u) {
-        const int64_t idx = t0 + q + u;
-        if (idx >= count)
-            break;
-        const float2 y = if4_fir(&v[q + u + 22], (int)((g0 + idx) & 3));
-        int64_t pos = pos0 + idx;
+        for (int k = 0; k < 7; ++k) {
+            const float4 f = v4[k];
+            x[4 * k] = f.x;
+            x[4 * k + 1] = f.y;
+            x[4 * k + 2] = f.z;
+            x[4 * k + 3] = f.w;
+        }
+        const int ph0 = (int)((g0 + idx0) & 3);
+        float2 y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            y[u] = if4_fir(&x[24 + u], (ph0 + u) & 3);
+        int64_t pos = pos0 + idx0;
         if (pos >= R)
             pos -= R;
-        ring_put(ring, R, apron, pos, y);
+        if (idx0 + 4 <= count && pos + 4 <= R && ((pos | R) & 1) == 0) {
+            const float4 a = make_float4(y[0].x, y[0].y, y[1].x, y[1].y);
+            const float4 b = make_float4(y[2].x, y[2].y, y[3].x, y[3].y);
+            float4* o = reinterpret_cast<float4*>(ring + pos);
+            o[0] = a;
+            o[1] = b;
+            if (pos + 4 <= apron) {
+                float4* m = reinterpret_cast<float4*>(ring + R + pos);
+                m[0] = a;
+                m[1] = b;
+            } else if (pos < apron) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (pos + u < apron)
+                        ring[R + pos + u] = y[u];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (idx0 + u >= count)
+                    break;
+                int64_t p = pos + u;
+                if (p >= R)
+                    p -= R;
+                ring_put(ring, R, apron, p, y[u]);
+            }
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x < 22) {
         const int64_t idx = count - 22 + threadIdx.x;
