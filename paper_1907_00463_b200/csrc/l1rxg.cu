@@ -1104,6 +1104,21 @@ int l1rxg_tracker_create(l1rxg_ctx* c, const l1rxg_tracker_desc* d, const l1rxg_
                 t->csize = K;
                 t->share = K > 1 ? share : n;
                 t->nt = pick_threads(t->share, nullptr, MAX_NT - 32) + 32;
+                {   // phase B deals the work threads to the taps, so more threads than runs shorten its walk:
+                    // measured (profiles/r3l_lat_nwork.txt, 16.368 MHz) E/P/L at one CTA per SM: 160-224 work
+                    // threads, about one transition per thread, -3.7 % per epoch (128 and 256 are no gain: more
+                    // warps cost barrier and reduction time); 13 taps at two CTAs per SM: 160, -2 %
+                    // (L1RXG_LAT_NWORK overrides the minimum)
+                    static const char* ev_nw = std::getenv("L1RXG_LAT_NWORK");
+                    int min_nw = 0;
+                    if ((t->T <= 5 && d->n_channels * K <= nsm && t->share >= 1500) ||
+                        (t->T >= 11 && d->n_channels * K > nsm))
+                        min_nw = 160;
+                    if (ev_nw)
+                        min_nw = std::atoi(ev_nw);
+                    if (min_nw > 0)
+                        t->nt = std::max(t->nt, std::min(MAX_NT, (min_nw + 31) / 32 * 32 + 32));
+                }
                 // a second tile when it fits: the copy of epoch e+1 is then issued
                 // while epoch e is still being correlated (a full epoch ahead)
                 static const char* ev_nb1 = std::getenv("L1RXG_LAT_NBUF");
