@@ -1555,9 +1555,12 @@ int l1rxg_tracker_run(l1rxg_tracker* t, int max_epochs) {
             static const char* ev_gangs = std::getenv("L1RXG_SEG_GANGS");
             static const char* ev_chunk = std::getenv("L1RXG_SEG_CHUNK");
             const bool use_gangs = t->gang_max > 1 && !(ev_gangs && ev_gangs[0] == '0');
-            const int chunk = ev_chunk ? std::max(1, std::atoi(ev_chunk))
-                              : use_gangs ? 16
-                                          : static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
+            int chunk = ev_chunk ? std::max(1, std::atoi(ev_chunk))
+                        : use_gangs ? 16
+                                    : static_cast<int>(std::max<int64_t>(16, (max_e + 7) / 8));
+            // very long launches: at most ~4 M gang-chunks (the ticket table is 32 B per gang-chunk)
+            if (use_gangs && (max_e + chunk - 1) / chunk * t->n_gangs > (4LL << 20))
+                chunk = static_cast<int>((max_e * t->n_gangs + (4LL << 20) - 1) / (4LL << 20));
             const int64_t nchunk = std::max<int64_t>(1, (max_e + chunk - 1) / chunk);
             const int64_t items = nchunk * t->d.n_channels;
             if (items > 0x7fffffff)

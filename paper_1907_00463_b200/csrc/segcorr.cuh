@@ -724,8 +724,14 @@ __global__ void __launch_bounds__(SEG_NT, QD ? L1RXG_SEG_MINB_QD : L1RXG_SEG_MIN
                         g = atomicAdd(sa.next, 1);
                         *slot = g;
                     } else {
-                        while ((g = *slot) < 0)
+                        // (published right after its drawer's atomicAdd; bounded so that a broken
+                        // invariant ends this CTA -- and is reported by the chunk-order wait -- instead
+                        // of hanging the GPU)
+                        long long spins = 0;
+                        while ((g = *slot) < 0 && ++spins < (1LL << 22))
                             __nanosleep(100);
+                        if (g < 0)
+                            break;
                     }
                     if (g >= n_gc)
                         break;
