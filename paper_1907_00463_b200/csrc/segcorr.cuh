@@ -34,10 +34,13 @@
 //     entered by all threads), the runs, the warps' partial sums, the loop
 //     update on warp 0 (warp0_update / loop_fast, shared with track_kernel);
 //     the last warp finishes the previous epoch (loop_metrics, record) before
-//     its runs and takes one unit fewer -- all five warps correlate;
-//   * persistent CTAs (4 per SM) take work items (chunk of epochs, channel)
-//     in chunk-major order; a chunk waits for its channel's previous chunk,
-//     so a launch has no wave-quantisation tail.
+//     its runs -- all warps correlate (the QD variant below locates each
+//     run's crossings itself and has no step table);
+//   * persistent CTAs (five or six per SM) take work items of 16 epochs of
+//     one channel; a chunk waits for its channel's previous chunk, so a
+//     launch has no wave-quantisation tail; the channels of one recording
+//     are drawn together by CTAs of one warp-slot class (gang tickets,
+//     SegArgs) so that they share the recording's samples through L2.
 // DESIGN.md section 3 has the measurements behind each choice.
 #pragma once
 
@@ -52,7 +55,8 @@ namespace l1rxg {
 // Defaults (measured, config 4): four correlating warps per CTA and five
 // CTAs per SM (44 KB of shared memory each: the unit buffers first at the
 // 1024-B aligned dynamic base, no transition-count table) beat five warps x
-// four CTAs by 2 %.
+// four CTAs by 2 %; the QD variant (36 KB, 80 registers) runs six per SM;
+// two or three warps per CTA are no gain (profiles/r3g_seg_qd6_fullsize.txt).
 #ifndef L1RXG_SEG_NW
 #define L1RXG_SEG_NW 4
 #endif
