@@ -1224,7 +1224,7 @@ def run_stream(args, cfg_id, rank, world, local, dist, emit=True):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if batch else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if cfg_id in (2, 3) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded, paper_1907_00463_b200/simsource.py; loops start from truth)",
         "config": {"workload": c["desc"], "blocks": blocks, "channels": C_ch, "taps_counted": T,
                    "samples_per_block": n,
